@@ -1,0 +1,135 @@
+/*
+ * msfft_b200.h -- C ABI of the B200-native sFFT4.0 hot path.
+ *
+ * Drop-in boundary for
+ *     msfft::SfftResult msfft::sfft4(const ComplexSignal& x, int64_t k,
+ *                                    const MultiscaleConfig& cfg,
+ *                                    uint64_t seed, double delta = 1e-8);
+ * (reference: proj/include/msfft/sfft4.hpp:64-65, result/stat types :32-45,
+ * implementation proj/src/sfft4.cpp:131-187).  Plain pointers and sizes only;
+ * no torch or C++ types cross this boundary.  A C++ wrapper with the
+ * reference's exact signature and exception types is include/msfft_b200.hpp.
+ *
+ * Errors: every entry point returns an msfft_status.  MSFFT_ERR_INVALID_ARGUMENT
+ * and MSFFT_ERR_DOMAIN carry the reference's std::invalid_argument /
+ * std::domain_error messages verbatim in err[errlen] (e.g. "sfft4: need 1 <= K
+ * <= n/8", proj/src/sfft4.cpp:135; "MultiscaleConfig: l/(q+1) must exceed 1",
+ * proj/src/locate.cpp:29).  There is no CPU fallback: without a usable CUDA
+ * device every call fails with MSFFT_ERR_CUDA.
+ *
+ * Thread safety: all entry points are reentrant.  Windows and response tables
+ * live in a process-wide cache keyed (device, n, b, delta) like
+ * get_flat_window (proj/src/window.cpp:179-193).  A plan handle may be used by
+ * one thread at a time.
+ */
+#ifndef MSFFT_B200_H
+#define MSFFT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MSFFT_B200_ABI_VERSION 1
+#define MSFFT_MAX_ITERATIONS 64
+
+typedef enum msfft_status {
+    MSFFT_OK = 0,
+    MSFFT_ERR_INVALID_ARGUMENT = 1, /* std::invalid_argument in the reference */
+    MSFFT_ERR_DOMAIN = 2,           /* std::domain_error escaping sfft4       */
+    MSFFT_ERR_CUDA = 3,             /* no device / CUDA failure               */
+    MSFFT_ERR_RUNTIME = 4           /* anything else                          */
+} msfft_status;
+
+typedef enum msfft_dtype {
+    MSFFT_C128 = 0, /* interleaved (re, im) float64: cplx, proj/include/msfft/fft.hpp:9 */
+    MSFFT_C64 = 1   /* interleaved (re, im) float32, upcast exactly to float64            */
+} msfft_dtype;
+
+typedef enum msfft_location { MSFFT_HOST = 0, MSFFT_DEVICE = 1 } msfft_location;
+
+enum msfft_flags {
+    /* Skip the O(n) finiteness scan of x (ComplexSignal::validate,
+     * proj/src/signal.cpp:18-26) because the caller validated at ingest. */
+    MSFFT_FLAG_ASSUME_VALID = 1u << 0
+};
+
+/* TransformStats (proj/include/msfft/sfft4.hpp:32-40). */
+typedef struct msfft_stats {
+    int64_t samples_used;      /* distinct time indices read            */
+    int64_t samples_round_sum; /* sum_m (R_m + 1) * w_m                 */
+    double sample_fraction;    /* samples_used / n                      */
+    double runtime_ms;         /* device time of the transform          */
+    int32_t iterations;
+    int32_t reserved;
+    int64_t b_first;
+    int32_t stage_counts[MSFFT_MAX_ITERATIONS]; /* R_m per iteration */
+} msfft_stats;
+
+typedef struct msfft_plan_s* msfft_plan;
+
+const char* msfft_version(void);
+int msfft_device_count(void);
+
+/* ---- one-shot drop-in: msfft::sfft4 ----------------------------------------
+ * x: n complex samples (dtype) in host or device memory.  Output: at most
+ * `cap` entries in ascending frequency (the std::map order of SparseSpectrum);
+ * *out_count is the entry count (<= k).  stats may be NULL. */
+int msfft_sfft4(const void* x, int64_t n, int32_t dtype, int32_t x_location, int64_t k,
+                int64_t l, double q, uint64_t seed, double delta, int64_t cap, int64_t* out_f,
+                double* out_c, int64_t* out_count, msfft_stats* stats, char* err, size_t errlen);
+
+/* ---- plans: batches of independent signals sharing (n, k, l, q, delta) ----
+ * Creating a plan designs every window of the halving schedule on `device`
+ * (the reference resolves them before its timer too, sfft4.cpp:146-154). */
+int msfft_plan_create(int64_t n, int64_t k, int64_t l, double q, double delta, int32_t dtype,
+                      int32_t device, msfft_plan* out, char* err, size_t errlen);
+void msfft_plan_destroy(msfft_plan plan);
+
+/* Data-independent stats of the plan (samples_used/runtime left 0). */
+int msfft_plan_stats(msfft_plan plan, msfft_stats* stats);
+
+/* Transforms `batch` signals x[s * x_stride .. + n), s < batch, with seeds
+ * seeds[s] (host array).  Outputs are [batch][k] (out_f int64, out_c
+ * interleaved float64) and out_count[batch], in host or device memory per
+ * out_location.  Host inputs are streamed to the device in chunks overlapped
+ * with compute.  stream: cudaStream_t (NULL = the plan's own stream); the
+ * call returns after the outputs are complete.  *device_ms (optional): CUDA
+ * event time from the first device operation to the last. */
+int msfft_execute(msfft_plan plan, int64_t batch, const void* x, int64_t x_stride,
+                  int32_t x_location, const uint64_t* seeds, int64_t* out_f, double* out_c,
+                  int64_t* out_count, int32_t out_location, uint32_t flags, void* stream,
+                  double* device_ms, char* err, size_t errlen);
+
+/* Number of device kernel launches one msfft_execute of `batch` device-
+ * resident signals issues (for bench accounting). */
+int64_t msfft_plan_launches(msfft_plan plan, int64_t batch, uint32_t flags);
+
+/* ---- kernel-level entry points (parity tests) ------------------------------
+ * Window taps/support exactly as design_flat_window (window.cpp:105-177). */
+int msfft_window(int64_t n, int64_t b, double delta, int32_t device, int64_t* w, double* taps,
+                 int64_t taps_cap, char* err, size_t errlen);
+/* G_d from the device response table (FlatWindow::response_at, window.cpp:89-99);
+ * |idx| <= 3L/2 + 1. */
+int msfft_window_response(int64_t n, int64_t b, double delta, int32_t device,
+                          const int64_t* idx, int64_t count, double* out, char* err,
+                          size_t errlen);
+/* One signal (host memory), returning every iteration's bucket vectors before
+ * (pre: encode output, BucketSet::values of bucketize) and after (post) the
+ * subtraction of known tones, iteration-major then round-major, plus the
+ * final spectrum.  pre/post hold the plan's sum_m rounds_m*b_m complex
+ * values.  sel_* (optional, sum_m budget_m slots, iteration-major then by
+ * rank of |y0|): bucket id, located frequency f (-1 when below threshold,
+ * not located or rejected by the estimate) and the estimate value
+ * (run_iteration, proj/src/sfft4.cpp:75-103). */
+int msfft_trace(const void* x, int64_t n, int32_t dtype, int64_t k, int64_t l, double q,
+                uint64_t seed, double delta, double* pre, double* post, int64_t* sel_bucket,
+                int64_t* sel_f, double* sel_value, int64_t cap, int64_t* out_f, double* out_c,
+                int64_t* out_count, char* err, size_t errlen);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MSFFT_B200_H */

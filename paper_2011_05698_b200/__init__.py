@@ -1,0 +1,315 @@
+"""B200-native sFFT4.0 hot path -- Python mirror of the reference interface.
+
+The reference entry point (proj/include/msfft/sfft4.hpp:64-65)
+
+    SfftResult sfft4(const ComplexSignal& x, int64_t k,
+                     const MultiscaleConfig& cfg, uint64_t seed,
+                     double delta = 1e-8);
+
+is mirrored by :func:`sfft4` with the same argument meaning and the same
+error behaviour: ``std::invalid_argument`` -> :class:`InvalidArgument`
+(a ``ValueError``) and ``std::domain_error`` -> :class:`DomainError`, with the
+reference's messages.  Everything runs through ``libmsfft_b200.so`` (the
+C ABI in ``include/msfft_b200.h``); there is no CPU fallback.
+
+:class:`Plan` is the batched form (independent signals sharing n, k, l, q,
+delta; one seed each), used for the batched-throughput configuration.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib as _L
+
+__all__ = [
+    "MultiscaleConfig", "TransformStats", "SparseSpectrum", "SfftResult", "sfft4", "Plan",
+    "window", "window_response", "trace", "InvalidArgument", "DomainError", "CudaError",
+    "splitmix64", "device_count",
+]
+
+
+class InvalidArgument(ValueError):
+    """std::invalid_argument in the reference."""
+
+
+class DomainError(ArithmeticError):
+    """std::domain_error escaping the reference's sfft4."""
+
+
+class CudaError(RuntimeError):
+    """No usable CUDA device, or a CUDA failure (there is no CPU fallback)."""
+
+
+def _raise(status: int, err) -> None:
+    if status == _L.MSFFT_OK:
+        return
+    msg = err.value.decode(errors="replace") if err is not None else ""
+    if status == _L.MSFFT_ERR_INVALID_ARGUMENT:
+        raise InvalidArgument(msg)
+    if status == _L.MSFFT_ERR_DOMAIN:
+        raise DomainError(msg)
+    if status == _L.MSFFT_ERR_CUDA:
+        raise CudaError(msg)
+    raise RuntimeError(msg)
+
+
+def splitmix64(x: int) -> int:
+    """splitmix64 (proj/include/msfft/rng.hpp:9-14): seed derivation used by
+    the reference bench (algo seed = splitmix64(seed ^ 0x53), bench.cpp:117)."""
+    m = (1 << 64) - 1
+    x = (x + 0x9E3779B97F4A7C15) & m
+    x = ((x ^ (x >> 30)) * 0xBF58476D1CE4E5B9) & m
+    x = ((x ^ (x >> 27)) * 0x94D049BB133111EB) & m
+    return x ^ (x >> 31)
+
+
+@dataclass
+class MultiscaleConfig:
+    """proj/include/msfft/locate.hpp:13-19."""
+    l: int = 16
+    q: float = 1.0
+
+    def shrink(self) -> float:
+        return float(self.l) / (self.q + 1.0)
+
+    def validate(self) -> None:
+        if self.l < 2:
+            raise InvalidArgument("MultiscaleConfig: l must be >= 2")
+        if self.q < 0.0:
+            raise InvalidArgument("MultiscaleConfig: q must be >= 0")
+        if not (self.shrink() > 1.0):
+            raise InvalidArgument("MultiscaleConfig: l/(q+1) must exceed 1")
+
+
+@dataclass
+class TransformStats:
+    """proj/include/msfft/sfft4.hpp:32-40 (runtime_ms is device time)."""
+    samples_used: int = 0
+    samples_round_sum: int = 0
+    sample_fraction: float = 0.0
+    runtime_ms: float = 0.0
+    iterations: int = 0
+    b_first: int = 0
+    stage_counts: list = field(default_factory=list)
+
+    @classmethod
+    def _from(cls, s: _L.Stats) -> "TransformStats":
+        it = int(s.iterations)
+        return cls(int(s.samples_used), int(s.samples_round_sum), float(s.sample_fraction),
+                   float(s.runtime_ms), it, int(s.b_first), [int(v) for v in s.stage_counts[:it]])
+
+
+@dataclass
+class SparseSpectrum:
+    """proj/include/msfft/signal.hpp:23-28; entries in ascending position."""
+    n: int
+    positions: np.ndarray
+    coeffs: np.ndarray
+
+    @property
+    def entries(self) -> dict:
+        return {int(f): complex(c) for f, c in zip(self.positions, self.coeffs)}
+
+
+@dataclass
+class SfftResult:
+    spectrum: SparseSpectrum
+    stats: TransformStats
+
+
+def _is_torch(x) -> bool:
+    return type(x).__module__.startswith("torch")
+
+
+def _signal_arg(x):
+    """-> (pointer, n, dtype code, location, keepalive)."""
+    if _is_torch(x):
+        import torch
+        if x.dtype not in (torch.complex64, torch.complex128):
+            raise InvalidArgument("sfft4: x must be complex64 or complex128")
+        if not x.is_contiguous():
+            x = x.contiguous()
+        dt = _L.MSFFT_C128 if x.dtype == torch.complex128 else _L.MSFFT_C64
+        loc = _L.MSFFT_DEVICE if x.is_cuda else _L.MSFFT_HOST
+        return C.c_void_p(x.data_ptr()), int(x.shape[-1]), dt, loc, x
+    a = np.asarray(x)
+    if a.dtype == np.complex64:
+        dt = _L.MSFFT_C64
+    else:
+        a = a.astype(np.complex128, copy=False)
+        dt = _L.MSFFT_C128
+    a = np.ascontiguousarray(a)
+    return C.c_void_p(a.ctypes.data), int(a.shape[-1]), dt, _L.MSFFT_HOST, a
+
+
+def device_count() -> int:
+    return int(_L.lib().msfft_device_count())
+
+
+def sfft4(x, k: int, cfg: MultiscaleConfig | None = None, seed: int = 0,
+          delta: float = 1e-8) -> SfftResult:
+    """Drop-in for msfft::sfft4 (proj/src/sfft4.cpp:131-187) on the GPU.
+
+    x: 1-D complex array (numpy, or torch CPU/CUDA tensor), complex128 or
+    complex64 (upcast exactly).  Returns the K-pruned spectrum in ascending
+    position and the transform stats.
+    """
+    cfg = cfg or MultiscaleConfig()
+    L = _L.lib()
+    ptr, n, dt, loc, keep = _signal_arg(x)
+    cap = max(int(k), 1)
+    f = np.zeros(cap, np.int64)
+    c = np.zeros(2 * cap, np.float64)
+    cnt = C.c_int64()
+    st = _L.Stats()
+    err = C.create_string_buffer(1024)
+    status = L.msfft_sfft4(ptr, n, dt, loc, int(k), int(cfg.l), float(cfg.q),
+                           int(seed) & ((1 << 64) - 1), float(delta), cap,
+                           f.ctypes.data_as(C.POINTER(C.c_int64)),
+                           c.ctypes.data_as(C.POINTER(C.c_double)), C.byref(cnt), C.byref(st),
+                           err, 1024)
+    del keep
+    _raise(status, err)
+    m = cnt.value
+    spec = SparseSpectrum(n, f[:m].copy(), c.view(np.complex128)[:m].copy())
+    return SfftResult(spec, TransformStats._from(st))
+
+
+class Plan:
+    """Batched sfft4 over independent signals sharing (n, k, l, q, delta).
+
+    Window design for the whole halving schedule happens here (cold path),
+    as the reference pre-resolves windows before its timer
+    (proj/src/sfft4.cpp:146-154).
+    """
+
+    def __init__(self, n: int, k: int, cfg: MultiscaleConfig | None = None,
+                 delta: float = 1e-8, dtype: str = "complex64", device: int = -1):
+        cfg = cfg or MultiscaleConfig()
+        self.n, self.k, self.cfg, self.delta = int(n), int(k), cfg, float(delta)
+        self.dtype = dtype
+        dt = _L.MSFFT_C64 if dtype in ("complex64", "c64") else _L.MSFFT_C128
+        self._lib = _L.lib()
+        h = C.c_void_p()
+        err = C.create_string_buffer(1024)
+        _raise(self._lib.msfft_plan_create(self.n, self.k, int(cfg.l), float(cfg.q),
+                                           self.delta, dt, int(device), C.byref(h), err, 1024),
+               err)
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            self._lib.msfft_plan_destroy(h)
+            self._h = None
+
+    def stats(self) -> TransformStats:
+        s = _L.Stats()
+        self._lib.msfft_plan_stats(self._h, C.byref(s))
+        return TransformStats._from(s)
+
+    def launches(self, batch: int, assume_valid: bool = False) -> int:
+        flags = _L.MSFFT_FLAG_ASSUME_VALID if assume_valid else 0
+        return int(self._lib.msfft_plan_launches(self._h, int(batch), flags))
+
+    def execute(self, x, seeds, out=None, assume_valid: bool = False, stream=None):
+        """x: (batch, n) complex array/tensor (host or CUDA).  seeds: batch
+        integers.  out: optional (f, c, count) preallocated outputs -- torch
+        CUDA tensors (int64 [B,k], complex128 [B,k], int64 [B]) keep the
+        results on the device; otherwise numpy arrays are returned.
+        Returns (f, c, count, device_ms)."""
+        ptr, n, dt, loc, keep = _signal_arg(x)
+        if n != self.n:
+            raise InvalidArgument("ComplexSignal: sample count != n")
+        shape = tuple(keep.shape)
+        batch = 1 if len(shape) == 1 else int(shape[0])
+        seeds = np.ascontiguousarray(np.asarray(seeds, dtype=np.uint64).reshape(-1))
+        if seeds.size != batch:
+            raise InvalidArgument("Plan.execute: need one seed per signal")
+        if out is None:
+            f = np.zeros((batch, self.k), np.int64)
+            c = np.zeros((batch, self.k), np.complex128)
+            cnt = np.zeros(batch, np.int64)
+            fptr, cptr, nptr = f.ctypes.data, c.ctypes.data, cnt.ctypes.data
+            oloc = _L.MSFFT_HOST
+        else:
+            f, c, cnt = out
+            if _is_torch(f):
+                fptr, cptr, nptr = f.data_ptr(), c.data_ptr(), cnt.data_ptr()
+                oloc = _L.MSFFT_DEVICE if f.is_cuda else _L.MSFFT_HOST
+            else:
+                fptr, cptr, nptr = f.ctypes.data, c.ctypes.data, cnt.ctypes.data
+                oloc = _L.MSFFT_HOST
+        ms = C.c_double()
+        err = C.create_string_buffer(1024)
+        flags = _L.MSFFT_FLAG_ASSUME_VALID if assume_valid else 0
+        status = self._lib.msfft_execute(
+            self._h, batch, ptr, n, loc, seeds.ctypes.data_as(C.POINTER(C.c_uint64)),
+            C.c_void_p(fptr), C.c_void_p(cptr), C.c_void_p(nptr), oloc, flags,
+            C.c_void_p(stream or 0), C.byref(ms), err, 1024)
+        _raise(status, err)
+        return f, c, cnt, ms.value
+
+
+def window(n: int, b: int, delta: float, device: int = -1):
+    """(w, taps) exactly as design_flat_window (proj/src/window.cpp:105-177)."""
+    L = _L.lib()
+    w = C.c_int64()
+    err = C.create_string_buffer(1024)
+    _raise(L.msfft_window(n, b, float(delta), device, C.byref(w), None, 0, err, 1024), err)
+    taps = np.zeros(w.value, np.float64)
+    _raise(L.msfft_window(n, b, float(delta), device, C.byref(w),
+                          taps.ctypes.data_as(C.POINTER(C.c_double)), w.value, err, 1024), err)
+    return w.value, taps
+
+
+def window_response(n: int, b: int, delta: float, idx, device: int = -1) -> np.ndarray:
+    """G_d from the device response table (FlatWindow::response_at)."""
+    L = _L.lib()
+    idx = np.ascontiguousarray(np.asarray(idx, dtype=np.int64))
+    out = np.zeros(idx.size, np.float64)
+    err = C.create_string_buffer(1024)
+    _raise(L.msfft_window_response(n, b, float(delta), device,
+                                   idx.ctypes.data_as(C.POINTER(C.c_int64)), idx.size,
+                                   out.ctypes.data_as(C.POINTER(C.c_double)), err, 1024), err)
+    return out
+
+
+def trace(x, k: int, cfg: MultiscaleConfig | None = None, seed: int = 0, delta: float = 1e-8,
+          values_per_signal: int = 0, selections: int = 0):
+    """Kernel-level view of one transform: every iteration's bucket vectors
+    before (encode output) and after the subtraction of known tones, the
+    per-rank selection results (bucket, f or -1, value) and the final
+    spectrum.  values_per_signal = sum_m rounds_m*b_m and selections =
+    sum_m min(k_m, b_m) size the buffers (both follow from the plan)."""
+    cfg = cfg or MultiscaleConfig()
+    L = _L.lib()
+    a = np.asarray(x)
+    dt = _L.MSFFT_C64 if a.dtype == np.complex64 else _L.MSFFT_C128
+    a = np.ascontiguousarray(a if dt == _L.MSFFT_C64 else a.astype(np.complex128))
+    n = a.shape[-1]
+    pre = np.zeros(2 * values_per_signal, np.float64)
+    post = np.zeros(2 * values_per_signal, np.float64)
+    sb = np.full(max(selections, 1), -2, np.int64)
+    sf = np.full(max(selections, 1), -2, np.int64)
+    sv = np.zeros(2 * max(selections, 1), np.float64)
+    cap = max(int(k), 1)
+    f = np.zeros(cap, np.int64)
+    c = np.zeros(2 * cap, np.float64)
+    cnt = C.c_int64()
+    err = C.create_string_buffer(1024)
+    PD = C.POINTER(C.c_double)
+    PI = C.POINTER(C.c_int64)
+    _raise(L.msfft_trace(C.c_void_p(a.ctypes.data), n, dt, int(k), int(cfg.l), float(cfg.q),
+                         int(seed) & ((1 << 64) - 1), float(delta), pre.ctypes.data_as(PD),
+                         post.ctypes.data_as(PD), sb.ctypes.data_as(PI), sf.ctypes.data_as(PI),
+                         sv.ctypes.data_as(PD), cap, f.ctypes.data_as(PI),
+                         c.ctypes.data_as(PD), C.byref(cnt), err, 1024), err)
+    m = cnt.value
+    return dict(pre=pre.view(np.complex128), post=post.view(np.complex128),
+                sel_bucket=sb[:selections], sel_f=sf[:selections],
+                sel_value=sv.view(np.complex128)[:selections],
+                f=f[:m].copy(), c=c.view(np.complex128)[:m].copy())

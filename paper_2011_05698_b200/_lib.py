@@ -1,0 +1,79 @@
+"""ctypes binding of include/msfft_b200.h (libmsfft_b200.so, built in-tree).
+
+There is deliberately no fallback: if the CUDA library is missing or no GPU
+is visible, every call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libmsfft_b200.so")
+
+MSFFT_OK, MSFFT_ERR_INVALID_ARGUMENT, MSFFT_ERR_DOMAIN, MSFFT_ERR_CUDA, MSFFT_ERR_RUNTIME = range(5)
+MSFFT_C128, MSFFT_C64 = 0, 1
+MSFFT_HOST, MSFFT_DEVICE = 0, 1
+MSFFT_FLAG_ASSUME_VALID = 1
+MAX_ITERATIONS = 64
+
+# Every symbol include/msfft_b200.h declares.
+EXPORTED = (
+    "msfft_version", "msfft_device_count", "msfft_sfft4", "msfft_plan_create",
+    "msfft_plan_destroy", "msfft_plan_stats", "msfft_execute", "msfft_plan_launches",
+    "msfft_window", "msfft_window_response", "msfft_trace",
+)
+
+i64, u64, f64, i32, u32 = C.c_int64, C.c_uint64, C.c_double, C.c_int32, C.c_uint32
+P = C.POINTER
+VP = C.c_void_p
+
+
+class Stats(C.Structure):
+    _fields_ = [
+        ("samples_used", i64),
+        ("samples_round_sum", i64),
+        ("sample_fraction", f64),
+        ("runtime_ms", f64),
+        ("iterations", i32),
+        ("reserved", i32),
+        ("b_first", i64),
+        ("stage_counts", i32 * MAX_ITERATIONS),
+    ]
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load (once) and return the CUDA library; raises if it was not built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(
+            f"{LIB_PATH} is missing: build it with `python -m paper_2011_05698_b200.build` "
+            "(there is no CPU fallback)")
+    L = C.CDLL(LIB_PATH)
+    E = [C.c_char_p, C.c_size_t]
+    L.msfft_version.restype = C.c_char_p
+    L.msfft_device_count.restype = C.c_int
+    L.msfft_sfft4.argtypes = [VP, i64, i32, i32, i64, i64, f64, u64, f64, i64, P(i64), P(f64),
+                              P(i64), P(Stats)] + E
+    L.msfft_plan_create.argtypes = [i64, i64, i64, f64, f64, i32, i32, P(VP)] + E
+    L.msfft_plan_destroy.argtypes = [VP]
+    L.msfft_plan_destroy.restype = None
+    L.msfft_plan_stats.argtypes = [VP, P(Stats)]
+    L.msfft_execute.argtypes = [VP, i64, VP, i64, i32, P(u64), VP, VP, VP, i32, u32, VP,
+                                P(f64)] + E
+    L.msfft_plan_launches.argtypes = [VP, i64, u32]
+    L.msfft_plan_launches.restype = i64
+    L.msfft_window.argtypes = [i64, i64, f64, i32, P(i64), P(f64), i64] + E
+    L.msfft_window_response.argtypes = [i64, i64, f64, i32, P(i64), i64, P(f64)] + E
+    L.msfft_trace.argtypes = [VP, i64, i32, i64, i64, f64, u64, f64, P(f64), P(f64), P(i64),
+                              P(i64), P(f64), i64, P(i64), P(f64), P(i64)] + E
+    for fn in ("msfft_sfft4", "msfft_plan_create", "msfft_plan_stats", "msfft_execute",
+               "msfft_window", "msfft_window_response", "msfft_trace"):
+        getattr(L, fn).restype = C.c_int
+    _lib = L
+    return L

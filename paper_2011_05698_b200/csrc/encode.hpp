@@ -1,0 +1,43 @@
+// encode.hpp / decode.hpp launch interfaces (host side).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+#include "cuda_check.hpp"
+#include "plan_dev.cuh"
+
+namespace msfft_b200 {
+
+// K1+K2 (encode.cu).  smem_bytes >= max(staged taps, 256*kEncRounds*16).
+void launch_encode(const DevPlan& plan, const EncTask* d_tasks, int64_t ntasks, const void* x,
+                   bool x_c128, int64_t x_stride, int64_t batch, const int64_t* d_sigma,
+                   double2* d_y, size_t smem_bytes, cudaStream_t stream);
+
+// Per-signal decode scratch, carved from shared memory when it fits,
+// otherwise from a global workspace of `stride_bytes` per signal.
+struct DecLayout {
+    int64_t off_acc_f[2], off_acc_c[2];
+    int64_t off_tone_u, off_tone_i;
+    int64_t off_mag, off_order;
+    int64_t off_cand_f, off_cand_v, off_cand_first, off_cand_sum;
+    int64_t bytes;      // per signal
+    int32_t in_smem;
+};
+
+DecLayout make_dec_layout(int64_t acc_cap, int64_t b_max, int64_t budget_max);
+
+// K3..K7 (decode.cu).  out_f/out_c are [batch][k]; out_count [batch].
+void launch_decode(const DevPlan& plan, const DecLayout& lay, double2* d_y,
+                   const int64_t* d_sigma, const int64_t* d_sigma_inv, int64_t batch,
+                   unsigned char* d_work, int64_t* d_out_f, double2* d_out_c,
+                   int64_t* d_out_count, int32_t* d_err, cudaStream_t stream,
+                   int64_t* tr_bucket = nullptr, int64_t* tr_f = nullptr,
+                   double2* tr_v = nullptr);
+
+// Error flags raised by the decode (mirrors exceptions that escape sfft4).
+enum : int32_t { kDecErrNone = 0, kDecErrPhaseZero = 1, kDecErrRounds = 2 };
+
+}  // namespace msfft_b200

@@ -1,0 +1,365 @@
+// engine.cu -- see engine.hpp.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <tuple>
+
+#include "engine.hpp"
+#include "fft.hpp"
+
+namespace msfft_b200 {
+
+namespace {
+
+constexpr size_t kTapsSmemMax = 96 * 1024;
+constexpr size_t kChunkBytes = size_t{1} << 30;  // host-input pipeline chunk
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        MSFFT_CUDA(cudaGetDevice(&prev));
+        if (prev != dev) MSFFT_CUDA(cudaSetDevice(dev));
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        if (cudaGetDevice(&cur) == cudaSuccess && cur != prev && prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+// ComplexSignal::validate's finiteness scan (proj/src/signal.cpp:22-25).
+template <class T>
+__global__ void validate_kernel(const T* __restrict__ x, int64_t n, int64_t x_stride,
+                                int64_t batch, int32_t* __restrict__ bad) {
+    const int64_t total = n * batch;
+    bool ok = true;
+    for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t s = e / n;
+        const T v = __ldcs(x + s * x_stride + (e - s * n));
+        ok &= isfinite(static_cast<double>(v.x)) && isfinite(static_cast<double>(v.y));
+    }
+    if (!__all_sync(0xffffffffu, ok) && (threadIdx.x & 31) == 0) atomicExch(bad, 1);
+}
+
+}  // namespace
+
+Plan::Plan(int64_t n, int64_t k, int64_t l, double q, double delta, bool c128, int device)
+    : device_(device), c128_(c128) {
+    DeviceGuard dg(device);
+    if (n < 4 || !is_pow2_u(static_cast<uint64_t>(n)))
+        throw std::invalid_argument("ComplexSignal: n must be a power of two >= 4");
+    sched_ = build_schedule(n, k, l, q, delta, [](int64_t nn, int64_t bb, double dd) {
+        return window_support(nn, bb, dd);
+    });
+    if (sched_.iterations > kMaxIters)
+        throw std::invalid_argument("sfft4: iteration count exceeds the device plan limit");
+    // Scatter-free L2 fills: the gather touches one 32-B sector per sample.
+    cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, 32);
+
+    DevPlan& P = dplan_;
+    std::memset(&P, 0, sizeof(P));
+    P.n = n;
+    P.k = k;
+    P.l = l;
+    P.q = q;
+    P.inv_n = 1.0 / static_cast<double>(n);
+    P.iters = sched_.iterations;
+    P.values_per_signal = sched_.values_per_signal;
+    P.acc_cap = sched_.acc_cap;
+    int tau_off = 0;
+    int64_t yoff = 0;
+    for (int m = 0; m < sched_.iterations; ++m) {
+        const IterationPlan& ip = sched_.iters[m];
+        auto win = get_device_window(n, ip.b, delta);
+        windows_.push_back(win);
+        DevIter& it = P.it[m];
+        it.b = ip.b;
+        it.l_width = ip.l_width;
+        it.w = win->w;
+        it.h = win->h;
+        it.budget = ip.budget;
+        it.k_m = ip.k_m;
+        it.yoff = yoff;
+        it.gmax = win->gmax;
+        it.taps = win->d_taps;
+        it.ghat = win->d_ghat;
+        it.tw = device_twiddles(ip.b);
+        int lb = 0;
+        while ((int64_t{1} << lb) < ip.b) ++lb;
+        it.log2b = lb;
+        it.nrounds = static_cast<int32_t>(ip.taus.size());
+        it.tau_off = tau_off;
+        const size_t taps_bytes = static_cast<size_t>(win->w + 1) * sizeof(double);
+        it.taps_in_smem = taps_bytes <= kTapsSmemMax ? 1 : 0;
+        if (tau_off + it.nrounds > kMaxTaus)
+            throw std::invalid_argument("sfft4: tau plan exceeds the device plan limit");
+        for (int r = 0; r < it.nrounds; ++r) P.taus[tau_off + r] = ip.taus[r];
+        tau_off += it.nrounds;
+        yoff += static_cast<int64_t>(it.nrounds) * ip.b;
+        if (it.taps_in_smem) enc_smem_ = std::max(enc_smem_, taps_bytes);
+        if (ip.b <= kEncThreads)
+            enc_smem_ = std::max(enc_smem_, static_cast<size_t>(kEncThreads) *
+                                                std::min(it.nrounds, kEncRounds) * sizeof(double2));
+        else
+            big_b_iters_.push_back(m);
+        b_max_ = std::max(b_max_, ip.b);
+        budget_max_ = std::max(budget_max_, ip.budget);
+    }
+    lay_ = make_dec_layout(sched_.acc_cap, b_max_, budget_max_);
+    MSFFT_CUDA(cudaStreamCreateWithFlags(&own_stream_, cudaStreamNonBlocking));
+    MSFFT_CUDA(cudaStreamCreateWithFlags(&copy_stream_, cudaStreamNonBlocking));
+    MSFFT_CUDA(cudaEventCreate(&ev_start_));
+    MSFFT_CUDA(cudaEventCreate(&ev_end_));
+    for (int i = 0; i < 2; ++i) {
+        MSFFT_CUDA(cudaEventCreateWithFlags(&ev_copied_[i], cudaEventDisableTiming));
+        MSFFT_CUDA(cudaEventCreateWithFlags(&ev_free_[i], cudaEventDisableTiming));
+    }
+    flags_.reset(2);
+}
+
+Plan::~Plan() {
+    int cur = 0;
+    if (cudaGetDevice(&cur) != cudaSuccess) return;
+    cudaSetDevice(device_);
+    if (own_stream_) cudaStreamDestroy(own_stream_);
+    if (copy_stream_) cudaStreamDestroy(copy_stream_);
+    if (ev_start_) cudaEventDestroy(ev_start_);
+    if (ev_end_) cudaEventDestroy(ev_end_);
+    for (int i = 0; i < 2; ++i) {
+        if (ev_copied_[i]) cudaEventDestroy(ev_copied_[i]);
+        if (ev_free_[i]) cudaEventDestroy(ev_free_[i]);
+    }
+    cudaSetDevice(cur);
+}
+
+const Plan::TaskSet& Plan::tasks_for(int64_t batch) {
+    auto it = tasks_.find(batch);
+    if (it != tasks_.end()) return it->second;
+    std::vector<EncTask> v;
+    for (int m = 0; m < sched_.iterations; ++m) {
+        const DevIter& di = dplan_.it[m];
+        const IterationPlan& ip = sched_.iters[m];
+        for (int r0 = 0; r0 < di.nrounds; r0 += kEncRounds) {
+            EncTask t{};
+            t.m = m;
+            t.r0 = r0;
+            t.nr = std::min(kEncRounds, di.nrounds - r0);
+            // merged t' intervals [-h - tau, h - tau] of the chunk's rounds
+            std::vector<std::pair<int64_t, int64_t>> iv;
+            for (int r = r0; r < r0 + t.nr; ++r) iv.emplace_back(-di.h - ip.taus[r], di.h - ip.taus[r]);
+            std::sort(iv.begin(), iv.end());
+            std::vector<std::pair<int64_t, int64_t>> merged;
+            for (const auto& s : iv) {
+                if (!merged.empty() && s.first <= merged.back().second + 1)
+                    merged.back().second = std::max(merged.back().second, s.second);
+                else
+                    merged.push_back(s);
+            }
+            t.nseg = static_cast<int32_t>(merged.size());
+            for (size_t i = 0; i < merged.size(); ++i) {
+                t.seg_lo[i] = static_cast<int32_t>(merged[i].first);
+                t.seg_hi[i] = static_cast<int32_t>(merged[i].second);
+            }
+            if (di.b <= kEncThreads) {
+                t.fused = 1;
+                t.nsig = static_cast<int32_t>(kEncThreads / di.b);
+                t.lane0 = 0;
+                for (int64_t s0 = 0; s0 < batch; s0 += t.nsig) {
+                    t.sig0 = s0;
+                    v.push_back(t);
+                }
+            } else {
+                t.fused = 0;
+                t.nsig = 1;
+                for (int64_t s0 = 0; s0 < batch; ++s0)
+                    for (int64_t lane0 = 0; lane0 < di.b; lane0 += kEncThreads) {
+                        t.sig0 = s0;
+                        t.lane0 = static_cast<int32_t>(lane0);
+                        v.push_back(t);
+                    }
+            }
+        }
+    }
+    TaskSet ts;
+    ts.count = static_cast<int64_t>(v.size());
+    ts.d.reset(v.size());
+    MSFFT_CUDA(cudaMemcpy(ts.d.get(), v.data(), v.size() * sizeof(EncTask),
+                          cudaMemcpyHostToDevice));
+    return tasks_.emplace(batch, std::move(ts)).first->second;
+}
+
+int64_t Plan::launches(int64_t /*batch*/, bool validate) const {
+    int64_t count = 2 + (validate ? 1 : 0);  // encode + decode (+ validate)
+    for (int m : big_b_iters_) {
+        int lb = dplan_.it[m].log2b;
+        int64_t passes = 0, s0 = 0;
+        while (s0 < lb) {
+            s0 += (s0 == 0) ? std::min(lb, 11) : std::min<int64_t>(lb - s0, 7);
+            ++passes;
+        }
+        count += 1 + passes;  // bitrev + stage passes
+    }
+    return count;
+}
+
+void Plan::run_chunk(int64_t batch, const void* d_x, int64_t x_stride, const int64_t* d_sig,
+                     const int64_t* d_sig_inv, int64_t* d_out_f, double2* d_out_c,
+                     int64_t* d_out_count, bool validate, cudaStream_t st,
+                     const ExecOptions& opt) {
+    const int64_t n = sched_.n;
+    if (validate) {
+        const int64_t total = n * batch;
+        const unsigned blocks =
+            static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, 148 * 16));
+        if (c128_)
+            validate_kernel<double2><<<blocks, 256, 0, st>>>(
+                static_cast<const double2*>(d_x), n, x_stride, batch, flags_.get() + 1);
+        else
+            validate_kernel<float2><<<blocks, 256, 0, st>>>(
+                static_cast<const float2*>(d_x), n, x_stride, batch, flags_.get() + 1);
+        MSFFT_LAUNCH_CHECK("validate_kernel");
+    }
+    const TaskSet& ts = tasks_for(batch);
+    launch_encode(dplan_, ts.d.get(), ts.count, d_x, c128_, x_stride, batch, d_sig, y_.get(),
+                  enc_smem_, st);
+    for (int m : big_b_iters_) {
+        const DevIter& di = dplan_.it[m];
+        fft_radix2_batched(y_.get() + di.yoff, di.b, batch * di.nrounds, di.nrounds,
+                           dplan_.values_per_signal, -1, dplan_.inv_n, st);
+    }
+    const size_t ybytes = sizeof(double2) * static_cast<size_t>(dplan_.values_per_signal);
+    if (opt.pre) {
+        MSFFT_CUDA(cudaMemcpyAsync(opt.pre, y_.get(), ybytes, cudaMemcpyDeviceToHost, st));
+    }
+    DeviceBuffer<int64_t> tb, tf;
+    DeviceBuffer<double2> tv;
+    if (opt.sel_bucket) {
+        tb.reset(static_cast<size_t>(sched_.acc_cap));
+        tf.reset(static_cast<size_t>(sched_.acc_cap));
+        tv.reset(static_cast<size_t>(sched_.acc_cap));
+    }
+    launch_decode(dplan_, lay_, y_.get(), d_sig, d_sig_inv, batch, dec_work_.get(), d_out_f,
+                  d_out_c, d_out_count, flags_.get(), st, tb.get(), tf.get(), tv.get());
+    if (opt.post) {
+        MSFFT_CUDA(cudaMemcpyAsync(opt.post, y_.get(), ybytes, cudaMemcpyDeviceToHost, st));
+    }
+    if (opt.sel_bucket) {
+        const size_t nb = static_cast<size_t>(sched_.acc_cap);
+        MSFFT_CUDA(cudaMemcpyAsync(opt.sel_bucket, tb.get(), nb * 8, cudaMemcpyDeviceToHost, st));
+        MSFFT_CUDA(cudaMemcpyAsync(opt.sel_f, tf.get(), nb * 8, cudaMemcpyDeviceToHost, st));
+        MSFFT_CUDA(cudaMemcpyAsync(opt.sel_value, tv.get(), nb * 16, cudaMemcpyDeviceToHost, st));
+        MSFFT_CUDA(cudaStreamSynchronize(st));
+    }
+}
+
+void Plan::execute(int64_t batch, const void* x, int64_t x_stride, const uint64_t* seeds,
+                   int64_t* out_f, double* out_c, int64_t* out_count, const ExecOptions& opt,
+                   double* device_ms) {
+    DeviceGuard dg(device_);
+    if (batch <= 0) return;
+    const int64_t n = sched_.n, k = sched_.k;
+    const int iters = sched_.iterations;
+    if (x_stride < n) throw std::invalid_argument("msfft_execute: x_stride < n");
+    cudaStream_t st = opt.stream ? opt.stream : own_stream_;
+    const size_t elem = c128_ ? sizeof(double2) : sizeof(float2);
+
+    // sigma plan (host, exact mt19937_64 draws)
+    h_sig_.resize(static_cast<size_t>(batch * iters));
+    h_sig_inv_.resize(static_cast<size_t>(batch * iters));
+    for (int64_t s = 0; s < batch; ++s)
+        draw_sigmas(seeds[s], n, iters, h_sig_.data() + s * iters, h_sig_inv_.data() + s * iters);
+
+    // chunking: device inputs run as one chunk; host inputs stream through
+    // two staging buffers overlapped with compute
+    const int64_t sig_bytes = static_cast<int64_t>(elem) * n;
+    const int64_t chunk =
+        opt.x_on_device ? batch
+                        : std::max<int64_t>(1, std::min<int64_t>(batch, kChunkBytes / sig_bytes));
+    sig_.ensure(static_cast<size_t>(batch * iters));
+    sig_inv_.ensure(static_cast<size_t>(batch * iters));
+    y_.ensure(static_cast<size_t>(chunk * dplan_.values_per_signal));
+    if (!lay_.in_smem) dec_work_.ensure(static_cast<size_t>(chunk * lay_.bytes));
+    if (!opt.out_on_device) {
+        out_f_.ensure(static_cast<size_t>(batch * k));
+        out_c_.ensure(static_cast<size_t>(batch * k));
+        out_count_.ensure(static_cast<size_t>(batch));
+    }
+    if (!opt.x_on_device)
+        for (int i = 0; i < 2; ++i) xstage_[i].ensure(static_cast<size_t>(chunk * sig_bytes));
+
+    int64_t* d_of = opt.out_on_device ? out_f : out_f_.get();
+    double2* d_oc = opt.out_on_device ? reinterpret_cast<double2*>(out_c) : out_c_.get();
+    int64_t* d_ocnt = opt.out_on_device ? out_count : out_count_.get();
+
+    MSFFT_CUDA(cudaEventRecord(ev_start_, st));
+    MSFFT_CUDA(cudaMemsetAsync(flags_.get(), 0, 2 * sizeof(int32_t), st));
+    MSFFT_CUDA(cudaMemcpyAsync(sig_.get(), h_sig_.data(), sizeof(int64_t) * batch * iters,
+                               cudaMemcpyHostToDevice, st));
+    MSFFT_CUDA(cudaMemcpyAsync(sig_inv_.get(), h_sig_inv_.data(),
+                               sizeof(int64_t) * batch * iters, cudaMemcpyHostToDevice, st));
+    const bool validate = !opt.assume_valid;
+    if (opt.x_on_device) {
+        run_chunk(batch, x, x_stride, sig_.get(), sig_inv_.get(), d_of, d_oc, d_ocnt, validate,
+                  st, opt);
+    } else {
+        MSFFT_CUDA(cudaStreamWaitEvent(copy_stream_, ev_start_, 0));
+        const unsigned char* hx = static_cast<const unsigned char*>(x);
+        int64_t idx = 0;
+        for (int64_t s0 = 0; s0 < batch; s0 += chunk, ++idx) {
+            const int64_t cb = std::min(chunk, batch - s0);
+            const int slot = static_cast<int>(idx & 1);
+            if (idx >= 2) MSFFT_CUDA(cudaStreamWaitEvent(copy_stream_, ev_free_[slot], 0));
+            unsigned char* dst = xstage_[slot].get();
+            if (x_stride == n) {
+                MSFFT_CUDA(cudaMemcpyAsync(dst, hx + s0 * x_stride * elem, cb * sig_bytes,
+                                           cudaMemcpyHostToDevice, copy_stream_));
+            } else {
+                MSFFT_CUDA(cudaMemcpy2DAsync(dst, sig_bytes, hx + s0 * x_stride * elem,
+                                             x_stride * elem, sig_bytes, cb,
+                                             cudaMemcpyHostToDevice, copy_stream_));
+            }
+            MSFFT_CUDA(cudaEventRecord(ev_copied_[slot], copy_stream_));
+            MSFFT_CUDA(cudaStreamWaitEvent(st, ev_copied_[slot], 0));
+            run_chunk(cb, dst, n, sig_.get() + s0 * iters, sig_inv_.get() + s0 * iters,
+                      d_of + s0 * k, d_oc + s0 * k, d_ocnt + s0, validate, st, opt);
+            MSFFT_CUDA(cudaEventRecord(ev_free_[slot], st));
+        }
+    }
+    if (!opt.out_on_device) {
+        MSFFT_CUDA(cudaMemcpyAsync(out_f, d_of, sizeof(int64_t) * batch * k,
+                                   cudaMemcpyDeviceToHost, st));
+        MSFFT_CUDA(cudaMemcpyAsync(out_c, d_oc, sizeof(double2) * batch * k,
+                                   cudaMemcpyDeviceToHost, st));
+        MSFFT_CUDA(cudaMemcpyAsync(out_count, d_ocnt, sizeof(int64_t) * batch,
+                                   cudaMemcpyDeviceToHost, st));
+    }
+    int32_t hflags[2] = {0, 0};
+    MSFFT_CUDA(cudaMemcpyAsync(hflags, flags_.get(), sizeof(hflags), cudaMemcpyDeviceToHost, st));
+    MSFFT_CUDA(cudaEventRecord(ev_end_, st));
+    MSFFT_CUDA(cudaEventSynchronize(ev_end_));
+    if (device_ms) {
+        float ms = 0.f;
+        MSFFT_CUDA(cudaEventElapsedTime(&ms, ev_start_, ev_end_));
+        *device_ms = ms;
+    }
+    if (hflags[1]) throw std::invalid_argument("ComplexSignal: non-finite sample");
+    if (hflags[0] == kDecErrPhaseZero) throw std::domain_error("phase_of: zero value");
+    if (hflags[0] == kDecErrRounds)
+        throw std::invalid_argument("locate_frequency: not enough rounds for the schedule");
+}
+
+std::shared_ptr<Plan> cached_plan(int64_t n, int64_t k, int64_t l, double q, double delta,
+                                  bool c128, int device) {
+    using Key = std::tuple<int, int64_t, int64_t, int64_t, double, double, bool>;
+    static std::mutex mu;
+    static std::map<Key, std::shared_ptr<Plan>> cache;
+    const Key key{device, n, k, l, q, delta, c128};
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    auto p = std::make_shared<Plan>(n, k, l, q, delta, c128, device);
+    cache.emplace(key, p);
+    return p;
+}
+
+}  // namespace msfft_b200

@@ -1,0 +1,101 @@
+// engine.hpp -- host orchestration of one sfft4 plan on one B200.
+//
+// A Plan resolves everything that does not depend on the signal (windows,
+// response tables, halving schedule, tau plans, encode task list), keeps the
+// device workspaces, and executes batches:
+//   [H2D chunk] -> validate -> encode (K1+K2, one launch for all rounds of all
+//   iterations) -> batched FFT for b > 256 -> decode (K3..K7, one CTA per
+//   signal) -> outputs.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <vector>
+
+#include "cuda_check.hpp"
+#include "encode.hpp"
+#include "host_plan.hpp"
+#include "plan_dev.cuh"
+#include "window.hpp"
+
+namespace msfft_b200 {
+
+struct ExecOptions {
+    bool x_on_device = false;
+    bool out_on_device = false;
+    bool assume_valid = false;
+    cudaStream_t stream = nullptr;
+    double* pre = nullptr;   // trace: encode output (batch must be 1, host)
+    double* post = nullptr;  // trace: post-subtract values
+    int64_t* sel_bucket = nullptr;  // trace: per ranked bucket (sum of budgets)
+    int64_t* sel_f = nullptr;
+    double* sel_value = nullptr;
+};
+
+class Plan {
+public:
+    Plan(int64_t n, int64_t k, int64_t l, double q, double delta, bool c128, int device);
+    ~Plan();
+    Plan(const Plan&) = delete;
+    Plan& operator=(const Plan&) = delete;
+
+    const SchedulePlan& schedule() const { return sched_; }
+    int device() const { return device_; }
+    bool c128() const { return c128_; }
+
+    // out_c: interleaved (re, im) doubles, [batch][k].
+    void execute(int64_t batch, const void* x, int64_t x_stride, const uint64_t* seeds,
+                 int64_t* out_f, double* out_c, int64_t* out_count, const ExecOptions& opt,
+                 double* device_ms);
+
+    int64_t launches(int64_t batch, bool validate) const;
+
+    std::mutex& mutex() { return mu_; }
+
+private:
+    struct TaskSet {
+        DeviceBuffer<EncTask> d;
+        int64_t count = 0;
+    };
+    const TaskSet& tasks_for(int64_t batch);
+    void run_chunk(int64_t batch, const void* d_x, int64_t x_stride, const int64_t* d_sig,
+                   const int64_t* d_sig_inv, int64_t* d_out_f, double2* d_out_c,
+                   int64_t* d_out_count, bool validate, cudaStream_t st,
+                   const ExecOptions& opt);
+
+    int device_;
+    bool c128_;
+    SchedulePlan sched_;
+    std::vector<std::shared_ptr<const DeviceWindow>> windows_;
+    DevPlan dplan_{};
+    DecLayout lay_{};
+    size_t enc_smem_ = 0;
+    int64_t b_max_ = 0, budget_max_ = 0;
+    std::vector<int> big_b_iters_;  // iterations needing the separate FFT
+    std::map<int64_t, TaskSet> tasks_;
+
+    cudaStream_t own_stream_ = nullptr, copy_stream_ = nullptr;
+    cudaEvent_t ev_start_ = nullptr, ev_end_ = nullptr;
+    cudaEvent_t ev_copied_[2] = {nullptr, nullptr}, ev_free_[2] = {nullptr, nullptr};
+
+    DeviceBuffer<double2> y_;
+    DeviceBuffer<int64_t> sig_, sig_inv_;
+    DeviceBuffer<unsigned char> dec_work_;
+    DeviceBuffer<int64_t> out_f_, out_count_;
+    DeviceBuffer<double2> out_c_;
+    DeviceBuffer<int32_t> flags_;  // [0] decode error, [1] non-finite input
+    DeviceBuffer<unsigned char> xstage_[2];
+    std::vector<int64_t> h_sig_, h_sig_inv_;
+    std::mutex mu_;
+};
+
+// Process-wide plan cache for the one-shot API (keyed by device and all
+// plan parameters).
+std::shared_ptr<Plan> cached_plan(int64_t n, int64_t k, int64_t l, double q, double delta,
+                                  bool c128, int device);
+
+}  // namespace msfft_b200

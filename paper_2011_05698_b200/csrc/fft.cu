@@ -1,0 +1,180 @@
+// fft.cu -- see fft.hpp.  Compiled with --fmad=false.
+#include <cmath>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <thread>
+#include <vector>
+
+#include "common.cuh"
+#include "cuda_check.hpp"
+#include "fft.hpp"
+
+namespace msfft_b200 {
+
+namespace {
+
+std::mutex g_tw_mu;
+std::map<int64_t, std::unique_ptr<std::vector<double>>> g_host_tw;
+std::map<std::pair<int, int64_t>, double2*> g_dev_tw;
+
+// twiddle_table (proj/src/fft.cpp:14-28): step = -2 pi / n, a = step * k.
+std::vector<double> make_twiddles(int64_t n) {
+    const int64_t half = n / 2;
+    std::vector<double> t(static_cast<size_t>(2 * std::max<int64_t>(half, 1)));
+    const double step = -2.0 * 3.141592653589793 / static_cast<double>(n);
+    auto work = [&](int64_t lo, int64_t hi) {
+        for (int64_t k = lo; k < hi; ++k) {
+            const double a = step * static_cast<double>(k);
+            t[2 * k] = std::cos(a);
+            t[2 * k + 1] = std::sin(a);
+        }
+    };
+    const int64_t chunk = 1 << 18;
+    if (half <= chunk) {
+        work(0, half);
+    } else {
+        const int nt = static_cast<int>(
+            std::max<unsigned>(1u, std::min<unsigned>(16u, std::thread::hardware_concurrency())));
+        std::vector<std::thread> pool;
+        const int64_t per = (half + nt - 1) / nt;
+        for (int i = 0; i < nt; ++i)
+            pool.emplace_back(work, std::min(half, i * per), std::min(half, (i + 1) * per));
+        for (auto& th : pool) th.join();
+    }
+    return t;
+}
+
+__global__ void bitrev_inplace_kernel(double2* __restrict__ data, int64_t size, int log2size,
+                                      int64_t inner, int64_t outer_stride, int64_t total) {
+    const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (gid >= total) return;
+    const int64_t bi = gid / size;
+    const unsigned i = static_cast<unsigned>(gid - bi * size);
+    const unsigned j = bitrev_bits(i, log2size);
+    if (j <= i) return;
+    double2* a = data + (bi / inner) * outer_stride + (bi % inner) * size;
+    const double2 t = a[i];
+    a[i] = a[j];
+    a[j] = t;
+}
+
+// Stages s0+1 .. s1 (1-based; stage s has butterfly span 2^(s-1)).  A CTA
+// owns `lo_tile` consecutive low indices of one high block, i.e. the
+// elements j = hi*2^s1 + kk*2^s0 + lo for all kk < 2^(s1-s0).  Every
+// butterfly is the reference's:  t = a[j+half]*w; a[j+half] = a[j]-t; a[j] += t.
+__global__ void __launch_bounds__(512) stages_kernel(double2* __restrict__ data, int64_t size,
+                                                     int64_t inner, int64_t outer_stride,
+                                                     int s0, int s1, int lo_tile, int sign,
+                                                     const double2* __restrict__ tw,
+                                                     double scale) {
+    extern __shared__ double2 tile[];
+    const int G = s1 - s0;
+    const int64_t span = int64_t{1} << s0;       // distance between kk neighbours
+    const int64_t tiles_per_hi = span / lo_tile;
+    const int64_t groups = (size >> s1) * tiles_per_hi;
+    const int64_t bi = blockIdx.x / groups;
+    const int64_t g = blockIdx.x - bi * groups;
+    const int64_t hi = g / tiles_per_hi;
+    const int64_t lo0 = (g - hi * tiles_per_hi) * lo_tile;
+    double2* a = data + (bi / inner) * outer_stride + (bi % inner) * size;
+    const int nk = 1 << G;
+    const int count = nk * lo_tile;
+    const int64_t base = (hi << s1) + lo0;
+    for (int e = threadIdx.x; e < count; e += blockDim.x) {
+        const int kk = e / lo_tile, li = e - kk * lo_tile;
+        tile[e] = a[base + static_cast<int64_t>(kk) * span + li];
+    }
+    __syncthreads();
+    for (int s = s0 + 1; s <= s1; ++s) {
+        const int hkk = 1 << (s - 1 - s0);   // half span in kk units
+        const int64_t step = size >> s;      // twiddle stride n/size
+        for (int bf = threadIdx.x; bf < count / 2; bf += blockDim.x) {
+            const int li = bf % lo_tile;
+            const int p = bf / lo_tile;
+            const int blk = p / hkk, off = p - blk * hkk;
+            const int kk = blk * 2 * hkk + off;
+            const int64_t k = ((static_cast<int64_t>(off) << s0) + lo0 + li) * step;
+            double2 w = tw[k];
+            if (sign > 0) w.y = -w.y;
+            const int e0 = kk * lo_tile + li, e1 = (kk + hkk) * lo_tile + li;
+            const double2 x0 = tile[e0];
+            const double2 t = cmul(tile[e1], w);
+            tile[e1] = make_double2(x0.x - t.x, x0.y - t.y);
+            tile[e0] = make_double2(x0.x + t.x, x0.y + t.y);
+        }
+        __syncthreads();
+    }
+    const bool do_scale = scale != 1.0;
+    for (int e = threadIdx.x; e < count; e += blockDim.x) {
+        const int kk = e / lo_tile, li = e - kk * lo_tile;
+        double2 v = tile[e];
+        if (do_scale) v = make_double2(v.x * scale, v.y * scale);
+        a[base + static_cast<int64_t>(kk) * span + li] = v;
+    }
+}
+
+}  // namespace
+
+const double* host_twiddles(int64_t n) {
+    std::lock_guard<std::mutex> lock(g_tw_mu);
+    auto it = g_host_tw.find(n);
+    if (it == g_host_tw.end())
+        it = g_host_tw.emplace(n, std::make_unique<std::vector<double>>(make_twiddles(n))).first;
+    return it->second->data();
+}
+
+const double2* device_twiddles(int64_t n) {
+    int dev = 0;
+    MSFFT_CUDA(cudaGetDevice(&dev));
+    {
+        std::lock_guard<std::mutex> lock(g_tw_mu);
+        auto it = g_dev_tw.find({dev, n});
+        if (it != g_dev_tw.end()) return it->second;
+    }
+    const double* h = host_twiddles(n);
+    const size_t count = static_cast<size_t>(std::max<int64_t>(n / 2, 1));
+    double2* d = nullptr;
+    MSFFT_CUDA(cudaMalloc(&d, count * sizeof(double2)));
+    MSFFT_CUDA(cudaMemcpy(d, h, count * sizeof(double2), cudaMemcpyHostToDevice));
+    std::lock_guard<std::mutex> lock(g_tw_mu);
+    auto [it, inserted] = g_dev_tw.emplace(std::make_pair(dev, n), d);
+    if (!inserted) cudaFree(d);
+    return it->second;
+}
+
+void fft_radix2_batched(double2* data, int64_t size, int64_t batch, int64_t inner,
+                        int64_t outer_stride, int sign, double scale, cudaStream_t stream) {
+    if (size <= 1 || batch <= 0) return;
+    int log2size = 0;
+    while ((int64_t{1} << log2size) < size) ++log2size;
+    const double2* tw = device_twiddles(size);
+    const int64_t total = size * batch;
+    bitrev_inplace_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, stream>>>(
+        data, size, log2size, inner, outer_stride, total);
+    MSFFT_LAUNCH_CHECK("bitrev_inplace_kernel");
+    int s0 = 0;
+    while (s0 < log2size) {
+        int lo_tile, G;
+        if (s0 == 0) {
+            lo_tile = 1;
+            G = std::min(log2size, 11);
+        } else {
+            lo_tile = static_cast<int>(std::min<int64_t>(int64_t{1} << s0, 16));
+            G = std::min(log2size - s0, lo_tile == 16 ? 7 : 11 - s0);
+            if (G < 1) G = 1;
+        }
+        const int s1 = s0 + G;
+        const int64_t groups = (size >> s1) * ((int64_t{1} << s0) / lo_tile);
+        const int64_t blocks = groups * batch;
+        const size_t smem = sizeof(double2) * (static_cast<size_t>(1) << G) * lo_tile;
+        const int threads = static_cast<int>(std::min<size_t>(512, std::max<size_t>(32, smem / 32)));
+        const double sc = (s1 == log2size) ? scale : 1.0;
+        stages_kernel<<<static_cast<unsigned>(blocks), threads, smem, stream>>>(
+            data, size, inner, outer_stride, s0, s1, lo_tile, sign, tw, sc);
+        MSFFT_LAUNCH_CHECK("stages_kernel");
+        s0 = s1;
+    }
+}
+
+}  // namespace msfft_b200

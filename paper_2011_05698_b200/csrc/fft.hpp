@@ -1,0 +1,30 @@
+// fft.hpp -- batched power-of-two FFT on the device whose every butterfly
+// performs the same IEEE operations, on the same operands and twiddles, as
+// the reference's radix-2 DIT (proj/src/fft.cpp:32-66), so results are
+// bit-identical to it.  Used by the window designer (n-point, cold path) and
+// for bucket transforms too large for one CTA's shared memory.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace msfft_b200 {
+
+// Twiddles e^{-2 pi i k/n}, k < n/2, evaluated on the host with the same libm
+// calls as twiddle_table (proj/src/fft.cpp:14-28) and cached on the current
+// device per size.  Returned pointer stays valid for the process lifetime.
+const double2* device_twiddles(int64_t n);
+
+// Host copy of the same table (for tests / host-side use).
+const double* host_twiddles(int64_t n);
+
+// In-place transform of `batch` arrays of `size` complex doubles.  Array i
+// starts at data + (i / inner) * outer_stride + (i % inner) * size.
+// sign < 0: forward kernel; sign > 0: conjugated twiddles (fft_radix2 sign).
+// After the last butterfly every value is multiplied by `scale` (component
+// wise, as `v *= scale` in the reference) unless scale == 1.
+void fft_radix2_batched(double2* data, int64_t size, int64_t batch, int64_t inner,
+                        int64_t outer_stride, int sign, double scale, cudaStream_t stream);
+
+}  // namespace msfft_b200

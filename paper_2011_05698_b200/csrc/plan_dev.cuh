@@ -1,0 +1,56 @@
+// plan_dev.cuh -- the per-transform plan as the kernels see it.
+//
+// HBM layout of one batch:
+//   x      [batch][x_stride] complex64 (float2) or complex128 (double2)
+//   sigma  [batch][iters]    int64      (sigma_m, drawn on the host)
+//   y      [batch][values_per_signal] double2, iteration-major then
+//          round-major: y[s][yoff_m + r*b_m + j] is bucket j of round r
+//          of iteration m (BucketSet::values, proj/include/msfft/bucketize.hpp:24-30)
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace msfft_b200 {
+
+constexpr int kMaxIters = 40;
+constexpr int kMaxTaus = 1024;
+constexpr int kEncRounds = 8;       // rounds fused into one gather pass
+constexpr int kEncThreads = 256;    // encode CTA size
+constexpr int kDecThreads = 256;    // decode CTA size
+
+struct DevIter {
+    int64_t b, l_width, w, h;
+    int64_t budget, k_m;
+    int64_t yoff;            // offset of round 0 of this iteration in a signal's y block
+    int64_t gmax;            // response table covers d in [-gmax, gmax]
+    const double* taps;      // w + 1 doubles (zero pad)
+    const double* ghat;      // 2*gmax + 1 doubles, index d + gmax
+    const double2* tw;       // b/2 forward twiddles for the b-point transform
+    int32_t log2b, nrounds;
+    int32_t tau_off;         // first tau of this iteration in DevPlan::taus
+    int32_t taps_in_smem;    // taps staged in shared memory by a TMA bulk copy
+};
+
+struct DevPlan {
+    int64_t n, k, l;
+    double q, inv_n;
+    int64_t values_per_signal, acc_cap;
+    int32_t iters, pad_;
+    DevIter it[kMaxIters];
+    int64_t taus[kMaxTaus];
+};
+
+// One CTA of the encode kernel.
+struct EncTask {
+    int32_t m;               // iteration
+    int32_t r0, nr;          // rounds [r0, r0 + nr) of that iteration
+    int32_t fused;           // 1: CTA holds all b lanes -> fused b-point FFT
+    int64_t sig0;            // first signal
+    int32_t nsig;            // signals handled (fused: 256/b)
+    int32_t lane0;           // first residue class (non-fused: 256-wide slice)
+    int32_t nseg, pad_;
+    int32_t seg_lo[kEncRounds], seg_hi[kEncRounds];  // merged t' intervals
+};
+
+}  // namespace msfft_b200
