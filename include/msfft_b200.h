@@ -53,7 +53,10 @@ typedef enum msfft_location { MSFFT_HOST = 0, MSFFT_DEVICE = 1 } msfft_location;
 enum msfft_flags {
     /* Skip the O(n) finiteness scan of x (ComplexSignal::validate,
      * proj/src/signal.cpp:18-26) because the caller validated at ingest. */
-    MSFFT_FLAG_ASSUME_VALID = 1u << 0
+    MSFFT_FLAG_ASSUME_VALID = 1u << 0,
+    /* Record CUDA events around each stage on the execution stream; read
+     * them back with msfft_plan_stage_times. */
+    MSFFT_FLAG_STAGE_TIMES = 1u << 1
 };
 
 /* TransformStats (proj/include/msfft/sfft4.hpp:32-40). */
@@ -103,9 +106,31 @@ int msfft_execute(msfft_plan plan, int64_t batch, const void* x, int64_t x_strid
                   int64_t* out_count, int32_t out_location, uint32_t flags, void* stream,
                   double* device_ms, char* err, size_t errlen);
 
+/* Algorithmic traffic of the fused gather for `batch` signals with these
+ * seeds (host computation from the plan, data independent): *loads = samples
+ * loaded (each distinct t' of an iteration once), *sectors = distinct 32-byte
+ * sectors they touch, summed over iterations and signals. */
+int msfft_plan_gather_traffic(msfft_plan plan, int64_t batch, const uint64_t* seeds,
+                              int64_t* loads, int64_t* sectors);
+
+/* [encode, bucket FFT for b > 256, decode] milliseconds of the last
+ * msfft_execute issued with MSFFT_FLAG_STAGE_TIMES (summed over chunks). */
+int msfft_plan_stage_times(msfft_plan plan, double* ms3);
+
 /* Number of device kernel launches one msfft_execute of `batch` device-
  * resident signals issues (for bench accounting). */
 int64_t msfft_plan_launches(msfft_plan plan, int64_t batch, uint32_t flags);
+
+/* ---- host-only plan pieces (no device needed) -------------------------------
+ * sigma_m, sigma^-1_m for the first `iterations` iterations of a transform
+ * seeded `seed`: random_params(n, Rng(seed), 0) per iteration
+ * (proj/src/bucketize.cpp:39-48, proj/src/sfft4.cpp:48). */
+int msfft_sigma_plan(uint64_t seed, int64_t n, int32_t iterations, int64_t* sigma,
+                     int64_t* sigma_inv, char* err, size_t errlen);
+/* The tau plan {0, tau_1..tau_R} of an iteration with bucket width l_width
+ * (stage_count + tau_schedule, proj/src/sfft4.cpp:49-55, locate.cpp:39-53). */
+int msfft_tau_plan(double l_width, int64_t n, int64_t l, double q, int64_t* taus, int32_t cap,
+                   int32_t* rounds, char* err, size_t errlen);
 
 /* ---- kernel-level entry points (parity tests) ------------------------------
  * Window taps/support exactly as design_flat_window (window.cpp:105-177). */

@@ -215,7 +215,25 @@ class Plan:
         flags = _L.MSFFT_FLAG_ASSUME_VALID if assume_valid else 0
         return int(self._lib.msfft_plan_launches(self._h, int(batch), flags))
 
-    def execute(self, x, seeds, out=None, assume_valid: bool = False, stream=None):
+    def gather_traffic(self, seeds):
+        """(samples loaded, distinct 32-B sectors) of the fused gather for
+        these signals -- the algorithmic bytes behind the roofline."""
+        seeds = np.ascontiguousarray(np.asarray(seeds, dtype=np.uint64).reshape(-1))
+        a, b = C.c_int64(), C.c_int64()
+        self._lib.msfft_plan_gather_traffic(self._h, seeds.size,
+                                            seeds.ctypes.data_as(C.POINTER(C.c_uint64)),
+                                            C.byref(a), C.byref(b))
+        return a.value, b.value
+
+    def stage_times(self):
+        """[encode, bucket FFT (b > 256), decode] ms of the last execute run
+        with stage_times=True."""
+        ms = (C.c_double * 3)()
+        self._lib.msfft_plan_stage_times(self._h, ms)
+        return [float(v) for v in ms]
+
+    def execute(self, x, seeds, out=None, assume_valid: bool = False, stream=None,
+                stage_times: bool = False):
         """x: (batch, n) complex array/tensor (host or CUDA).  seeds: batch
         integers.  out: optional (f, c, count) preallocated outputs -- torch
         CUDA tensors (int64 [B,k], complex128 [B,k], int64 [B]) keep the
@@ -246,6 +264,8 @@ class Plan:
         ms = C.c_double()
         err = C.create_string_buffer(1024)
         flags = _L.MSFFT_FLAG_ASSUME_VALID if assume_valid else 0
+        if stage_times:
+            flags |= _L.MSFFT_FLAG_STAGE_TIMES
         status = self._lib.msfft_execute(
             self._h, batch, ptr, n, loc, seeds.ctypes.data_as(C.POINTER(C.c_uint64)),
             C.c_void_p(fptr), C.c_void_p(cptr), C.c_void_p(nptr), oloc, flags,

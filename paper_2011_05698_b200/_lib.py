@@ -15,13 +15,15 @@ MSFFT_OK, MSFFT_ERR_INVALID_ARGUMENT, MSFFT_ERR_DOMAIN, MSFFT_ERR_CUDA, MSFFT_ER
 MSFFT_C128, MSFFT_C64 = 0, 1
 MSFFT_HOST, MSFFT_DEVICE = 0, 1
 MSFFT_FLAG_ASSUME_VALID = 1
+MSFFT_FLAG_STAGE_TIMES = 2
 MAX_ITERATIONS = 64
 
 # Every symbol include/msfft_b200.h declares.
 EXPORTED = (
     "msfft_version", "msfft_device_count", "msfft_sfft4", "msfft_plan_create",
     "msfft_plan_destroy", "msfft_plan_stats", "msfft_execute", "msfft_plan_launches",
-    "msfft_window", "msfft_window_response", "msfft_trace",
+    "msfft_window", "msfft_window_response", "msfft_trace", "msfft_plan_stage_times",
+    "msfft_plan_gather_traffic", "msfft_sigma_plan", "msfft_tau_plan",
 )
 
 i64, u64, f64, i32, u32 = C.c_int64, C.c_uint64, C.c_double, C.c_int32, C.c_uint32
@@ -66,6 +68,14 @@ def lib() -> C.CDLL:
     L.msfft_plan_stats.argtypes = [VP, P(Stats)]
     L.msfft_execute.argtypes = [VP, i64, VP, i64, i32, P(u64), VP, VP, VP, i32, u32, VP,
                                 P(f64)] + E
+    L.msfft_sigma_plan.argtypes = [u64, i64, i32, P(i64), P(i64)] + E
+    L.msfft_sigma_plan.restype = C.c_int
+    L.msfft_tau_plan.argtypes = [f64, i64, i64, f64, P(i64), i32, P(i32)] + E
+    L.msfft_tau_plan.restype = C.c_int
+    L.msfft_plan_gather_traffic.argtypes = [VP, i64, P(u64), P(i64), P(i64)]
+    L.msfft_plan_gather_traffic.restype = C.c_int
+    L.msfft_plan_stage_times.argtypes = [VP, P(f64)]
+    L.msfft_plan_stage_times.restype = C.c_int
     L.msfft_plan_launches.argtypes = [VP, i64, u32]
     L.msfft_plan_launches.restype = i64
     L.msfft_window.argtypes = [i64, i64, f64, i32, P(i64), P(f64), i64] + E

@@ -6,6 +6,7 @@
 #include <cstring>
 #include <memory>
 #include <stdexcept>
+#include <thread>
 #include <vector>
 
 #include "../../include/msfft_b200.h"
@@ -190,9 +191,63 @@ int msfft_execute(msfft_plan plan, int64_t batch, const void* x, int64_t x_strid
         opt.x_on_device = x_location == MSFFT_DEVICE;
         opt.out_on_device = out_location == MSFFT_DEVICE;
         opt.assume_valid = (flags & MSFFT_FLAG_ASSUME_VALID) != 0;
+        opt.stage_times = (flags & MSFFT_FLAG_STAGE_TIMES) != 0;
         opt.stream = static_cast<cudaStream_t>(stream);
         plan->plan->execute(batch, x, x_stride, seeds, out_f, out_c, out_count, opt, device_ms);
     });
+}
+
+int msfft_sigma_plan(uint64_t seed, int64_t n, int32_t iterations, int64_t* sigma,
+                     int64_t* sigma_inv, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] { draw_sigmas(seed, n, iterations, sigma, sigma_inv); });
+}
+
+int msfft_tau_plan(double l_width, int64_t n, int64_t l, double q, int64_t* taus,
+                   int32_t cap, int32_t* rounds, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        validate_cfg(l, q);
+        const int stages = stage_count(l_width, l, q);
+        *rounds = stages + 1;
+        if (stages + 1 > cap) throw std::invalid_argument("msfft_tau_plan: cap too small");
+        taus[0] = 0;
+        double len = l_width;
+        for (int s = 0; s < stages; ++s) {
+            taus[s + 1] = tau_schedule(len, n);
+            len *= (q + 1.0) / static_cast<double>(l);
+        }
+    });
+}
+
+int msfft_plan_gather_traffic(msfft_plan plan, int64_t batch, const uint64_t* seeds,
+                              int64_t* loads, int64_t* sectors) {
+    if (!plan || !seeds || !loads || !sectors) return MSFFT_ERR_INVALID_ARGUMENT;
+    const SchedulePlan& sp = plan->plan->schedule();
+    const int elem = plan->plan->c128() ? 16 : 8;
+    const int nt = static_cast<int>(std::max<unsigned>(1u, std::thread::hardware_concurrency()));
+    std::vector<int64_t> L(nt, 0), S(nt, 0);
+    std::vector<std::thread> pool;
+    for (int t = 0; t < nt; ++t)
+        pool.emplace_back([&, t] {
+            std::vector<int64_t> sg(sp.iterations), sgi(sp.iterations);
+            for (int64_t s = t; s < batch; s += nt) {
+                draw_sigmas(seeds[s], sp.n, sp.iterations, sg.data(), sgi.data());
+                gather_traffic(sp, sg.data(), elem, &L[t], &S[t]);
+            }
+        });
+    for (auto& th : pool) th.join();
+    *loads = 0;
+    *sectors = 0;
+    for (int t = 0; t < nt; ++t) {
+        *loads += L[t];
+        *sectors += S[t];
+    }
+    return MSFFT_OK;
+}
+
+int msfft_plan_stage_times(msfft_plan plan, double* ms3) {
+    if (!plan || !ms3) return MSFFT_ERR_INVALID_ARGUMENT;
+    for (int i = 0; i < 3; ++i) ms3[i] = plan->plan->stage_ms()[i];
+    return MSFFT_OK;
 }
 
 int msfft_window(int64_t n, int64_t b, double delta, int32_t device, int64_t* w, double* taps,

@@ -61,7 +61,9 @@ decode_kernel(const __grid_constant__ DevPlan plan, DecLayout lay, double2* __re
     __shared__ double s_thr;
 
     const int64_t s = blockIdx.x;
-    if (s >= batch) return;
+    // err[1]: the validation pass found a non-finite sample; the call will
+    // throw (ComplexSignal::validate) so there is nothing to decode.
+    if (s >= batch || err[1] != 0) return;
     const int tid = threadIdx.x;
     const int lane = tid & 31, warp = tid >> 5;
     constexpr int kWarps = kDecThreads / 32;
@@ -145,7 +147,8 @@ decode_kernel(const __grid_constant__ DevPlan plan, DecLayout lay, double2* __re
         // ---- K4: stable descending order of |y0|, budget and threshold
         for (int64_t j = tid; j < b; j += kDecThreads) {
             const double2 v = Y[j];
-            S.mag[j] = cabs_ref(v.x, v.y);
+            const double mg = cabs_ref(v.x, v.y);
+            S.mag[j] = mg == mg ? mg : -1.0;  // NaN (unvalidated input) ranks last
         }
         __syncthreads();
         for (int64_t j = tid; j < b; j += kDecThreads) {
@@ -327,7 +330,8 @@ decode_kernel(const __grid_constant__ DevPlan plan, DecLayout lay, double2* __re
     const int64_t K = plan.k;
     for (int j = tid; j < acc_n; j += kDecThreads) {
         const double2 c = S.acc_c[cur][j];
-        S.mag[j] = cabs_ref(c.x, c.y);
+        const double mg = cabs_ref(c.x, c.y);
+        S.mag[j] = mg == mg ? mg : -1.0;
     }
     __syncthreads();
     for (int j = tid; j < acc_n; j += kDecThreads) {

@@ -6,6 +6,7 @@
 
 #include "engine.hpp"
 #include "fft.hpp"
+#include "sigma.hpp"
 
 namespace msfft_b200 {
 
@@ -106,14 +107,17 @@ Plan::Plan(int64_t n, int64_t k, int64_t l, double q, double delta, bool c128, i
         budget_max_ = std::max(budget_max_, ip.budget);
     }
     lay_ = make_dec_layout(sched_.acc_cap, b_max_, budget_max_);
-    MSFFT_CUDA(cudaStreamCreateWithFlags(&own_stream_, cudaStreamNonBlocking));
-    MSFFT_CUDA(cudaStreamCreateWithFlags(&copy_stream_, cudaStreamNonBlocking));
+    // Blocking streams: ordered after work on the legacy default stream, so
+    // callers that pass no stream (e.g. torch default-stream producers) are safe.
+    MSFFT_CUDA(cudaStreamCreateWithFlags(&own_stream_, cudaStreamDefault));
+    MSFFT_CUDA(cudaStreamCreateWithFlags(&copy_stream_, cudaStreamDefault));
     MSFFT_CUDA(cudaEventCreate(&ev_start_));
     MSFFT_CUDA(cudaEventCreate(&ev_end_));
     for (int i = 0; i < 2; ++i) {
         MSFFT_CUDA(cudaEventCreateWithFlags(&ev_copied_[i], cudaEventDisableTiming));
         MSFFT_CUDA(cudaEventCreateWithFlags(&ev_free_[i], cudaEventDisableTiming));
     }
+    for (int i = 0; i < 4; ++i) MSFFT_CUDA(cudaEventCreate(&ev_stage_[i]));
     flags_.reset(2);
 }
 
@@ -129,6 +133,9 @@ Plan::~Plan() {
         if (ev_copied_[i]) cudaEventDestroy(ev_copied_[i]);
         if (ev_free_[i]) cudaEventDestroy(ev_free_[i]);
     }
+    for (int i = 0; i < 4; ++i)
+        if (ev_stage_[i]) cudaEventDestroy(ev_stage_[i]);
+    if (h_seeds_) cudaFreeHost(h_seeds_);
     cudaSetDevice(cur);
 }
 
@@ -189,7 +196,7 @@ const Plan::TaskSet& Plan::tasks_for(int64_t batch) {
 }
 
 int64_t Plan::launches(int64_t /*batch*/, bool validate) const {
-    int64_t count = 2 + (validate ? 1 : 0);  // encode + decode (+ validate)
+    int64_t count = 3 + (validate ? 1 : 0);  // sigma + encode + decode (+ validate)
     for (int m : big_b_iters_) {
         int lb = dplan_.it[m].log2b;
         int64_t passes = 0, s0 = 0;
@@ -220,13 +227,16 @@ void Plan::run_chunk(int64_t batch, const void* d_x, int64_t x_stride, const int
         MSFFT_LAUNCH_CHECK("validate_kernel");
     }
     const TaskSet& ts = tasks_for(batch);
+    if (opt.stage_times) MSFFT_CUDA(cudaEventRecord(ev_stage_[0], st));
     launch_encode(dplan_, ts.d.get(), ts.count, d_x, c128_, x_stride, batch, d_sig, y_.get(),
                   enc_smem_, st);
+    if (opt.stage_times) MSFFT_CUDA(cudaEventRecord(ev_stage_[1], st));
     for (int m : big_b_iters_) {
         const DevIter& di = dplan_.it[m];
         fft_radix2_batched(y_.get() + di.yoff, di.b, batch * di.nrounds, di.nrounds,
                            dplan_.values_per_signal, -1, dplan_.inv_n, st);
     }
+    if (opt.stage_times) MSFFT_CUDA(cudaEventRecord(ev_stage_[2], st));
     const size_t ybytes = sizeof(double2) * static_cast<size_t>(dplan_.values_per_signal);
     if (opt.pre) {
         MSFFT_CUDA(cudaMemcpyAsync(opt.pre, y_.get(), ybytes, cudaMemcpyDeviceToHost, st));
@@ -240,6 +250,15 @@ void Plan::run_chunk(int64_t batch, const void* d_x, int64_t x_stride, const int
     }
     launch_decode(dplan_, lay_, y_.get(), d_sig, d_sig_inv, batch, dec_work_.get(), d_out_f,
                   d_out_c, d_out_count, flags_.get(), st, tb.get(), tf.get(), tv.get());
+    if (opt.stage_times) {
+        MSFFT_CUDA(cudaEventRecord(ev_stage_[3], st));
+        MSFFT_CUDA(cudaEventSynchronize(ev_stage_[3]));
+        for (int i = 0; i < 3; ++i) {
+            float ms = 0.f;
+            MSFFT_CUDA(cudaEventElapsedTime(&ms, ev_stage_[i], ev_stage_[i + 1]));
+            stage_ms_[i] += ms;
+        }
+    }
     if (opt.post) {
         MSFFT_CUDA(cudaMemcpyAsync(opt.post, y_.get(), ybytes, cudaMemcpyDeviceToHost, st));
     }
@@ -263,11 +282,12 @@ void Plan::execute(int64_t batch, const void* x, int64_t x_stride, const uint64_
     cudaStream_t st = opt.stream ? opt.stream : own_stream_;
     const size_t elem = c128_ ? sizeof(double2) : sizeof(float2);
 
-    // sigma plan (host, exact mt19937_64 draws)
-    h_sig_.resize(static_cast<size_t>(batch * iters));
-    h_sig_inv_.resize(static_cast<size_t>(batch * iters));
-    for (int64_t s = 0; s < batch; ++s)
-        draw_sigmas(seeds[s], n, iters, h_sig_.data() + s * iters, h_sig_inv_.data() + s * iters);
+    if (h_seeds_cap_ < batch) {
+        if (h_seeds_) cudaFreeHost(h_seeds_);
+        h_seeds_ = nullptr;
+        MSFFT_CUDA(cudaMallocHost(&h_seeds_, sizeof(uint64_t) * batch));
+        h_seeds_cap_ = batch;
+    }
 
     // chunking: device inputs run as one chunk; host inputs stream through
     // two staging buffers overlapped with compute
@@ -277,6 +297,7 @@ void Plan::execute(int64_t batch, const void* x, int64_t x_stride, const uint64_
                         : std::max<int64_t>(1, std::min<int64_t>(batch, kChunkBytes / sig_bytes));
     sig_.ensure(static_cast<size_t>(batch * iters));
     sig_inv_.ensure(static_cast<size_t>(batch * iters));
+    seeds_.ensure(static_cast<size_t>(batch));
     y_.ensure(static_cast<size_t>(chunk * dplan_.values_per_signal));
     if (!lay_.in_smem) dec_work_.ensure(static_cast<size_t>(chunk * lay_.bytes));
     if (!opt.out_on_device) {
@@ -291,12 +312,15 @@ void Plan::execute(int64_t batch, const void* x, int64_t x_stride, const uint64_
     double2* d_oc = opt.out_on_device ? reinterpret_cast<double2*>(out_c) : out_c_.get();
     int64_t* d_ocnt = opt.out_on_device ? out_count : out_count_.get();
 
+    stage_ms_[0] = stage_ms_[1] = stage_ms_[2] = 0.0;
     MSFFT_CUDA(cudaEventRecord(ev_start_, st));
     MSFFT_CUDA(cudaMemsetAsync(flags_.get(), 0, 2 * sizeof(int32_t), st));
-    MSFFT_CUDA(cudaMemcpyAsync(sig_.get(), h_sig_.data(), sizeof(int64_t) * batch * iters,
+    // sigma plan: exact mt19937_64 draws on the device, one thread per signal
+    MSFFT_CUDA(cudaStreamSynchronize(st));  // previous use of the pinned seed staging
+    std::memcpy(h_seeds_, seeds, sizeof(uint64_t) * batch);
+    MSFFT_CUDA(cudaMemcpyAsync(seeds_.get(), h_seeds_, sizeof(uint64_t) * batch,
                                cudaMemcpyHostToDevice, st));
-    MSFFT_CUDA(cudaMemcpyAsync(sig_inv_.get(), h_sig_inv_.data(),
-                               sizeof(int64_t) * batch * iters, cudaMemcpyHostToDevice, st));
+    launch_sigma(seeds_.get(), batch, iters, n, sig_.get(), sig_inv_.get(), st);
     const bool validate = !opt.assume_valid;
     if (opt.x_on_device) {
         run_chunk(batch, x, x_stride, sig_.get(), sig_inv_.get(), d_of, d_oc, d_ocnt, validate,

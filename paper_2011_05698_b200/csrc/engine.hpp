@@ -28,6 +28,7 @@ struct ExecOptions {
     bool x_on_device = false;
     bool out_on_device = false;
     bool assume_valid = false;
+    bool stage_times = false;  // CUDA events around encode / fft / decode
     cudaStream_t stream = nullptr;
     double* pre = nullptr;   // trace: encode output (batch must be 1, host)
     double* post = nullptr;  // trace: post-subtract values
@@ -53,6 +54,10 @@ public:
                  double* device_ms);
 
     int64_t launches(int64_t batch, bool validate) const;
+
+    // [encode, bucket fft (b > 256), decode] ms of the last execute run with
+    // stage_times (summed over chunks).
+    const double* stage_ms() const { return stage_ms_; }
 
     std::mutex& mutex() { return mu_; }
 
@@ -81,6 +86,8 @@ private:
     cudaStream_t own_stream_ = nullptr, copy_stream_ = nullptr;
     cudaEvent_t ev_start_ = nullptr, ev_end_ = nullptr;
     cudaEvent_t ev_copied_[2] = {nullptr, nullptr}, ev_free_[2] = {nullptr, nullptr};
+    cudaEvent_t ev_stage_[4] = {nullptr, nullptr, nullptr, nullptr};
+    double stage_ms_[3] = {0, 0, 0};
 
     DeviceBuffer<double2> y_;
     DeviceBuffer<int64_t> sig_, sig_inv_;
@@ -89,7 +96,9 @@ private:
     DeviceBuffer<double2> out_c_;
     DeviceBuffer<int32_t> flags_;  // [0] decode error, [1] non-finite input
     DeviceBuffer<unsigned char> xstage_[2];
-    std::vector<int64_t> h_sig_, h_sig_inv_;
+    DeviceBuffer<uint64_t> seeds_;
+    uint64_t* h_seeds_ = nullptr;  // pinned staging
+    int64_t h_seeds_cap_ = 0;
     std::mutex mu_;
 };
 

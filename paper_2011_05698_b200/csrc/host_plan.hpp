@@ -85,6 +85,13 @@ void draw_sigmas(uint64_t seed, int64_t n, int iterations, int64_t* sigma, int64
 // on the plan, never on the data.
 int64_t count_samples_used(const SchedulePlan& plan, const int64_t* sigma);
 
+// Algorithmic traffic of the fused gather for one signal: per iteration the
+// kernel loads every distinct t' of the union of the rounds' tap intervals
+// once.  Adds to *loads the number of such samples and to *sectors the
+// number of distinct 32-byte sectors they fall in (elem_bytes per sample).
+void gather_traffic(const SchedulePlan& plan, const int64_t* sigma, int elem_bytes,
+                    int64_t* loads, int64_t* sectors);
+
 // ---- template definition ----
 template <class WindowW>
 SchedulePlan build_schedule(int64_t n, int64_t k, int64_t l, double q, double delta,

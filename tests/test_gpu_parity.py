@@ -1,0 +1,180 @@
+"""Parity of the CUDA path (through the C ABI) with the reference.
+
+Bars (BASELINE.json north_star): identical support; per-coefficient relative
+error <= 1e-9 for complex128 and <= 1e-4 for complex64 inputs, with the
+absolute floor 10*K*delta*max|c| for leakage-level entries.
+In practice the encode is bit-identical and coefficients agree to ~1e-15.
+Run on a B200: pytest -m gpu.
+"""
+import hashlib
+
+import numpy as np
+import pytest
+
+import paper_2011_05698_b200 as M
+from helpers import assert_parity, golden_result, make_signal
+
+pytestmark = pytest.mark.gpu
+TOL = {"complex128": 1e-9, "complex64": 1e-4}
+
+
+def test_device_present():
+    assert M.device_count() >= 1
+
+
+def test_windows_bit_exact(golden):
+    g = golden("windows")
+    for rec in g["ok"]:
+        w, taps = M.window(rec["n"], rec["b"], rec["delta"])
+        assert w == rec["w"], (rec["n"], rec["b"], rec["delta"])
+        assert hashlib.sha256(taps.astype("<f8").tobytes()).hexdigest() == rec["taps_sha256"]
+
+
+def test_window_errors_same_messages(golden):
+    for rec in golden("windows")["error"]:
+        with pytest.raises(M.InvalidArgument) as ei:
+            M.window(rec["n"], rec["b"], rec["delta"])
+        assert str(ei.value) == rec["msg"]
+
+
+def test_response_table(golden):
+    """G_d from the device table vs response_at: only libm-vs-CUDA cos ulps."""
+    for rec in golden("windows")["ok"]:
+        offs = [a for a, _ in rec["response"]]
+        want = np.array([float.fromhex(h) for _, h in rec["response"]])
+        got = M.window_response(rec["n"], rec["b"], rec["delta"], offs)
+        assert np.max(np.abs(got - want)) <= 1e-14, (rec["n"], rec["b"])
+
+
+def test_sfft4_small_goldens(oracle, golden):
+    for rec in golden("sfft4_small"):
+        x = make_signal(oracle, rec)
+        cfg = M.MultiscaleConfig(rec["l"], rec["q"])
+        if "error" in rec:
+            with pytest.raises(M.InvalidArgument) as ei:
+                M.sfft4(x, rec["k"], cfg, rec["algo_seed"], rec["delta"])
+            assert str(ei.value) == rec["error"]["msg"]
+            continue
+        r = M.sfft4(x, rec["k"], cfg, rec["algo_seed"], rec["delta"])
+        f, c, stats = golden_result(rec)
+        assert_parity(f, c, r.spectrum.positions, r.spectrum.coeffs, rec["k"], rec["delta"],
+                      TOL[rec["dtype"]])
+        assert r.stats.samples_used == stats["samples_used"]
+        assert r.stats.samples_round_sum == stats["samples_round_sum"]
+        assert r.stats.iterations == stats["iterations"]
+        assert r.stats.b_first == stats["b_first"]
+        assert r.stats.stage_counts == stats["stage_counts"]
+        assert r.stats.sample_fraction == stats["sample_fraction"]
+
+
+TRACE_CASES = [
+    dict(gen="ref", n=1 << 16, k=50, seed=1, snr=None, l=16, q=1.0, dtype="complex128"),
+    dict(gen="ref", n=1 << 20, k=100, seed=2, snr=20.0, l=8, q=2.0, dtype="complex128"),
+    dict(gen="np", n=1 << 18, k=64, seed=3, snr=25.0, l=16, q=1.0, dtype="complex64"),
+    dict(gen="np", n=1 << 20, k=100, seed=4, snr=20.0, l=4, q=1.0, dtype="complex128"),
+]
+
+
+@pytest.mark.parametrize("rec", TRACE_CASES, ids=lambda r: f"{r['n']}-{r['k']}-{r['l']}-{r['q']}")
+def test_stage_parity(oracle, rec):
+    """Kernel-level parity against the reference's per-stage trace:
+    K1+K2 (encode) bit-identical; K3 (subtract) to rounding; K4 (selection
+    order) and K5/K6 (located f per rank) identical; values to rounding."""
+    from paper_2011_05698_b200 import splitmix64
+    x = make_signal(oracle, rec)
+    delta = 1e-6 if rec["snr"] is not None else 1e-8
+    a = splitmix64(rec["seed"] ^ 0x53)
+    tr = oracle.sfft4_trace(x.astype(np.complex128), rec["k"], rec["l"], rec["q"], a, delta)
+    plan = tr["plan"]
+    vps = sum(r * b for r, b in zip(plan.rounds, plan.b))
+    nsel = sum(plan.budget)
+    g = M.trace(x, rec["k"], M.MultiscaleConfig(rec["l"], rec["q"]), a, delta, vps, nsel)
+    assert np.array_equal(g["pre"].view(np.float64), tr["pre"].view(np.float64)), "encode"
+    scale = np.max(np.abs(tr["pre"]))
+    assert np.max(np.abs(g["post"] - tr["post"])) <= 1e-13 * scale, "subtract"
+    assert np.array_equal(g["sel_bucket"], tr["sel_bucket"]), "selection order"
+    want_f = np.where(tr["sel_status"] == 0, tr["sel_f"], -1)
+    assert np.array_equal(g["sel_f"], want_f), "located frequencies"
+    ok = want_f >= 0
+    assert np.max(np.abs(g["sel_value"][ok] - tr["sel_value"][ok]) /
+                  np.abs(tr["sel_value"][ok])) <= 1e-12
+    assert_parity(tr["result"].f, tr["result"].c, g["f"], g["c"], rec["k"], delta,
+                  TOL[rec["dtype"]])
+
+
+def test_batch_plan_equals_single_calls(oracle):
+    """Plan.execute over a batch == one sfft4 per signal, bitwise, for host
+    and device inputs and outputs."""
+    import torch
+    n, k, delta = 1 << 18, 40, 1e-6
+    xs = np.stack([make_signal(oracle, dict(gen="np", n=n, k=k, seed=s, snr=20.0,
+                                            dtype="complex64")) for s in range(6)])
+    seeds = np.arange(100, 106, dtype=np.uint64)
+    plan = M.Plan(n, k, M.MultiscaleConfig(), delta, "complex64")
+    f, c, cnt, _ = plan.execute(xs, seeds)
+    xd = torch.as_tensor(xs).cuda()
+    out = (torch.empty((6, k), dtype=torch.int64, device="cuda"),
+           torch.empty((6, k), dtype=torch.complex128, device="cuda"),
+           torch.empty((6,), dtype=torch.int64, device="cuda"))
+    plan.execute(xd, seeds, out=out)
+    for i in range(6):
+        r = M.sfft4(xs[i], k, M.MultiscaleConfig(), int(seeds[i]), delta)
+        m = int(cnt[i])
+        assert np.array_equal(f[i, :m], r.spectrum.positions)
+        assert np.array_equal(c[i, :m], r.spectrum.coeffs)
+        assert np.array_equal(out[0][i, :m].cpu().numpy(), r.spectrum.positions)
+        assert np.array_equal(out[1][i, :m].cpu().numpy(), r.spectrum.coeffs)
+        ref = oracle.sfft4(xs[i].astype(np.complex128), k, 16, 1.0, int(seeds[i]), delta)
+        assert_parity(ref.f, ref.c, f[i, :m], c[i, :m], k, delta, 1e-4)
+
+
+def test_device_input_single(oracle):
+    import torch
+    rec = dict(gen="ref", n=1 << 16, k=50, seed=3, snr=None)
+    x = make_signal(oracle, rec)
+    from paper_2011_05698_b200 import splitmix64
+    a = splitmix64(3 ^ 0x53)
+    r_host = M.sfft4(x, 50, seed=a, delta=1e-8)
+    r_dev = M.sfft4(torch.as_tensor(x).cuda(), 50, seed=a, delta=1e-8)
+    assert np.array_equal(r_host.spectrum.positions, r_dev.spectrum.positions)
+    assert np.array_equal(r_host.spectrum.coeffs, r_dev.spectrum.coeffs)
+
+
+def test_non_finite_input_rejected():
+    import torch
+    x = np.zeros(1 << 12, np.complex128)
+    x[77] = np.nan
+    for arg in (x, torch.as_tensor(x).cuda()):
+        with pytest.raises(M.InvalidArgument, match="ComplexSignal: non-finite sample"):
+            M.sfft4(arg, 10)
+    # x is validated before K (proj/src/sfft4.cpp:133-135)
+    with pytest.raises(M.InvalidArgument, match="ComplexSignal: non-finite sample"):
+        M.sfft4(x, 100000)
+
+
+def test_bad_length_rejected():
+    with pytest.raises(M.InvalidArgument, match="ComplexSignal: n must be a power of two >= 4"):
+        M.sfft4(np.zeros(1000, np.complex128), 10)
+
+
+@pytest.mark.slow
+def test_c4_goldens(oracle, golden):
+    """Full-size C4 signals (N=2^22, K=64, complex64, 25 dB) vs the reference."""
+    for rec in golden("sfft4_c4"):
+        x = make_signal(oracle, rec)
+        r = M.sfft4(x, rec["k"], M.MultiscaleConfig(), rec["algo_seed"], rec["delta"])
+        f, c, stats = golden_result(rec)
+        assert_parity(f, c, r.spectrum.positions, r.spectrum.coeffs, rec["k"], rec["delta"], 1e-4)
+        assert r.stats.samples_used == stats["samples_used"]
+
+
+@pytest.mark.slow
+def test_c3_goldens(oracle, golden):
+    """C3: N=2^24, K=1000, min-separated support, 30 dB, c128 and c64."""
+    for rec in golden("sfft4_c3"):
+        x = make_signal(oracle, rec)
+        r = M.sfft4(x, rec["k"], M.MultiscaleConfig(), rec["algo_seed"], rec["delta"])
+        f, c, stats = golden_result(rec)
+        assert_parity(f, c, r.spectrum.positions, r.spectrum.coeffs, rec["k"], rec["delta"],
+                      TOL[rec["dtype"]])
+        assert r.stats.samples_used == stats["samples_used"]
