@@ -110,12 +110,14 @@ __host__ __device__ inline double fmod_pow2(double x, double n) {
     return x - trunc(x / n) * n;
 }
 
-// position_phase (proj/src/locate.cpp:19-23).
-__host__ __device__ inline double position_phase(double u, int64_t tau, int64_t n) {
+// position_phase (proj/src/locate.cpp:19-23).  inv_n = 1/n is exact for a
+// power of two, so the multiplications below equal the reference's divisions.
+__host__ __device__ inline double position_phase(double u, int64_t tau, int64_t n, double inv_n) {
     const double nd = static_cast<double>(n);
-    double x = fmod_pow2(u * static_cast<double>(tau), nd);
+    const double p = u * static_cast<double>(tau);
+    double x = p - trunc(p * inv_n) * nd;  // fmod(p, n), exact
     if (x < 0) x += nd;
-    return x * kTwoPi / nd;
+    return x * kTwoPi * inv_n;
 }
 
 // circular_phase_distance (proj/src/locate.cpp:14-17).  Both phases lie in

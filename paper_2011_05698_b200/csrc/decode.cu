@@ -34,22 +34,24 @@ struct Scratch {
     double2* cand_v;
     int32_t* cand_first;
     double2* cand_sum;
+    double2* contrib;  // [tone][round][3] predicted contributions
 };
 
 __device__ __forceinline__ double ghat_at(const DevIter& it, int64_t d) {
     return it.ghat[d + it.gmax];
 }
 
-// unit_root (proj/src/bucketize.cpp:12-18): e^{-2 pi i (e mod n)/n}.
-__device__ __forceinline__ double2 unit_root(int64_t n, int64_t e) {
+// unit_root (proj/src/bucketize.cpp:12-18): e^{-2 pi i (e mod n)/n}; the
+// division by the power of two n is an exact multiplication by 1/n.
+__device__ __forceinline__ double2 unit_root(int64_t n, double inv_n, int64_t e) {
     e &= (n - 1);
-    const double a = -kTwoPi * static_cast<double>(e) / static_cast<double>(n);
+    const double a = -kTwoPi * static_cast<double>(e) * inv_n;
     double s, c;
     sincos(a, &s, &c);
     return make_double2(c, s);
 }
 
-__global__ void __launch_bounds__(kDecThreads)
+__global__ void __launch_bounds__(kDecThreads, 2)
 decode_kernel(const __grid_constant__ DevPlan plan, DecLayout lay, double2* __restrict__ y,
               const int64_t* __restrict__ sigma, const int64_t* __restrict__ sigma_inv,
               int64_t batch, unsigned char* __restrict__ work, int64_t* __restrict__ out_f,
@@ -65,8 +67,7 @@ decode_kernel(const __grid_constant__ DevPlan plan, DecLayout lay, double2* __re
     // throw (ComplexSignal::validate) so there is nothing to decode.
     if (s >= batch || err[1] != 0) return;
     const int tid = threadIdx.x;
-    const int lane = tid & 31, warp = tid >> 5;
-    constexpr int kWarps = kDecThreads / 32;
+    const int lane = tid & 31;
 
     unsigned char* base = lay.in_smem ? dsm : work + s * lay.bytes;
     Scratch S;
@@ -82,6 +83,7 @@ decode_kernel(const __grid_constant__ DevPlan plan, DecLayout lay, double2* __re
     S.cand_v = reinterpret_cast<double2*>(base + lay.off_cand_v);
     S.cand_first = reinterpret_cast<int32_t*>(base + lay.off_cand_first);
     S.cand_sum = reinterpret_cast<double2*>(base + lay.off_cand_sum);
+    S.contrib = reinterpret_cast<double2*>(base + lay.off_contrib);
 
     if (tid == 0) {
         s_acc_n = 0;
@@ -91,6 +93,7 @@ decode_kernel(const __grid_constant__ DevPlan plan, DecLayout lay, double2* __re
 
     const int64_t n = plan.n;
     const int64_t nmask = n - 1;
+    const double inv_n = plan.inv_n;
     double2* ysig = y + s * plan.values_per_signal;
 
     int64_t sel_off = 0;  // trace offset: sum of earlier budgets
@@ -98,6 +101,7 @@ decode_kernel(const __grid_constant__ DevPlan plan, DecLayout lay, double2* __re
         const DevIter& it = plan.it[m];
         const int64_t b = it.b, L = it.l_width;
         const double Ld = static_cast<double>(L);
+        const double invL = 1.0 / Ld;  // exact: L is a power of two
         const int nr = it.nrounds;
         const int64_t* taus = plan.taus + it.tau_off;
         double2* Y = ysig + it.yoff;
@@ -105,36 +109,50 @@ decode_kernel(const __grid_constant__ DevPlan plan, DecLayout lay, double2* __re
         const int64_t sgi = sigma_inv[s * plan.iters + m];
         const int acc_n = s_acc_n;
         const int cur = s_cur;
+        const int64_t* AF = cur ? S.acc_f[1] : S.acc_f[0];
+        const double2* AC = cur ? S.acc_c[1] : S.acc_c[0];
 
-        // ---- K3: subtract the prediction of everything already known
+        // ---- K3: subtract the prediction of everything already known.
+        // predict_buckets (bucketize.cpp:84-93) adds, per known tone in
+        // ascending f, (G_{jL-u} * c) * e^{-2 pi i tau u/n} into buckets
+        // j = i-1, i, i+1.  Step 1 evaluates each (tone, round) rotation and
+        // its three contributions once; step 2 sums, per (round, bucket), the
+        // contributions in ascending tone order -- the reference's order.
         if (acc_n > 0) {
             for (int j = tid; j < acc_n; j += kDecThreads) {
-                const int64_t u = (sg * S.acc_f[cur][j]) & nmask;
+                const int64_t u = (sg * AF[j]) & nmask;
                 S.tone_u[j] = u;
-                S.tone_i[j] = static_cast<int64_t>(floor(static_cast<double>(u) / Ld + 0.5));
+                S.tone_i[j] = static_cast<int64_t>(floor(static_cast<double>(u) * invL + 0.5));
+            }
+            __syncthreads();
+            for (int e = tid; e < acc_n * nr; e += kDecThreads) {
+                const int j = e / nr, r = e - j * nr;
+                const int64_t u = S.tone_u[j], i = S.tone_i[j];
+                const double2 rot = unit_root(n, inv_n, taus[r] * u);
+                const double2 c = AC[j];
+                double2* dst = S.contrib + static_cast<int64_t>(e) * 3;
+#pragma unroll
+                for (int d = 0; d < 3; ++d) {
+                    const double g = ghat_at(it, (i - 1 + d) * L - u);
+                    dst[d] = cmul(make_double2(g * c.x, g * c.y), rot);
+                }
             }
             __syncthreads();
             const int64_t total = static_cast<int64_t>(nr) * b;
             for (int64_t e = tid; e < total; e += kDecThreads) {
                 const int r = static_cast<int>(e / b);
                 const int64_t beta = e - r * b;
-                const int64_t tau = taus[r];
                 double2 pred = make_double2(0.0, 0.0);
                 bool any = false;
                 for (int j = 0; j < acc_n; ++j) {
-                    const int64_t i = S.tone_i[j];
                     // which of the buckets i-1, i, i+1 (mod b) is beta?
-                    const int64_t dlt = (beta - (i - 1)) & (b - 1);
-                    if (dlt > 2) continue;
-                    const int64_t jj = i - 1 + dlt;
-                    const int64_t u = S.tone_u[j];
-                    const double g = ghat_at(it, jj * L - u);
-                    const double2 c = S.acc_c[cur][j];
-                    const double2 gc = make_double2(g * c.x, g * c.y);
-                    const double2 v = cmul(gc, unit_root(n, tau * u));
-                    pred.x += v.x;
-                    pred.y += v.y;
-                    any = true;
+                    const int64_t dlt = (beta - S.tone_i[j] + 1) & (b - 1);
+                    if (dlt <= 2) {
+                        const double2 v = S.contrib[(static_cast<int64_t>(j) * nr + r) * 3 + dlt];
+                        pred.x += v.x;
+                        pred.y += v.y;
+                        any = true;
+                    }
                 }
                 if (any) {
                     const double2 o = Y[e];
@@ -166,54 +184,67 @@ decode_kernel(const __grid_constant__ DevPlan plan, DecLayout lay, double2* __re
         __syncthreads();
         const double thr = s_thr;
 
-        // ---- K5 + K6: locate and estimate, one warp per ranked bucket
+        // ---- K5 + K6: locate and estimate.  A group of `gsz` lanes (the l
+        // candidate blocks rounded up to a power of two, at most 32) takes one
+        // ranked bucket, so l = 16 runs two buckets per warp.  The region
+        // length evolves identically for every bucket, so all groups run the
+        // same number of stages and the shuffles stay convergent.
         const int64_t lcfg = plan.l;
         const double q = plan.q;
-        for (int64_t rank = warp; rank < budget; rank += kWarps) {
-            const int64_t beta = S.order[rank];
+        const int gsz = lcfg >= 32 ? 32 : (lcfg > 16 ? 32 : (lcfg > 8 ? 16 : (lcfg > 4 ? 8 : 4)));
+        const int glane = lane & (gsz - 1);
+        const int groups = kDecThreads / gsz;
+        const int gid = tid / gsz;
+        const int64_t rounds_up = (budget + groups - 1) / groups * groups;
+        for (int64_t rank = gid; rank < rounds_up; rank += groups) {
+            const bool live = rank < budget;
+            const int64_t beta = live ? S.order[rank] : 0;
             int64_t f_out = -1;
             double2 v_out = make_double2(0.0, 0.0);
             const double2 y0 = Y[beta];
-            bool ok = S.mag[beta] > thr;
+            bool ok = live && S.mag[beta] > thr;
             if (ok && y0.x == 0.0 && y0.y == 0.0) ok = false;
             double u_min = (2.0 * static_cast<double>(beta) - 1.0) * Ld / 2.0;
             double len = Ld;
             int stage = 0;
-            while (ok && len > 1.0 + 1e-9) {
+            while (len > 1.0 + 1e-9) {
                 ++stage;
-                if (stage >= nr) {
-                    if (lane == 0) atomicCAS(err, 0, kDecErrRounds);
+                if (stage >= nr) {  // cannot happen for sfft4's own tau plans
+                    if (ok && glane == 0) atomicCAS(err, 0, kDecErrRounds);
                     ok = false;
-                    break;
+                    break;  // uniform: every group sees the same stage count
                 }
-                const double2 yt = Y[static_cast<int64_t>(stage) * b + beta];
-                if (yt.x == 0.0 && yt.y == 0.0) {
-                    ok = false;
-                    break;
+                double phi = 0.0;
+                if (ok) {
+                    const double2 yt = Y[static_cast<int64_t>(stage) * b + beta];
+                    if (yt.x == 0.0 && yt.y == 0.0) {
+                        ok = false;  // locate_frequency returns nullopt
+                    } else {
+                        const double2 z = cdiv_ref(y0.x, y0.y, yt.x, yt.y);
+                        if (z.x == 0.0 && z.y == 0.0) {  // phase_of throws
+                            if (glane == 0) atomicCAS(err, 0, kDecErrPhaseZero);
+                            ok = false;
+                        }
+                        phi = atan2(z.y, z.x);
+                        if (phi < 0.0) phi += kTwoPi;
+                        phi = phi + 0.0;
+                    }
                 }
-                const double2 z = cdiv_ref(y0.x, y0.y, yt.x, yt.y);
-                if (z.x == 0.0 && z.y == 0.0) {
-                    if (lane == 0) atomicCAS(err, 0, kDecErrPhaseZero);
-                    ok = false;
-                    break;
-                }
-                double phi = atan2(z.y, z.x);
-                if (phi < 0.0) phi += kTwoPi;
-                phi = phi + 0.0;
                 const int64_t tau = taus[stage];
                 const double rblk = len / static_cast<double>(lcfg);
                 double best_d = INFINITY;
                 int best_j = 0x7fffffff;
-                for (int64_t j = lane; j < lcfg; j += 32) {
+                for (int64_t j = glane; j < lcfg; j += gsz) {
                     const double center = u_min + (static_cast<double>(j) + 0.5) * rblk;
-                    const double d = circular_phase_distance(position_phase(center, tau, n), phi);
+                    const double d = circular_phase_distance(
+                        position_phase(center, tau, n, inv_n), phi);
                     if (d < best_d) {
                         best_d = d;
                         best_j = static_cast<int>(j);
                     }
                 }
                 // lowest block index wins ties (strict < in ascending order)
-                for (int o = 16; o > 0; o >>= 1) {
+                for (int o = gsz >> 1; o > 0; o >>= 1) {
                     const double od = __shfl_xor_sync(0xffffffffu, best_d, o);
                     const int oj = __shfl_xor_sync(0xffffffffu, best_j, o);
                     if (od < best_d || (od == best_d && oj < best_j)) {
@@ -231,14 +262,14 @@ decode_kernel(const __grid_constant__ DevPlan plan, DecLayout lay, double2* __re
                 if (!(static_cast<double>(u) < hi)) u = llround(0.5 * (lo + hi));
                 u %= n;
                 if (u < 0) u += n;
-                const int64_t i = static_cast<int64_t>(floor(static_cast<double>(u) / Ld + 0.5));
+                const int64_t i = static_cast<int64_t>(floor(static_cast<double>(u) * invL + 0.5));
                 const double g = ghat_at(it, i * L - u);
                 if (!(fabs(g) < 0.5)) {
                     v_out = make_double2(y0.x / g, y0.y / g);
                     f_out = (sgi * u) & nmask;
                 }
             }
-            if (lane == 0) {
+            if (live && glane == 0) {
                 S.cand_f[rank] = f_out;
                 S.cand_v[rank] = v_out;
                 if (tr_bucket) {
@@ -255,6 +286,8 @@ decode_kernel(const __grid_constant__ DevPlan plan, DecLayout lay, double2* __re
         // accepted rank of each f carries the sum; the found set is merged
         // into the ascending acc list (ping-pong buffers).
         const int nxt = cur ^ 1;
+        int64_t* NF = nxt ? S.acc_f[1] : S.acc_f[0];
+        double2* NC = nxt ? S.acc_c[1] : S.acc_c[0];
         if (tid == 0) s_new_n = 0;
         // cand_first[r]: 0 = not the first accepted rank of its f,
         // 1 = first and f is new, 2 = first and f already accumulated.
@@ -273,16 +306,16 @@ decode_kernel(const __grid_constant__ DevPlan plan, DecLayout lay, double2* __re
                 int lo = 0, hi = acc_n;
                 while (lo < hi) {
                     const int mid = (lo + hi) >> 1;
-                    if (S.acc_f[cur][mid] < fr) lo = mid + 1; else hi = mid;
+                    if (AF[mid] < fr) lo = mid + 1; else hi = mid;
                 }
-                if (lo < acc_n && S.acc_f[cur][lo] == fr) first = 2;
+                if (lo < acc_n && AF[lo] == fr) first = 2;
             }
             S.cand_first[r] = first;
         }
         __syncthreads();
         // acc entries move up by the number of NEW found f below them
         for (int j = tid; j < acc_n; j += kDecThreads) {
-            const int64_t fj = S.acc_f[cur][j];
+            const int64_t fj = AF[j];
             int64_t before = 0;
             int64_t hit = -1;
             for (int64_t r = 0; r < budget; ++r) {
@@ -292,10 +325,10 @@ decode_kernel(const __grid_constant__ DevPlan plan, DecLayout lay, double2* __re
                 if (cf == 1 && fr < fj) ++before;
                 if (cf == 2 && fr == fj) hit = r;
             }
-            double2 c = S.acc_c[cur][j];
+            double2 c = AC[j];
             if (hit >= 0) c = make_double2(c.x + S.cand_sum[hit].x, c.y + S.cand_sum[hit].y);
-            S.acc_f[nxt][j + before] = fj;
-            S.acc_c[nxt][j + before] = c;
+            NF[j + before] = fj;
+            NC[j + before] = c;
         }
         // new f: insert at #{acc f < f} + #{new found f < f}
         for (int64_t r = tid; r < budget; r += kDecThreads) {
@@ -304,15 +337,15 @@ decode_kernel(const __grid_constant__ DevPlan plan, DecLayout lay, double2* __re
             int lo = 0, hi = acc_n;
             while (lo < hi) {
                 const int mid = (lo + hi) >> 1;
-                if (S.acc_f[cur][mid] < fr) lo = mid + 1; else hi = mid;
+                if (AF[mid] < fr) lo = mid + 1; else hi = mid;
             }
             int64_t ubefore = 0;
             for (int64_t r3 = 0; r3 < budget; ++r3)
                 ubefore += S.cand_first[r3] == 1 && S.cand_f[r3] < fr;
             const int64_t pos = lo + ubefore;
             const double2 sum = S.cand_sum[r];
-            S.acc_f[nxt][pos] = fr;
-            S.acc_c[nxt][pos] = make_double2(0.0 + sum.x, 0.0 + sum.y);
+            NF[pos] = fr;
+            NC[pos] = make_double2(0.0 + sum.x, 0.0 + sum.y);
             atomicAdd(&s_new_n, 1);
         }
         __syncthreads();
@@ -327,9 +360,11 @@ decode_kernel(const __grid_constant__ DevPlan plan, DecLayout lay, double2* __re
     // ---- K7: keep the K largest |c| (stable over ascending f), emit in f order
     const int acc_n = s_acc_n;
     const int cur = s_cur;
+    const int64_t* AF = cur ? S.acc_f[1] : S.acc_f[0];
+    const double2* AC = cur ? S.acc_c[1] : S.acc_c[0];
     const int64_t K = plan.k;
     for (int j = tid; j < acc_n; j += kDecThreads) {
-        const double2 c = S.acc_c[cur][j];
+        const double2 c = AC[j];
         const double mg = cabs_ref(c.x, c.y);
         S.mag[j] = mg == mg ? mg : -1.0;
     }
@@ -348,15 +383,16 @@ decode_kernel(const __grid_constant__ DevPlan plan, DecLayout lay, double2* __re
         if (!S.tone_i[j]) continue;
         int64_t pos = 0;
         for (int i = 0; i < j; ++i) pos += S.tone_i[i];
-        out_f[s * K + pos] = S.acc_f[cur][j];
-        out_c[s * K + pos] = S.acc_c[cur][j];
+        out_f[s * K + pos] = AF[j];
+        out_c[s * K + pos] = AC[j];
     }
     if (tid == 0) out_count[s] = acc_n < K ? acc_n : K;
 }
 
 }  // namespace
 
-DecLayout make_dec_layout(int64_t acc_cap, int64_t b_max, int64_t budget_max) {
+DecLayout make_dec_layout(int64_t acc_cap, int64_t b_max, int64_t budget_max,
+                          int64_t rounds_max) {
     DecLayout L{};
     int64_t off = 0;
     auto take = [&](int64_t bytes) {
@@ -377,8 +413,9 @@ DecLayout make_dec_layout(int64_t acc_cap, int64_t b_max, int64_t budget_max) {
     L.off_cand_v = take(budget_max * 16);
     L.off_cand_first = take(budget_max * 4);
     L.off_cand_sum = take(budget_max * 16);
+    L.off_contrib = take(cap * rounds_max * 3 * 16);
     L.bytes = off;
-    L.in_smem = off <= 160 * 1024 ? 1 : 0;
+    L.in_smem = off <= 96 * 1024 ? 1 : 0;
     return L;
 }
 

@@ -22,12 +22,13 @@ struct DecLayout {
     int64_t off_acc_f[2], off_acc_c[2];
     int64_t off_tone_u, off_tone_i;
     int64_t off_mag, off_order;
-    int64_t off_cand_f, off_cand_v, off_cand_first, off_cand_sum;
+    int64_t off_cand_f, off_cand_v, off_cand_first, off_cand_sum, off_contrib;
     int64_t bytes;      // per signal
     int32_t in_smem;
 };
 
-DecLayout make_dec_layout(int64_t acc_cap, int64_t b_max, int64_t budget_max);
+DecLayout make_dec_layout(int64_t acc_cap, int64_t b_max, int64_t budget_max,
+                          int64_t rounds_max);
 
 // K3..K7 (decode.cu).  out_f/out_c are [batch][k]; out_count [batch].
 void launch_decode(const DevPlan& plan, const DecLayout& lay, double2* d_y,

@@ -2,6 +2,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <cstdlib>
 #include <tuple>
 
 #include "engine.hpp"
@@ -106,7 +107,10 @@ Plan::Plan(int64_t n, int64_t k, int64_t l, double q, double delta, bool c128, i
         b_max_ = std::max(b_max_, ip.b);
         budget_max_ = std::max(budget_max_, ip.budget);
     }
-    lay_ = make_dec_layout(sched_.acc_cap, b_max_, budget_max_);
+    int64_t rounds_max = 0;
+    for (const auto& ip : sched_.iters)
+        rounds_max = std::max<int64_t>(rounds_max, static_cast<int64_t>(ip.taus.size()));
+    lay_ = make_dec_layout(sched_.acc_cap, b_max_, budget_max_, rounds_max);
     // Blocking streams: ordered after work on the legacy default stream, so
     // callers that pass no stream (e.g. torch default-stream producers) are safe.
     MSFFT_CUDA(cudaStreamCreateWithFlags(&own_stream_, cudaStreamDefault));
@@ -118,6 +122,12 @@ Plan::Plan(int64_t n, int64_t k, int64_t l, double q, double delta, bool c128, i
         MSFFT_CUDA(cudaEventCreateWithFlags(&ev_free_[i], cudaEventDisableTiming));
     }
     for (int i = 0; i < 4; ++i) MSFFT_CUDA(cudaEventCreate(&ev_stage_[i]));
+    int lo_prio = 0, hi_prio = 0;
+    MSFFT_CUDA(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
+    MSFFT_CUDA(cudaStreamCreateWithPriority(&dec_stream_, cudaStreamDefault, hi_prio));
+    MSFFT_CUDA(cudaEventCreateWithFlags(&ev_chunk_, cudaEventDisableTiming));
+    MSFFT_CUDA(cudaEventCreateWithFlags(&ev_dec_done_, cudaEventDisableTiming));
+    if (const char* e = std::getenv("MSFFT_OVERLAP_CHUNK")) overlap_chunk_ = std::atoll(e);
     flags_.reset(2);
 }
 
@@ -135,6 +145,9 @@ Plan::~Plan() {
     }
     for (int i = 0; i < 4; ++i)
         if (ev_stage_[i]) cudaEventDestroy(ev_stage_[i]);
+    if (dec_stream_) cudaStreamDestroy(dec_stream_);
+    if (ev_chunk_) cudaEventDestroy(ev_chunk_);
+    if (ev_dec_done_) cudaEventDestroy(ev_dec_done_);
     if (h_seeds_) cudaFreeHost(h_seeds_);
     cudaSetDevice(cur);
 }
@@ -195,8 +208,9 @@ const Plan::TaskSet& Plan::tasks_for(int64_t batch) {
     return tasks_.emplace(batch, std::move(ts)).first->second;
 }
 
-int64_t Plan::launches(int64_t /*batch*/, bool validate) const {
-    int64_t count = 3 + (validate ? 1 : 0);  // sigma + encode + decode (+ validate)
+int64_t Plan::launches(int64_t batch, bool validate) const {
+    // per (sub-)chunk: encode + bucket FFTs for b > 256 + decode
+    int64_t per_chunk = 2;
     for (int m : big_b_iters_) {
         int lb = dplan_.it[m].log2b;
         int64_t passes = 0, s0 = 0;
@@ -204,9 +218,12 @@ int64_t Plan::launches(int64_t /*batch*/, bool validate) const {
             s0 += (s0 == 0) ? std::min(lb, 11) : std::min<int64_t>(lb - s0, 7);
             ++passes;
         }
-        count += 1 + passes;  // bitrev + stage passes
+        per_chunk += 1 + passes;  // bitrev + stage passes
     }
-    return count;
+    const int64_t chunks =
+        (overlap_chunk_ > 0 && batch > overlap_chunk_) ? (batch + overlap_chunk_ - 1) / overlap_chunk_
+                                                       : 1;
+    return 1 + (validate ? 1 : 0) + chunks * per_chunk;  // + sigma (+ validate)
 }
 
 void Plan::run_chunk(int64_t batch, const void* d_x, int64_t x_stride, const int64_t* d_sig,
@@ -225,6 +242,37 @@ void Plan::run_chunk(int64_t batch, const void* d_x, int64_t x_stride, const int
             validate_kernel<float2><<<blocks, 256, 0, st>>>(
                 static_cast<const float2*>(d_x), n, x_stride, batch, flags_.get() + 1);
         MSFFT_LAUNCH_CHECK("validate_kernel");
+    }
+    const bool traced = opt.pre || opt.post || opt.sel_bucket;
+    if (!traced && !opt.stage_times && overlap_chunk_ > 0 && batch > overlap_chunk_) {
+        // Overlapped pipeline: the encode of sub-chunk c+1 (HBM-bound) runs
+        // while the decode of sub-chunk c (SM-bound) runs on a higher-priority
+        // stream; an event per sub-chunk orders decode after its encode.
+        const size_t elem = c128_ ? sizeof(double2) : sizeof(float2);
+        const int iters = sched_.iterations;
+        const int64_t k = sched_.k, vps = dplan_.values_per_signal;
+        for (int64_t c0 = 0; c0 < batch; c0 += overlap_chunk_) {
+            const int64_t cb = std::min(overlap_chunk_, batch - c0);
+            const TaskSet& tsc = tasks_for(cb);
+            const void* xc = static_cast<const unsigned char*>(d_x) + c0 * x_stride * elem;
+            double2* yc = y_.get() + c0 * vps;
+            launch_encode(dplan_, tsc.d.get(), tsc.count, xc, c128_, x_stride, cb,
+                          d_sig + c0 * iters, yc, enc_smem_, st);
+            for (int m : big_b_iters_) {
+                const DevIter& di = dplan_.it[m];
+                fft_radix2_batched(yc + di.yoff, di.b, cb * di.nrounds, di.nrounds, vps, -1,
+                                   dplan_.inv_n, st);
+            }
+            MSFFT_CUDA(cudaEventRecord(ev_chunk_, st));
+            MSFFT_CUDA(cudaStreamWaitEvent(dec_stream_, ev_chunk_, 0));
+            launch_decode(dplan_, lay_, yc, d_sig + c0 * iters, d_sig_inv + c0 * iters, cb,
+                          lay_.in_smem ? nullptr : dec_work_.get() + c0 * lay_.bytes,
+                          d_out_f + c0 * k, d_out_c + c0 * k, d_out_count + c0, flags_.get(),
+                          dec_stream_);
+        }
+        MSFFT_CUDA(cudaEventRecord(ev_dec_done_, dec_stream_));
+        MSFFT_CUDA(cudaStreamWaitEvent(st, ev_dec_done_, 0));
+        return;
     }
     const TaskSet& ts = tasks_for(batch);
     if (opt.stage_times) MSFFT_CUDA(cudaEventRecord(ev_stage_[0], st));

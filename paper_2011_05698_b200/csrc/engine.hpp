@@ -87,6 +87,9 @@ private:
     cudaEvent_t ev_start_ = nullptr, ev_end_ = nullptr;
     cudaEvent_t ev_copied_[2] = {nullptr, nullptr}, ev_free_[2] = {nullptr, nullptr};
     cudaEvent_t ev_stage_[4] = {nullptr, nullptr, nullptr, nullptr};
+    cudaStream_t dec_stream_ = nullptr;  // high-priority decode stream (overlap)
+    cudaEvent_t ev_chunk_ = nullptr, ev_dec_done_ = nullptr;
+    int64_t overlap_chunk_ = 0;          // signals per encode/decode sub-chunk (0 = serial)
     double stage_ms_[3] = {0, 0, 0};
 
     DeviceBuffer<double2> y_;
