@@ -59,6 +59,8 @@ def parse():
                     help="signals per CPU step (default: 2 per host thread)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: --batch signals per GPU; strong: --batch signals in total")
     return ap.parse_args()
 
 
@@ -201,8 +203,9 @@ def main():
     n, k, delta = 1 << args.log2n, args.k, 1e-6
     config = {"workload": f"C4: batch of N=2^{args.log2n}, K={k}, complex64, |c|=1, "
                           f"AWGN {args.snr:g} dB, per-signal seeds (BASELINE.json configs[3])",
-              "n": n, "k": k, "l": 16, "q": 1.0, "delta": delta, "per_gpu_batch": args.batch,
-              "global_batch": args.batch * world, "snr_db": args.snr,
+              "n": n, "k": k, "l": 16, "q": 1.0, "delta": delta, "per_gpu_batch": args.batch if args.scaling == "weak" else
+              -(-args.batch // world), "global_batch": args.batch * world
+              if args.scaling == "weak" else args.batch, "snr_db": args.snr,
               "parallelism": f"signal-sharded x{world} (no collective on the data path)",
               "l2_policy": "inputs (32 GiB/GPU) >> L2 (126 MB); no flush"}
 
@@ -219,13 +222,15 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
 
-    seeds = [signal_seed(SIG_BASE + (rank << 24), i) for i in range(args.batch)]
+    from paper_2011_05698_b200.dist import max_over_ranks, rank_seeds, sum_over_ranks
+    seeds = rank_seeds(SIG_BASE, args.batch, rank, world, args.scaling)
     aseeds = np.array([algo_seed(s) for s in seeds], dtype=np.uint64)
     x, _ = make_batch(n, k, seeds, args.snr, dev, "complex64")
     torch.cuda.synchronize()
 
     plan = M.Plan(n, k, M.MultiscaleConfig(16, 1.0), delta, "complex64", local)
-    B = args.batch
+    B = len(seeds)  # this rank's signals
+    total = sum_over_ranks(B, dev) if world > 1 else B
     out_f = torch.empty((B, k), dtype=torch.int64, device=dev)
     out_c = torch.empty((B, k), dtype=torch.complex128, device=dev)
     out_n = torch.empty((B,), dtype=torch.int64, device=dev)
@@ -259,10 +264,8 @@ def main():
     clk = clocks.stop()
     ms = ev0.elapsed_time(ev1) / args.steps
     if world > 1:
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms = float(t.item())
-    value = B * world / (ms / 1e3)
+        ms = max_over_ranks(ms, dev)
+    value = total / (ms / 1e3)
 
     # roofline of the dominant kernel (fused gather/encode)
     loads, sectors = plan.gather_traffic(aseeds)
@@ -291,12 +294,10 @@ def main():
             fh, ch, nh, _ = plan.execute(xh, aseeds)  # validates on the device, D2H results
         et = (time.perf_counter() - t0) / args.e2e_steps
         if world > 1:
-            t = torch.tensor([et], device=dev, dtype=torch.float64)
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            et = float(t.item())
-        e2e = {"value": B * world / et, "unit": "transforms/s",
-               "h2d_bytes_per_step": int(B * n * 8),
-               "d2h_bytes_per_step": int(B * k * (8 + 16) + B * 8),
+            et = max_over_ranks(et, dev)
+        e2e = {"value": total / et, "unit": "transforms/s",
+               "h2d_bytes_per_step": int(total * n * 8),
+               "d2h_bytes_per_step": int(total * k * (8 + 16) + total * 8),
                "ms_per_step": et * 1e3, "timing": "wall clock around msfft_execute (blocking)"}
         del xh
 
@@ -335,7 +336,8 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": "transforms/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c64->f64",
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
+        "dtype": "c64->f64",
         "data": "synthetic (seeded K-sparse spectra + AWGN, BASELINE.json configs[3] law)",
         "config": config,
         "roofline": {"bound": "hbm", "kernel": "encode_kernel (fused gather/window/fold/FFT)",
