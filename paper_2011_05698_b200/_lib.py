@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmsfft_b200.so")
+LIB_PATH = os.environ.get("MSFFT_B200_LIB") or os.path.join(HERE, "libmsfft_b200.so")
 
 MSFFT_OK, MSFFT_ERR_INVALID_ARGUMENT, MSFFT_ERR_DOMAIN, MSFFT_ERR_CUDA, MSFFT_ERR_RUNTIME = range(5)
 MSFFT_C128, MSFFT_C64 = 0, 1

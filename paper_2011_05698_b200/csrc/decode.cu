@@ -19,6 +19,10 @@
 #include "common.cuh"
 #include "encode.hpp"
 
+#ifndef MSFFT_DEC_MINB
+#define MSFFT_DEC_MINB 3  // 3 CTAs per SM: <= 85 registers, no spills
+#endif
+
 namespace msfft_b200 {
 
 namespace {
@@ -51,7 +55,7 @@ __device__ __forceinline__ double2 unit_root(int64_t n, double inv_n, int64_t e)
     return make_double2(c, s);
 }
 
-__global__ void __launch_bounds__(kDecThreads, 2)
+__global__ void __launch_bounds__(kDecThreads, MSFFT_DEC_MINB)
 decode_kernel(const __grid_constant__ DevPlan plan, DecLayout lay, double2* __restrict__ y,
               const int64_t* __restrict__ sigma, const int64_t* __restrict__ sigma_inv,
               int64_t batch, unsigned char* __restrict__ work, int64_t* __restrict__ out_f,
@@ -191,7 +195,10 @@ decode_kernel(const __grid_constant__ DevPlan plan, DecLayout lay, double2* __re
         // same number of stages and the shuffles stay convergent.
         const int64_t lcfg = plan.l;
         const double q = plan.q;
-        const int gsz = lcfg >= 32 ? 32 : (lcfg > 16 ? 32 : (lcfg > 8 ? 16 : (lcfg > 4 ? 8 : 4)));
+        // group size: enough lanes for the l blocks, shrunk (each lane then
+        // scans several blocks) until every ranked bucket fits in one pass
+        int gsz = lcfg > 16 ? 32 : (lcfg > 8 ? 16 : (lcfg > 4 ? 8 : 4));
+        while (gsz > 1 && kDecThreads / gsz < budget) gsz >>= 1;
         const int glane = lane & (gsz - 1);
         const int groups = kDecThreads / gsz;
         const int gid = tid / gsz;
