@@ -56,7 +56,10 @@ enum msfft_flags {
     MSFFT_FLAG_ASSUME_VALID = 1u << 0,
     /* Record CUDA events around each stage on the execution stream; read
      * them back with msfft_plan_stage_times. */
-    MSFFT_FLAG_STAGE_TIMES = 1u << 1
+    MSFFT_FLAG_STAGE_TIMES = 1u << 1,
+    /* Run the encode and the decode as separate launches instead of the
+     * persistent fused kernel (diagnostics: per-kernel rooflines). */
+    MSFFT_FLAG_SERIAL = 1u << 2
 };
 
 /* TransformStats (proj/include/msfft/sfft4.hpp:32-40). */

@@ -211,8 +211,10 @@ class Plan:
         self._lib.msfft_plan_stats(self._h, C.byref(s))
         return TransformStats._from(s)
 
-    def launches(self, batch: int, assume_valid: bool = False) -> int:
+    def launches(self, batch: int, assume_valid: bool = False, serial: bool = False) -> int:
         flags = _L.MSFFT_FLAG_ASSUME_VALID if assume_valid else 0
+        if serial:
+            flags |= _L.MSFFT_FLAG_SERIAL
         return int(self._lib.msfft_plan_launches(self._h, int(batch), flags))
 
     def gather_traffic(self, seeds):
@@ -233,7 +235,7 @@ class Plan:
         return [float(v) for v in ms]
 
     def execute(self, x, seeds, out=None, assume_valid: bool = False, stream=None,
-                stage_times: bool = False):
+                stage_times: bool = False, serial: bool = False):
         """x: (batch, n) complex array/tensor (host or CUDA).  seeds: batch
         integers.  out: optional (f, c, count) preallocated outputs -- torch
         CUDA tensors (int64 [B,k], complex128 [B,k], int64 [B]) keep the
@@ -264,6 +266,8 @@ class Plan:
         ms = C.c_double()
         err = C.create_string_buffer(1024)
         flags = _L.MSFFT_FLAG_ASSUME_VALID if assume_valid else 0
+        if serial:
+            flags |= _L.MSFFT_FLAG_SERIAL
         if stage_times:
             flags |= _L.MSFFT_FLAG_STAGE_TIMES
         status = self._lib.msfft_execute(

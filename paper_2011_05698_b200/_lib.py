@@ -16,6 +16,7 @@ MSFFT_C128, MSFFT_C64 = 0, 1
 MSFFT_HOST, MSFFT_DEVICE = 0, 1
 MSFFT_FLAG_ASSUME_VALID = 1
 MSFFT_FLAG_STAGE_TIMES = 2
+MSFFT_FLAG_SERIAL = 4
 MAX_ITERATIONS = 64
 
 # Every symbol include/msfft_b200.h declares.

@@ -177,7 +177,8 @@ int msfft_plan_stats(msfft_plan plan, msfft_stats* stats) {
 
 int64_t msfft_plan_launches(msfft_plan plan, int64_t batch, uint32_t flags) {
     if (!plan) return -1;
-    return plan->plan->launches(batch, !(flags & MSFFT_FLAG_ASSUME_VALID));
+    return plan->plan->launches(batch, !(flags & MSFFT_FLAG_ASSUME_VALID),
+                                (flags & MSFFT_FLAG_SERIAL) != 0);
 }
 
 int msfft_execute(msfft_plan plan, int64_t batch, const void* x, int64_t x_stride,
@@ -192,6 +193,7 @@ int msfft_execute(msfft_plan plan, int64_t batch, const void* x, int64_t x_strid
         opt.out_on_device = out_location == MSFFT_DEVICE;
         opt.assume_valid = (flags & MSFFT_FLAG_ASSUME_VALID) != 0;
         opt.stage_times = (flags & MSFFT_FLAG_STAGE_TIMES) != 0;
+        opt.force_serial = (flags & MSFFT_FLAG_SERIAL) != 0;
         opt.stream = static_cast<cudaStream_t>(stream);
         plan->plan->execute(batch, x, x_stride, seeds, out_f, out_c, out_count, opt, device_ms);
     });

@@ -1,0 +1,560 @@
+// decode_body.cuh -- K3..K7 for one signal with the whole CTA: the
+// sequential part of sfft4 over the bucket vectors produced by the encode.
+// Shared by decode_kernel (one signal per CTA) and fused_kernel.
+//   for every iteration m (proj/src/sfft4.cpp:38-113):
+//     K3  subtract the prediction of the tones already found
+//         (predict_buckets + subtract, proj/src/bucketize.cpp:70-104);
+//     K4  stable order of buckets by |y0| desc, budget, 0.2*kth threshold
+//         (sfft4.cpp:75-91);
+//     K5  multiscale location, a lane group per selected bucket, lanes = the
+//         l candidate blocks (locate_frequency / locate_step,
+//         proj/src/locate.cpp:63-123);
+//     K6  estimate y0/G, |G| < 0.5 reject, f = sigma^-1 u, per-iteration
+//         found map, accumulate (sfft4.cpp:27-36, 92-105);
+//   K7  keep the K largest (stable by |c| desc over ascending f), output in
+//       ascending f (sfft4.cpp:170-178).
+// Compiled with --fmad=false; every decision reads FP64 values computed with
+// the reference's operation order.  G comes from the window's device table.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "encode.hpp"
+#include "plan_dev.cuh"
+
+namespace msfft_b200 {
+namespace {
+
+struct DecShared {
+    int acc_n, new_n, cur;
+    double thr;
+};
+
+struct DecArgs {
+    double2* y;
+    const int64_t* sigma;
+    const int64_t* sigma_inv;
+    int64_t* out_f;
+    double2* out_c;
+    int64_t* out_count;
+    int32_t* err;
+    int64_t* tr_bucket;
+    int64_t* tr_f;
+    double2* tr_v;
+    // fused kernel only: before iteration m, wait until gate_done[m] reaches
+    // gate_need[m] (encode tasks of this signal's chunk and iteration m)
+    const int32_t* gate_done;
+    const int32_t* gate_need;
+};
+
+__device__ __forceinline__ int32_t load_acquire(const int32_t* p) {
+    int32_t v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+struct Scratch {
+    int64_t* acc_f[2];
+    double2* acc_c[2];
+    int64_t* tone_u;
+    int64_t* tone_i;
+    double* mag;
+    int32_t* order;
+    int64_t* cand_f;
+    double2* cand_v;
+    int32_t* cand_first;
+    double2* cand_sum;
+    double2* contrib;  // [tone][round][3] predicted contributions
+    int32_t* bstart;   // [b + 1] per-bucket list offsets
+    int32_t* blist;    // [acc] tone indices grouped by bucket
+    double2* gc;       // [acc][3] G * c per tone and bucket offset
+    double* phi;       // [budget][stages] phase of y0 / y_tau
+    int32_t* pcode;    // [budget][stages] 0 ok, 1 y_tau == 0, 2 quotient == 0
+};
+
+__device__ __forceinline__ double ghat_at(const DevIter& it, int64_t d) {
+    return it.ghat[d + it.gmax];
+}
+
+// unit_root (proj/src/bucketize.cpp:12-18): e^{-2 pi i (e mod n)/n}; the
+// division by the power of two n is an exact multiplication by 1/n.
+__device__ __forceinline__ double2 unit_root(int64_t n, double inv_n, int64_t e) {
+    e &= (n - 1);
+    const double a = -kTwoPi * static_cast<double>(e) * inv_n;
+    double s, c;
+    sincos(a, &s, &c);
+    return make_double2(c, s);
+}
+
+// Decodes signal s; base = this signal's scratch (shared or global memory).
+__device__ __forceinline__ void decode_signal(const DevPlan& plan, const DecLayout& lay,
+                                           const DecArgs& A, int64_t s, unsigned char* base,
+                                           DecShared& sh) {
+    constexpr int kThreads = kDecThreads;
+    const int tid = threadIdx.x;
+    const int lane = tid & 31;
+
+    Scratch S;
+    for (int p = 0; p < 2; ++p) {
+        S.acc_f[p] = reinterpret_cast<int64_t*>(base + lay.off_acc_f[p]);
+        S.acc_c[p] = reinterpret_cast<double2*>(base + lay.off_acc_c[p]);
+    }
+    S.tone_u = reinterpret_cast<int64_t*>(base + lay.off_tone_u);
+    S.tone_i = reinterpret_cast<int64_t*>(base + lay.off_tone_i);
+    S.mag = reinterpret_cast<double*>(base + lay.off_mag);
+    S.order = reinterpret_cast<int32_t*>(base + lay.off_order);
+    S.cand_f = reinterpret_cast<int64_t*>(base + lay.off_cand_f);
+    S.cand_v = reinterpret_cast<double2*>(base + lay.off_cand_v);
+    S.cand_first = reinterpret_cast<int32_t*>(base + lay.off_cand_first);
+    S.cand_sum = reinterpret_cast<double2*>(base + lay.off_cand_sum);
+    S.contrib = reinterpret_cast<double2*>(base + lay.off_contrib);
+    S.bstart = reinterpret_cast<int32_t*>(base + lay.off_bstart);
+    S.blist = reinterpret_cast<int32_t*>(base + lay.off_blist);
+    S.gc = reinterpret_cast<double2*>(base + lay.off_gc);
+    S.phi = reinterpret_cast<double*>(base + lay.off_phi);
+    S.pcode = reinterpret_cast<int32_t*>(base + lay.off_pcode);
+
+    if (tid == 0) {
+        sh.acc_n = 0;
+        sh.cur = 0;
+    }
+    __syncthreads();
+
+    const int64_t n = plan.n;
+    const int64_t nmask = n - 1;
+    const double inv_n = plan.inv_n;
+    double2* ysig = A.y + s * plan.values_per_signal;
+
+    int64_t sel_off = 0;  // trace offset: sum of earlier budgets
+#ifdef MSFFT_DECODE_PROFILE
+    long long prof_t[16];
+#define DEC_MARK(id) do { if (tid == 0) prof_t[id] = clock64(); } while (0)
+#else
+#define DEC_MARK(id) do { } while (0)
+#endif
+    for (int m = 0; m < plan.iters; ++m) {
+        DEC_MARK(0);
+        if (A.gate_done) {  // fused: iteration m's buckets must be encoded
+            if (threadIdx.x == 0) {
+                while (load_acquire(&A.gate_done[m]) < A.gate_need[m]) __nanosleep(64);
+                __threadfence();
+            }
+            __syncthreads();
+        }
+        const DevIter& it = plan.it[m];
+        const int64_t b = it.b, L = it.l_width;
+        const double Ld = static_cast<double>(L);
+        const double invL = 1.0 / Ld;  // exact: L is a power of two
+        const int nr = it.nrounds;
+        const int64_t* taus = plan.taus + it.tau_off;
+        double2* Y = ysig + it.yoff;
+        const int64_t sg = A.sigma[s * plan.iters + m];
+        const int64_t sgi = A.sigma_inv[s * plan.iters + m];
+        const int acc_n = sh.acc_n;
+        const int cur = sh.cur;
+        const int64_t* AF = cur ? S.acc_f[1] : S.acc_f[0];
+        const double2* AC = cur ? S.acc_c[1] : S.acc_c[0];
+
+        // ---- K3: subtract the prediction of everything already known.
+        // predict_buckets (bucketize.cpp:84-93) adds, per known tone in
+        // ascending f, (G_{jL-u} * c) * e^{-2 pi i tau u/n} into buckets
+        // j = i-1, i, i+1.  Step 1 evaluates each (tone, round) rotation and
+        // its three contributions once; step 2 sums, per (round, bucket), the
+        // contributions in ascending tone order -- the reference's order.
+        if (acc_n > 0) {
+            for (int j = tid; j < acc_n; j += kThreads) {
+                const int64_t u = (sg * AF[j]) & nmask;
+                const int64_t i = static_cast<int64_t>(floor(static_cast<double>(u) * invL + 0.5));
+                S.tone_u[j] = u;
+                S.tone_i[j] = i;
+                // G_{jL-u} * c for the three buckets: independent of the round
+                const double2 c = AC[j];
+#pragma unroll
+                for (int d = 0; d < 3; ++d) {
+                    const double g = ghat_at(it, (i - 1 + d) * L - u);
+                    S.gc[j * 3 + d] = make_double2(g * c.x, g * c.y);
+                }
+            }
+            __syncthreads();
+            DEC_MARK(1);
+            for (int e = tid; e < acc_n * nr; e += kThreads) {
+                const int j = e / nr, r = e - j * nr;
+                const double2 rot = unit_root(n, inv_n, taus[r] * S.tone_u[j]);
+                double2* dst = S.contrib + static_cast<int64_t>(e) * 3;
+#pragma unroll
+                for (int d = 0; d < 3; ++d) dst[d] = cmul(S.gc[j * 3 + d], rot);
+            }
+            // per-bucket tone lists (ascending tone index = ascending f),
+            // built by warp 0 while the other warps evaluate contributions:
+            // counts, a scan, then a stable fill; lanes of a 32-tone chunk
+            // that share a bucket are ranked with __match_any_sync.
+            if (tid < 32) {
+                int32_t* cnt = S.order;  // free until K4
+                for (int64_t bk = tid; bk < b; bk += 32) cnt[bk] = 0;
+                __syncwarp();
+                for (int j0 = 0; j0 < acc_n; j0 += 32) {
+                    const int j = j0 + tid;
+                    const int bk = j < acc_n ? static_cast<int>(S.tone_i[j] & (b - 1)) : -1;
+                    const unsigned grp = __match_any_sync(0xffffffffu, bk);
+                    if (bk >= 0 && (grp & ((1u << tid) - 1u)) == 0) cnt[bk] += __popc(grp);
+                    __syncwarp();
+                }
+                int carry = 0;  // exclusive scan -> bstart, cnt becomes the fill cursor
+                for (int64_t base0 = 0; base0 < b; base0 += 32) {
+                    const int64_t idx = base0 + tid;
+                    const int c0 = idx < b ? cnt[idx] : 0;
+                    int v = c0;
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const int w = __shfl_up_sync(0xffffffffu, v, o);
+                        if (tid >= o) v += w;
+                    }
+                    if (idx < b) {
+                        S.bstart[idx] = carry + v - c0;
+                        cnt[idx] = carry + v - c0;
+                    }
+                    carry += __shfl_sync(0xffffffffu, v, 31);
+                }
+                if (tid == 0) S.bstart[b] = carry;
+                __syncwarp();
+                for (int j0 = 0; j0 < acc_n; j0 += 32) {
+                    const int j = j0 + tid;
+                    const int bk = j < acc_n ? static_cast<int>(S.tone_i[j] & (b - 1)) : -1;
+                    const unsigned grp = __match_any_sync(0xffffffffu, bk);
+                    if (bk >= 0) {
+                        const int pos = cnt[bk] + __popc(grp & ((1u << tid) - 1u));
+                        S.blist[pos] = j;
+                    }
+                    __syncwarp();
+                    if (bk >= 0 && (grp & ((1u << tid) - 1u)) == 0) cnt[bk] += __popc(grp);
+                    __syncwarp();
+                }
+            }
+            __syncthreads();
+            DEC_MARK(2);
+            // bucket beta collects, in ascending tone order, the tones whose
+            // own bucket is beta+1 (offset jj = i-1), beta (jj = i) and
+            // beta-1 (jj = i+1): a three-way merge of the sorted lists.
+            const int64_t total = static_cast<int64_t>(nr) * b;
+            for (int64_t e = tid; e < total; e += kThreads) {
+                const int r = static_cast<int>(e / b);
+                const int64_t beta = e - r * b;
+                int p[3], q3[3];
+#pragma unroll
+                for (int d = 0; d < 3; ++d) {
+                    const int64_t bk = (beta + 1 - d) & (b - 1);
+                    p[d] = S.bstart[bk];
+                    q3[d] = S.bstart[bk + 1];
+                }
+                double2 pred = make_double2(0.0, 0.0);
+                bool any = false;
+                for (;;) {
+                    int best = -1, bj = 0x7fffffff;
+#pragma unroll
+                    for (int d = 0; d < 3; ++d)
+                        if (p[d] < q3[d] && S.blist[p[d]] < bj) {
+                            bj = S.blist[p[d]];
+                            best = d;
+                        }
+                    if (best < 0) break;
+                    ++p[best];
+                    const double2 v = S.contrib[(static_cast<int64_t>(bj) * nr + r) * 3 + best];
+                    pred.x += v.x;
+                    pred.y += v.y;
+                    any = true;
+                }
+                if (any) {
+                    const double2 o = Y[e];
+                    Y[e] = make_double2(o.x - pred.x, o.y - pred.y);
+                }
+            }
+            __syncthreads();
+            DEC_MARK(3);
+        }
+
+        // ---- K4: stable descending order of |y0|, budget and threshold
+        for (int64_t j = tid; j < b; j += kThreads) {
+            const double2 v = Y[j];
+            const double mg = cabs_ref(v.x, v.y);
+            S.mag[j] = mg == mg ? mg : -1.0;  // NaN (unvalidated input) ranks last
+        }
+        __syncthreads();
+        DEC_MARK(4);
+        for (int64_t j = tid; j < b; j += kThreads) {
+            const double mj = S.mag[j];
+            int64_t rank = 0;
+            for (int64_t i = 0; i < b; ++i) {
+                const double mi = S.mag[i];
+                rank += (mi > mj) || (mi == mj && i < j);
+            }
+            S.order[rank] = static_cast<int32_t>(j);
+        }
+        __syncthreads();
+        DEC_MARK(5);
+        const int64_t budget = it.budget;
+        if (tid == 0) sh.thr = 0.2 * S.mag[S.order[budget - 1]];
+        __syncthreads();
+        DEC_MARK(6);
+        const double thr = sh.thr;
+        // every ranked bucket's round values, staged in shared memory in one
+        // pass (the contribution area is free after K3): the locate stages
+        // then never wait on L2
+        double2* yr = S.contrib;
+        for (int64_t e = tid; e < budget * nr; e += kThreads) {
+            const int64_t rk = e / nr, st = e - rk * nr;
+            yr[e] = Y[st * b + S.order[rk]];
+        }
+        __syncthreads();
+        DEC_MARK(11);
+        // phase_of(y0 / y_tau) (locate.cpp:110) depends only on the bucket
+        // values, not on the narrowing region, so every (rank, stage) pair is
+        // evaluated at once here; the stage chain below only scans blocks.
+        // pcode: 0 ok, 1 y_tau == 0 (nullopt), 2 quotient == 0 (phase_of throws)
+        const int ns = nr - 1;
+        for (int64_t e = tid; e < budget * ns; e += kThreads) {
+            const int64_t rk = e / ns, st = e - rk * ns + 1;
+            const double2 y0e = yr[rk * nr], yt = yr[rk * nr + st];
+            int code = 0;
+            double ph = 0.0;
+            if (yt.x == 0.0 && yt.y == 0.0) {
+                code = 1;
+            } else {
+                const double2 z = cdiv_ref(y0e.x, y0e.y, yt.x, yt.y);
+                if (z.x == 0.0 && z.y == 0.0) code = 2;
+                ph = atan2(z.y, z.x);
+                if (ph < 0.0) ph += kTwoPi;
+                ph = ph + 0.0;
+            }
+            S.phi[e] = ph;
+            S.pcode[e] = code;
+        }
+        __syncthreads();
+        DEC_MARK(12);
+
+        // ---- K5 + K6: locate and estimate.  A group of `gsz` lanes takes one
+        // ranked bucket; the region length evolves identically for every
+        // bucket, so all groups run the same number of stages and the
+        // shuffles stay convergent.
+        const int64_t lcfg = plan.l;
+        const double q = plan.q;
+        // group size: enough lanes for the l blocks, shrunk (each lane then
+        // scans several blocks) until every ranked bucket fits in one pass
+        int gsz = lcfg > 16 ? 32 : (lcfg > 8 ? 16 : (lcfg > 4 ? 8 : 4));
+        while (gsz > 1 && kThreads / gsz < budget) gsz >>= 1;
+        const int glane = lane & (gsz - 1);
+        const int groups = kThreads / gsz;
+        const int gid = tid / gsz;
+        const int64_t rounds_up = (budget + groups - 1) / groups * groups;
+        const int first_gid_of_warp = (tid & ~31) / gsz;
+        for (int64_t rank = gid; rank < rounds_up; rank += groups) {
+            // a warp whose groups are all past the budget has nothing to
+            // locate (warp-uniform, so no shuffle loses a participant)
+            if (rank - (gid - first_gid_of_warp) >= budget) continue;
+            const bool live = rank < budget;
+            const int64_t beta = live ? S.order[rank] : 0;
+            int64_t f_out = -1;
+            double2 v_out = make_double2(0.0, 0.0);
+            const double2 y0 = live ? yr[rank * nr] : make_double2(0.0, 0.0);
+            bool ok = live && S.mag[beta] > thr;
+            if (ok && y0.x == 0.0 && y0.y == 0.0) ok = false;
+            double u_min = (2.0 * static_cast<double>(beta) - 1.0) * Ld / 2.0;
+            double len = Ld;
+            int stage = 0;
+            const int nst = it.nstage_tab;  // host-precomputed stage lengths (or -1)
+            while (nst >= 0 ? stage < nst : len > 1.0 + 1e-9) {
+                ++stage;
+                if (stage >= nr) {  // cannot happen for sfft4's own tau plans
+                    if (ok && glane == 0) atomicCAS(A.err, 0, kDecErrRounds);
+                    ok = false;
+                    break;  // uniform: every group sees the same stage count
+                }
+                double phi = 0.0;
+                if (ok) {
+                    const int64_t pe = rank * ns + (stage - 1);
+                    const int code = S.pcode[pe];
+                    if (code == 1) {
+                        ok = false;  // locate_frequency returns nullopt
+                    } else {
+                        if (code == 2) {  // phase_of throws
+                            if (glane == 0) atomicCAS(A.err, 0, kDecErrPhaseZero);
+                            ok = false;
+                        }
+                        phi = S.phi[pe];
+                    }
+                }
+                const int64_t tau = taus[stage];
+                const double rblk =
+                    nst >= 0 ? it.stage_blk[stage - 1] : len / static_cast<double>(lcfg);
+                double best_d = INFINITY;
+                int best_j = 0x7fffffff;
+                for (int64_t j = glane; j < lcfg; j += gsz) {
+                    const double center = u_min + (static_cast<double>(j) + 0.5) * rblk;
+                    const double d = circular_phase_distance(
+                        position_phase(center, tau, n, inv_n), phi);
+                    if (d < best_d) {
+                        best_d = d;
+                        best_j = static_cast<int>(j);
+                    }
+                }
+                // lowest block index wins ties (strict < in ascending order)
+                for (int o = gsz >> 1; o > 0; o >>= 1) {
+                    const double od = __shfl_xor_sync(0xffffffffu, best_d, o);
+                    const int oj = __shfl_xor_sync(0xffffffffu, best_j, o);
+                    if (od < best_d || (od == best_d && oj < best_j)) {
+                        best_d = od;
+                        best_j = oj;
+                    }
+                }
+                if (best_j == 0x7fffffff) best_j = 0;  // all distances NaN: reference keeps 0
+                u_min = u_min + (static_cast<double>(best_j) - q / 2.0) * rblk;
+                len = nst >= 0 ? it.stage_len[stage] : len * (q + 1.0) / static_cast<double>(lcfg);
+            }
+            if (ok) {
+                const double lo = u_min, hi = u_min + len;
+                int64_t u = static_cast<int64_t>(ceil(lo));
+                if (!(static_cast<double>(u) < hi)) u = llround(0.5 * (lo + hi));
+                u %= n;
+                if (u < 0) u += n;
+                const int64_t i = static_cast<int64_t>(floor(static_cast<double>(u) * invL + 0.5));
+                const double g = ghat_at(it, i * L - u);
+                if (!(fabs(g) < 0.5)) {
+                    v_out = make_double2(y0.x / g, y0.y / g);
+                    f_out = (sgi * u) & nmask;
+                }
+            }
+            if (live && glane == 0) {
+                S.cand_f[rank] = f_out;
+                S.cand_v[rank] = v_out;
+                if (A.tr_bucket) {
+                    A.tr_bucket[sel_off + rank] = beta;
+                    A.tr_f[sel_off + rank] = f_out;
+                    A.tr_v[sel_off + rank] = v_out;
+                }
+            }
+        }
+        __syncthreads();
+        DEC_MARK(7);
+
+        // ---- K6 (merge): found[f] = 0 + v_r1 + v_r2 + ... in rank order
+        // (std::map operator[] then +=), then acc[f] += found[f].  The first
+        // accepted rank of each f carries the sum; the found set is merged
+        // into the ascending acc list (ping-pong buffers).
+        const int nxt = cur ^ 1;
+        int64_t* NF = nxt ? S.acc_f[1] : S.acc_f[0];
+        double2* NC = nxt ? S.acc_c[1] : S.acc_c[0];
+        if (tid == 0) sh.new_n = 0;
+        // cand_first[r]: 0 = not the first accepted rank of its f,
+        // 1 = first and f is new, 2 = first and f already accumulated.
+        for (int64_t r = tid; r < budget; r += kThreads) {
+            const int64_t fr = S.cand_f[r];
+            int first = fr >= 0;
+            for (int64_t r2 = 0; first && r2 < r; ++r2) first = S.cand_f[r2] != fr;
+            if (first) {
+                double2 sum = make_double2(0.0, 0.0);
+                for (int64_t r2 = r; r2 < budget; ++r2)
+                    if (S.cand_f[r2] == fr) {
+                        sum.x += S.cand_v[r2].x;
+                        sum.y += S.cand_v[r2].y;
+                    }
+                S.cand_sum[r] = sum;
+                int lo = 0, hi = acc_n;
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (AF[mid] < fr) lo = mid + 1; else hi = mid;
+                }
+                if (lo < acc_n && AF[lo] == fr) first = 2;
+            }
+            S.cand_first[r] = first;
+        }
+        __syncthreads();
+        DEC_MARK(8);
+        // acc entries move up by the number of NEW found f below them
+        for (int j = tid; j < acc_n; j += kThreads) {
+            const int64_t fj = AF[j];
+            int64_t before = 0;
+            int64_t hit = -1;
+            for (int64_t r = 0; r < budget; ++r) {
+                const int cf = S.cand_first[r];
+                if (!cf) continue;
+                const int64_t fr = S.cand_f[r];
+                if (cf == 1 && fr < fj) ++before;
+                if (cf == 2 && fr == fj) hit = r;
+            }
+            double2 c = AC[j];
+            if (hit >= 0) c = make_double2(c.x + S.cand_sum[hit].x, c.y + S.cand_sum[hit].y);
+            NF[j + before] = fj;
+            NC[j + before] = c;
+        }
+        // new f: insert at #{acc f < f} + #{new found f < f}
+        for (int64_t r = tid; r < budget; r += kThreads) {
+            if (S.cand_first[r] != 1) continue;
+            const int64_t fr = S.cand_f[r];
+            int lo = 0, hi = acc_n;
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (AF[mid] < fr) lo = mid + 1; else hi = mid;
+            }
+            int64_t ubefore = 0;
+            for (int64_t r3 = 0; r3 < budget; ++r3)
+                ubefore += S.cand_first[r3] == 1 && S.cand_f[r3] < fr;
+            const int64_t pos = lo + ubefore;
+            const double2 sum = S.cand_sum[r];
+            NF[pos] = fr;
+            NC[pos] = make_double2(0.0 + sum.x, 0.0 + sum.y);
+            atomicAdd(&sh.new_n, 1);
+        }
+        __syncthreads();
+        DEC_MARK(9);
+        if (tid == 0) {
+            sh.acc_n = acc_n + sh.new_n;
+            sh.cur = nxt;
+        }
+        sel_off += budget;
+        __syncthreads();
+        DEC_MARK(10);
+#ifdef MSFFT_DECODE_PROFILE
+        if (tid == 0 && s < 2)
+            printf("DECPROF s=%lld m=%d acc=%d b=%lld budget=%lld | K3 %lld %lld %lld | K4 %lld %lld %lld | K5 %lld %lld %lld | K6 %lld %lld %lld\n",
+                   (long long)s, m, acc_n, (long long)b, (long long)budget,
+                   acc_n ? prof_t[1] - prof_t[0] : 0LL, acc_n ? prof_t[2] - prof_t[1] : 0LL,
+                   acc_n ? prof_t[3] - prof_t[2] : 0LL,
+                   prof_t[4] - (acc_n ? prof_t[3] : prof_t[0]), prof_t[5] - prof_t[4],
+                   prof_t[6] - prof_t[5], prof_t[11] - prof_t[6], prof_t[12] - prof_t[11], prof_t[7] - prof_t[12], prof_t[8] - prof_t[7],
+                   prof_t[9] - prof_t[8], prof_t[10] - prof_t[9]);
+#endif
+    }
+
+    // ---- K7: keep the K largest |c| (stable over ascending f), emit in f order
+    const int acc_n = sh.acc_n;
+    const int cur = sh.cur;
+    const int64_t* AF = cur ? S.acc_f[1] : S.acc_f[0];
+    const double2* AC = cur ? S.acc_c[1] : S.acc_c[0];
+    const int64_t K = plan.k;
+    for (int j = tid; j < acc_n; j += kThreads) {
+        const double2 c = AC[j];
+        const double mg = cabs_ref(c.x, c.y);
+        S.mag[j] = mg == mg ? mg : -1.0;
+    }
+    __syncthreads();
+    for (int j = tid; j < acc_n; j += kThreads) {
+        const double mj = S.mag[j];
+        int64_t rank = 0;
+        for (int i = 0; i < acc_n; ++i) {
+            const double mi = S.mag[i];
+            rank += (mi > mj) || (mi == mj && i < j);
+        }
+        S.tone_i[j] = rank < K ? 1 : 0;
+    }
+    __syncthreads();
+    for (int j = tid; j < acc_n; j += kThreads) {
+        if (!S.tone_i[j]) continue;
+        int64_t pos = 0;
+        for (int i = 0; i < j; ++i) pos += S.tone_i[i];
+        A.out_f[s * K + pos] = AF[j];
+        A.out_c[s * K + pos] = AC[j];
+    }
+    if (tid == 0) A.out_count[s] = acc_n < K ? acc_n : K;
+}
+
+}  // namespace
+}  // namespace msfft_b200

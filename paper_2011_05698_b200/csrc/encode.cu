@@ -1,42 +1,14 @@
-// encode.cu -- K1+K2: fused multi-round gather / flat window / bucket fold /
-// b-point FFT for every round of every iteration of a whole batch in ONE
-// launch.  Compiled with --fmad=false.
-//
-// Reference semantics (bucketize_fn, proj/include/msfft/bucketize.hpp:63-86),
-// per round (sigma, tau):
-//     for t = -h..h:  fold[t mod b] += g[h+t] * x[sigma*(t - tau) mod n]
-//     values = FFT_b(fold) / n
-// Rewritten in t' = t - tau: round r reads x[sigma*t'] for t' in
-// [-h - tau_r, h - tau_r].  All rounds of one iteration share sigma, so a
-// sample needed by several rounds is loaded ONCE: a thread owns the residue
-// class t' = c (mod b), walks the union of the rounds' intervals in
-// increasing t', and for each covering round r adds g[h + t' + tau_r] * x into
-// that round's accumulator, which is bin (c + tau_r) mod b.  Each (round,
-// bin) therefore accumulates exactly the reference's terms in exactly the
-// reference's order (increasing t), without FMA: the folds are bit-identical
-// to the CPU's.  The b-point transform is the reference's radix-2 DIT in
-// shared memory, again bit-identical.
-//
-// Work split: a CTA (256 threads) takes one iteration m, a chunk of <= 8
-// rounds, and either 256/b whole signals (b <= 256: fused FFT epilogue) or a
-// 256-lane slice of one signal (b > 256: folds go to HBM and the batched FFT
-// in fft.cu finishes them).  The iteration's window taps are staged into
-// shared memory with one TMA bulk copy (cp.async.bulk + mbarrier).
+// encode.cu -- K1+K2 as a standalone launch: one encode task per CTA (the
+// task list covers every round of every iteration of the whole batch).
+// The task body is encode_body.cuh.  Compiled with --fmad=false.
 #include <cuda_runtime.h>
 
-#include "common.cuh"
 #include "encode.hpp"
+#include "encode_body.cuh"
 
 namespace msfft_b200 {
 
 namespace {
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ float2 ld_sample(const float2* p) { return __ldcs(p); }
-__device__ __forceinline__ double2 ld_sample(const double2* p) { return __ldcs(p); }
 
 template <class T>
 __global__ void __launch_bounds__(kEncThreads, 2)
@@ -45,164 +17,9 @@ encode_kernel(const __grid_constant__ DevPlan plan, const EncTask* __restrict__ 
               const int64_t* __restrict__ sigma, double2* __restrict__ y) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ __align__(8) uint64_t bar;
-
-    const EncTask& task = tasks[blockIdx.x];
-    const DevIter& it = plan.it[task.m];
-    const int tid = threadIdx.x;
-    const int64_t b = it.b;
-    const int log2b = it.log2b;
-    const int nr = task.nr;
-    const int64_t h = it.h;
-    const uint32_t wu = static_cast<uint32_t>(it.w);
-    const int64_t* taus = plan.taus + it.tau_off + task.r0;
-
-    // ---- stage the window taps: one TMA bulk copy, completion on an mbarrier
-    const double* taps = it.taps;
-    if (it.taps_in_smem) {
-        double* staps = reinterpret_cast<double*>(smem_raw);
-        const uint32_t bytes = static_cast<uint32_t>((it.w + 1) * sizeof(double));
-        if (tid == 0) {
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
-            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        }
-        __syncthreads();
-        if (tid == 0) {
-            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
-                         ::"r"(smem_u32(&bar)), "r"(bytes) : "memory");
-            const uint32_t chunk = 32768;
-            for (uint32_t off = 0; off < bytes; off += chunk) {
-                const uint32_t len = bytes - off < chunk ? bytes - off : chunk;
-                asm volatile(
-                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes "
-                    "[%0], [%1], %2, [%3];"
-                    ::"r"(smem_u32(smem_raw + off)),
-                    "l"(reinterpret_cast<const unsigned char*>(it.taps) + off), "r"(len),
-                    "r"(smem_u32(&bar))
-                    : "memory");
-            }
-        }
-        asm volatile(
-            "{\n .reg .pred p;\n WAIT_%=:\n"
-            " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n"
-            " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(&bar))
-            : "memory");
-        taps = staps;
-    }
-
-    // ---- thread -> (signal, residue class)
-    int sl, c;
-    if (task.fused) {
-        sl = tid >> log2b;
-        c = tid & static_cast<int>(b - 1);
-    } else {
-        sl = 0;
-        c = task.lane0 + tid;
-    }
-    const int64_t s = task.sig0 + sl;
-    const bool active = sl < task.nsig && s < batch;
-
-    double2 acc[kEncRounds];
-#pragma unroll
-    for (int r = 0; r < kEncRounds; ++r) acc[r] = make_double2(0.0, 0.0);
-
-    if (active) {
-        const uint32_t sg = static_cast<uint32_t>(sigma[s * plan.iters + task.m]);
-        const uint32_t mask = static_cast<uint32_t>(plan.n - 1);
-        const T* xs = x + s * x_stride;
-        uint32_t th[kEncRounds];  // tau_r + h: tap index = t' + tau_r + h (mod 2^32)
-#pragma unroll
-        for (int r = 0; r < kEncRounds; ++r)
-            th[r] = r < nr ? static_cast<uint32_t>(taus[r] + h) : 0u;
-        const int32_t bm = static_cast<int32_t>(b - 1);
-        for (int sgi = 0; sgi < task.nseg; ++sgi) {
-            const int32_t A = task.seg_lo[sgi], B = task.seg_hi[sgi];
-            int64_t t = A + ((c - A) & bm);
-            constexpr int U = 8;
-            const int64_t stride = b;
-            for (; t <= B; t += U * stride) {
-                T v[U];
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const int64_t tt = t + u * stride;
-                    if (tt <= B) v[u] = ld_sample(xs + ((sg * static_cast<uint32_t>(tt)) & mask));
-                }
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const int64_t tt = t + u * stride;
-                    if (tt <= B) {
-                        const double xr = static_cast<double>(v[u].x);
-                        const double xi = static_cast<double>(v[u].y);
-#pragma unroll
-                        for (int r = 0; r < kEncRounds; ++r) {
-                            if (r < nr) {
-                                const uint32_t idx = static_cast<uint32_t>(tt) + th[r];
-                                if (idx < wu) {
-                                    const double g = taps[idx];
-                                    acc[r].x += g * xr;
-                                    acc[r].y += g * xi;
-                                }
-                            }
-                        }
-                    }
-                }
-            }
-        }
-    }
-
-    const double inv_n = plan.inv_n;
-    const int64_t vps = plan.values_per_signal;
-    if (!task.fused) {
-        if (active) {
-            double2* ys = y + s * vps + it.yoff + static_cast<int64_t>(task.r0) * b;
-#pragma unroll
-            for (int r = 0; r < kEncRounds; ++r)
-                if (r < nr) ys[static_cast<int64_t>(r) * b + ((c + taus[r]) & (b - 1))] = acc[r];
-        }
-        return;
-    }
-
-    // ---- fused epilogue: b-point radix-2 DIT of every (signal, round) in smem
-    __syncthreads();  // taps region is reused for the folds
-    double2* F = reinterpret_cast<double2*>(smem_raw);
-    const int nsig_cta = kEncThreads >> log2b;
-    const int per_sig = nr << log2b;  // nr * b
-#pragma unroll
-    for (int r = 0; r < kEncRounds; ++r) {
-        if (r < nr) {
-            const unsigned bin = static_cast<unsigned>((c + taus[r]) & (b - 1));
-            F[sl * per_sig + (r << log2b) + bitrev_bits(bin, log2b)] = acc[r];
-        }
-    }
-    __syncthreads();
-    const int nbf = (nsig_cta * per_sig) >> 1;
-    for (int st = 1; st <= log2b; ++st) {
-        const int half = 1 << (st - 1);
-        const int step_sh = log2b - st;  // twiddle stride b / 2^st
-        for (int bf = tid; bf < nbf; bf += kEncThreads) {
-            const int arr = bf >> (log2b - 1);
-            const int p = bf & ((1 << (log2b - 1)) - 1);
-            const int blk = p >> (st - 1);
-            const int off = p & (half - 1);
-            const int j = (arr << log2b) + (blk << st) + off;
-            const double2 w = it.tw[off << step_sh];
-            const double2 x0 = F[j];
-            const double2 tv = cmul(F[j + half], w);
-            F[j + half] = make_double2(x0.x - tv.x, x0.y - tv.y);
-            F[j] = make_double2(x0.x + tv.x, x0.y + tv.y);
-        }
-        __syncthreads();
-    }
-    const int total = nsig_cta * per_sig;
-    for (int e = tid; e < total; e += kEncThreads) {
-        const int es = e / per_sig;
-        const int rem = e - es * per_sig;
-        const int64_t sig = task.sig0 + es;
-        if (es < task.nsig && sig < batch) {
-            const double2 v = F[e];
-            y[sig * vps + it.yoff + static_cast<int64_t>(task.r0) * b + rem] =
-                make_double2(v.x * inv_n, v.y * inv_n);
-        }
-    }
+    encode_barrier_init(&bar);
+    uint32_t phase = 0;
+    encode_task(plan, tasks[blockIdx.x], x, x_stride, batch, sigma, y, smem_raw, &bar, phase);
 }
 
 }  // namespace

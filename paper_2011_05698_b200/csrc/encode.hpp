@@ -23,6 +23,7 @@ struct DecLayout {
     int64_t off_tone_u, off_tone_i;
     int64_t off_mag, off_order;
     int64_t off_cand_f, off_cand_v, off_cand_first, off_cand_sum, off_contrib;
+    int64_t off_bstart, off_blist, off_gc, off_phi, off_pcode;
     int64_t bytes;      // per signal
     int32_t in_smem;
 };

@@ -91,6 +91,19 @@ Plan::Plan(int64_t n, int64_t k, int64_t l, double q, double delta, bool c128, i
         it.log2b = lb;
         it.nrounds = static_cast<int32_t>(ip.taus.size());
         it.tau_off = tau_off;
+        {
+            // locate stage lengths, same IEEE operations as locate_step
+            double len = static_cast<double>(ip.l_width);
+            int st = 0;
+            while (len > 1.0 + 1e-9 && st < kMaxStageTable - 1) {
+                it.stage_len[st] = len;
+                it.stage_blk[st] = len / static_cast<double>(l);
+                len = len * (q + 1.0) / static_cast<double>(l);
+                ++st;
+            }
+            it.stage_len[st] = len;
+            it.nstage_tab = (len > 1.0 + 1e-9) ? -1 : st;
+        }
         const size_t taps_bytes = static_cast<size_t>(win->w + 1) * sizeof(double);
         it.taps_in_smem = taps_bytes <= kTapsSmemMax ? 1 : 0;
         if (tau_off + it.nrounds > kMaxTaus)
@@ -128,6 +141,10 @@ Plan::Plan(int64_t n, int64_t k, int64_t l, double q, double delta, bool c128, i
     MSFFT_CUDA(cudaEventCreateWithFlags(&ev_chunk_, cudaEventDisableTiming));
     MSFFT_CUDA(cudaEventCreateWithFlags(&ev_dec_done_, cudaEventDisableTiming));
     if (const char* e = std::getenv("MSFFT_OVERLAP_CHUNK")) overlap_chunk_ = std::atoll(e);
+    if (const char* e = std::getenv("MSFFT_FUSED")) fused_enabled_ = std::atoi(e) != 0;
+    if (const char* e = std::getenv("MSFFT_FUSED_CHUNK")) fused_chunk_ = std::max(1LL, std::atoll(e));
+    if (const char* e = std::getenv("MSFFT_FUSED_LAG")) fused_lag_ = std::max(1LL, std::atoll(e));
+    fused_smem_ = std::max(enc_smem_, lay_.in_smem ? static_cast<size_t>(lay_.bytes) : size_t{0});
     flags_.reset(2);
 }
 
@@ -156,6 +173,71 @@ const Plan::TaskSet& Plan::tasks_for(int64_t batch) {
     auto it = tasks_.find(batch);
     if (it != tasks_.end()) return it->second;
     std::vector<EncTask> v;
+    append_tasks(v, 0, batch);
+    TaskSet ts;
+    ts.count = static_cast<int64_t>(v.size());
+    ts.d.reset(v.size());
+    MSFFT_CUDA(cudaMemcpy(ts.d.get(), v.data(), v.size() * sizeof(EncTask),
+                          cudaMemcpyHostToDevice));
+    return tasks_.emplace(batch, std::move(ts)).first->second;
+}
+
+const Plan::FusedSet& Plan::fused_for(int64_t batch) {
+    auto it = fused_.find(batch);
+    if (it != fused_.end()) return it->second;
+    // chunk: a multiple of the largest signal group of a fused encode task
+    int64_t group = 1;
+    for (int m = 0; m < sched_.iterations; ++m)
+        group = std::max<int64_t>(group, kEncThreads / dplan_.it[m].b);
+    const int64_t chunk = std::max<int64_t>(group, (fused_chunk_ + group - 1) / group * group);
+    const int64_t nchunks = (batch + chunk - 1) / chunk;
+    std::vector<EncTask> tasks;
+    std::vector<std::vector<int32_t>> enc(nchunks);
+    // need[c * iters + m]: encode tasks of chunk c and iteration m
+    const int iters = sched_.iterations;
+    std::vector<int32_t> need(static_cast<size_t>(nchunks * iters), 0);
+    for (int64_t c = 0; c < nchunks; ++c) {
+        const size_t before = tasks.size();
+        append_tasks(tasks, c * chunk, std::min(batch, (c + 1) * chunk));
+        for (size_t i = before; i < tasks.size(); ++i) {
+            enc[c].push_back(static_cast<int32_t>(i));
+            ++need[c * iters + tasks[i].m];
+        }
+    }
+    // E(0) .. E(lag) D(0) E(lag+1) D(1) ...: decodes trail their encodes
+    std::vector<int32_t> items;
+    auto decodes = [&](int64_t c) {
+        for (int64_t s = c * chunk; s < std::min(batch, (c + 1) * chunk); ++s)
+            items.push_back(static_cast<int32_t>(-(s + 1)));
+    };
+    for (int64_t c = 0; c < nchunks; ++c) {
+        items.insert(items.end(), enc[c].begin(), enc[c].end());
+        if (c - fused_lag_ >= 0) decodes(c - fused_lag_);
+    }
+    for (int64_t c = std::max<int64_t>(0, nchunks - fused_lag_); c < nchunks; ++c) decodes(c);
+    FusedSet fs;
+    fs.tasks.reset(tasks.size());
+    fs.items.reset(items.size());
+    fs.need.reset(need.size());
+    fs.counters.reset(need.size() + 1);
+    MSFFT_CUDA(cudaMemcpy(fs.tasks.get(), tasks.data(), tasks.size() * sizeof(EncTask),
+                          cudaMemcpyHostToDevice));
+    MSFFT_CUDA(cudaMemcpy(fs.items.get(), items.data(), items.size() * sizeof(int32_t),
+                          cudaMemcpyHostToDevice));
+    MSFFT_CUDA(cudaMemcpy(fs.need.get(), need.data(), need.size() * sizeof(int32_t),
+                          cudaMemcpyHostToDevice));
+    fs.fw.tasks = fs.tasks.get();
+    fs.fw.items = fs.items.get();
+    fs.fw.n_items = static_cast<int32_t>(items.size());
+    fs.fw.chunk = chunk;
+    fs.fw.need = fs.need.get();
+    fs.fw.counters = fs.counters.get();
+    fs.fw.n_chunks = nchunks;
+    fs.fw.n_counters = static_cast<int64_t>(need.size()) + 1;
+    return fused_.emplace(batch, std::move(fs)).first->second;
+}
+
+void Plan::append_tasks(std::vector<EncTask>& v, int64_t s_begin, int64_t s_end) const {
     for (int m = 0; m < sched_.iterations; ++m) {
         const DevIter& di = dplan_.it[m];
         const IterationPlan& ip = sched_.iters[m];
@@ -184,14 +266,14 @@ const Plan::TaskSet& Plan::tasks_for(int64_t batch) {
                 t.fused = 1;
                 t.nsig = static_cast<int32_t>(kEncThreads / di.b);
                 t.lane0 = 0;
-                for (int64_t s0 = 0; s0 < batch; s0 += t.nsig) {
+                for (int64_t s0 = s_begin; s0 < s_end; s0 += t.nsig) {
                     t.sig0 = s0;
                     v.push_back(t);
                 }
             } else {
                 t.fused = 0;
                 t.nsig = 1;
-                for (int64_t s0 = 0; s0 < batch; ++s0)
+                for (int64_t s0 = s_begin; s0 < s_end; ++s0)
                     for (int64_t lane0 = 0; lane0 < di.b; lane0 += kEncThreads) {
                         t.sig0 = s0;
                         t.lane0 = static_cast<int32_t>(lane0);
@@ -200,15 +282,11 @@ const Plan::TaskSet& Plan::tasks_for(int64_t batch) {
             }
         }
     }
-    TaskSet ts;
-    ts.count = static_cast<int64_t>(v.size());
-    ts.d.reset(v.size());
-    MSFFT_CUDA(cudaMemcpy(ts.d.get(), v.data(), v.size() * sizeof(EncTask),
-                          cudaMemcpyHostToDevice));
-    return tasks_.emplace(batch, std::move(ts)).first->second;
 }
 
-int64_t Plan::launches(int64_t batch, bool validate) const {
+int64_t Plan::launches(int64_t batch, bool validate, bool serial) const {
+    if (!serial && fused_enabled_ && big_b_iters_.empty())
+        return 2 + (validate ? 1 : 0);  // sigma + fused (+ validate)
     // per (sub-)chunk: encode + bucket FFTs for b > 256 + decode
     int64_t per_chunk = 2;
     for (int m : big_b_iters_) {
@@ -244,7 +322,24 @@ void Plan::run_chunk(int64_t batch, const void* d_x, int64_t x_stride, const int
         MSFFT_LAUNCH_CHECK("validate_kernel");
     }
     const bool traced = opt.pre || opt.post || opt.sel_bucket;
-    if (!traced && !opt.stage_times && overlap_chunk_ > 0 && batch > overlap_chunk_) {
+    if (!traced && !opt.force_serial && fused_enabled_ && big_b_iters_.empty()) {
+        // one persistent launch: encode and decode share the SMs
+        const FusedSet& fs = fused_for(batch);
+        if (opt.stage_times) MSFFT_CUDA(cudaEventRecord(ev_stage_[0], st));
+        launch_fused(dplan_, lay_, fs.fw, d_x, c128_, x_stride, batch, d_sig, d_sig_inv,
+                     y_.get(), dec_work_.get(), d_out_f, d_out_c, d_out_count, flags_.get(),
+                     fused_smem_, st);
+        if (opt.stage_times) {
+            MSFFT_CUDA(cudaEventRecord(ev_stage_[1], st));
+            MSFFT_CUDA(cudaEventSynchronize(ev_stage_[1]));
+            float ms = 0.f;
+            MSFFT_CUDA(cudaEventElapsedTime(&ms, ev_stage_[0], ev_stage_[1]));
+            stage_ms_[0] += ms;  // fused encode+decode
+        }
+        return;
+    }
+    if (!traced && !opt.stage_times && !opt.force_serial && overlap_chunk_ > 0 &&
+        batch > overlap_chunk_) {
         // Overlapped pipeline: the encode of sub-chunk c+1 (HBM-bound) runs
         // while the decode of sub-chunk c (SM-bound) runs on a higher-priority
         // stream; an event per sub-chunk orders decode after its encode.

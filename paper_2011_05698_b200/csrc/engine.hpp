@@ -18,6 +18,7 @@
 
 #include "cuda_check.hpp"
 #include "encode.hpp"
+#include "fused.hpp"
 #include "host_plan.hpp"
 #include "plan_dev.cuh"
 #include "window.hpp"
@@ -28,7 +29,8 @@ struct ExecOptions {
     bool x_on_device = false;
     bool out_on_device = false;
     bool assume_valid = false;
-    bool stage_times = false;  // CUDA events around encode / fft / decode
+    bool stage_times = false;  // CUDA events around encode / fft / decode (or fused)
+    bool force_serial = false; // separate encode and decode launches (diagnostics)
     cudaStream_t stream = nullptr;
     double* pre = nullptr;   // trace: encode output (batch must be 1, host)
     double* post = nullptr;  // trace: post-subtract values
@@ -53,7 +55,7 @@ public:
                  int64_t* out_f, double* out_c, int64_t* out_count, const ExecOptions& opt,
                  double* device_ms);
 
-    int64_t launches(int64_t batch, bool validate) const;
+    int64_t launches(int64_t batch, bool validate, bool serial = false) const;
 
     // [encode, bucket fft (b > 256), decode] ms of the last execute run with
     // stage_times (summed over chunks).
@@ -66,7 +68,14 @@ private:
         DeviceBuffer<EncTask> d;
         int64_t count = 0;
     };
+    struct FusedSet {
+        DeviceBuffer<EncTask> tasks;
+        DeviceBuffer<int32_t> items, need, counters;
+        FusedWork fw;
+    };
     const TaskSet& tasks_for(int64_t batch);
+    const FusedSet& fused_for(int64_t batch);
+    void append_tasks(std::vector<EncTask>& v, int64_t s_begin, int64_t s_end) const;
     void run_chunk(int64_t batch, const void* d_x, int64_t x_stride, const int64_t* d_sig,
                    const int64_t* d_sig_inv, int64_t* d_out_f, double2* d_out_c,
                    int64_t* d_out_count, bool validate, cudaStream_t st,
@@ -82,6 +91,11 @@ private:
     int64_t b_max_ = 0, budget_max_ = 0;
     std::vector<int> big_b_iters_;  // iterations needing the separate FFT
     std::map<int64_t, TaskSet> tasks_;
+    std::map<int64_t, FusedSet> fused_;
+    bool fused_enabled_ = true;   // persistent encode+decode launch when all b <= 256
+    int64_t fused_chunk_ = 64;    // signals per fused chunk
+    int64_t fused_lag_ = 2;       // chunks a decode trails its encode by
+    size_t fused_smem_ = 0;
 
     cudaStream_t own_stream_ = nullptr, copy_stream_ = nullptr;
     cudaEvent_t ev_start_ = nullptr, ev_end_ = nullptr;

@@ -1,0 +1,113 @@
+// fused.cu -- one persistent launch that runs the encode (K1+K2) and the
+// decode (K3..K7) of a whole batch, so the HBM-bound gather and the
+// issue-bound decode share every SM instead of running back to back.
+//
+// CTAs pull work items from a global ticket counter.  The item list is
+// E(c0) E(c1) D(c0) E(c2) D(c1) ... D(c_last): E = the encode tasks of a
+// chunk of signals, D = one decode per signal of a chunk.  A decode item waits
+// until its chunk's encode-completion counter reaches the chunk's task count.
+// Every encode item with a smaller ticket is already held by a running CTA
+// and never waits, so the spin always terminates (no deadlock), and the
+// encode->decode hand-off follows the threadfence-reduction pattern
+// (producer: stores, __syncthreads, __threadfence, atomicAdd; consumer: spin
+// on the counter, __threadfence, __syncthreads).  Compiled with --fmad=false.
+#include <cuda_runtime.h>
+
+#include "decode_body.cuh"
+#include "encode_body.cuh"
+#include "fused.hpp"
+
+#ifndef MSFFT_FUSED_MINB
+#define MSFFT_FUSED_MINB 2
+#endif
+
+namespace msfft_b200 {
+
+namespace {
+
+template <class T>
+__global__ void __launch_bounds__(kEncThreads, MSFFT_FUSED_MINB)
+fused_kernel(const __grid_constant__ DevPlan plan, DecLayout lay, DecArgs args,
+             const EncTask* __restrict__ tasks, const int32_t* __restrict__ items,
+             int32_t n_items, int64_t chunk, const int32_t* __restrict__ need,
+             int32_t* __restrict__ done, int32_t* __restrict__ ticket, const T* __restrict__ x,
+             int64_t x_stride, int64_t batch, unsigned char* __restrict__ work) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ __align__(8) uint64_t bar;
+    __shared__ DecShared sh;
+    __shared__ int s_item;
+    static_assert(kEncThreads == kDecThreads, "fused CTA runs both bodies");
+    encode_barrier_init(&bar);
+    uint32_t phase = 0;
+    const bool bad_input = args.err[1] != 0;  // set by the validation pass
+    for (;;) {
+        if (threadIdx.x == 0) s_item = atomicAdd(ticket, 1);
+        __syncthreads();
+        const int item = s_item;
+        if (item >= n_items) break;
+        const int32_t code = items[item];
+        if (code >= 0) {
+            const EncTask& t = tasks[code];
+            encode_task(plan, t, x, x_stride, batch, args.sigma, args.y, smem, &bar, phase);
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                __threadfence();
+                atomicAdd(&done[(t.sig0 / chunk) * plan.iters + t.m], 1);
+            }
+        } else if (!bad_input) {
+            // the decode waits per iteration (DecArgs::gate_*), so it can run
+            // while the later iterations of its chunk are still being encoded
+            const int64_t s = -static_cast<int64_t>(code) - 1;
+            const int64_t c = s / chunk;
+            DecArgs a = args;
+            a.gate_done = done + c * plan.iters;
+            a.gate_need = need + c * plan.iters;
+            decode_signal(plan, lay, a, s, lay.in_smem ? smem : work + s * lay.bytes, sh);
+        }
+        __syncthreads();
+    }
+}
+
+template <class T>
+void launch_t(const DevPlan& plan, const DecLayout& lay, const FusedWork& fw, const T* x,
+              int64_t x_stride, int64_t batch, const int64_t* d_sigma,
+              const int64_t* d_sigma_inv, double2* d_y, unsigned char* d_work, int64_t* d_out_f,
+              double2* d_out_c, int64_t* d_out_count, int32_t* d_err, size_t smem,
+              cudaStream_t stream) {
+    auto k = fused_kernel<T>;
+    MSFFT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(smem)));
+    int dev = 0, sms = 0, per_sm = 0;
+    MSFFT_CUDA(cudaGetDevice(&dev));
+    MSFFT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    MSFFT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kEncThreads, smem));
+    if (per_sm < 1) throw CudaError("fused_kernel: does not fit on an SM");
+    const int64_t grid = std::min<int64_t>(static_cast<int64_t>(sms) * per_sm, fw.n_items);
+    MSFFT_CUDA(cudaMemsetAsync(fw.counters, 0, sizeof(int32_t) * fw.n_counters, stream));
+    DecArgs args{d_y, d_sigma, d_sigma_inv, d_out_f, d_out_c, d_out_count, d_err,
+                 nullptr, nullptr, nullptr};
+    k<<<static_cast<unsigned>(grid), kEncThreads, smem, stream>>>(
+        plan, lay, args, fw.tasks, fw.items, fw.n_items, fw.chunk, fw.need, fw.counters + 1,
+        fw.counters, x, x_stride, batch, d_work);
+    MSFFT_LAUNCH_CHECK("fused_kernel");
+}
+
+}  // namespace
+
+void launch_fused(const DevPlan& plan, const DecLayout& lay, const FusedWork& fw, const void* x,
+                  bool x_c128, int64_t x_stride, int64_t batch, const int64_t* d_sigma,
+                  const int64_t* d_sigma_inv, double2* d_y, unsigned char* d_work,
+                  int64_t* d_out_f, double2* d_out_c, int64_t* d_out_count, int32_t* d_err,
+                  size_t smem_bytes, cudaStream_t stream) {
+    if (fw.n_items <= 0) return;
+    if (x_c128)
+        launch_t(plan, lay, fw, static_cast<const double2*>(x), x_stride, batch, d_sigma,
+                 d_sigma_inv, d_y, d_work, d_out_f, d_out_c, d_out_count, d_err, smem_bytes,
+                 stream);
+    else
+        launch_t(plan, lay, fw, static_cast<const float2*>(x), x_stride, batch, d_sigma,
+                 d_sigma_inv, d_y, d_work, d_out_f, d_out_c, d_out_count, d_err, smem_bytes,
+                 stream);
+}
+
+}  // namespace msfft_b200

@@ -1,0 +1,32 @@
+// fused.hpp -- persistent encode+decode launch (see fused.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+#include "encode.hpp"
+#include "plan_dev.cuh"
+
+namespace msfft_b200 {
+
+// Device-side work description for one batch size.
+struct FusedWork {
+    const EncTask* tasks = nullptr;  // encode tasks, absolute signal indices
+    const int32_t* items = nullptr;  // >= 0: encode task index; < 0: -(signal+1)
+    int32_t n_items = 0;
+    int64_t chunk = 0;               // signals per chunk
+    const int32_t* need = nullptr;   // [chunk][iteration] encode tasks
+    int32_t* counters = nullptr;     // [0] ticket, [1 + c*iters + m] tasks done
+    int64_t n_chunks = 0;
+    int64_t n_counters = 0;
+};
+
+void launch_fused(const DevPlan& plan, const DecLayout& lay, const FusedWork& fw, const void* x,
+                  bool x_c128, int64_t x_stride, int64_t batch, const int64_t* d_sigma,
+                  const int64_t* d_sigma_inv, double2* d_y, unsigned char* d_work,
+                  int64_t* d_out_f, double2* d_out_c, int64_t* d_out_count, int32_t* d_err,
+                  size_t smem_bytes, cudaStream_t stream);
+
+}  // namespace msfft_b200

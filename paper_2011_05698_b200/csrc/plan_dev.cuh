@@ -18,8 +18,15 @@ constexpr int kMaxTaus = 1024;
 constexpr int kEncRounds = 8;       // rounds fused into one gather pass
 constexpr int kEncThreads = 256;    // encode CTA size
 constexpr int kDecThreads = 256;    // decode CTA size
+constexpr int kMaxStageTable = 24;  // precomputed locate stage lengths
 
 struct DevIter {
+    // Locate region lengths of every stage, len_0 = L, len_{k+1} =
+    // len_k*(q+1)/l, and block widths len_k/l (locate.cpp:64, 78), computed on
+    // the host with the same IEEE operations; nstage_tab = stages the locate
+    // loop runs (len_k > 1 + 1e-9), or -1 if the table is too short.
+    double stage_len[kMaxStageTable], stage_blk[kMaxStageTable];
+    int32_t nstage_tab, pad0_;
     int64_t b, l_width, w, h;
     int64_t budget, k_m;
     int64_t yoff;            // offset of round 0 of this iteration in a signal's y block
@@ -53,4 +60,8 @@ struct EncTask {
     int32_t seg_lo[kEncRounds], seg_hi[kEncRounds];  // merged t' intervals
 };
 
+}  // namespace msfft_b200
+
+namespace msfft_b200 {
+static_assert(sizeof(DevPlan) <= 31 * 1024, "DevPlan must fit the 32 KB kernel-parameter limit");
 }  // namespace msfft_b200
