@@ -21,7 +21,8 @@ decode_kernel(const __grid_constant__ DevPlan plan, DecLayout lay, DecArgs args,
     // err[1]: the validation pass found a non-finite sample; the call will
     // throw (ComplexSignal::validate) so there is nothing to decode.
     if (s >= batch || args.err[1] != 0) return;
-    decode_signal(plan, lay, args, s, lay.in_smem ? dsm : work + s * lay.bytes, sh);
+    decode_signal(plan, lay, args, s, lay.in_smem ? dsm : work + s * lay.bytes, sh,
+                  lay.big ? reinterpret_cast<int*>(dsm) : nullptr);
 }
 
 }  // namespace
@@ -54,8 +55,20 @@ DecLayout make_dec_layout(int64_t acc_cap, int64_t b_max, int64_t budget_max,
     L.off_gc = take(cap * 3 * 16);
     L.off_phi = take(budget_max * rounds_max * 8);
     L.off_pcode = take(budget_max * rounds_max * 4);
+    // large sizes (C3/C5): radix-sort scratch replaces the O(n^2) ranks
+    L.big = (b_max > kSmallRank || budget_max > kSmallBudget || cap > kSmallAcc) ? 1 : 0;
+    if (L.big) {
+        const int64_t ncap = std::max(std::max(b_max, budget_max), cap);
+        L.sort_n = ncap;
+        for (int p = 0; p < 2; ++p) {
+            L.off_sk[p] = take(ncap * 8);
+            L.off_sv[p] = take(ncap * 4);
+        }
+        L.off_flag = take((ncap + kDecThreads) * 4);
+        L.off_nfs = take(ncap * 8);
+    }
     L.bytes = off;
-    L.in_smem = off <= 96 * 1024 ? 1 : 0;
+    L.in_smem = (!L.big && off <= 96 * 1024) ? 1 : 0;
     return L;
 }
 
@@ -65,7 +78,8 @@ void launch_decode(const DevPlan& plan, const DecLayout& lay, double2* d_y,
                    int64_t* d_out_count, int32_t* d_err, cudaStream_t stream,
                    int64_t* tr_bucket, int64_t* tr_f, double2* tr_v) {
     if (batch <= 0) return;
-    const size_t smem = lay.in_smem ? static_cast<size_t>(lay.bytes) : 0;
+    const size_t smem =
+        lay.in_smem ? static_cast<size_t>(lay.bytes) : (lay.big ? kSortSmemBytes : 0);
     MSFFT_CUDA(cudaFuncSetAttribute(decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(smem)));
     DecArgs args{d_y, d_sigma, d_sigma_inv, d_out_f, d_out_c, d_out_count, d_err,

@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 
 #include "common.cuh"
+#include "cta_sort.cuh"
 #include "encode.hpp"
 #include "plan_dev.cuh"
 
@@ -71,6 +72,10 @@ struct Scratch {
     double2* gc;       // [acc][3] G * c per tone and bucket offset
     double* phi;       // [budget][stages] phase of y0 / y_tau
     int32_t* pcode;    // [budget][stages] 0 ok, 1 y_tau == 0, 2 quotient == 0
+    uint64_t* sk[2];   // large sizes: radix-sort keys (ping-pong)
+    int32_t* sv[2];    //              and values
+    int32_t* flag;     //              scan flags
+    int64_t* nfs;      //              new found frequencies
 };
 
 __device__ __forceinline__ double ghat_at(const DevIter& it, int64_t d) {
@@ -90,7 +95,7 @@ __device__ __forceinline__ double2 unit_root(int64_t n, double inv_n, int64_t e)
 // Decodes signal s; base = this signal's scratch (shared or global memory).
 __device__ __forceinline__ void decode_signal(const DevPlan& plan, const DecLayout& lay,
                                            const DecArgs& A, int64_t s, unsigned char* base,
-                                           DecShared& sh) {
+                                           DecShared& sh, int* sort_smem) {
     constexpr int kThreads = kDecThreads;
     const int tid = threadIdx.x;
     const int lane = tid & 31;
@@ -114,6 +119,13 @@ __device__ __forceinline__ void decode_signal(const DevPlan& plan, const DecLayo
     S.gc = reinterpret_cast<double2*>(base + lay.off_gc);
     S.phi = reinterpret_cast<double*>(base + lay.off_phi);
     S.pcode = reinterpret_cast<int32_t*>(base + lay.off_pcode);
+    for (int p = 0; p < 2; ++p) {
+        S.sk[p] = lay.big ? reinterpret_cast<uint64_t*>(base + lay.off_sk[p]) : nullptr;
+        S.sv[p] = lay.big ? reinterpret_cast<int32_t*>(base + lay.off_sv[p]) : nullptr;
+    }
+    S.flag = lay.big ? reinterpret_cast<int32_t*>(base + lay.off_flag) : nullptr;
+    S.nfs = lay.big ? reinterpret_cast<int64_t*>(base + lay.off_nfs) : nullptr;
+    if (!lay.big) sort_smem = nullptr;
 
     if (tid == 0) {
         sh.acc_n = 0;
@@ -280,14 +292,28 @@ __device__ __forceinline__ void decode_signal(const DevPlan& plan, const DecLayo
         }
         __syncthreads();
         DEC_MARK(4);
-        for (int64_t j = tid; j < b; j += kThreads) {
-            const double mj = S.mag[j];
-            int64_t rank = 0;
-            for (int64_t i = 0; i < b; ++i) {
-                const double mi = S.mag[i];
-                rank += (mi > mj) || (mi == mj && i < j);
+        if (b > kSmallRank && sort_smem) {
+            // stable radix sort by |y0| descending (ties: lower bucket first)
+            for (int64_t j = tid; j < b; j += kThreads) {
+                S.sk[0][j] = desc_key(S.mag[j]);
+                S.sv[0][j] = static_cast<int32_t>(j);
             }
-            S.order[rank] = static_cast<int32_t>(j);
+            __syncthreads();
+            const bool fl = cta_radix_sort<kThreads>(S.sk[0], S.sv[0], S.sk[1], S.sv[1],
+                                                     static_cast<int>(b), 64, sort_smem,
+                                                     sort_smem + 16 * kThreads);
+            const int32_t* V = fl ? S.sv[1] : S.sv[0];
+            for (int64_t j = tid; j < b; j += kThreads) S.order[j] = V[j];
+        } else {
+            for (int64_t j = tid; j < b; j += kThreads) {
+                const double mj = S.mag[j];
+                int64_t rank = 0;
+                for (int64_t i = 0; i < b; ++i) {
+                    const double mi = S.mag[i];
+                    rank += (mi > mj) || (mi == mj && i < j);
+                }
+                S.order[rank] = static_cast<int32_t>(j);
+            }
         }
         __syncthreads();
         DEC_MARK(5);
@@ -443,6 +469,91 @@ __device__ __forceinline__ void decode_signal(const DevPlan& plan, const DecLayo
         int64_t* NF = nxt ? S.acc_f[1] : S.acc_f[0];
         double2* NC = nxt ? S.acc_c[1] : S.acc_c[0];
         if (tid == 0) sh.new_n = 0;
+        if (budget > kSmallBudget && sort_smem) {
+            // large budgets: stable sort of the accepted ranks by f (equal f
+            // keep rank order), runs summed in rank order, then a merge of
+            // the new f into the ascending acc list by binary searches
+            const int padded = static_cast<int>((budget + kThreads - 1) / kThreads * kThreads);
+            int key_bits = 4;
+            while (key_bits < 62 && (uint64_t{1} << key_bits) <= static_cast<uint64_t>(n)) key_bits += 4;
+            for (int64_t r = tid; r < budget; r += kThreads) {
+                const int64_t fr = S.cand_f[r];
+                S.sk[0][r] = fr >= 0 ? static_cast<uint64_t>(fr) : static_cast<uint64_t>(n);
+                S.sv[0][r] = static_cast<int32_t>(r);
+            }
+            for (int r = tid; r < padded; r += kThreads) S.flag[r] = 0;
+            __syncthreads();
+            const bool fl = cta_radix_sort<kThreads>(S.sk[0], S.sv[0], S.sk[1], S.sv[1],
+                                                     static_cast<int>(budget), key_bits,
+                                                     sort_smem, sort_smem + 16 * kThreads);
+            const uint64_t* Ks = fl ? S.sk[1] : S.sk[0];
+            const int32_t* Vs = fl ? S.sv[1] : S.sv[0];
+            for (int64_t p = tid; p < budget; p += kThreads) {
+                const uint64_t f = Ks[p];
+                if (f >= static_cast<uint64_t>(n) || (p > 0 && Ks[p - 1] == f)) continue;
+                double2 sum = make_double2(0.0, 0.0);
+                for (int64_t p2 = p; p2 < budget && Ks[p2] == f; ++p2) {
+                    const double2 v = S.cand_v[Vs[p2]];
+                    sum.x += v.x;
+                    sum.y += v.y;
+                }
+                S.cand_sum[Vs[p]] = sum;
+                int lo = 0, hi = acc_n;
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (static_cast<uint64_t>(AF[mid]) < f) lo = mid + 1; else hi = mid;
+                }
+                const bool present = lo < acc_n && static_cast<uint64_t>(AF[lo]) == f;
+                S.flag[p] = present ? 0 : 1;
+                S.nfs[p] = present ? -2 : -1;  // marks a run start (-1 new, -2 present)
+            }
+            __syncthreads();
+            // flag -> index among the new f; remember which positions start runs
+            for (int64_t p = tid; p < budget; p += kThreads) {
+                const uint64_t f = Ks[p];
+                const bool start = f < static_cast<uint64_t>(n) && !(p > 0 && Ks[p - 1] == f);
+                S.cand_first[p] = start ? (S.flag[p] ? 1 : 2) : 0;  // indexed by position here
+            }
+            __syncthreads();
+            const int nnew = cta_exclusive_scan<kThreads>(S.flag, padded, sort_smem + 16 * kThreads);
+            for (int64_t p = tid; p < budget; p += kThreads)
+                if (S.cand_first[p] == 1) S.nfs[S.flag[p]] = static_cast<int64_t>(Ks[p]);
+            __syncthreads();
+            for (int j = tid; j < acc_n; j += kThreads) {
+                const int64_t fj = AF[j];
+                int lo = 0, hi = nnew;  // new f below fj
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (S.nfs[mid] < fj) lo = mid + 1; else hi = mid;
+                }
+                const int before = lo;
+                int plo = 0, phi2 = static_cast<int>(budget);  // run of fj among the found
+                while (plo < phi2) {
+                    const int mid = (plo + phi2) >> 1;
+                    if (Ks[mid] < static_cast<uint64_t>(fj)) plo = mid + 1; else phi2 = mid;
+                }
+                double2 c = AC[j];
+                if (plo < budget && Ks[plo] == static_cast<uint64_t>(fj)) {
+                    const double2 add = S.cand_sum[Vs[plo]];
+                    c = make_double2(c.x + add.x, c.y + add.y);
+                }
+                NF[j + before] = fj;
+                NC[j + before] = c;
+            }
+            for (int64_t p = tid; p < budget; p += kThreads) {
+                if (S.cand_first[p] != 1) continue;
+                const int64_t fr = static_cast<int64_t>(Ks[p]);
+                int lo = 0, hi = acc_n;
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (AF[mid] < fr) lo = mid + 1; else hi = mid;
+                }
+                const double2 sum = S.cand_sum[Vs[p]];
+                NF[lo + S.flag[p]] = fr;
+                NC[lo + S.flag[p]] = make_double2(0.0 + sum.x, 0.0 + sum.y);
+            }
+            if (tid == 0) sh.new_n = nnew;
+        } else {
         // cand_first[r]: 0 = not the first accepted rank of its f,
         // 1 = first and f is new, 2 = first and f already accumulated.
         for (int64_t r = tid; r < budget; r += kThreads) {
@@ -503,6 +614,7 @@ __device__ __forceinline__ void decode_signal(const DevPlan& plan, const DecLayo
             NC[pos] = make_double2(0.0 + sum.x, 0.0 + sum.y);
             atomicAdd(&sh.new_n, 1);
         }
+        }  // small-budget merge
         __syncthreads();
         DEC_MARK(9);
         if (tid == 0) {
@@ -536,22 +648,48 @@ __device__ __forceinline__ void decode_signal(const DevPlan& plan, const DecLayo
         S.mag[j] = mg == mg ? mg : -1.0;
     }
     __syncthreads();
-    for (int j = tid; j < acc_n; j += kThreads) {
-        const double mj = S.mag[j];
-        int64_t rank = 0;
-        for (int i = 0; i < acc_n; ++i) {
-            const double mi = S.mag[i];
-            rank += (mi > mj) || (mi == mj && i < j);
+    if (acc_n > kSmallAcc && sort_smem) {
+        // stable sort by |c| descending over ascending f; keep ranks < K;
+        // output positions by a prefix count over f order
+        const int padded = (acc_n + kThreads - 1) / kThreads * kThreads;
+        for (int j = tid; j < acc_n; j += kThreads) {
+            S.sk[0][j] = desc_key(S.mag[j]);
+            S.sv[0][j] = j;
         }
-        S.tone_i[j] = rank < K ? 1 : 0;
-    }
-    __syncthreads();
-    for (int j = tid; j < acc_n; j += kThreads) {
-        if (!S.tone_i[j]) continue;
-        int64_t pos = 0;
-        for (int i = 0; i < j; ++i) pos += S.tone_i[i];
-        A.out_f[s * K + pos] = AF[j];
-        A.out_c[s * K + pos] = AC[j];
+        for (int j = tid; j < padded; j += kThreads) S.flag[j] = 0;
+        __syncthreads();
+        const bool fl = cta_radix_sort<kThreads>(S.sk[0], S.sv[0], S.sk[1], S.sv[1], acc_n, 64,
+                                                 sort_smem, sort_smem + 16 * kThreads);
+        const int32_t* V = fl ? S.sv[1] : S.sv[0];
+        for (int r = tid; r < acc_n && r < K; r += kThreads) S.flag[V[r]] = 1;
+        __syncthreads();
+        for (int j = tid; j < acc_n; j += kThreads) S.tone_i[j] = S.flag[j];
+        __syncthreads();
+        cta_exclusive_scan<kThreads>(S.flag, padded, sort_smem + 16 * kThreads);
+        for (int j = tid; j < acc_n; j += kThreads) {
+            if (!S.tone_i[j]) continue;
+            const int64_t pos = S.flag[j];
+            A.out_f[s * K + pos] = AF[j];
+            A.out_c[s * K + pos] = AC[j];
+        }
+    } else {
+        for (int j = tid; j < acc_n; j += kThreads) {
+            const double mj = S.mag[j];
+            int64_t rank = 0;
+            for (int i = 0; i < acc_n; ++i) {
+                const double mi = S.mag[i];
+                rank += (mi > mj) || (mi == mj && i < j);
+            }
+            S.tone_i[j] = rank < K ? 1 : 0;
+        }
+        __syncthreads();
+        for (int j = tid; j < acc_n; j += kThreads) {
+            if (!S.tone_i[j]) continue;
+            int64_t pos = 0;
+            for (int i = 0; i < j; ++i) pos += S.tone_i[i];
+            A.out_f[s * K + pos] = AF[j];
+            A.out_c[s * K + pos] = AC[j];
+        }
     }
     if (tid == 0) A.out_count[s] = acc_n < K ? acc_n : K;
 }

@@ -24,9 +24,19 @@ struct DecLayout {
     int64_t off_mag, off_order;
     int64_t off_cand_f, off_cand_v, off_cand_first, off_cand_sum, off_contrib;
     int64_t off_bstart, off_blist, off_gc, off_phi, off_pcode;
+    // large-size scratch (radix sorts), present when big != 0
+    int64_t off_sk[2], off_sv[2], off_flag, off_nfs, sort_n;
     int64_t bytes;      // per signal
     int32_t in_smem;
+    int32_t big;        // large-size paths: sort counters live in shared memory
 };
+
+// Above these sizes the decode switches from O(n^2) rank counting to
+// block-wide radix sorts (cta_sort.cuh).
+constexpr int64_t kSmallRank = 1024;    // buckets (selection order, K4)
+constexpr int64_t kSmallBudget = 512;   // ranked buckets (found-map merge, K6)
+constexpr int64_t kSmallAcc = 2048;     // accumulated tones (K-prune, K7)
+constexpr size_t kSortSmemBytes = (16 * 256 + 32) * sizeof(int);
 
 DecLayout make_dec_layout(int64_t acc_cap, int64_t b_max, int64_t budget_max,
                           int64_t rounds_max);

@@ -285,7 +285,7 @@ void Plan::append_tasks(std::vector<EncTask>& v, int64_t s_begin, int64_t s_end)
 }
 
 int64_t Plan::launches(int64_t batch, bool validate, bool serial) const {
-    if (!serial && fused_enabled_ && big_b_iters_.empty())
+    if (!serial && fused_enabled_ && big_b_iters_.empty() && !lay_.big)
         return 2 + (validate ? 1 : 0);  // sigma + fused (+ validate)
     // per (sub-)chunk: encode + bucket FFTs for b > 256 + decode
     int64_t per_chunk = 2;
@@ -322,7 +322,7 @@ void Plan::run_chunk(int64_t batch, const void* d_x, int64_t x_stride, const int
         MSFFT_LAUNCH_CHECK("validate_kernel");
     }
     const bool traced = opt.pre || opt.post || opt.sel_bucket;
-    if (!traced && !opt.force_serial && fused_enabled_ && big_b_iters_.empty()) {
+    if (!traced && !opt.force_serial && fused_enabled_ && big_b_iters_.empty() && !lay_.big) {
         // one persistent launch: encode and decode share the SMs
         const FusedSet& fs = fused_for(batch);
         if (opt.stage_times) MSFFT_CUDA(cudaEventRecord(ev_stage_[0], st));

@@ -62,7 +62,8 @@ fused_kernel(const __grid_constant__ DevPlan plan, DecLayout lay, DecArgs args,
             DecArgs a = args;
             a.gate_done = done + c * plan.iters;
             a.gate_need = need + c * plan.iters;
-            decode_signal(plan, lay, a, s, lay.in_smem ? smem : work + s * lay.bytes, sh);
+            decode_signal(plan, lay, a, s, lay.in_smem ? smem : work + s * lay.bytes, sh,
+                          nullptr);
         }
         __syncthreads();
     }

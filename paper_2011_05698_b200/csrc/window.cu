@@ -174,6 +174,28 @@ __global__ void response_table_kernel(double* __restrict__ ghat, const double* _
     ghat[idx] = acc / nd;
 }
 
+// Wide windows (few entries, h up to ~10^6): a warp per entry, lanes take
+// every 32nd tap, then a shuffle reduction.  The summation order differs from
+// the sequential series only by rounding (the table is cos-limited anyway).
+__global__ void response_table_warp_kernel(double* __restrict__ ghat,
+                                           const double* __restrict__ taps, int64_t n,
+                                           int64_t h, int64_t gmax) {
+    const int64_t idx = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (idx > 2 * gmax) return;
+    const int64_t d = idx - gmax;
+    const uint64_t mask = static_cast<uint64_t>(n - 1);
+    const uint64_t i0 = static_cast<uint64_t>(d) & mask;
+    const double nd = static_cast<double>(n);
+    double acc = 0.0;
+    for (int64_t t = 1 + lane; t <= h; t += 32) {
+        const uint64_t m = (i0 * static_cast<uint64_t>(t)) & mask;
+        acc += 2.0 * taps[h + t] * cos(kTwoPi * static_cast<double>(m) / nd);
+    }
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) ghat[idx] = (taps[h] + acc) / nd;
+}
+
 struct Key {
     int device;
     int64_t n, b;
@@ -283,8 +305,13 @@ std::shared_ptr<DeviceWindow> design_on_device(int device, int64_t n, int64_t b,
     MSFFT_CUDA(cudaMalloc(&win->d_ghat, sizeof(double) * static_cast<size_t>(2 * win->gmax + 1)));
     extract_taps_kernel<<<blocks_for(h + 1, T), T, 0, st>>>(win->d_taps, g.get(), n, h);
     MSFFT_LAUNCH_CHECK("extract_taps_kernel");
-    response_table_kernel<<<blocks_for(2 * win->gmax + 1, 128), 128, 0, st>>>(
-        win->d_ghat, win->d_taps, n, h, win->gmax);
+    if (h <= 8192) {
+        response_table_kernel<<<blocks_for(2 * win->gmax + 1, 128), 128, 0, st>>>(
+            win->d_ghat, win->d_taps, n, h, win->gmax);
+    } else {
+        response_table_warp_kernel<<<blocks_for((2 * win->gmax + 1) * 32, 256), 256, 0, st>>>(
+            win->d_ghat, win->d_taps, n, h, win->gmax);
+    }
     MSFFT_LAUNCH_CHECK("response_table_kernel");
     win->taps.resize(static_cast<size_t>(w));
     MSFFT_CUDA(cudaMemcpyAsync(win->taps.data(), win->d_taps, sizeof(double) * w,

@@ -166,6 +166,15 @@ def c3_cases():
                  min_sep=4 * n // b1) for dt in ("complex128", "complex64")]
 
 
+def big_cases():
+    """C5-law signals at sizes the reference finishes in minutes: large b
+    (8192), budget (2000) and accumulated list (~4000) -- the decode's
+    radix-sort paths."""
+    return [case("np", 1 << 20, 2000, 501, 20.0, magnitude="loguniform_0.1_10"),
+            case("np", 1 << 19, 1200, 502, 20.0, dtype="complex64",
+                 magnitude="loguniform_0.1_10")]
+
+
 def prewarm(o, n, k, delta):
     b = o.initial_bucket_count(n, k, delta)
     bs = set()
@@ -194,6 +203,10 @@ def main(names):
     if "c4" in names:
         prewarm(o, 1 << 22, 64, 1e-6)
         dump("sfft4_c4", [run_case(o, c) for c in c4_cases()])
+    if "big" in names:
+        for c in big_cases():
+            prewarm(o, c["n"], c["k"], c["delta"])
+        dump("sfft4_big", [run_case(o, c) for c in big_cases()])
     if "c3" in names:
         prewarm(o, 1 << 24, 1000, 1e-6)
         dump("sfft4_c3", [run_case(o, c) for c in c3_cases()])

@@ -178,3 +178,18 @@ def test_c3_goldens(oracle, golden):
         assert_parity(f, c, r.spectrum.positions, r.spectrum.coeffs, rec["k"], rec["delta"],
                       TOL[rec["dtype"]])
         assert r.stats.samples_used == stats["samples_used"]
+
+
+@pytest.mark.slow
+def test_large_size_goldens(oracle, golden):
+    """C5-law signals that drive the decode's large-size paths (radix-sorted
+    selection order at b = 8192, sorted found-map merge at budget 2000,
+    sorted K-prune over ~4000 accumulated tones) against the reference."""
+    for rec in golden("sfft4_big"):
+        x = make_signal(oracle, rec)
+        r = M.sfft4(x, rec["k"], M.MultiscaleConfig(), rec["algo_seed"], rec["delta"])
+        f, c, stats = golden_result(rec)
+        assert_parity(f, c, r.spectrum.positions, r.spectrum.coeffs, rec["k"], rec["delta"],
+                      TOL[rec["dtype"]])
+        assert r.stats.samples_used == stats["samples_used"]
+        assert r.stats.stage_counts == stats["stage_counts"]
