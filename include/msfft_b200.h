@@ -124,6 +124,35 @@ int msfft_plan_stage_times(msfft_plan plan, double* ms3);
  * resident signals issues (for bench accounting). */
 int64_t msfft_plan_launches(msfft_plan plan, int64_t batch, uint32_t flags);
 
+/* Samples per signal that msfft_execute moves host->device for HOST inputs:
+ * with sparse ingest, only the samples the transform reads (gathered on the
+ * host by all its threads into pinned staging; the finiteness scan of the
+ * whole signal also runs on the host); 0 = dense path (whole signals are
+ * copied).  Sparse ingest is used when it moves at most n/4 samples per
+ * signal and the environment does not set MSFFT_SPARSE_INGEST=0. */
+int64_t msfft_plan_ingest_samples(msfft_plan plan);
+
+/* ---- split phases: one signal sharded by index range over several GPUs ----
+ * No reference counterpart (the reference transforms one signal on one host,
+ * sfft4.cpp:133-200); this is the SURVEY §8(e) multi-GPU path.  A rank holding
+ * x[x_lo, x_hi) of each signal calls msfft_encode_values to get PARTIAL
+ * bucket values (every round of every iteration; the samples it does not hold
+ * count as 0).  Bucketize is linear in x, so summing the partial vectors of
+ * ranks whose ranges tile [0, n) (one all-reduce) gives the full vector, up to
+ * the order of that final sum.  msfft_decode_values then runs selection,
+ * locate and estimate on it exactly as msfft_execute does after its encode.
+ * x (x_stride >= x_hi - x_lo samples per signal), y ([batch][values_per_signal]
+ * complex128), out_f/out_c/out_count ([batch][k], [batch]) are DEVICE
+ * pointers; seeds is a host array.  decode consumes y (subtraction happens in
+ * place).  flags: MSFFT_FLAG_ASSUME_VALID skips the finite check of the slice. */
+int64_t msfft_plan_values_per_signal(msfft_plan plan);
+int msfft_encode_values(msfft_plan plan, int64_t batch, const void* x, int64_t x_stride,
+                        int64_t x_lo, int64_t x_hi, const uint64_t* seeds, double* y,
+                        uint32_t flags, void* stream, char* err, size_t errlen);
+int msfft_decode_values(msfft_plan plan, int64_t batch, double* y, const uint64_t* seeds,
+                        int64_t* out_f, double* out_c, int64_t* out_count, void* stream,
+                        char* err, size_t errlen);
+
 /* ---- host-only plan pieces (no device needed) -------------------------------
  * sigma_m, sigma^-1_m for the first `iterations` iterations of a transform
  * seeded `seed`: random_params(n, Rng(seed), 0) per iteration

@@ -277,6 +277,73 @@ class Plan:
         _raise(status, err)
         return f, c, cnt, ms.value
 
+    @property
+    def ingest_samples_per_signal(self) -> int:
+        """Samples per signal moved host->device for host inputs (sparse
+        ingest); 0 when whole signals are copied."""
+        return int(self._lib.msfft_plan_ingest_samples(self._h))
+
+    # ---- split phases: one signal sharded by index range over GPUs ----------
+    @property
+    def values_per_signal(self) -> int:
+        """Bucket values per signal: sum over iterations of rounds x b."""
+        return int(self._lib.msfft_plan_values_per_signal(self._h))
+
+    def encode_values(self, x_local, seeds, x_lo: int, y=None, assume_valid: bool = False):
+        """Partial bucket values of the samples x[x_lo, x_lo + span) held in
+        x_local (CUDA tensor, (batch, span) or (span,)); the rest of the signal
+        counts as 0.  Summing the results of ranks whose ranges tile [0, n)
+        gives the full bucket vector (see paper_2011_05698_b200.dist).
+        Returns y: complex128 CUDA tensor (batch, values_per_signal)."""
+        import torch
+        if not (_is_torch(x_local) and x_local.is_cuda):
+            raise InvalidArgument("Plan.encode_values: x_local must be a CUDA tensor")
+        want = torch.complex128 if self.dtype in ("complex128", "c128") else torch.complex64
+        if x_local.dtype != want:
+            raise InvalidArgument(f"Plan.encode_values: x_local must be {want}")
+        xl = x_local.reshape(1, -1) if x_local.dim() == 1 else x_local
+        if xl.stride(-1) != 1:
+            raise InvalidArgument("Plan.encode_values: x_local rows must be contiguous")
+        batch, span = int(xl.shape[0]), int(xl.shape[1])
+        row_stride = span if batch == 1 else int(xl.stride(0))  # size-1 dims carry any stride
+        seeds = np.ascontiguousarray(np.asarray(seeds, dtype=np.uint64).reshape(-1))
+        if seeds.size != batch:
+            raise InvalidArgument("Plan.encode_values: need one seed per signal")
+        if y is None:
+            y = torch.empty((batch, self.values_per_signal), dtype=torch.complex128,
+                            device=xl.device)
+        err = C.create_string_buffer(1024)
+        status = self._lib.msfft_encode_values(
+            self._h, batch, C.c_void_p(xl.data_ptr()), row_stride, int(x_lo),
+            int(x_lo) + span, seeds.ctypes.data_as(C.POINTER(C.c_uint64)),
+            C.c_void_p(y.data_ptr()), _L.MSFFT_FLAG_ASSUME_VALID if assume_valid else 0,
+            C.c_void_p(0), err, 1024)
+        _raise(status, err)
+        return y
+
+    def decode_values(self, y, seeds, out=None):
+        """Selection / locate / estimate on summed bucket values y (consumed).
+        Returns (f, c, count) CUDA tensors ([B,k] int64, [B,k] complex128, [B])."""
+        import torch
+        if not (_is_torch(y) and y.is_cuda and y.dtype == torch.complex128 and y.is_contiguous()):
+            raise InvalidArgument("Plan.decode_values: y must be a contiguous complex128 CUDA tensor")
+        batch = int(y.numel() // self.values_per_signal)
+        seeds = np.ascontiguousarray(np.asarray(seeds, dtype=np.uint64).reshape(-1))
+        if seeds.size != batch:
+            raise InvalidArgument("Plan.decode_values: need one seed per signal")
+        if out is None:
+            out = (torch.zeros((batch, self.k), dtype=torch.int64, device=y.device),
+                   torch.zeros((batch, self.k), dtype=torch.complex128, device=y.device),
+                   torch.zeros(batch, dtype=torch.int64, device=y.device))
+        f, c, cnt = out
+        err = C.create_string_buffer(1024)
+        status = self._lib.msfft_decode_values(
+            self._h, batch, C.c_void_p(y.data_ptr()), seeds.ctypes.data_as(C.POINTER(C.c_uint64)),
+            C.c_void_p(f.data_ptr()), C.c_void_p(c.data_ptr()), C.c_void_p(cnt.data_ptr()),
+            C.c_void_p(0), err, 1024)
+        _raise(status, err)
+        return f, c, cnt
+
 
 def window(n: int, b: int, delta: float, device: int = -1):
     """(w, taps) exactly as design_flat_window (proj/src/window.cpp:105-177)."""

@@ -25,6 +25,8 @@ EXPORTED = (
     "msfft_plan_destroy", "msfft_plan_stats", "msfft_execute", "msfft_plan_launches",
     "msfft_window", "msfft_window_response", "msfft_trace", "msfft_plan_stage_times",
     "msfft_plan_gather_traffic", "msfft_sigma_plan", "msfft_tau_plan",
+    "msfft_plan_values_per_signal", "msfft_encode_values", "msfft_decode_values",
+    "msfft_plan_ingest_samples",
 )
 
 i64, u64, f64, i32, u32 = C.c_int64, C.c_uint64, C.c_double, C.c_int32, C.c_uint32
@@ -79,6 +81,14 @@ def lib() -> C.CDLL:
     L.msfft_plan_stage_times.restype = C.c_int
     L.msfft_plan_launches.argtypes = [VP, i64, u32]
     L.msfft_plan_launches.restype = i64
+    L.msfft_plan_ingest_samples.argtypes = [VP]
+    L.msfft_plan_ingest_samples.restype = i64
+    L.msfft_plan_values_per_signal.argtypes = [VP]
+    L.msfft_plan_values_per_signal.restype = i64
+    L.msfft_encode_values.argtypes = [VP, i64, VP, i64, i64, i64, P(u64), VP, u32, VP] + E
+    L.msfft_encode_values.restype = C.c_int
+    L.msfft_decode_values.argtypes = [VP, i64, VP, P(u64), VP, VP, VP, VP] + E
+    L.msfft_decode_values.restype = C.c_int
     L.msfft_window.argtypes = [i64, i64, f64, i32, P(i64), P(f64), i64] + E
     L.msfft_window_response.argtypes = [i64, i64, f64, i32, P(i64), i64, P(f64)] + E
     L.msfft_trace.argtypes = [VP, i64, i32, i64, i64, f64, u64, f64, P(f64), P(f64), P(i64),

@@ -21,11 +21,14 @@ LIB = os.path.join(HERE, "libmsfft_b200.so")
 CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
 CU_SOURCES = ["fft.cu", "window.cu", "sigma.cu", "encode.cu", "decode.cu", "fused.cu", "engine.cu"]
-CXX_SOURCES = ["host_plan.cpp", "capi.cpp"]
+CXX_SOURCES = ["host_plan.cpp", "ingest.cpp", "capi.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC",
                      "-Xcompiler", "-ffp-contract=off", "--expt-relaxed-constexpr"]
 CXX_FLAGS = ["-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", f"-I{CUDA_HOME}/include"]
+# the host gather / finiteness scan (integer and copy loops only) wants the
+# vectorizer
+CXX_FILE_FLAGS = {"ingest.cpp": ["-O3"]}
 
 
 def _headers():
@@ -72,7 +75,7 @@ def build(verbose: bool = False, ptxas_verbose: bool = False) -> str:
         o = os.path.join(OBJ, src + ".o")
         objs.append(o)
         if _stale(o, [s] + hdrs):
-            _run([cxx] + CXX_FLAGS + ["-c", s, "-o", o], verbose)
+            _run([cxx] + CXX_FLAGS + CXX_FILE_FLAGS.get(src, []) + ["-c", s, "-o", o], verbose)
     if _stale(LIB, objs):
         tmp = LIB + ".tmp"
         _run([NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", tmp] + objs +

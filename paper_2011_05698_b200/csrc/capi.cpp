@@ -199,6 +199,41 @@ int msfft_execute(msfft_plan plan, int64_t batch, const void* x, int64_t x_strid
     });
 }
 
+int64_t msfft_plan_ingest_samples(msfft_plan plan) {
+    if (!plan) return -1;
+    return plan->plan->ingest_samples_per_signal();
+}
+
+int64_t msfft_plan_values_per_signal(msfft_plan plan) {
+    if (!plan) return -1;
+    return plan->plan->values_per_signal();
+}
+
+int msfft_encode_values(msfft_plan plan, int64_t batch, const void* x, int64_t x_stride,
+                        int64_t x_lo, int64_t x_hi, const uint64_t* seeds, double* y,
+                        uint32_t flags, void* stream, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        if (!plan) throw std::invalid_argument("msfft_encode_values: null plan");
+        std::lock_guard<std::mutex> lock(plan->plan->mutex());
+        plan->plan->encode_values(batch, x, x_stride, x_lo, x_hi, seeds,
+                                  reinterpret_cast<double2*>(y),
+                                  !(flags & MSFFT_FLAG_ASSUME_VALID),
+                                  static_cast<cudaStream_t>(stream));
+    });
+}
+
+int msfft_decode_values(msfft_plan plan, int64_t batch, double* y, const uint64_t* seeds,
+                        int64_t* out_f, double* out_c, int64_t* out_count, void* stream,
+                        char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        if (!plan) throw std::invalid_argument("msfft_decode_values: null plan");
+        std::lock_guard<std::mutex> lock(plan->plan->mutex());
+        plan->plan->decode_values(batch, reinterpret_cast<double2*>(y), seeds, out_f,
+                                  reinterpret_cast<double2*>(out_c), out_count,
+                                  static_cast<cudaStream_t>(stream));
+    });
+}
+
 int msfft_sigma_plan(uint64_t seed, int64_t n, int32_t iterations, int64_t* sigma,
                      int64_t* sigma_inv, char* err, size_t errlen) {
     return guarded(err, errlen, [&] { draw_sigmas(seed, n, iterations, sigma, sigma_inv); });

@@ -117,6 +117,11 @@ __device__ __forceinline__ void encode_task(const DevPlan& plan, const EncTask& 
         const uint32_t sg = static_cast<uint32_t>(sigma[s * plan.iters + task.m]);
         const uint32_t mask = static_cast<uint32_t>(plan.n - 1);
         const T* xs = x + s * x_stride;
+        // index-range shard: samples outside [x_lo, x_hi) belong to another
+        // GPU and contribute 0 here (the partial bucket vectors are summed)
+        const uint32_t lo = static_cast<uint32_t>(plan.x_lo);
+        const uint32_t span = static_cast<uint32_t>(plan.x_hi - plan.x_lo);
+        const bool full = plan.x_lo == 0 && plan.x_hi == plan.n;
         uint32_t th[kEncRounds];  // tau_r + h: tap index = t' + tau_r + h (mod 2^32)
 #pragma unroll
         for (int r = 0; r < kEncRounds; ++r)
@@ -132,7 +137,18 @@ __device__ __forceinline__ void encode_task(const DevPlan& plan, const EncTask& 
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
                     const int64_t tt = t + u * stride;
-                    if (tt <= B) v[u] = ld_sample(xs + ((sg * static_cast<uint32_t>(tt)) & mask));
+                    if (tt <= B) {
+                        const uint32_t src = (sg * static_cast<uint32_t>(tt)) & mask;
+                        if (plan.x_compact) {
+                            v[u] = ld_sample(xs + task.seg_cpos[sgi] + static_cast<int32_t>(tt - A));
+                        } else if (full) {
+                            v[u] = ld_sample(xs + src);
+                        } else {
+                            v[u].x = 0;
+                            v[u].y = 0;
+                            if (src - lo < span) v[u] = ld_sample(xs + (src - lo));
+                        }
+                    }
                 }
 #pragma unroll
                 for (int u = 0; u < U; ++u) {

@@ -1,5 +1,6 @@
 // engine.cu -- see engine.hpp.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <cstdlib>
@@ -65,6 +66,8 @@ Plan::Plan(int64_t n, int64_t k, int64_t l, double q, double delta, bool c128, i
     P.l = l;
     P.q = q;
     P.inv_n = 1.0 / static_cast<double>(n);
+    P.x_lo = 0;
+    P.x_hi = n;
     P.iters = sched_.iterations;
     P.values_per_signal = sched_.values_per_signal;
     P.acc_cap = sched_.acc_cap;
@@ -146,6 +149,18 @@ Plan::Plan(int64_t n, int64_t k, int64_t l, double q, double delta, bool c128, i
     if (const char* e = std::getenv("MSFFT_FUSED_LAG")) fused_lag_ = std::max(1LL, std::atoll(e));
     fused_smem_ = std::max(enc_smem_, lay_.in_smem ? static_cast<size_t>(lay_.bytes) : size_t{0});
     flags_.reset(2);
+    imap_ = make_ingest_map(sched_);
+    dplan_compact_ = dplan_;
+    dplan_compact_.x_compact = 1;
+    if (const char* e = std::getenv("MSFFT_SPARSE_INGEST")) ingest_enabled_ = std::atoi(e) != 0;
+    if (const char* e = std::getenv("MSFFT_INGEST_CHUNK")) ingest_chunk_ = std::max(1LL, std::atoll(e));
+    if (const char* e = std::getenv("MSFFT_DMA_VALIDATE_SHARE")) {
+        dma_share_ = std::min(1.0, std::max(0.0, std::atof(e)));
+        dma_share_fixed_ = true;
+    }
+    MSFFT_CUDA(cudaStreamCreateWithFlags(&vstream_, cudaStreamNonBlocking));
+    MSFFT_CUDA(cudaEventCreate(&ev_vbeg_));
+    MSFFT_CUDA(cudaEventCreate(&ev_vend_));
 }
 
 Plan::~Plan() {
@@ -166,6 +181,11 @@ Plan::~Plan() {
     if (ev_chunk_) cudaEventDestroy(ev_chunk_);
     if (ev_dec_done_) cudaEventDestroy(ev_dec_done_);
     if (h_seeds_) cudaFreeHost(h_seeds_);
+    for (int i = 0; i < 2; ++i)
+        if (gstage_[i]) cudaFreeHost(gstage_[i]);
+    if (vstream_) cudaStreamDestroy(vstream_);
+    if (ev_vbeg_) cudaEventDestroy(ev_vbeg_);
+    if (ev_vend_) cudaEventDestroy(ev_vend_);
     cudaSetDevice(cur);
 }
 
@@ -261,6 +281,7 @@ void Plan::append_tasks(std::vector<EncTask>& v, int64_t s_begin, int64_t s_end)
             for (size_t i = 0; i < merged.size(); ++i) {
                 t.seg_lo[i] = static_cast<int32_t>(merged[i].first);
                 t.seg_hi[i] = static_cast<int32_t>(merged[i].second);
+                t.seg_cpos[i] = static_cast<int32_t>(imap_.position(m, merged[i].first));
             }
             if (di.b <= kEncThreads) {
                 t.fused = 1;
@@ -307,8 +328,9 @@ int64_t Plan::launches(int64_t batch, bool validate, bool serial) const {
 void Plan::run_chunk(int64_t batch, const void* d_x, int64_t x_stride, const int64_t* d_sig,
                      const int64_t* d_sig_inv, int64_t* d_out_f, double2* d_out_c,
                      int64_t* d_out_count, bool validate, cudaStream_t st,
-                     const ExecOptions& opt) {
+                     const ExecOptions& opt, bool compact) {
     const int64_t n = sched_.n;
+    const DevPlan& P = compact ? dplan_compact_ : dplan_;
     if (validate) {
         const int64_t total = n * batch;
         const unsigned blocks =
@@ -326,7 +348,7 @@ void Plan::run_chunk(int64_t batch, const void* d_x, int64_t x_stride, const int
         // one persistent launch: encode and decode share the SMs
         const FusedSet& fs = fused_for(batch);
         if (opt.stage_times) MSFFT_CUDA(cudaEventRecord(ev_stage_[0], st));
-        launch_fused(dplan_, lay_, fs.fw, d_x, c128_, x_stride, batch, d_sig, d_sig_inv,
+        launch_fused(P, lay_, fs.fw, d_x, c128_, x_stride, batch, d_sig, d_sig_inv,
                      y_.get(), dec_work_.get(), d_out_f, d_out_c, d_out_count, flags_.get(),
                      fused_smem_, st);
         if (opt.stage_times) {
@@ -351,7 +373,7 @@ void Plan::run_chunk(int64_t batch, const void* d_x, int64_t x_stride, const int
             const TaskSet& tsc = tasks_for(cb);
             const void* xc = static_cast<const unsigned char*>(d_x) + c0 * x_stride * elem;
             double2* yc = y_.get() + c0 * vps;
-            launch_encode(dplan_, tsc.d.get(), tsc.count, xc, c128_, x_stride, cb,
+            launch_encode(P, tsc.d.get(), tsc.count, xc, c128_, x_stride, cb,
                           d_sig + c0 * iters, yc, enc_smem_, st);
             for (int m : big_b_iters_) {
                 const DevIter& di = dplan_.it[m];
@@ -371,7 +393,7 @@ void Plan::run_chunk(int64_t batch, const void* d_x, int64_t x_stride, const int
     }
     const TaskSet& ts = tasks_for(batch);
     if (opt.stage_times) MSFFT_CUDA(cudaEventRecord(ev_stage_[0], st));
-    launch_encode(dplan_, ts.d.get(), ts.count, d_x, c128_, x_stride, batch, d_sig, y_.get(),
+    launch_encode(P, ts.d.get(), ts.count, d_x, c128_, x_stride, batch, d_sig, y_.get(),
                   enc_smem_, st);
     if (opt.stage_times) MSFFT_CUDA(cudaEventRecord(ev_stage_[1], st));
     for (int m : big_b_iters_) {
@@ -425,22 +447,14 @@ void Plan::execute(int64_t batch, const void* x, int64_t x_stride, const uint64_
     cudaStream_t st = opt.stream ? opt.stream : own_stream_;
     const size_t elem = c128_ ? sizeof(double2) : sizeof(float2);
 
-    if (h_seeds_cap_ < batch) {
-        if (h_seeds_) cudaFreeHost(h_seeds_);
-        h_seeds_ = nullptr;
-        MSFFT_CUDA(cudaMallocHost(&h_seeds_, sizeof(uint64_t) * batch));
-        h_seeds_cap_ = batch;
-    }
-
     // chunking: device inputs run as one chunk; host inputs stream through
     // two staging buffers overlapped with compute
     const int64_t sig_bytes = static_cast<int64_t>(elem) * n;
+    const bool sparse = !opt.x_on_device && sparse_ingest();
     const int64_t chunk =
         opt.x_on_device ? batch
+        : sparse        ? std::min(batch, ingest_chunk_)
                         : std::max<int64_t>(1, std::min<int64_t>(batch, kChunkBytes / sig_bytes));
-    sig_.ensure(static_cast<size_t>(batch * iters));
-    sig_inv_.ensure(static_cast<size_t>(batch * iters));
-    seeds_.ensure(static_cast<size_t>(batch));
     y_.ensure(static_cast<size_t>(chunk * dplan_.values_per_signal));
     if (!lay_.in_smem) dec_work_.ensure(static_cast<size_t>(chunk * lay_.bytes));
     if (!opt.out_on_device) {
@@ -448,7 +462,7 @@ void Plan::execute(int64_t batch, const void* x, int64_t x_stride, const uint64_
         out_c_.ensure(static_cast<size_t>(batch * k));
         out_count_.ensure(static_cast<size_t>(batch));
     }
-    if (!opt.x_on_device)
+    if (!opt.x_on_device && !sparse)
         for (int i = 0; i < 2; ++i) xstage_[i].ensure(static_cast<size_t>(chunk * sig_bytes));
 
     int64_t* d_of = opt.out_on_device ? out_f : out_f_.get();
@@ -458,16 +472,14 @@ void Plan::execute(int64_t batch, const void* x, int64_t x_stride, const uint64_
     stage_ms_[0] = stage_ms_[1] = stage_ms_[2] = 0.0;
     MSFFT_CUDA(cudaEventRecord(ev_start_, st));
     MSFFT_CUDA(cudaMemsetAsync(flags_.get(), 0, 2 * sizeof(int32_t), st));
-    // sigma plan: exact mt19937_64 draws on the device, one thread per signal
-    MSFFT_CUDA(cudaStreamSynchronize(st));  // previous use of the pinned seed staging
-    std::memcpy(h_seeds_, seeds, sizeof(uint64_t) * batch);
-    MSFFT_CUDA(cudaMemcpyAsync(seeds_.get(), h_seeds_, sizeof(uint64_t) * batch,
-                               cudaMemcpyHostToDevice, st));
-    launch_sigma(seeds_.get(), batch, iters, n, sig_.get(), sig_inv_.get(), st);
+    upload_sigmas(batch, seeds, st);
     const bool validate = !opt.assume_valid;
+    bool host_bad = false;
     if (opt.x_on_device) {
         run_chunk(batch, x, x_stride, sig_.get(), sig_inv_.get(), d_of, d_oc, d_ocnt, validate,
                   st, opt);
+    } else if (sparse) {
+        host_bad = execute_sparse(batch, x, x_stride, seeds, d_of, d_oc, d_ocnt, validate, st, opt);
     } else {
         MSFFT_CUDA(cudaStreamWaitEvent(copy_stream_, ev_start_, 0));
         const unsigned char* hx = static_cast<const unsigned char*>(x);
@@ -500,19 +512,203 @@ void Plan::execute(int64_t batch, const void* x, int64_t x_stride, const uint64_
         MSFFT_CUDA(cudaMemcpyAsync(out_count, d_ocnt, sizeof(int64_t) * batch,
                                    cudaMemcpyDeviceToHost, st));
     }
-    int32_t hflags[2] = {0, 0};
-    MSFFT_CUDA(cudaMemcpyAsync(hflags, flags_.get(), sizeof(hflags), cudaMemcpyDeviceToHost, st));
     MSFFT_CUDA(cudaEventRecord(ev_end_, st));
-    MSFFT_CUDA(cudaEventSynchronize(ev_end_));
     if (device_ms) {
+        MSFFT_CUDA(cudaEventSynchronize(ev_end_));
         float ms = 0.f;
         MSFFT_CUDA(cudaEventElapsedTime(&ms, ev_start_, ev_end_));
         *device_ms = ms;
     }
+    if (host_bad) {
+        MSFFT_CUDA(cudaStreamSynchronize(st));
+        throw std::invalid_argument("ComplexSignal: non-finite sample");
+    }
+    check_flags(st);
+}
+
+bool Plan::execute_sparse(int64_t batch, const void* x, int64_t x_stride, const uint64_t* seeds,
+                          int64_t* d_of, double2* d_oc, int64_t* d_ocnt, bool validate,
+                          cudaStream_t st, const ExecOptions& opt) {
+    const int64_t n = sched_.n, k = sched_.k, C = imap_.per_signal;
+    const int iters = sched_.iterations;
+    const size_t elem = c128_ ? sizeof(double2) : sizeof(float2);
+    const int64_t chunk = std::min(batch, ingest_chunk_);
+    const size_t stage_bytes = static_cast<size_t>(chunk * C) * elem;
+    if (!pool_) pool_ = std::make_unique<HostPool>(ingest_threads());
+    if (gstage_cap_ < stage_bytes) {
+        MSFFT_CUDA(cudaStreamSynchronize(copy_stream_));
+        for (int i = 0; i < 2; ++i) {
+            if (gstage_[i]) cudaFreeHost(gstage_[i]);
+            gstage_[i] = nullptr;
+            MSFFT_CUDA(cudaHostAlloc(&gstage_[i], stage_bytes, cudaHostAllocDefault));
+        }
+        gstage_cap_ = stage_bytes;
+    }
+    for (int i = 0; i < 2; ++i) xstage_[i].ensure(stage_bytes);
+    // the host's copy of the sigma plan (the device draws the same values)
+    hsig_.resize(static_cast<size_t>(batch * iters));
+    hsig_inv_.resize(static_cast<size_t>(batch * iters));
+    pool_->run(batch, [&](int64_t s) {
+        draw_sigmas(seeds[s], n, iters, hsig_.data() + s * iters, hsig_inv_.data() + s * iters);
+    });
+    const unsigned char* hx = static_cast<const unsigned char*>(x);
+    bool bad = false;
+    // validation split (see engine.hpp): rebalance from the last split's
+    // timings, then queue the DMA + device check of rows [0, n_dma)
+    if (dma_pending_) {
+        float dma_ms = 0.f;
+        if (cudaEventElapsedTime(&dma_ms, ev_vbeg_, ev_vend_) == cudaSuccess && dma_ms > 0.f &&
+            last_host_ms_ > 0.0 && !dma_share_fixed_) {
+            const double gap = (last_host_ms_ - dma_ms) / (last_host_ms_ + dma_ms);
+            dma_share_ = std::min(0.9, std::max(0.0, dma_share_ + 0.5 * gap * (1.0 - dma_share_)));
+        }
+        dma_pending_ = false;
+    }
+    // the copy engine only runs asynchronously from page-locked memory
+    cudaPointerAttributes pa{};
+    const bool pinned = cudaPointerGetAttributes(&pa, x) == cudaSuccess &&
+                        pa.type == cudaMemoryTypeHost;
+    cudaGetLastError();
+    const int64_t n_dma =
+        validate && pinned ? static_cast<int64_t>(dma_share_ * static_cast<double>(batch)) : 0;
+    if (n_dma > 0) {
+        const size_t sig_bytes = static_cast<size_t>(n) * elem;
+        const int64_t vchunk = std::max<int64_t>(1, static_cast<int64_t>((size_t{256} << 20) / sig_bytes));
+        vstage_.ensure(static_cast<size_t>(vchunk) * sig_bytes);
+        MSFFT_CUDA(cudaEventRecord(ev_chunk_, st));  // after the flag reset
+        MSFFT_CUDA(cudaStreamWaitEvent(vstream_, ev_chunk_, 0));
+        MSFFT_CUDA(cudaEventRecord(ev_vbeg_, vstream_));
+        for (int64_t s0 = 0; s0 < n_dma; s0 += vchunk) {
+            const int64_t cb = std::min(vchunk, n_dma - s0);
+            if (x_stride == n)
+                MSFFT_CUDA(cudaMemcpyAsync(vstage_.get(), hx + s0 * x_stride * elem, cb * sig_bytes,
+                                           cudaMemcpyHostToDevice, vstream_));
+            else
+                MSFFT_CUDA(cudaMemcpy2DAsync(vstage_.get(), sig_bytes, hx + s0 * x_stride * elem,
+                                             x_stride * elem, sig_bytes, cb,
+                                             cudaMemcpyHostToDevice, vstream_));
+            const int64_t total = n * cb;
+            const unsigned blocks =
+                static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, 148 * 16));
+            if (c128_)
+                validate_kernel<double2><<<blocks, 256, 0, vstream_>>>(
+                    reinterpret_cast<const double2*>(vstage_.get()), n, n, cb, flags_.get() + 1);
+            else
+                validate_kernel<float2><<<blocks, 256, 0, vstream_>>>(
+                    reinterpret_cast<const float2*>(vstage_.get()), n, n, cb, flags_.get() + 1);
+            MSFFT_LAUNCH_CHECK("validate_kernel");
+        }
+        MSFFT_CUDA(cudaEventRecord(ev_vend_, vstream_));
+    }
+    const auto host_t0 = std::chrono::steady_clock::now();
+    MSFFT_CUDA(cudaStreamWaitEvent(copy_stream_, ev_start_, 0));
+    int64_t idx = 0;
+    for (int64_t s0 = 0; s0 < batch; s0 += chunk, ++idx) {
+        const int64_t cb = std::min(chunk, batch - s0);
+        const int slot = static_cast<int>(idx & 1);
+        // the pinned slot's previous H2D must be done before it is refilled
+        if (idx >= 2) MSFFT_CUDA(cudaEventSynchronize(ev_copied_[slot]));
+        bad |= gather_compact(*pool_, imap_, n, iters, hx + s0 * x_stride * elem, x_stride,
+                              static_cast<int>(elem), cb, hsig_.data() + s0 * iters, gstage_[slot],
+                              validate, n_dma - s0);
+        if (idx >= 2) MSFFT_CUDA(cudaStreamWaitEvent(copy_stream_, ev_free_[slot], 0));
+        MSFFT_CUDA(cudaMemcpyAsync(xstage_[slot].get(), gstage_[slot],
+                                   static_cast<size_t>(cb * C) * elem, cudaMemcpyHostToDevice,
+                                   copy_stream_));
+        MSFFT_CUDA(cudaEventRecord(ev_copied_[slot], copy_stream_));
+        MSFFT_CUDA(cudaStreamWaitEvent(st, ev_copied_[slot], 0));
+        run_chunk(cb, xstage_[slot].get(), C, sig_.get() + s0 * iters, sig_inv_.get() + s0 * iters,
+                  d_of + s0 * k, d_oc + s0 * k, d_ocnt + s0, false, st, opt, true);
+        MSFFT_CUDA(cudaEventRecord(ev_free_[slot], st));
+    }
+    if (n_dma > 0) {
+        last_host_ms_ = std::chrono::duration<double, std::milli>(
+                            std::chrono::steady_clock::now() - host_t0).count();
+        dma_pending_ = true;
+        MSFFT_CUDA(cudaStreamWaitEvent(st, ev_vend_, 0));  // flags_[1] complete before the check
+    }
+    return bad;
+}
+
+void Plan::upload_sigmas(int64_t batch, const uint64_t* seeds, cudaStream_t st) {
+    // sigma plan: exact mt19937_64 draws on the device, one thread per signal
+    const int iters = sched_.iterations;
+    if (h_seeds_cap_ < batch) {
+        MSFFT_CUDA(cudaStreamSynchronize(st));
+        if (h_seeds_) cudaFreeHost(h_seeds_);
+        h_seeds_ = nullptr;
+        MSFFT_CUDA(cudaMallocHost(&h_seeds_, sizeof(uint64_t) * batch));
+        h_seeds_cap_ = batch;
+    }
+    sig_.ensure(static_cast<size_t>(batch * iters));
+    sig_inv_.ensure(static_cast<size_t>(batch * iters));
+    seeds_.ensure(static_cast<size_t>(batch));
+    MSFFT_CUDA(cudaStreamSynchronize(st));  // previous use of the pinned seed staging
+    std::memcpy(h_seeds_, seeds, sizeof(uint64_t) * batch);
+    MSFFT_CUDA(cudaMemcpyAsync(seeds_.get(), h_seeds_, sizeof(uint64_t) * batch,
+                               cudaMemcpyHostToDevice, st));
+    launch_sigma(seeds_.get(), batch, iters, sched_.n, sig_.get(), sig_inv_.get(), st);
+}
+
+void Plan::check_flags(cudaStream_t st) {
+    int32_t hflags[2] = {0, 0};
+    MSFFT_CUDA(cudaMemcpyAsync(hflags, flags_.get(), sizeof(hflags), cudaMemcpyDeviceToHost, st));
+    MSFFT_CUDA(cudaStreamSynchronize(st));
     if (hflags[1]) throw std::invalid_argument("ComplexSignal: non-finite sample");
     if (hflags[0] == kDecErrPhaseZero) throw std::domain_error("phase_of: zero value");
     if (hflags[0] == kDecErrRounds)
         throw std::invalid_argument("locate_frequency: not enough rounds for the schedule");
+}
+
+void Plan::encode_values(int64_t batch, const void* d_x, int64_t x_stride, int64_t x_lo,
+                         int64_t x_hi, const uint64_t* seeds, double2* d_y, bool validate,
+                         cudaStream_t stream) {
+    DeviceGuard dg(device_);
+    if (batch <= 0) return;
+    const int64_t n = sched_.n;
+    if (x_lo < 0 || x_hi > n || x_lo >= x_hi)
+        throw std::invalid_argument("msfft_encode_values: need 0 <= x_lo < x_hi <= n");
+    if (x_stride < x_hi - x_lo) throw std::invalid_argument("msfft_encode_values: x_stride < x_hi - x_lo");
+    cudaStream_t st = stream ? stream : own_stream_;
+    MSFFT_CUDA(cudaMemsetAsync(flags_.get(), 0, 2 * sizeof(int32_t), st));
+    upload_sigmas(batch, seeds, st);
+    if (validate) {
+        const int64_t span = x_hi - x_lo, total = span * batch;
+        const unsigned blocks =
+            static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, 148 * 16));
+        if (c128_)
+            validate_kernel<double2><<<blocks, 256, 0, st>>>(
+                static_cast<const double2*>(d_x), span, x_stride, batch, flags_.get() + 1);
+        else
+            validate_kernel<float2><<<blocks, 256, 0, st>>>(
+                static_cast<const float2*>(d_x), span, x_stride, batch, flags_.get() + 1);
+        MSFFT_LAUNCH_CHECK("validate_kernel");
+    }
+    DevPlan p = dplan_;
+    p.x_lo = x_lo;
+    p.x_hi = x_hi;
+    const TaskSet& ts = tasks_for(batch);
+    launch_encode(p, ts.d.get(), ts.count, d_x, c128_, x_stride, batch, sig_.get(), d_y,
+                  enc_smem_, st);
+    for (int m : big_b_iters_) {
+        const DevIter& di = dplan_.it[m];
+        fft_radix2_batched(d_y + di.yoff, di.b, batch * di.nrounds, di.nrounds,
+                           dplan_.values_per_signal, -1, dplan_.inv_n, st);
+    }
+    check_flags(st);
+}
+
+void Plan::decode_values(int64_t batch, double2* d_y, const uint64_t* seeds, int64_t* d_out_f,
+                         double2* d_out_c, int64_t* d_out_count, cudaStream_t stream) {
+    DeviceGuard dg(device_);
+    if (batch <= 0) return;
+    cudaStream_t st = stream ? stream : own_stream_;
+    if (!lay_.in_smem) dec_work_.ensure(static_cast<size_t>(batch * lay_.bytes));
+    MSFFT_CUDA(cudaMemsetAsync(flags_.get(), 0, 2 * sizeof(int32_t), st));
+    upload_sigmas(batch, seeds, st);
+    launch_decode(dplan_, lay_, d_y, sig_.get(), sig_inv_.get(), batch, dec_work_.get(), d_out_f,
+                  d_out_c, d_out_count, flags_.get(), st);
+    check_flags(st);
 }
 
 std::shared_ptr<Plan> cached_plan(int64_t n, int64_t k, int64_t l, double q, double delta,

@@ -20,6 +20,7 @@
 #include "encode.hpp"
 #include "fused.hpp"
 #include "host_plan.hpp"
+#include "ingest.hpp"
 #include "plan_dev.cuh"
 #include "window.hpp"
 
@@ -55,7 +56,28 @@ public:
                  int64_t* out_f, double* out_c, int64_t* out_count, const ExecOptions& opt,
                  double* device_ms);
 
+    // Split phases for index-range sharding of one signal over several GPUs
+    // (DESIGN.md "Multi-GPU").  encode_values: the bucket values of every
+    // round of every iteration, reading only x[x_lo, x_hi) (d_x points at
+    // x_lo); samples outside contribute 0, so the partial vectors of ranks
+    // holding disjoint ranges sum to the full vector.  decode_values: the
+    // selection/locate/estimate of each iteration on a summed vector (d_y is
+    // consumed: subtraction happens in place).  All pointers are device
+    // pointers; seeds are host values.
+    void encode_values(int64_t batch, const void* d_x, int64_t x_stride, int64_t x_lo,
+                       int64_t x_hi, const uint64_t* seeds, double2* d_y, bool validate,
+                       cudaStream_t stream);
+    void decode_values(int64_t batch, double2* d_y, const uint64_t* seeds, int64_t* d_out_f,
+                       double2* d_out_c, int64_t* d_out_count, cudaStream_t stream);
+    int64_t values_per_signal() const { return dplan_.values_per_signal; }
+
     int64_t launches(int64_t batch, bool validate, bool serial = false) const;
+
+    // compact samples per signal moved by sparse host ingest (0 if the plan
+    // uses the dense H2D path for host inputs)
+    int64_t ingest_samples_per_signal() const { return sparse_ingest() ? imap_.per_signal : 0; }
+    double dma_validate_share() const { return dma_share_; }
+    bool sparse_ingest() const { return ingest_enabled_ && imap_.per_signal * 4 <= sched_.n; }
 
     // [encode, bucket fft (b > 256), decode] ms of the last execute run with
     // stage_times (summed over chunks).
@@ -76,16 +98,24 @@ private:
     const TaskSet& tasks_for(int64_t batch);
     const FusedSet& fused_for(int64_t batch);
     void append_tasks(std::vector<EncTask>& v, int64_t s_begin, int64_t s_end) const;
+    void upload_sigmas(int64_t batch, const uint64_t* seeds, cudaStream_t st);
+    void check_flags(cudaStream_t st);
     void run_chunk(int64_t batch, const void* d_x, int64_t x_stride, const int64_t* d_sig,
                    const int64_t* d_sig_inv, int64_t* d_out_f, double2* d_out_c,
                    int64_t* d_out_count, bool validate, cudaStream_t st,
-                   const ExecOptions& opt);
+                   const ExecOptions& opt, bool compact = false);
+    // host input, sparse ingest (ingest.hpp); returns true if the host scan
+    // saw a non-finite sample
+    bool execute_sparse(int64_t batch, const void* x, int64_t x_stride, const uint64_t* seeds,
+                        int64_t* d_of, double2* d_oc, int64_t* d_ocnt, bool validate,
+                        cudaStream_t st, const ExecOptions& opt);
 
     int device_;
     bool c128_;
     SchedulePlan sched_;
     std::vector<std::shared_ptr<const DeviceWindow>> windows_;
     DevPlan dplan_{};
+    DevPlan dplan_compact_{};  // dplan_ with x_compact = 1
     DecLayout lay_{};
     size_t enc_smem_ = 0;
     int64_t b_max_ = 0, budget_max_ = 0;
@@ -113,6 +143,24 @@ private:
     DeviceBuffer<double2> out_c_;
     DeviceBuffer<int32_t> flags_;  // [0] decode error, [1] non-finite input
     DeviceBuffer<unsigned char> xstage_[2];
+    // sparse host ingest
+    IngestMap imap_;
+    bool ingest_enabled_ = true;     // MSFFT_SPARSE_INGEST=0 forces dense H2D
+    int64_t ingest_chunk_ = 128;     // signals per gather / H2D chunk
+    std::unique_ptr<HostPool> pool_;
+    void* gstage_[2] = {nullptr, nullptr};  // pinned compact staging
+    size_t gstage_cap_ = 0;
+    std::vector<int64_t> hsig_, hsig_inv_;
+    // validation split: the first dma_share_ of a validating host batch is
+    // copied whole by the copy engine and checked by validate_kernel while
+    // host threads scan the rest; the share adapts so both finish together
+    double dma_share_ = 0.3;
+    bool dma_share_fixed_ = false;      // MSFFT_DMA_VALIDATE_SHARE given
+    bool dma_pending_ = false;          // timings of the last split to read
+    double last_host_ms_ = 0.0;
+    cudaStream_t vstream_ = nullptr;
+    cudaEvent_t ev_vbeg_ = nullptr, ev_vend_ = nullptr;
+    DeviceBuffer<unsigned char> vstage_;
     DeviceBuffer<uint64_t> seeds_;
     uint64_t* h_seeds_ = nullptr;  // pinned staging
     int64_t h_seeds_cap_ = 0;

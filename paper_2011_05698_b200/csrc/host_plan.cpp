@@ -91,23 +91,27 @@ int64_t count_samples_used(const SchedulePlan& plan, const int64_t* sigma) {
     return distinct;
 }
 
+std::vector<std::pair<int64_t, int64_t>> iteration_union(const IterationPlan& it) {
+    const int64_t h = (it.w - 1) / 2;
+    std::vector<std::pair<int64_t, int64_t>> iv;
+    for (int64_t tau : it.taus) iv.emplace_back(-h - tau, h - tau);
+    std::sort(iv.begin(), iv.end());
+    std::vector<std::pair<int64_t, int64_t>> merged;
+    for (const auto& seg : iv) {
+        if (!merged.empty() && seg.first <= merged.back().second + 1)
+            merged.back().second = std::max(merged.back().second, seg.second);
+        else
+            merged.push_back(seg);
+    }
+    return merged;
+}
+
 void gather_traffic(const SchedulePlan& plan, const int64_t* sigma, int elem_bytes,
                     int64_t* loads, int64_t* sectors) {
     const uint64_t mask = static_cast<uint64_t>(plan.n - 1);
     std::vector<uint64_t> sec;
     for (int m = 0; m < plan.iterations; ++m) {
-        const IterationPlan& it = plan.iters[m];
-        const int64_t h = (it.w - 1) / 2;
-        std::vector<std::pair<int64_t, int64_t>> iv;
-        for (int64_t tau : it.taus) iv.emplace_back(-h - tau, h - tau);
-        std::sort(iv.begin(), iv.end());
-        std::vector<std::pair<int64_t, int64_t>> merged;
-        for (const auto& seg : iv) {
-            if (!merged.empty() && seg.first <= merged.back().second + 1)
-                merged.back().second = std::max(merged.back().second, seg.second);
-            else
-                merged.push_back(seg);
-        }
+        const auto merged = iteration_union(plan.iters[m]);
         sec.clear();
         const uint64_t s = static_cast<uint64_t>(sigma[m]);
         for (const auto& seg : merged)

@@ -85,6 +85,10 @@ void draw_sigmas(uint64_t seed, int64_t n, int iterations, int64_t* sigma, int64
 // on the plan, never on the data.
 int64_t count_samples_used(const SchedulePlan& plan, const int64_t* sigma);
 
+// The t' intervals [-h - tau_r, h - tau_r] of all rounds of iteration `it`,
+// merged and ascending: the samples x[sigma * t' mod n] one iteration reads.
+std::vector<std::pair<int64_t, int64_t>> iteration_union(const IterationPlan& it);
+
 // Algorithmic traffic of the fused gather for one signal: per iteration the
 // kernel loads every distinct t' of the union of the rounds' tap intervals
 // once.  Adds to *loads the number of such samples and to *sectors the

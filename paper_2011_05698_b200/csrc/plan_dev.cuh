@@ -41,9 +41,15 @@ struct DevIter {
 
 struct DevPlan {
     int64_t n, k, l;
+    // the samples this encode may read: x holds x[x_lo, x_hi) (index-range
+    // sharding of one signal across GPUs; [0, n) otherwise)
+    int64_t x_lo, x_hi;
     double q, inv_n;
     int64_t values_per_signal, acc_cap;
-    int32_t iters, pad_;
+    int32_t iters;
+    // 1: x rows hold the compact samples of sparse host ingest (ingest.hpp):
+    // the sample of t' is x[task.seg_cpos[seg] + (t' - seg_lo[seg])]
+    int32_t x_compact;
     DevIter it[kMaxIters];
     int64_t taus[kMaxTaus];
 };
@@ -58,6 +64,7 @@ struct EncTask {
     int32_t lane0;           // first residue class (non-fused: 256-wide slice)
     int32_t nseg, pad_;
     int32_t seg_lo[kEncRounds], seg_hi[kEncRounds];  // merged t' intervals
+    int32_t seg_cpos[kEncRounds];  // compact position of seg_lo (sparse ingest)
 };
 
 }  // namespace msfft_b200

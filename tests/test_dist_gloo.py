@@ -80,3 +80,52 @@ def test_reference_arm_small_config_json():
     line = json.loads(r.stdout.strip().splitlines()[-1])
     assert line["impl"] == "reference" and line["value"] > 0
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["cpu_baseline"]["cores"] >= 1
+
+
+def _partial_worker(rank, world, port, q):
+    """Index-range sharding of one signal: each rank bucketizes only its
+    samples (the oracle stands in for the device encode), combine_partials
+    sums the partial vectors over gloo."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    sys.path.insert(0, REPO)
+    from oracle import load
+    from paper_2011_05698_b200 import dist as D
+    from paper_2011_05698_b200.workloads import make_signal_np
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    o = load("port")
+    n, b, delta = 1 << 14, 64, 1e-6
+    x, _, _ = make_signal_np(n, 20, 77, 20.0)
+    lo, hi = D.index_range(n, rank, world)
+    xm = np.zeros_like(x)
+    xm[lo:hi] = x[lo:hi]
+    rounds = [(12345, 0), (12345, 97), (4097, 5)]  # (sigma, tau)
+    part = np.concatenate([o.bucketize(xm, b, delta, s, t) for s, t in rounds])
+    y = torch.from_numpy(part.copy())
+    D.combine_partials(y)
+    full = np.concatenate([o.bucketize(x, b, delta, s, t) for s, t in rounds])
+    q.put((rank, lo, hi, float(np.max(np.abs(y.numpy() - full)) / np.max(np.abs(full)))))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_index_range_partials_sum_to_full(world):
+    from oracle import available
+    if not available("port"):
+        pytest.skip("oracle port not built")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_partial_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=180) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    # ranges tile [0, n) and the summed partials equal the full bucket values
+    assert res[0][1] == 0 and res[-1][2] == 1 << 14
+    assert all(a[2] == b[1] for a, b in zip(res, res[1:]))
+    assert max(r[3] for r in res) < 1e-13

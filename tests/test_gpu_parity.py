@@ -193,3 +193,55 @@ def test_large_size_goldens(oracle, golden):
                       TOL[rec["dtype"]])
         assert r.stats.samples_used == stats["samples_used"]
         assert r.stats.stage_counts == stats["stage_counts"]
+
+
+@pytest.mark.parametrize("dtype", ["complex64", "complex128"])
+def test_sparse_ingest_matches_device_and_dense(oracle, monkeypatch, dtype):
+    """Host inputs go through sparse ingest (host gather of the samples the
+    transform reads, compact H2D, coalesced encode reads): bitwise equal to
+    device-resident inputs and to the dense whole-signal H2D path, across
+    several pipeline chunks."""
+    import torch
+    n, k, delta = 1 << 20, 30, 1e-6
+    xs = np.stack([make_signal(oracle, dict(gen="np", n=n, k=k, seed=40 + s, snr=20.0,
+                                            dtype=dtype)) for s in range(5)]).astype(dtype)
+    seeds = np.arange(500, 505, dtype=np.uint64)
+    monkeypatch.setenv("MSFFT_INGEST_CHUNK", "2")
+    plan = M.Plan(n, k, M.MultiscaleConfig(), delta, dtype)
+    assert 0 < plan.ingest_samples_per_signal <= n // 4
+    f, c, cnt, _ = plan.execute(xs, seeds)
+    out = (torch.empty((5, k), dtype=torch.int64, device="cuda"),
+           torch.empty((5, k), dtype=torch.complex128, device="cuda"),
+           torch.empty((5,), dtype=torch.int64, device="cuda"))
+    plan.execute(torch.as_tensor(xs).cuda(), seeds, out=out)
+    assert np.array_equal(cnt, out[2].cpu().numpy())
+    assert np.array_equal(f, out[0].cpu().numpy())
+    assert np.array_equal(c, out[1].cpu().numpy())
+    monkeypatch.setenv("MSFFT_SPARSE_INGEST", "0")
+    dense = M.Plan(n, k, M.MultiscaleConfig(), delta, dtype)
+    assert dense.ingest_samples_per_signal == 0
+    f2, c2, cnt2, _ = dense.execute(xs, seeds)
+    assert np.array_equal(cnt, cnt2) and np.array_equal(f, f2) and np.array_equal(c, c2)
+    for i in range(5):
+        ref = oracle.sfft4(xs[i].astype(np.complex128), k, 16, 1.0, int(seeds[i]), delta)
+        m = int(cnt[i])
+        assert_parity(ref.f, ref.c, f[i, :m], c[i, :m], k, delta, TOL[dtype])
+
+
+def test_sparse_ingest_validates_every_sample():
+    """The host scan covers all n samples, not only the gathered ones
+    (ComplexSignal::validate, proj/src/signal.cpp:18-26)."""
+    n, k = 1 << 20, 10
+    plan = M.Plan(n, k, M.MultiscaleConfig(), 1e-6, "complex64")
+    assert plan.ingest_samples_per_signal > 0
+    x = np.zeros((3, n), np.complex64)
+    x[2, n - 1] = np.inf
+    with pytest.raises(M.InvalidArgument, match="ComplexSignal: non-finite sample"):
+        plan.execute(x, [1, 2, 3])
+    x[2, n - 1] = 0
+    x[1, 12345] = complex(0, np.nan)
+    with pytest.raises(M.InvalidArgument, match="ComplexSignal: non-finite sample"):
+        plan.execute(x, [1, 2, 3])
+    x[1, 12345] = 0
+    f, c, cnt, _ = plan.execute(x, [1, 2, 3])
+    assert list(cnt) == [0, 0, 0]

@@ -21,6 +21,9 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--log2n", type=int, default=27)
 ap.add_argument("--k", type=int, default=10000)
 ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--shards", type=int, default=0,
+                help="also run the index-range-sharded split path with G ranks, one "
+                     "after another on this GPU, and compare it with the single-GPU result")
 a = ap.parse_args()
 n, k, delta = 1 << a.log2n, a.k, 1e-6
 dev = torch.device("cuda", 0)
@@ -46,6 +49,35 @@ f1, c1, n1 = [t.cpu().numpy() for t in out]
 plan.execute(x * 2, seeds, out=out, assume_valid=True, stream=sh)
 f2, c2, n2 = [t.cpu().numpy() for t in out]
 m = int(n1[0])
+shard = None
+if a.shards:
+    from paper_2011_05698_b200.dist import index_range
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    enc_ms, y = [], None
+    for r in range(a.shards):
+        lo, hi = index_range(n, r, a.shards)
+        xl = x[:, lo:hi].contiguous()
+        plan.encode_values(xl, seeds, lo, assume_valid=True)  # warm
+        ev[0].record()
+        part = plan.encode_values(xl, seeds, lo, assume_valid=True)
+        ev[1].record()
+        torch.cuda.synchronize()
+        enc_ms.append(ev[0].elapsed_time(ev[1]))
+        y = part if y is None else y + part
+        del xl
+    ev[0].record()
+    fs, cs, ns = plan.decode_values(y, seeds)
+    ev[1].record()
+    torch.cuda.synchronize()
+    ms_ = int(ns[0])
+    fs, cs = fs.cpu().numpy(), cs.cpu().numpy()
+    same = bool(ms_ == m and np.array_equal(fs[0, :m], f1[0, :m]))
+    rel = float(np.max(np.abs(cs[0, :m] - c1[0, :m]) / np.maximum(np.abs(c1[0, :m]), 1e-300))) \
+        if same and m else None
+    shard = {"shards": a.shards, "encode_ms_per_rank": enc_ms,
+             "bucket_values_mb": y.numel() * 16 / 1e6,
+             "decode_ms": ev[0].elapsed_time(ev[1]), "same_support_as_single_gpu": same,
+             "max_rel_diff_vs_single_gpu": rel}
 pos, coef = truth[0]
 hit = len(set(f1[0, :m].tolist()) & set(pos.tolist()))
 print(json.dumps({
@@ -56,4 +88,5 @@ print(json.dumps({
     "entries": m, "sorted_distinct": bool(np.all(np.diff(f1[0, :m]) > 0)),
     "exact_doubling": bool(np.array_equal(f1, f2) and np.array_equal(c2[0, :m], 2 * c1[0, :m])),
     "true_tones_in_support": hit,
+    "sharded": shard,
 }))
