@@ -64,6 +64,7 @@ def parse():
                     help="signals per CPU step (default: 2 per host thread)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-clocks", action="store_true", help="diagnostics: no nvidia-smi sampler")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="weak: --batch signals per GPU; strong: --batch signals in total")
     return ap.parse_args()
@@ -252,7 +253,8 @@ def main():
         torch.distributed.barrier()
     torch.cuda.synchronize()
     clocks = ClockSampler(local)
-    clocks.start()
+    if not args.no_clocks:
+        clocks.start()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     main_ms = []  # live per-launch time of the dominant kernel (fused encode+decode)

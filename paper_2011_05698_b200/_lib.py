@@ -81,14 +81,18 @@ def lib() -> C.CDLL:
     L.msfft_plan_stage_times.restype = C.c_int
     L.msfft_plan_launches.argtypes = [VP, i64, u32]
     L.msfft_plan_launches.restype = i64
-    L.msfft_plan_ingest_samples.argtypes = [VP]
-    L.msfft_plan_ingest_samples.restype = i64
-    L.msfft_plan_values_per_signal.argtypes = [VP]
-    L.msfft_plan_values_per_signal.restype = i64
-    L.msfft_encode_values.argtypes = [VP, i64, VP, i64, i64, i64, P(u64), VP, u32, VP] + E
-    L.msfft_encode_values.restype = C.c_int
-    L.msfft_decode_values.argtypes = [VP, i64, VP, P(u64), VP, VP, VP, VP] + E
-    L.msfft_decode_values.restype = C.c_int
+    # split-phase / ingest entry points (absent from diagnostic builds of
+    # older sources, which tools/build_variant.py can produce)
+    if hasattr(L, "msfft_plan_ingest_samples"):
+        L.msfft_plan_ingest_samples.argtypes = [VP]
+        L.msfft_plan_ingest_samples.restype = i64
+    if hasattr(L, "msfft_encode_values"):
+        L.msfft_plan_values_per_signal.argtypes = [VP]
+        L.msfft_plan_values_per_signal.restype = i64
+        L.msfft_encode_values.argtypes = [VP, i64, VP, i64, i64, i64, P(u64), VP, u32, VP] + E
+        L.msfft_encode_values.restype = C.c_int
+        L.msfft_decode_values.argtypes = [VP, i64, VP, P(u64), VP, VP, VP, VP] + E
+        L.msfft_decode_values.restype = C.c_int
     L.msfft_window.argtypes = [i64, i64, f64, i32, P(i64), P(f64), i64] + E
     L.msfft_window_response.argtypes = [i64, i64, f64, i32, P(i64), i64, P(f64)] + E
     L.msfft_trace.argtypes = [VP, i64, i32, i64, i64, f64, u64, f64, P(f64), P(f64), P(i64),

@@ -48,6 +48,77 @@ __device__ __forceinline__ void encode_barrier_init(uint64_t* bar) {
     __syncthreads();
 }
 
+// Sample sources of the gather: the whole signal (x[sigma t' mod n]), an
+// index-range shard of it (x holds x[x_lo, x_hi); other samples count as 0),
+// or the compact rows of sparse host ingest (x[seg_cpos + t' - seg_lo]).
+enum LoadMode { kLoadFull = 0, kLoadShard = 1, kLoadCompact = 2 };
+
+// Walks the task's merged t' segments for residue class c (t' = c mod b) in
+// increasing t' and adds g[h + t' + tau_r] * x into acc[r] for every round r
+// whose tap interval covers t'.
+template <class T, int kMode>
+__device__ __forceinline__ void gather_accumulate(const DevPlan& plan, const EncTask& task,
+                                                  const T* __restrict__ xs, uint32_t sg,
+                                                  const double* taps, int64_t h, uint32_t wu,
+                                                  const int64_t* taus, int nr, int64_t b, int c,
+                                                  double2 (&acc)[kEncRounds]) {
+    const uint32_t mask = static_cast<uint32_t>(plan.n - 1);
+    const uint32_t lo = static_cast<uint32_t>(plan.x_lo);
+    const uint32_t span = static_cast<uint32_t>(plan.x_hi - plan.x_lo);
+    uint32_t th[kEncRounds];  // tau_r + h: tap index = t' + tau_r + h (mod 2^32)
+#pragma unroll
+    for (int r = 0; r < kEncRounds; ++r)
+        th[r] = r < nr ? static_cast<uint32_t>(taus[r] + h) : 0u;
+    const int32_t bm = static_cast<int32_t>(b - 1);
+    for (int sgi = 0; sgi < task.nseg; ++sgi) {
+        const int32_t A = task.seg_lo[sgi], B = task.seg_hi[sgi];
+        const T* cbase = xs + task.seg_cpos[sgi] - A;  // compact: sample of t' at cbase[t']
+        int64_t t = A + ((c - A) & bm);
+        constexpr int U = 8;
+        const int64_t stride = b;
+        for (; t <= B; t += U * stride) {
+            T v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int64_t tt = t + u * stride;
+                if (tt <= B) {
+                    if (kMode == kLoadCompact) {
+                        v[u] = ld_sample(cbase + tt);
+                    } else {
+                        const uint32_t src = (sg * static_cast<uint32_t>(tt)) & mask;
+                        if (kMode == kLoadFull) {
+                            v[u] = ld_sample(xs + src);
+                        } else {
+                            v[u].x = 0;
+                            v[u].y = 0;
+                            if (src - lo < span) v[u] = ld_sample(xs + (src - lo));
+                        }
+                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int64_t tt = t + u * stride;
+                if (tt <= B) {
+                    const double xr = static_cast<double>(v[u].x);
+                    const double xi = static_cast<double>(v[u].y);
+#pragma unroll
+                    for (int r = 0; r < kEncRounds; ++r) {
+                        if (r < nr) {
+                            const uint32_t idx = static_cast<uint32_t>(tt) + th[r];
+                            if (idx < wu) {
+                                const double g = taps[idx];
+                                acc[r].x += g * xr;
+                                acc[r].y += g * xi;
+                            }
+                        }
+                    }
+                }
+            }
+        }
+    }
+}
+
 // One encode task with the whole CTA.  The caller guarantees that no thread
 // still uses smem_raw from a previous item (a __syncthreads before).
 // `phase` is the mbarrier parity to wait on next; it flips once per staged
@@ -115,62 +186,14 @@ __device__ __forceinline__ void encode_task(const DevPlan& plan, const EncTask& 
 
     if (active) {
         const uint32_t sg = static_cast<uint32_t>(sigma[s * plan.iters + task.m]);
-        const uint32_t mask = static_cast<uint32_t>(plan.n - 1);
         const T* xs = x + s * x_stride;
-        // index-range shard: samples outside [x_lo, x_hi) belong to another
-        // GPU and contribute 0 here (the partial bucket vectors are summed)
-        const uint32_t lo = static_cast<uint32_t>(plan.x_lo);
-        const uint32_t span = static_cast<uint32_t>(plan.x_hi - plan.x_lo);
-        const bool full = plan.x_lo == 0 && plan.x_hi == plan.n;
-        uint32_t th[kEncRounds];  // tau_r + h: tap index = t' + tau_r + h (mod 2^32)
-#pragma unroll
-        for (int r = 0; r < kEncRounds; ++r)
-            th[r] = r < nr ? static_cast<uint32_t>(taus[r] + h) : 0u;
-        const int32_t bm = static_cast<int32_t>(b - 1);
-        for (int sgi = 0; sgi < task.nseg; ++sgi) {
-            const int32_t A = task.seg_lo[sgi], B = task.seg_hi[sgi];
-            int64_t t = A + ((c - A) & bm);
-            constexpr int U = 8;
-            const int64_t stride = b;
-            for (; t <= B; t += U * stride) {
-                T v[U];
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const int64_t tt = t + u * stride;
-                    if (tt <= B) {
-                        const uint32_t src = (sg * static_cast<uint32_t>(tt)) & mask;
-                        if (plan.x_compact) {
-                            v[u] = ld_sample(xs + task.seg_cpos[sgi] + static_cast<int32_t>(tt - A));
-                        } else if (full) {
-                            v[u] = ld_sample(xs + src);
-                        } else {
-                            v[u].x = 0;
-                            v[u].y = 0;
-                            if (src - lo < span) v[u] = ld_sample(xs + (src - lo));
-                        }
-                    }
-                }
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const int64_t tt = t + u * stride;
-                    if (tt <= B) {
-                        const double xr = static_cast<double>(v[u].x);
-                        const double xi = static_cast<double>(v[u].y);
-#pragma unroll
-                        for (int r = 0; r < kEncRounds; ++r) {
-                            if (r < nr) {
-                                const uint32_t idx = static_cast<uint32_t>(tt) + th[r];
-                                if (idx < wu) {
-                                    const double g = taps[idx];
-                                    acc[r].x += g * xr;
-                                    acc[r].y += g * xi;
-                                }
-                            }
-                        }
-                    }
-                }
-            }
-        }
+        // the load mode is uniform per launch: branch once, not per sample
+        if (plan.x_compact)
+            gather_accumulate<T, kLoadCompact>(plan, task, xs, sg, taps, h, wu, taus, nr, b, c, acc);
+        else if (plan.x_lo == 0 && plan.x_hi == plan.n)
+            gather_accumulate<T, kLoadFull>(plan, task, xs, sg, taps, h, wu, taus, nr, b, c, acc);
+        else
+            gather_accumulate<T, kLoadShard>(plan, task, xs, sg, taps, h, wu, taus, nr, b, c, acc);
     }
 
     const double inv_n = plan.inv_n;
