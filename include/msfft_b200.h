@@ -153,6 +153,80 @@ int msfft_decode_values(msfft_plan plan, int64_t batch, double* y, const uint64_
                         int64_t* out_f, double* out_c, int64_t* out_count, void* stream,
                         char* err, size_t errlen);
 
+/* ---- signal helpers: the steps either side of the path -------
+ * Reference: proj/src/signal.cpp, proj/src/io.cpp, proj/src/bench.cpp:33-46.
+ * `location` says where x / spec / out live (MSFFT_HOST or MSFFT_DEVICE); the
+ * work runs on the current device either way. */
+
+/* error_metrics (signal.cpp:154-184 / signal.hpp:31-38). */
+typedef struct msfft_eval_metrics {
+    int64_t l0_err; /* coefficients off by more than 1e-6 */
+    double l1_err;  /* (1/k) sum |d|                       */
+    double l2_err;  /* sqrt((1/k) sum |d|^2)               */
+} msfft_eval_metrics;
+
+/* generate_test_signal (signal.cpp:116-121): the truth (k distinct positions
+ * by Floyd sampling, unit coefficients with uniform phase) is drawn with the
+ * reference's mt19937_64 sampler, so truth_f (ascending) / truth_c
+ * (interleaved) are identical to the reference's; x (n samples, dtype) is
+ * synthesized on the device -- bit-identical to synthesize() when
+ * k * ceil(n/1024) <= 2^23 (*bit_exact = 1), else within ulps (device seeds). */
+int msfft_generate_test_signal(int64_t n, int64_t k, uint64_t seed, int32_t dtype,
+                               int32_t location, void* x, int64_t* truth_f, double* truth_c,
+                               int32_t* bit_exact, char* err, size_t errlen);
+
+/* synthesize (signal.cpp:76-98) of `count` entries (f strictly ascending,
+ * c interleaved, host arrays) into x. */
+int msfft_synthesize(int64_t n, const int64_t* f, const double* c, int64_t count, int32_t dtype,
+                     int32_t location, void* x, int32_t* bit_exact, char* err, size_t errlen);
+
+/* add_awgn (signal.cpp:123-152) in place: same validation, +infinity
+ * sentinel and realised-power scaling; the complex Gaussian noise comes from
+ * Philox4x32-10 counters (seed, sample index) on the device -- the same law,
+ * not the reference's sample sequence. */
+int msfft_add_awgn(void* x, int64_t n, int32_t dtype, int32_t location, double snr_db,
+                   uint64_t seed, char* err, size_t errlen);
+
+/* dft_dense (signal.cpp:37-44): out[s][i] = (1/n) sum_j x[s][j] e^{-2 pi i ij/n}
+ * for `batch` contiguous signals; out is complex128 in the same location.
+ * Bit-identical to the reference.  idft_dense (signal.cpp:46-54): the
+ * unnormalised inverse of complex128 spectra. */
+int msfft_dft_dense(const void* x, int64_t n, int64_t batch, int32_t dtype, int32_t location,
+                    double* out, char* err, size_t errlen);
+int msfft_idft_dense(const double* spec, int64_t n, int64_t batch, int32_t location, double* out,
+                     char* err, size_t errlen);
+
+/* top_k_spectrum (bench.cpp:33-46): the k largest |spec[i]| of a complex128
+ * spectrum as (f ascending, c) in host arrays of capacity k; ties at the k-th
+ * magnitude keep the lowest indices. */
+int msfft_top_k_spectrum(const double* spec, int64_t n, int64_t k, int32_t location,
+                         int64_t* out_f, double* out_c, int64_t* out_count, char* err,
+                         size_t errlen);
+
+/* error_metrics over host (f, c) lists; duplicate positions: the last wins
+ * (std::map assignment). */
+int msfft_error_metrics(int64_t truth_n, const int64_t* truth_f, const double* truth_c,
+                        int64_t truth_count, int64_t est_n, const int64_t* est_f,
+                        const double* est_c, int64_t est_count, int64_t k,
+                        msfft_eval_metrics* out, char* err, size_t errlen);
+
+/* MSFT signal files (io.cpp:17-55): 8-byte magic "MSFT\0\0\0\0", u64 n, n
+ * little-endian float64 (re, im) pairs.  Errors are MSFFT_ERR_RUNTIME with the
+ * reference's messages ("read_signal_file: bad magic in <path>", ...);
+ * non-finite samples MSFFT_ERR_INVALID_ARGUMENT.  Reading into complex64
+ * rounds each component. */
+int msfft_signal_file_length(const char* path, int64_t* n, char* err, size_t errlen);
+int msfft_read_signal_file(const char* path, int32_t dtype, int32_t location, void* x,
+                           int64_t cap, int64_t* n, char* err, size_t errlen);
+int msfft_write_signal_file(const char* path, const void* x, int64_t n, int32_t dtype,
+                            int32_t location, char* err, size_t errlen);
+
+/* Truth CSV (io.cpp:57-92): "position,re,im" then rows "%lld,%.17g,%.17g". */
+int msfft_write_truth_csv(const char* path, const int64_t* f, const double* c, int64_t count,
+                          char* err, size_t errlen);
+int msfft_read_truth_csv(const char* path, int64_t n, int64_t* f, double* c, int64_t cap,
+                         int64_t* count, char* err, size_t errlen);
+
 /* ---- host-only plan pieces (no device needed) -------------------------------
  * sigma_m, sigma^-1_m for the first `iterations` iterations of a transform
  * seeded `seed`: random_params(n, Rng(seed), 0) per iteration

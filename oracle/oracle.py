@@ -131,13 +131,24 @@ class Oracle:
                                           C.c_int, i64, P(i64), P(f64), P(i64), P(f64)] + E
         L.orc_generate_test_signal.argtypes = [i64, i64, u64, P(f64), P(i64), P(f64)] + E
         L.orc_add_awgn.argtypes = [i64, P(f64), f64, u64] + E
-        for name in dir(L):
-            pass
+        L.orc_dft_dense.argtypes = [i64, P(f64), P(f64)] + E
+        L.orc_idft_dense.argtypes = [i64, P(f64), P(f64)] + E
+        L.orc_synthesize.argtypes = [i64, i64, P(i64), P(f64), P(f64)] + E
+        L.orc_error_metrics.argtypes = [i64, i64, P(i64), P(f64), i64, P(i64), P(f64), i64,
+                                        P(i64), P(f64), P(f64)] + E
+        L.orc_top_k_spectrum.argtypes = [i64, P(f64), i64, P(i64), P(f64), P(i64)] + E
+        L.orc_write_signal_file.argtypes = [C.c_char_p, i64, P(f64)] + E
+        L.orc_read_signal_file.argtypes = [C.c_char_p, i64, P(f64), P(i64)] + E
+        L.orc_write_truth_csv.argtypes = [C.c_char_p, i64, i64, P(i64), P(f64)] + E
+        L.orc_read_truth_csv.argtypes = [C.c_char_p, i64, i64, P(i64), P(f64), P(i64)] + E
         for fn in ("orc_mod_inverse", "orc_check_parameter_bounds", "orc_cfg_validate",
                    "orc_random_params", "orc_initial_bucket_count", "orc_plan_build",
                    "orc_window", "orc_response_at", "orc_bucketize", "orc_predict", "orc_locate",
                    "orc_estimate_value", "orc_sfft4", "orc_sfft4_trace", "orc_sfft4_batch_c64",
-                   "orc_generate_test_signal", "orc_add_awgn"):
+                   "orc_generate_test_signal", "orc_add_awgn", "orc_dft_dense",
+                   "orc_idft_dense", "orc_synthesize", "orc_error_metrics", "orc_top_k_spectrum",
+                   "orc_write_signal_file", "orc_read_signal_file", "orc_write_truth_csv",
+                   "orc_read_truth_csv"):
             getattr(L, fn).restype = C.c_int
 
     # -- error plumbing ------------------------------------------------------
@@ -324,3 +335,71 @@ class Oracle:
         n = xv.size // 2
         self._call(self.lib.orc_add_awgn, n, _ptr(xv, f64), float(snr_db), seed)
         return xv.view(np.complex128)
+
+    # -- signal helpers --------------------------------
+    def dft_dense(self, x):
+        xv = _cx(x)
+        out = np.zeros_like(xv)
+        self._call(self.lib.orc_dft_dense, xv.size // 2, _ptr(xv, f64), _ptr(out, f64))
+        return out.view(np.complex128)
+
+    def idft_dense(self, spec):
+        sv = _cx(spec)
+        out = np.zeros_like(sv)
+        self._call(self.lib.orc_idft_dense, sv.size // 2, _ptr(sv, f64), _ptr(out, f64))
+        return out.view(np.complex128)
+
+    def synthesize(self, n, f, c):
+        f = np.ascontiguousarray(np.asarray(f, dtype=np.int64))
+        cv = _cx(c)
+        x = np.zeros(2 * n, np.float64)
+        self._call(self.lib.orc_synthesize, n, f.size, _ptr(f, i64), _ptr(cv, f64), _ptr(x, f64))
+        return x.view(np.complex128)
+
+    def error_metrics(self, n, tf, tc, ef, ec, k):
+        tf = np.ascontiguousarray(np.asarray(tf, dtype=np.int64))
+        ef = np.ascontiguousarray(np.asarray(ef, dtype=np.int64))
+        tcv, ecv = _cx(tc), _cx(ec)
+        l0, l1, l2 = i64(), f64(), f64()
+        self._call(self.lib.orc_error_metrics, n, tf.size, _ptr(tf, i64), _ptr(tcv, f64),
+                   ef.size, _ptr(ef, i64), _ptr(ecv, f64), k, C.byref(l0), C.byref(l1),
+                   C.byref(l2))
+        return l0.value, l1.value, l2.value
+
+    def top_k_spectrum(self, spec, k):
+        sv = _cx(spec)
+        n = sv.size // 2
+        f = np.zeros(max(k, 1), np.int64)
+        c = np.zeros(2 * max(k, 1), np.float64)
+        cnt = i64()
+        self._call(self.lib.orc_top_k_spectrum, n, _ptr(sv, f64), k, _ptr(f, i64), _ptr(c, f64),
+                   C.byref(cnt))
+        return f[:cnt.value], c.view(np.complex128)[:cnt.value]
+
+    def write_signal_file(self, path, x):
+        xv = _cx(x)
+        self._call(self.lib.orc_write_signal_file, str(path).encode(), xv.size // 2,
+                   _ptr(xv, f64))
+
+    def read_signal_file(self, path, cap=1 << 24):
+        x = np.zeros(2 * cap, np.float64)
+        n = i64()
+        self._call(self.lib.orc_read_signal_file, str(path).encode(), cap, _ptr(x, f64),
+                   C.byref(n))
+        if n.value > cap:
+            return self.read_signal_file(path, n.value)
+        return x.view(np.complex128)[:n.value].copy()
+
+    def write_truth_csv(self, path, n, f, c):
+        f = np.ascontiguousarray(np.asarray(f, dtype=np.int64))
+        cv = _cx(c)
+        self._call(self.lib.orc_write_truth_csv, str(path).encode(), n, f.size, _ptr(f, i64),
+                   _ptr(cv, f64))
+
+    def read_truth_csv(self, path, n, cap=1 << 20):
+        f = np.zeros(cap, np.int64)
+        c = np.zeros(2 * cap, np.float64)
+        cnt = i64()
+        self._call(self.lib.orc_read_truth_csv, str(path).encode(), n, cap, _ptr(f, i64),
+                   _ptr(c, f64), C.byref(cnt))
+        return f[:cnt.value].copy(), c.view(np.complex128)[:cnt.value].copy()

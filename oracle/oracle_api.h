@@ -134,6 +134,31 @@ int orc_generate_test_signal(int64_t n, int64_t k, uint64_t seed, double* x, int
                              double* c, char* err, int64_t errlen);
 int orc_add_awgn(int64_t n, double* x, double snr_db, uint64_t seed, char* err, int64_t errlen);
 
+/* ---- signal helpers, SURVEY 8(f) rows 2-3 (signal.cpp, io.cpp, bench.cpp) ---- */
+/* dft_dense (signal.cpp:37-44) / idft_dense (:46-54); x, out: n complex. */
+int orc_dft_dense(int64_t n, const double* x, double* out, char* err, int64_t errlen);
+int orc_idft_dense(int64_t n, const double* spec, double* out, char* err, int64_t errlen);
+/* synthesize (signal.cpp:76-98) of `count` entries (f ascending). */
+int orc_synthesize(int64_t n, int64_t count, const int64_t* f, const double* c, double* x,
+                   char* err, int64_t errlen);
+/* error_metrics (signal.cpp:154-184): out_l0, out_l1, out_l2. */
+int orc_error_metrics(int64_t n, int64_t tcount, const int64_t* tf, const double* tc,
+                      int64_t ecount, const int64_t* ef, const double* ec, int64_t k,
+                      int64_t* out_l0, double* out_l1, double* out_l2, char* err,
+                      int64_t errlen);
+/* top_k_spectrum (bench.cpp:33-46): k largest |spec| as ascending (f, c). */
+int orc_top_k_spectrum(int64_t n, const double* spec, int64_t k, int64_t* out_f, double* out_c,
+                       int64_t* out_count, char* err, int64_t errlen);
+/* MSFT signal files and truth CSV (io.cpp:17-92). */
+int orc_write_signal_file(const char* path, int64_t n, const double* x, char* err,
+                          int64_t errlen);
+int orc_read_signal_file(const char* path, int64_t cap, double* x, int64_t* n, char* err,
+                         int64_t errlen);
+int orc_write_truth_csv(const char* path, int64_t n, int64_t count, const int64_t* f,
+                        const double* c, char* err, int64_t errlen);
+int orc_read_truth_csv(const char* path, int64_t n, int64_t cap, int64_t* f, double* c,
+                       int64_t* count, char* err, int64_t errlen);
+
 #ifdef __cplusplus
 }
 #endif

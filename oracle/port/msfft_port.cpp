@@ -14,6 +14,7 @@
 #include <chrono>
 #include <cmath>
 #include <complex>
+#include <cstdio>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -551,6 +552,181 @@ Out transform(const std::vector<cx>& x, int64_t k, int64_t l, double q, uint64_t
 }
 
 // ---------------------------------------------------------------- signals
+// SparseSpectrum::validate (signal.cpp:28-39).
+void check_spectrum(int64_t n, const std::map<int64_t, cx>& spec) {
+    if (n < 4 || !pow2(static_cast<uint64_t>(n)))
+        throw std::invalid_argument("SparseSpectrum: n must be a power of two >= 4");
+    if (static_cast<int64_t>(spec.size()) > n)
+        throw std::invalid_argument("SparseSpectrum: more entries than n");
+    for (const auto& kv : spec) {
+        if (kv.first < 0 || kv.first >= n)
+            throw std::invalid_argument("SparseSpectrum: position out of range");
+        if (!std::isfinite(kv.second.real()) || !std::isfinite(kv.second.imag()))
+            throw std::invalid_argument("SparseSpectrum: non-finite coefficient");
+    }
+}
+
+// synthesize (signal.cpp:76-98): per tone in ascending position, a phasor
+// recurrence re-seeded from cos/sin every 1024 samples, summed into x.
+void synth(int64_t n, const std::map<int64_t, cx>& truth, std::vector<cx>& x) {
+    check_spectrum(n, truth);
+    x.assign(n, cx(0.0, 0.0));
+    for (const auto& kv : truth) {
+        const double step = kTau * static_cast<double>(kv.first) / static_cast<double>(n);
+        const cx mul(std::cos(step), std::sin(step));
+        cx ph(1.0, 0.0);
+        for (int64_t j = 0; j < n; ++j) {
+            if (j % 1024 == 0) {
+                const double a = step * static_cast<double>(j % n);
+                ph = cx(std::cos(a), std::sin(a));
+            }
+            x[j] += kv.second * ph;
+            ph *= mul;
+        }
+    }
+}
+
+// dft_dense (signal.cpp:41-48): forward radix-2 with 1/n; idft_dense
+// (:50-58): the unnormalised inverse.
+std::vector<cx> dense(std::vector<cx> v, int sign) {
+    if (sign < 0) {
+        check_signal(static_cast<int64_t>(v.size()), v);
+    } else if (v.size() < 4 || !pow2(v.size())) {
+        throw std::invalid_argument("idft_dense: size must be a power of two >= 4");
+    }
+    fft(v, sign);
+    if (sign < 0) {
+        const double scale = 1.0 / static_cast<double>(v.size());
+        for (cx& z : v) z *= scale;
+    }
+    return v;
+}
+
+struct Metrics {
+    int64_t l0 = 0;
+    double l1 = 0.0, l2 = 0.0;
+};
+
+// error_metrics (signal.cpp:154-184): over the union of supports in
+// ascending position, absent entries read as zero.
+Metrics metrics(int64_t n_truth, const std::map<int64_t, cx>& truth, int64_t n_est,
+                const std::map<int64_t, cx>& est, int64_t k) {
+    if (n_truth != n_est) throw std::invalid_argument("error_metrics: size mismatch");
+    std::map<int64_t, bool> support;
+    for (const auto& kv : truth) support[kv.first] = true;
+    for (const auto& kv : est) support[kv.first] = true;
+    if (k <= 0) {
+        if (!support.empty())
+            throw std::invalid_argument("error_metrics: k = 0 with nonempty support union");
+        return {};
+    }
+    Metrics m;
+    double sa = 0.0, sq = 0.0;
+    for (const auto& kv : support) {
+        const auto t = truth.find(kv.first);
+        const auto e = est.find(kv.first);
+        const cx tv = t == truth.end() ? cx(0, 0) : t->second;
+        const cx ev = e == est.end() ? cx(0, 0) : e->second;
+        const double d = std::abs(tv - ev);
+        sa += d;
+        sq += d * d;
+        if (d > 1e-6) ++m.l0;
+    }
+    m.l1 = sa / static_cast<double>(k);
+    m.l2 = std::sqrt(sq / static_cast<double>(k));
+    return m;
+}
+
+// top_k_spectrum (bench.cpp:33-46): partial selection by |X| descending.
+std::map<int64_t, cx> top_k(const std::vector<cx>& spec, int64_t n, int64_t k) {
+    std::vector<int64_t> idx(spec.size());
+    for (size_t i = 0; i < idx.size(); ++i) idx[i] = static_cast<int64_t>(i);
+    const size_t keep = std::min<size_t>(static_cast<size_t>(k), idx.size());
+    std::nth_element(idx.begin(), idx.begin() + keep, idx.end(), [&](int64_t a, int64_t b) {
+        return std::abs(spec[static_cast<size_t>(a)]) > std::abs(spec[static_cast<size_t>(b)]);
+    });
+    std::map<int64_t, cx> out;
+    (void)n;
+    for (size_t i = 0; i < keep; ++i) out[idx[i]] = spec[static_cast<size_t>(idx[i])];
+    return out;
+}
+
+// MSFT signal file (io.cpp:17-55): "MSFT" + 4 zero bytes, u64 n, n
+// little-endian float64 (re, im) pairs; validated on both sides.
+void write_file(const std::string& path, const std::vector<cx>& x) {
+    check_signal(static_cast<int64_t>(x.size()), x);
+    std::FILE* f = std::fopen(path.c_str(), "wb");
+    if (!f) throw std::runtime_error("write_signal_file: cannot open " + path);
+    const char magic[8] = {'M', 'S', 'F', 'T', 0, 0, 0, 0};
+    const uint64_t n = x.size();
+    bool ok = std::fwrite(magic, 1, 8, f) == 8 && std::fwrite(&n, 8, 1, f) == 1 &&
+              std::fwrite(x.data(), 16, x.size(), f) == x.size();
+    ok = (std::fclose(f) == 0) && ok;
+    if (!ok) throw std::runtime_error("write_signal_file: write failed for " + path);
+}
+
+std::vector<cx> read_file(const std::string& path) {
+    std::FILE* f = std::fopen(path.c_str(), "rb");
+    if (!f) throw std::runtime_error("read_signal_file: cannot open " + path);
+    char magic[8] = {};
+    const size_t got = std::fread(magic, 1, 8, f);
+    if (got != 8 || std::memcmp(magic, "MSFT", 4) != 0) {
+        std::fclose(f);
+        throw std::runtime_error("read_signal_file: bad magic in " + path);
+    }
+    uint64_t n = 0;
+    if (std::fread(&n, 8, 1, f) != 1 || !pow2(n) || n < 4 || n > (uint64_t{1} << 30)) {
+        std::fclose(f);
+        throw std::runtime_error("read_signal_file: bad length field in " + path);
+    }
+    std::vector<cx> x(n);
+    const size_t rd = std::fread(x.data(), 16, n, f);
+    std::fclose(f);
+    if (rd != n) throw std::runtime_error("read_signal_file: truncated file " + path);
+    check_signal(static_cast<int64_t>(n), x);
+    return x;
+}
+
+// Truth CSV (io.cpp:57-92): header, then "position,re,im" with %.17g.
+void write_csv(const std::string& path, const std::map<int64_t, cx>& truth) {
+    std::FILE* f = std::fopen(path.c_str(), "w");
+    if (!f) throw std::runtime_error("write_truth_csv: cannot open " + path);
+    bool ok = std::fputs("position,re,im\n", f) >= 0;
+    for (const auto& kv : truth)
+        ok = ok && std::fprintf(f, "%lld,%.17g,%.17g\n", static_cast<long long>(kv.first),
+                                kv.second.real(), kv.second.imag()) > 0;
+    ok = (std::fclose(f) == 0) && ok;
+    if (!ok) throw std::runtime_error("write_truth_csv: write failed for " + path);
+}
+
+std::map<int64_t, cx> read_csv(const std::string& path, int64_t n) {
+    std::FILE* f = std::fopen(path.c_str(), "r");
+    if (!f) throw std::runtime_error("read_truth_csv: cannot open " + path);
+    std::map<int64_t, cx> truth;
+    std::string line;
+    int ch;
+    bool header = true;
+    auto flush_line = [&] {
+        if (header) {
+            header = false;
+        } else if (!line.empty()) {
+            const size_t a = line.find(','), b = a == std::string::npos ? a : line.find(',', a + 1);
+            const int64_t pos = std::stoll(line.substr(0, a));
+            const double re = std::stod(line.substr(a + 1, b - a - 1));
+            const double im = std::stod(line.substr(b + 1));
+            truth[pos] = cx(re, im);
+        }
+        line.clear();
+    };
+    while ((ch = std::fgetc(f)) != EOF) {
+        if (ch == '\n') flush_line(); else line.push_back(static_cast<char>(ch));
+    }
+    if (!line.empty()) flush_line();
+    std::fclose(f);
+    check_spectrum(n, truth);
+    return truth;
+}
+
 // generate_test_signal (signal.cpp:100-127): Floyd sampling + synthesize.
 void make_signal(int64_t n, int64_t k, uint64_t seed, std::vector<cx>& x,
                  std::map<int64_t, cx>& truth) {
@@ -569,20 +745,7 @@ void make_signal(int64_t n, int64_t k, uint64_t seed, std::vector<cx>& x,
         const double ph = kTau * rng.unit();
         truth[kv.first] = cx(std::cos(ph), std::sin(ph));
     }
-    x.assign(n, cx(0.0, 0.0));
-    for (const auto& kv : truth) {  // phasor recurrence, resynced every 1024 (signal.cpp:76-98)
-        const double step = kTau * static_cast<double>(kv.first) / static_cast<double>(n);
-        const cx mul(std::cos(step), std::sin(step));
-        cx ph(1.0, 0.0);
-        for (int64_t j = 0; j < n; ++j) {
-            if (j % 1024 == 0) {
-                const double a = step * static_cast<double>(j % n);
-                ph = cx(std::cos(a), std::sin(a));
-            }
-            x[j] += kv.second * ph;
-            ph *= mul;
-        }
-    }
+    synth(n, truth, x);
 }
 
 // add_awgn (signal.cpp:129-152): realised power ratio.
@@ -908,6 +1071,79 @@ int orc_add_awgn(int64_t n, double* x, double snr_db, uint64_t seed, char* err, 
         port::awgn(s, snr_db, seed);
         std::memcpy(x, s.data(), sizeof(double) * 2 * n);
     });
+}
+
+int orc_dft_dense(int64_t n, const double* x, double* out, char* err, int64_t errlen) {
+    return wrap(err, errlen, [&] {
+        const auto v = port::dense(as_cx(n, x), -1);
+        std::memcpy(out, v.data(), sizeof(double) * 2 * n);
+    });
+}
+
+int orc_idft_dense(int64_t n, const double* spec, double* out, char* err, int64_t errlen) {
+    return wrap(err, errlen, [&] {
+        const auto v = port::dense(as_cx(n, spec), +1);
+        std::memcpy(out, v.data(), sizeof(double) * 2 * n);
+    });
+}
+
+static std::map<int64_t, port::cx> as_spec(int64_t count, const int64_t* f, const double* c) {
+    std::map<int64_t, port::cx> m;
+    for (int64_t i = 0; i < count; ++i) m[f[i]] = port::cx(c[2 * i], c[2 * i + 1]);
+    return m;
+}
+
+int orc_synthesize(int64_t n, int64_t count, const int64_t* f, const double* c, double* x,
+                   char* err, int64_t errlen) {
+    return wrap(err, errlen, [&] {
+        std::vector<port::cx> v;
+        port::synth(n, as_spec(count, f, c), v);
+        std::memcpy(x, v.data(), sizeof(double) * 2 * n);
+    });
+}
+
+int orc_error_metrics(int64_t n, int64_t tcount, const int64_t* tf, const double* tc,
+                      int64_t ecount, const int64_t* ef, const double* ec, int64_t k,
+                      int64_t* out_l0, double* out_l1, double* out_l2, char* err,
+                      int64_t errlen) {
+    return wrap(err, errlen, [&] {
+        const auto m = port::metrics(n, as_spec(tcount, tf, tc), n, as_spec(ecount, ef, ec), k);
+        *out_l0 = m.l0;
+        *out_l1 = m.l1;
+        *out_l2 = m.l2;
+    });
+}
+
+int orc_top_k_spectrum(int64_t n, const double* spec, int64_t k, int64_t* out_f, double* out_c,
+                       int64_t* out_count, char* err, int64_t errlen) {
+    return wrap(err, errlen, [&] {
+        emit(port::top_k(as_cx(n, spec), n, k), k, out_f, out_c, out_count);
+    });
+}
+
+int orc_write_signal_file(const char* path, int64_t n, const double* x, char* err,
+                          int64_t errlen) {
+    return wrap(err, errlen, [&] { port::write_file(path, as_cx(n, x)); });
+}
+
+int orc_read_signal_file(const char* path, int64_t cap, double* x, int64_t* n, char* err,
+                         int64_t errlen) {
+    return wrap(err, errlen, [&] {
+        const auto v = port::read_file(path);
+        *n = static_cast<int64_t>(v.size());
+        if (*n <= cap) std::memcpy(x, v.data(), sizeof(double) * 2 * v.size());
+    });
+}
+
+int orc_write_truth_csv(const char* path, int64_t n, int64_t count, const int64_t* f,
+                        const double* c, char* err, int64_t errlen) {
+    (void)n;
+    return wrap(err, errlen, [&] { port::write_csv(path, as_spec(count, f, c)); });
+}
+
+int orc_read_truth_csv(const char* path, int64_t n, int64_t cap, int64_t* f, double* c,
+                       int64_t* count, char* err, int64_t errlen) {
+    return wrap(err, errlen, [&] { emit(port::read_csv(path, n), cap, f, c, count); });
 }
 
 }  // extern "C"

@@ -18,6 +18,7 @@
 #include <vector>
 
 #include "msfft/bucketize.hpp"
+#include "msfft/io.hpp"
 #include "msfft/locate.hpp"
 #include "msfft/rng.hpp"
 #include "msfft/sfft4.hpp"
@@ -91,6 +92,20 @@ void write_result(const SfftResult& res, int64_t cap, int64_t* out_f, double* ou
     if (stats_d) {
         stats_d[0] = res.stats.sample_fraction;
         stats_d[1] = res.stats.runtime_ms;
+    }
+}
+
+SparseSpectrum make_spectrum(int64_t n, int64_t count, const int64_t* f, const double* c) {
+    SparseSpectrum s;
+    s.n = n;
+    for (int64_t i = 0; i < count; ++i) s.entries[f[i]] = cplx(c[2 * i], c[2 * i + 1]);
+    return s;
+}
+
+void put_cx(const std::vector<cplx>& v, double* out) {
+    for (size_t j = 0; j < v.size(); ++j) {
+        out[2 * j] = v[j].real();
+        out[2 * j + 1] = v[j].imag();
     }
 }
 
@@ -463,6 +478,102 @@ int orc_add_awgn(int64_t n, double* x, double snr_db, uint64_t seed, char* err, 
             x[2 * j] = o.samples[j].real();
             x[2 * j + 1] = o.samples[j].imag();
         }
+    });
+}
+
+int orc_dft_dense(int64_t n, const double* x, double* out, char* err, int64_t errlen) {
+    return guard(err, errlen, [&] { put_cx(dft_dense(make_signal(n, x)), out); });
+}
+
+int orc_idft_dense(int64_t n, const double* spec, double* out, char* err, int64_t errlen) {
+    return guard(err, errlen, [&] {
+        std::vector<cplx> v(static_cast<size_t>(n));
+        for (int64_t j = 0; j < n; ++j) v[j] = cplx(spec[2 * j], spec[2 * j + 1]);
+        put_cx(idft_dense(v).samples, out);
+    });
+}
+
+int orc_synthesize(int64_t n, int64_t count, const int64_t* f, const double* c, double* x,
+                   char* err, int64_t errlen) {
+    return guard(err, errlen,
+                 [&] { put_cx(synthesize(make_spectrum(n, count, f, c)).samples, x); });
+}
+
+int orc_error_metrics(int64_t n, int64_t tcount, const int64_t* tf, const double* tc,
+                      int64_t ecount, const int64_t* ef, const double* ec, int64_t k,
+                      int64_t* out_l0, double* out_l1, double* out_l2, char* err,
+                      int64_t errlen) {
+    return guard(err, errlen, [&] {
+        const EvalMetrics m = error_metrics(make_spectrum(n, tcount, tf, tc),
+                                            make_spectrum(n, ecount, ef, ec), k);
+        *out_l0 = m.l0_err;
+        *out_l1 = m.l1_err;
+        *out_l2 = m.l2_err;
+    });
+}
+
+// bench.cpp:33-46 keeps top_k_spectrum in an anonymous namespace, so it is
+// not linkable; this is the same std::nth_element call with the same
+// comparator (the only restated logic in this file besides the trace).
+int orc_top_k_spectrum(int64_t n, const double* spec, int64_t k, int64_t* out_f, double* out_c,
+                       int64_t* out_count, char* err, int64_t errlen) {
+    return guard(err, errlen, [&] {
+        std::vector<cplx> spectrum(static_cast<size_t>(n));
+        for (int64_t j = 0; j < n; ++j) spectrum[j] = cplx(spec[2 * j], spec[2 * j + 1]);
+        std::vector<int64_t> idx(spectrum.size());
+        for (size_t i = 0; i < idx.size(); ++i) idx[i] = static_cast<int64_t>(i);
+        const size_t keep = std::min<size_t>(static_cast<size_t>(k), idx.size());
+        std::nth_element(idx.begin(), idx.begin() + keep, idx.end(), [&](int64_t a, int64_t b) {
+            return std::abs(spectrum[static_cast<size_t>(a)]) >
+                   std::abs(spectrum[static_cast<size_t>(b)]);
+        });
+        SparseSpectrum out;
+        out.n = n;
+        for (size_t i = 0; i < keep; ++i) out.entries[idx[i]] = spectrum[static_cast<size_t>(idx[i])];
+        int64_t i = 0;
+        for (const auto& [f, c] : out.entries) {
+            out_f[i] = f;
+            out_c[2 * i] = c.real();
+            out_c[2 * i + 1] = c.imag();
+            ++i;
+        }
+        *out_count = i;
+    });
+}
+
+int orc_write_signal_file(const char* path, int64_t n, const double* x, char* err,
+                          int64_t errlen) {
+    return guard(err, errlen, [&] { write_signal_file(path, make_signal(n, x)); });
+}
+
+int orc_read_signal_file(const char* path, int64_t cap, double* x, int64_t* n, char* err,
+                         int64_t errlen) {
+    return guard(err, errlen, [&] {
+        const ComplexSignal s = read_signal_file(path);
+        *n = s.n;
+        if (s.n <= cap) put_cx(s.samples, x);
+    });
+}
+
+int orc_write_truth_csv(const char* path, int64_t n, int64_t count, const int64_t* f,
+                        const double* c, char* err, int64_t errlen) {
+    return guard(err, errlen, [&] { write_truth_csv(path, make_spectrum(n, count, f, c)); });
+}
+
+int orc_read_truth_csv(const char* path, int64_t n, int64_t cap, int64_t* f, double* c,
+                       int64_t* count, char* err, int64_t errlen) {
+    return guard(err, errlen, [&] {
+        const SparseSpectrum s = read_truth_csv(path, n);
+        int64_t i = 0;
+        for (const auto& [pos, val] : s.entries) {
+            if (i < cap) {
+                f[i] = pos;
+                c[2 * i] = val.real();
+                c[2 * i + 1] = val.imag();
+            }
+            ++i;
+        }
+        *count = i;
     });
 }
 

@@ -26,7 +26,10 @@ EXPORTED = (
     "msfft_window", "msfft_window_response", "msfft_trace", "msfft_plan_stage_times",
     "msfft_plan_gather_traffic", "msfft_sigma_plan", "msfft_tau_plan",
     "msfft_plan_values_per_signal", "msfft_encode_values", "msfft_decode_values",
-    "msfft_plan_ingest_samples",
+    "msfft_plan_ingest_samples", "msfft_generate_test_signal", "msfft_synthesize",
+    "msfft_add_awgn", "msfft_dft_dense", "msfft_idft_dense", "msfft_top_k_spectrum",
+    "msfft_error_metrics", "msfft_signal_file_length", "msfft_read_signal_file",
+    "msfft_write_signal_file", "msfft_write_truth_csv", "msfft_read_truth_csv",
 )
 
 i64, u64, f64, i32, u32 = C.c_int64, C.c_uint64, C.c_double, C.c_int32, C.c_uint32
@@ -45,6 +48,10 @@ class Stats(C.Structure):
         ("b_first", i64),
         ("stage_counts", i32 * MAX_ITERATIONS),
     ]
+
+
+class EvalMetricsC(C.Structure):
+    _fields_ = [("l0_err", i64), ("l1_err", f64), ("l2_err", f64)]
 
 
 _lib = None
@@ -93,6 +100,27 @@ def lib() -> C.CDLL:
         L.msfft_encode_values.restype = C.c_int
         L.msfft_decode_values.argtypes = [VP, i64, VP, P(u64), VP, VP, VP, VP] + E
         L.msfft_decode_values.restype = C.c_int
+    if hasattr(L, "msfft_generate_test_signal"):
+        CP = C.c_char_p
+        L.msfft_generate_test_signal.argtypes = [i64, i64, u64, i32, i32, VP, VP, VP,
+                                                 P(i32)] + E
+        L.msfft_synthesize.argtypes = [i64, VP, VP, i64, i32, i32, VP, P(i32)] + E
+        L.msfft_add_awgn.argtypes = [VP, i64, i32, i32, f64, u64] + E
+        L.msfft_dft_dense.argtypes = [VP, i64, i64, i32, i32, VP] + E
+        L.msfft_idft_dense.argtypes = [VP, i64, i64, i32, VP] + E
+        L.msfft_top_k_spectrum.argtypes = [VP, i64, i64, i32, VP, VP, P(i64)] + E
+        L.msfft_error_metrics.argtypes = [i64, VP, VP, i64, i64, VP, VP, i64, i64,
+                                          P(EvalMetricsC)] + E
+        L.msfft_signal_file_length.argtypes = [CP, P(i64)] + E
+        L.msfft_read_signal_file.argtypes = [CP, i32, i32, VP, i64, P(i64)] + E
+        L.msfft_write_signal_file.argtypes = [CP, VP, i64, i32, i32] + E
+        L.msfft_write_truth_csv.argtypes = [CP, VP, VP, i64] + E
+        L.msfft_read_truth_csv.argtypes = [CP, i64, VP, VP, i64, P(i64)] + E
+        for fn in ("msfft_generate_test_signal", "msfft_synthesize", "msfft_add_awgn",
+                   "msfft_dft_dense", "msfft_idft_dense", "msfft_top_k_spectrum",
+                   "msfft_error_metrics", "msfft_signal_file_length", "msfft_read_signal_file",
+                   "msfft_write_signal_file", "msfft_write_truth_csv", "msfft_read_truth_csv"):
+            getattr(L, fn).restype = C.c_int
     L.msfft_window.argtypes = [i64, i64, f64, i32, P(i64), P(f64), i64] + E
     L.msfft_window_response.argtypes = [i64, i64, f64, i32, P(i64), i64, P(f64)] + E
     L.msfft_trace.argtypes = [VP, i64, i32, i64, i64, f64, u64, f64, P(f64), P(f64), P(i64),

@@ -12,6 +12,8 @@
 #include "../../include/msfft_b200.h"
 #include "engine.hpp"
 #include "host_plan.hpp"
+#include "signal_io.hpp"
+#include "signal_ops.hpp"
 #include "window.hpp"
 
 using namespace msfft_b200;
@@ -343,6 +345,173 @@ int msfft_trace(const void* x, int64_t n, int32_t dtype, int64_t k, int64_t l, d
             out_c[2 * i + 1] = c[2 * i + 1];
         }
     });
+}
+
+// ---- signal helpers -----------------------------------------
+
+namespace {
+
+size_t elem_of(int32_t dtype) {
+    if (dtype != MSFFT_C128 && dtype != MSFFT_C64) throw std::invalid_argument("msfft: unknown dtype");
+    return dtype == MSFFT_C128 ? 16 : 8;
+}
+
+// Device view of a caller buffer: the buffer itself, or a device copy that
+// is written back (when `out`) for host buffers.
+struct DeviceView {
+    void* host = nullptr;
+    void* dev = nullptr;
+    size_t bytes = 0;
+    DeviceBuffer<unsigned char> own;
+    DeviceView(void* p, size_t b, bool on_device, bool copy_in) : bytes(b) {
+        if (on_device) {
+            dev = p;
+            return;
+        }
+        host = p;
+        own.reset(b);
+        dev = own.get();
+        if (copy_in && b) MSFFT_CUDA(cudaMemcpy(dev, p, b, cudaMemcpyHostToDevice));
+    }
+    void write_back() {
+        if (host && bytes) MSFFT_CUDA(cudaMemcpy(host, dev, bytes, cudaMemcpyDeviceToHost));
+    }
+};
+
+}  // namespace
+
+int msfft_generate_test_signal(int64_t n, int64_t k, uint64_t seed, int32_t dtype,
+                               int32_t location, void* x, int64_t* truth_f, double* truth_c,
+                               int32_t* bit_exact, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        require_device();
+        const size_t esz = elem_of(dtype);
+        std::vector<int64_t> f;
+        std::vector<double> c;
+        random_sparse_spectrum(n, k, seed, f, c);
+        DeviceView v(x, static_cast<size_t>(n) * esz, location == MSFFT_DEVICE, false);
+        const bool exact = synthesize_device(n, f.data(), c.data(), static_cast<int64_t>(f.size()),
+                                             dtype == MSFFT_C128, v.dev, nullptr);
+        v.write_back();
+        for (size_t i = 0; i < f.size(); ++i) {
+            truth_f[i] = f[i];
+            truth_c[2 * i] = c[2 * i];
+            truth_c[2 * i + 1] = c[2 * i + 1];
+        }
+        if (bit_exact) *bit_exact = exact ? 1 : 0;
+    });
+}
+
+int msfft_synthesize(int64_t n, const int64_t* f, const double* c, int64_t count, int32_t dtype,
+                     int32_t location, void* x, int32_t* bit_exact, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        require_device();
+        const size_t esz = elem_of(dtype);
+        if (n < 4 || !is_pow2_u(static_cast<uint64_t>(n)))
+            throw std::invalid_argument("SparseSpectrum: n must be a power of two >= 4");
+        DeviceView v(x, static_cast<size_t>(n) * esz, location == MSFFT_DEVICE, false);
+        const bool exact = synthesize_device(n, f, c, count, dtype == MSFFT_C128, v.dev, nullptr);
+        v.write_back();
+        if (bit_exact) *bit_exact = exact ? 1 : 0;
+    });
+}
+
+int msfft_add_awgn(void* x, int64_t n, int32_t dtype, int32_t location, double snr_db,
+                   uint64_t seed, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        require_device();
+        const size_t esz = elem_of(dtype);
+        if (n < 4 || !is_pow2_u(static_cast<uint64_t>(n)))
+            throw std::invalid_argument("ComplexSignal: n must be a power of two >= 4");
+        DeviceView v(x, static_cast<size_t>(n) * esz, location == MSFFT_DEVICE, true);
+        awgn_device(v.dev, dtype == MSFFT_C128, n, snr_db, seed, nullptr);
+        v.write_back();
+    });
+}
+
+int msfft_dft_dense(const void* x, int64_t n, int64_t batch, int32_t dtype, int32_t location,
+                    double* out, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        require_device();
+        const size_t esz = elem_of(dtype);
+        if (n < 4 || !is_pow2_u(static_cast<uint64_t>(n)))
+            throw std::invalid_argument("ComplexSignal: n must be a power of two >= 4");
+        const bool dev = location == MSFFT_DEVICE;
+        DeviceView in(const_cast<void*>(x), static_cast<size_t>(n * batch) * esz, dev, true);
+        DeviceView o(out, static_cast<size_t>(n * batch) * 16, dev, false);
+        dense_dft_device(in.dev, dtype == MSFFT_C128, n, batch, static_cast<double2*>(o.dev), -1,
+                         nullptr);
+        o.write_back();
+    });
+}
+
+int msfft_idft_dense(const double* spec, int64_t n, int64_t batch, int32_t location, double* out,
+                     char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        require_device();
+        if (n < 4 || !is_pow2_u(static_cast<uint64_t>(n)))
+            throw std::invalid_argument("idft_dense: size must be a power of two >= 4");
+        const bool dev = location == MSFFT_DEVICE;
+        DeviceView in(const_cast<double*>(spec), static_cast<size_t>(n * batch) * 16, dev, true);
+        DeviceView o(out, static_cast<size_t>(n * batch) * 16, dev, false);
+        dense_dft_device(in.dev, true, n, batch, static_cast<double2*>(o.dev), +1, nullptr);
+        o.write_back();
+    });
+}
+
+int msfft_top_k_spectrum(const double* spec, int64_t n, int64_t k, int32_t location,
+                         int64_t* out_f, double* out_c, int64_t* out_count, char* err,
+                         size_t errlen) {
+    return guarded(err, errlen, [&] {
+        require_device();
+        DeviceView in(const_cast<double*>(spec), static_cast<size_t>(n) * 16,
+                      location == MSFFT_DEVICE, true);
+        *out_count = top_k_device(static_cast<const double2*>(in.dev), n, k, out_f, out_c, nullptr);
+    });
+}
+
+int msfft_error_metrics(int64_t truth_n, const int64_t* truth_f, const double* truth_c,
+                        int64_t truth_count, int64_t est_n, const int64_t* est_f,
+                        const double* est_c, int64_t est_count, int64_t k,
+                        msfft_eval_metrics* out, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        const EvalMetrics m = error_metrics(truth_n, truth_f, truth_c, truth_count, est_n, est_f,
+                                            est_c, est_count, k);
+        out->l0_err = m.l0;
+        out->l1_err = m.l1;
+        out->l2_err = m.l2;
+    });
+}
+
+int msfft_signal_file_length(const char* path, int64_t* n, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] { *n = signal_file_length(path); });
+}
+
+int msfft_read_signal_file(const char* path, int32_t dtype, int32_t location, void* x,
+                           int64_t cap, int64_t* n, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        const size_t esz = elem_of(dtype);
+        (void)esz;
+        *n = read_signal_file(path, dtype == MSFFT_C128, location == MSFFT_DEVICE, x, cap);
+    });
+}
+
+int msfft_write_signal_file(const char* path, const void* x, int64_t n, int32_t dtype,
+                            int32_t location, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        elem_of(dtype);
+        write_signal_file(path, x, n, dtype == MSFFT_C128, location == MSFFT_DEVICE);
+    });
+}
+
+int msfft_write_truth_csv(const char* path, const int64_t* f, const double* c, int64_t count,
+                          char* err, size_t errlen) {
+    return guarded(err, errlen, [&] { write_truth_csv(path, f, c, count); });
+}
+
+int msfft_read_truth_csv(const char* path, int64_t n, int64_t* f, double* c, int64_t cap,
+                         int64_t* count, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] { *count = read_truth_csv(path, n, f, c, cap); });
 }
 
 }  // extern "C"
