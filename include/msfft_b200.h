@@ -227,6 +227,29 @@ int msfft_write_truth_csv(const char* path, const int64_t* f, const double* c, i
 int msfft_read_truth_csv(const char* path, int64_t n, int64_t* f, double* c, int64_t cap,
                          int64_t* count, char* err, size_t errlen);
 
+/* ---- phase-error Monte Carlo (phase_mc.hpp:14-56, paper Fig. 5) ---------------
+ * run_phase_experiment: per SNR, the accepted-trial histogram of the
+ * locator's phase error.  The attempts (spectra, sigma, noise seeds, bucket
+ * picks) replay the reference's Rng streams exactly on the host; the two
+ * lazy-source bucketizations of every trial run on the device.  trials_out
+ * (nullable) receives [nsnr][trials] accepted trials in order. */
+#define MSFFT_PHASE_BINS 70
+typedef struct msfft_phase_histogram {
+    double snr_db;
+    int64_t n, k, l_width, trials;
+    double bin_mass[MSFFT_PHASE_BINS]; /* 0.1-wide log10 bins over [-6, 1) */
+    double p50, p99, max;
+} msfft_phase_histogram;
+typedef struct msfft_phase_trial {
+    double dphi;
+    int64_t u, bucket, tau;
+    double y0[2], y_tau[2];
+    double measured_phi, true_phi;
+} msfft_phase_trial;
+int msfft_phase_experiment(int64_t n, int64_t k, int64_t b, const double* snr_list, int64_t nsnr,
+                           int64_t trials, uint64_t seed, msfft_phase_histogram* out,
+                           msfft_phase_trial* trials_out, char* err, size_t errlen);
+
 /* ---- host-only plan pieces (no device needed) -------------------------------
  * sigma_m, sigma^-1_m for the first `iterations` iterations of a transform
  * seeded `seed`: random_params(n, Rng(seed), 0) per iteration

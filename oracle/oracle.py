@@ -141,6 +141,11 @@ class Oracle:
         L.orc_read_signal_file.argtypes = [C.c_char_p, i64, P(f64), P(i64)] + E
         L.orc_write_truth_csv.argtypes = [C.c_char_p, i64, i64, P(i64), P(f64)] + E
         L.orc_read_truth_csv.argtypes = [C.c_char_p, i64, i64, P(i64), P(f64), P(i64)] + E
+        if hasattr(L, "orc_phase_experiment"):
+            L.orc_phase_experiment.argtypes = [i64, i64, i64, P(f64), i64, i64, u64, P(f64)] + E
+            L.orc_phase_trials.argtypes = [i64, i64, i64, f64, i64, i64, u64, P(i64), P(f64)] + E
+            L.orc_phase_experiment.restype = C.c_int
+            L.orc_phase_trials.restype = C.c_int
         for fn in ("orc_mod_inverse", "orc_check_parameter_bounds", "orc_cfg_validate",
                    "orc_random_params", "orc_initial_bucket_count", "orc_plan_build",
                    "orc_window", "orc_response_at", "orc_bucketize", "orc_predict", "orc_locate",
@@ -403,3 +408,23 @@ class Oracle:
         self._call(self.lib.orc_read_truth_csv, str(path).encode(), n, cap, _ptr(f, i64),
                    _ptr(c, f64), C.byref(cnt))
         return f[:cnt.value].copy(), c.view(np.complex128)[:cnt.value].copy()
+
+    # -- phase-error Monte Carlo (reference only) --------------------------------
+    def phase_experiment(self, n, k, b, snr_list, trials, seed):
+        """-> list of dicts {bin_mass (70), p50, p99, max} per SNR."""
+        if not hasattr(self.lib, "orc_phase_experiment"):
+            raise OracleError("other", "phase_mc is not in this oracle")
+        snr = np.ascontiguousarray(np.asarray(snr_list, dtype=np.float64))
+        out = np.zeros(73 * snr.size, np.float64)
+        self._call(self.lib.orc_phase_experiment, n, k, b, _ptr(snr, f64), snr.size, trials,
+                   seed, _ptr(out, f64))
+        out = out.reshape(-1, 73)
+        return [{"bin_mass": r[:70].copy(), "p50": r[70], "p99": r[71], "max": r[72]} for r in out]
+
+    def phase_trials(self, n, k, b, snr, si, trials, seed):
+        """Accepted trials of SNR index si: (ints [t,3] u/bucket/tau, doubles [t,7])."""
+        oi = np.zeros(3 * trials, np.int64)
+        od = np.zeros(7 * trials, np.float64)
+        self._call(self.lib.orc_phase_trials, n, k, b, float(snr), si, trials, seed,
+                   _ptr(oi, i64), _ptr(od, f64))
+        return oi.reshape(-1, 3), od.reshape(-1, 7)

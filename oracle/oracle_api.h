@@ -159,6 +159,18 @@ int orc_write_truth_csv(const char* path, int64_t n, int64_t count, const int64_
 int orc_read_truth_csv(const char* path, int64_t n, int64_t cap, int64_t* f, double* c,
                        int64_t* count, char* err, int64_t errlen);
 
+/* ---- phase-error Monte Carlo (phase_mc.cpp:94-212) ----
+ * run_phase_experiment: per SNR, bin_mass[70], p50, p99, max (out_hist is
+ * [nsnr][73]: 70 masses then p50, p99, max). */
+int orc_phase_experiment(int64_t n, int64_t k, int64_t b, const double* snr, int64_t nsnr,
+                         int64_t trials, uint64_t seed, double* out_hist, char* err,
+                         int64_t errlen);
+/* The accepted trials of SNR index si of the same experiment, in order:
+ * out_i [trials][3] = u, bucket, tau; out_d [trials][7] = y0 (re, im),
+ * y_tau (re, im), measured_phi, true_phi, dphi. */
+int orc_phase_trials(int64_t n, int64_t k, int64_t b, double snr, int64_t si, int64_t trials,
+                     uint64_t seed, int64_t* out_i, double* out_d, char* err, int64_t errlen);
+
 #ifdef __cplusplus
 }
 #endif

@@ -19,6 +19,7 @@
 
 #include "msfft/bucketize.hpp"
 #include "msfft/io.hpp"
+#include "msfft/phase_mc.hpp"
 #include "msfft/locate.hpp"
 #include "msfft/rng.hpp"
 #include "msfft/sfft4.hpp"
@@ -574,6 +575,50 @@ int orc_read_truth_csv(const char* path, int64_t n, int64_t cap, int64_t* f, dou
             ++i;
         }
         *count = i;
+    });
+}
+
+int orc_phase_experiment(int64_t n, int64_t k, int64_t b, const double* snr, int64_t nsnr,
+                         int64_t trials, uint64_t seed, double* out_hist, char* err,
+                         int64_t errlen) {
+    return guard(err, errlen, [&] {
+        const auto hs = run_phase_experiment(n, k, b, std::vector<double>(snr, snr + nsnr), trials,
+                                             seed);
+        for (size_t i = 0; i < hs.size(); ++i) {
+            double* o = out_hist + 73 * i;
+            for (int j = 0; j < PhaseErrorHistogram::kBinCount; ++j) o[j] = hs[i].bin_mass[j];
+            o[70] = hs[i].p50;
+            o[71] = hs[i].p99;
+            o[72] = hs[i].max;
+        }
+    });
+}
+
+// run_phase_experiment's accept loop for one SNR (phase_mc.cpp:175-186),
+// keeping each accepted trial's details (sample_phase_error discards them).
+int orc_phase_trials(int64_t n, int64_t k, int64_t b, double snr, int64_t si, int64_t trials,
+                     uint64_t seed, int64_t* out_i, double* out_d, char* err, int64_t errlen) {
+    return guard(err, errlen, [&] {
+        Rng rng = Rng::stream(seed, 0x5eed0000ull + static_cast<uint64_t>(si));
+        int64_t got = 0, attempts = 0;
+        const int64_t cap = 200 * trials + 1000;
+        while (got < trials) {
+            if (++attempts > cap) throw std::runtime_error("run_phase_experiment: rejection rate too high");
+            const auto t = sample_phase_trial(n, k, b, snr, rng);
+            if (!t) continue;
+            out_i[3 * got] = t->u;
+            out_i[3 * got + 1] = t->bucket;
+            out_i[3 * got + 2] = t->tau;
+            double* d = out_d + 7 * got;
+            d[0] = t->y0.real();
+            d[1] = t->y0.imag();
+            d[2] = t->y_tau.real();
+            d[3] = t->y_tau.imag();
+            d[4] = t->measured_phi;
+            d[5] = t->true_phi;
+            d[6] = t->dphi;
+            ++got;
+        }
     });
 }
 

@@ -30,6 +30,7 @@ EXPORTED = (
     "msfft_add_awgn", "msfft_dft_dense", "msfft_idft_dense", "msfft_top_k_spectrum",
     "msfft_error_metrics", "msfft_signal_file_length", "msfft_read_signal_file",
     "msfft_write_signal_file", "msfft_write_truth_csv", "msfft_read_truth_csv",
+    "msfft_phase_experiment",
 )
 
 i64, u64, f64, i32, u32 = C.c_int64, C.c_uint64, C.c_double, C.c_int32, C.c_uint32
@@ -48,6 +49,16 @@ class Stats(C.Structure):
         ("b_first", i64),
         ("stage_counts", i32 * MAX_ITERATIONS),
     ]
+
+
+class PhaseHistogramC(C.Structure):
+    _fields_ = [("snr_db", f64), ("n", i64), ("k", i64), ("l_width", i64), ("trials", i64),
+                ("bin_mass", f64 * 70), ("p50", f64), ("p99", f64), ("max", f64)]
+
+
+class PhaseTrialC(C.Structure):
+    _fields_ = [("dphi", f64), ("u", i64), ("bucket", i64), ("tau", i64), ("y0", f64 * 2),
+                ("y_tau", f64 * 2), ("measured_phi", f64), ("true_phi", f64)]
 
 
 class EvalMetricsC(C.Structure):
@@ -116,6 +127,10 @@ def lib() -> C.CDLL:
         L.msfft_write_signal_file.argtypes = [CP, VP, i64, i32, i32] + E
         L.msfft_write_truth_csv.argtypes = [CP, VP, VP, i64] + E
         L.msfft_read_truth_csv.argtypes = [CP, i64, VP, VP, i64, P(i64)] + E
+        if hasattr(L, "msfft_phase_experiment"):
+            L.msfft_phase_experiment.argtypes = [i64, i64, i64, VP, i64, i64, u64,
+                                                 P(PhaseHistogramC), P(PhaseTrialC)] + E
+            L.msfft_phase_experiment.restype = C.c_int
         for fn in ("msfft_generate_test_signal", "msfft_synthesize", "msfft_add_awgn",
                    "msfft_dft_dense", "msfft_idft_dense", "msfft_top_k_spectrum",
                    "msfft_error_metrics", "msfft_signal_file_length", "msfft_read_signal_file",

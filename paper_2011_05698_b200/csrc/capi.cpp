@@ -12,6 +12,7 @@
 #include "../../include/msfft_b200.h"
 #include "engine.hpp"
 #include "host_plan.hpp"
+#include "phase_mc.hpp"
 #include "signal_io.hpp"
 #include "signal_ops.hpp"
 #include "window.hpp"
@@ -512,6 +513,44 @@ int msfft_write_truth_csv(const char* path, const int64_t* f, const double* c, i
 int msfft_read_truth_csv(const char* path, int64_t n, int64_t* f, double* c, int64_t cap,
                          int64_t* count, char* err, size_t errlen) {
     return guarded(err, errlen, [&] { *count = read_truth_csv(path, n, f, c, cap); });
+}
+
+int msfft_phase_experiment(int64_t n, int64_t k, int64_t b, const double* snr_list, int64_t nsnr,
+                           int64_t trials, uint64_t seed, msfft_phase_histogram* out,
+                           msfft_phase_trial* trials_out, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        require_device();
+        std::vector<std::vector<PhaseTrialOut>> tr;
+        const auto hs = phase_experiment(n, k, b, std::vector<double>(snr_list, snr_list + nsnr),
+                                         trials, seed, trials_out ? &tr : nullptr);
+        for (size_t i = 0; i < hs.size(); ++i) {
+            msfft_phase_histogram& o = out[i];
+            o.snr_db = hs[i].snr_db;
+            o.n = hs[i].n;
+            o.k = hs[i].k;
+            o.l_width = hs[i].l_width;
+            o.trials = hs[i].trials;
+            for (int j = 0; j < MSFFT_PHASE_BINS; ++j) o.bin_mass[j] = hs[i].bin_mass[j];
+            o.p50 = hs[i].p50;
+            o.p99 = hs[i].p99;
+            o.max = hs[i].max;
+            if (trials_out)
+                for (size_t t = 0; t < tr[i].size(); ++t) {
+                    const PhaseTrialOut& a = tr[i][t];
+                    msfft_phase_trial& d = trials_out[i * static_cast<size_t>(trials) + t];
+                    d.dphi = a.dphi;
+                    d.u = a.u;
+                    d.bucket = a.bucket;
+                    d.tau = a.tau;
+                    d.y0[0] = a.y0[0];
+                    d.y0[1] = a.y0[1];
+                    d.y_tau[0] = a.y_tau[0];
+                    d.y_tau[1] = a.y_tau[1];
+                    d.measured_phi = a.measured_phi;
+                    d.true_phi = a.true_phi;
+                }
+        }
+    });
 }
 
 }  // extern "C"

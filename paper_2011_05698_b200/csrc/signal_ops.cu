@@ -334,10 +334,15 @@ void parallel_for(int64_t items, F&& fn) {
 
 void random_sparse_spectrum(int64_t n, int64_t k, uint64_t seed, std::vector<int64_t>& f,
                             std::vector<double>& c) {
+    HostRng rng(seed);
+    random_sparse_spectrum(n, k, rng, f, c);
+}
+
+void random_sparse_spectrum(int64_t n, int64_t k, HostRng& rng, std::vector<int64_t>& f,
+                            std::vector<double>& c) {
     if (n < 4 || !is_pow2_u(static_cast<uint64_t>(n)))
         throw std::invalid_argument("random_sparse_spectrum: bad n");
     if (k < 0 || k > n) throw std::invalid_argument("random_sparse_spectrum: k out of range");
-    HostRng rng(seed);
     std::set<int64_t> positions;  // Floyd's sampling (signal.cpp:107-112)
     for (int64_t j = n - k; j < n; ++j) {
         const int64_t t = static_cast<int64_t>(rng.below(static_cast<uint64_t>(j) + 1));

@@ -15,11 +15,16 @@
 #include <cstdint>
 #include <vector>
 
+#include "host_plan.hpp"
+
 namespace msfft_b200 {
 
 // Truth of generate_test_signal (random_sparse_spectrum with the reference's
 // Rng: Floyd sampling + uniform phases, signal.cpp:100-121), ascending f.
 void random_sparse_spectrum(int64_t n, int64_t k, uint64_t seed, std::vector<int64_t>& f,
+                            std::vector<double>& c);
+// Same draws from a caller's stream (random_sparse_spectrum(n, k, rng)).
+void random_sparse_spectrum(int64_t n, int64_t k, HostRng& rng, std::vector<int64_t>& f,
                             std::vector<double>& c);
 
 // synthesize (signal.cpp:76-98) of `count` tones (f ascending, c interleaved)

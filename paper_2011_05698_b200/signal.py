@@ -20,7 +20,8 @@ from . import InvalidArgument, _is_torch, _raise
 
 __all__ = ["EvalMetrics", "generate_test_signal", "synthesize", "add_awgn", "dft_dense",
            "idft_dense", "top_k_spectrum", "error_metrics", "read_signal_file",
-           "write_signal_file", "read_truth_csv", "write_truth_csv", "signal_file_length"]
+           "write_signal_file", "read_truth_csv", "write_truth_csv", "signal_file_length",
+           "PhaseErrorHistogram", "run_phase_experiment"]
 
 
 @dataclass
@@ -239,3 +240,54 @@ def read_truth_csv(path, n: int):
         if cnt.value <= cap:
             return f[:cnt.value], c[:cnt.value]
         cap = cnt.value
+
+
+@dataclass
+class PhaseErrorHistogram:
+    """phase_mc.hpp:19-30."""
+    snr_db: float
+    n: int
+    k: int
+    l_width: int
+    trials: int
+    bin_mass: np.ndarray
+    p50: float
+    p99: float
+    max: float
+    samples: np.ndarray | None = None  # accepted dphi in acceptance order (if requested)
+
+    kBinLo = -6.0
+    kBinWidth = 0.1
+    kBinCount = 70
+
+    @staticmethod
+    def bin_center(i: int) -> float:
+        return -6.0 + 0.1 * (i + 0.5)
+
+
+def run_phase_experiment(n: int, k: int, b: int, snr_list, trials: int, seed: int,
+                         keep_trials: bool = False):
+    """run_phase_experiment (phase_mc.cpp:166-212) on the GPU -> list of
+    PhaseErrorHistogram; with keep_trials, also a list (per SNR) of structured
+    trial records (dphi, u, bucket, tau, y0, y_tau, measured_phi, true_phi)."""
+    snr = np.ascontiguousarray(np.asarray(list(snr_list), dtype=np.float64))
+    hs = (_L.PhaseHistogramC * max(snr.size, 1))()
+    tr = (_L.PhaseTrialC * (snr.size * int(trials)))() if keep_trials and trials > 0 else None
+    e = _err()
+    _raise(_L.lib().msfft_phase_experiment(int(n), int(k), int(b), C.c_void_p(snr.ctypes.data),
+                                           snr.size, int(trials), int(seed) & (2**64 - 1), hs,
+                                           tr, e, 1024), e)
+    out, trials_out = [], []
+    for i in range(snr.size):
+        h = hs[i]
+        out.append(PhaseErrorHistogram(h.snr_db, h.n, h.k, h.l_width, h.trials,
+                                       np.array(h.bin_mass[:]), h.p50, h.p99, h.max))
+        if tr is not None:
+            rows = [tr[i * trials + t] for t in range(trials)]
+            trials_out.append([{"dphi": r.dphi, "u": r.u, "bucket": r.bucket, "tau": r.tau,
+                                "y0": complex(r.y0[0], r.y0[1]),
+                                "y_tau": complex(r.y_tau[0], r.y_tau[1]),
+                                "measured_phi": r.measured_phi, "true_phi": r.true_phi}
+                               for r in rows])
+            out[-1].samples = np.array([r["dphi"] for r in trials_out[-1]])
+    return (out, trials_out) if keep_trials else out
