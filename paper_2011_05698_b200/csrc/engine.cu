@@ -127,6 +127,7 @@ Plan::Plan(int64_t n, int64_t k, int64_t l, double q, double delta, bool c128, i
     for (const auto& ip : sched_.iters)
         rounds_max = std::max<int64_t>(rounds_max, static_cast<int64_t>(ip.taus.size()));
     lay_ = make_dec_layout(sched_.acc_cap, b_max_, budget_max_, rounds_max);
+    rounds_max_ = rounds_max;
     // Blocking streams: ordered after work on the legacy default stream, so
     // callers that pass no stream (e.g. torch default-stream producers) are safe.
     MSFFT_CUDA(cudaStreamCreateWithFlags(&own_stream_, cudaStreamDefault));
@@ -154,6 +155,7 @@ Plan::Plan(int64_t n, int64_t k, int64_t l, double q, double delta, bool c128, i
     dplan_compact_.x_compact = 1;
     if (const char* e = std::getenv("MSFFT_SPARSE_INGEST")) ingest_enabled_ = std::atoi(e) != 0;
     if (const char* e = std::getenv("MSFFT_INGEST_CHUNK")) ingest_chunk_ = std::max(1LL, std::atoll(e));
+    if (const char* e = std::getenv("MSFFT_WIDE_MAX_BATCH")) wide_max_batch_ = std::atoll(e);
     if (const char* e = std::getenv("MSFFT_DMA_VALIDATE_SHARE")) {
         dma_share_ = std::min(1.0, std::max(0.0, std::atof(e)));
         dma_share_fixed_ = true;
@@ -413,8 +415,25 @@ void Plan::run_chunk(int64_t batch, const void* d_x, int64_t x_stride, const int
         tf.reset(static_cast<size_t>(sched_.acc_cap));
         tv.reset(static_cast<size_t>(sched_.acc_cap));
     }
-    launch_decode(dplan_, lay_, y_.get(), d_sig, d_sig_inv, batch, dec_work_.get(), d_out_f,
-                  d_out_c, d_out_count, flags_.get(), st, tb.get(), tf.get(), tv.get());
+    if (!traced && lay_.big && batch <= wide_max_batch_) {
+        // large single signals: every phase of the decode over the whole GPU
+        if (!wide_)
+            wide_ = std::make_unique<WideDecoder>(dplan_, sched_.acc_cap, b_max_, budget_max_,
+                                                  rounds_max_);
+        int32_t bad = 0;  // unvalidated non-finite input: the call throws, skip the decode
+        MSFFT_CUDA(cudaMemcpyAsync(&bad, flags_.get() + 1, sizeof(bad), cudaMemcpyDeviceToHost, st));
+        MSFFT_CUDA(cudaStreamSynchronize(st));
+        if (!bad) {
+            const int iters = sched_.iterations;
+            const int64_t k = sched_.k, vps = dplan_.values_per_signal;
+            for (int64_t s = 0; s < batch; ++s)
+                wide_->run(y_.get() + s * vps, d_sig + s * iters, d_sig_inv + s * iters,
+                           d_out_f + s * k, d_out_c + s * k, d_out_count + s, flags_.get(), st);
+        }
+    } else {
+        launch_decode(dplan_, lay_, y_.get(), d_sig, d_sig_inv, batch, dec_work_.get(), d_out_f,
+                      d_out_c, d_out_count, flags_.get(), st, tb.get(), tf.get(), tv.get());
+    }
     if (opt.stage_times) {
         MSFFT_CUDA(cudaEventRecord(ev_stage_[3], st));
         MSFFT_CUDA(cudaEventSynchronize(ev_stage_[3]));
@@ -706,8 +725,19 @@ void Plan::decode_values(int64_t batch, double2* d_y, const uint64_t* seeds, int
     if (!lay_.in_smem) dec_work_.ensure(static_cast<size_t>(batch * lay_.bytes));
     MSFFT_CUDA(cudaMemsetAsync(flags_.get(), 0, 2 * sizeof(int32_t), st));
     upload_sigmas(batch, seeds, st);
-    launch_decode(dplan_, lay_, d_y, sig_.get(), sig_inv_.get(), batch, dec_work_.get(), d_out_f,
-                  d_out_c, d_out_count, flags_.get(), st);
+    if (lay_.big && batch <= wide_max_batch_) {
+        if (!wide_)
+            wide_ = std::make_unique<WideDecoder>(dplan_, sched_.acc_cap, b_max_, budget_max_,
+                                                  rounds_max_);
+        const int iters = sched_.iterations;
+        const int64_t k = sched_.k, vps = dplan_.values_per_signal;
+        for (int64_t s = 0; s < batch; ++s)
+            wide_->run(d_y + s * vps, sig_.get() + s * iters, sig_inv_.get() + s * iters,
+                       d_out_f + s * k, d_out_c + s * k, d_out_count + s, flags_.get(), st);
+    } else {
+        launch_decode(dplan_, lay_, d_y, sig_.get(), sig_inv_.get(), batch, dec_work_.get(),
+                      d_out_f, d_out_c, d_out_count, flags_.get(), st);
+    }
     check_flags(st);
 }
 

@@ -22,6 +22,7 @@
 #include "host_plan.hpp"
 #include "ingest.hpp"
 #include "plan_dev.cuh"
+#include "wide_decode.hpp"
 #include "window.hpp"
 
 namespace msfft_b200 {
@@ -151,6 +152,12 @@ private:
     void* gstage_[2] = {nullptr, nullptr};  // pinned compact staging
     size_t gstage_cap_ = 0;
     std::vector<int64_t> hsig_, hsig_inv_;
+    // grid-wide decode of large single signals (wide_decode.hpp): used in the
+    // serial path when the decode needs the large-size layout and the batch
+    // is too small to fill the GPU with one CTA per signal
+    std::unique_ptr<WideDecoder> wide_;
+    int64_t wide_max_batch_ = 8;     // MSFFT_WIDE_MAX_BATCH (0 disables)
+    int64_t rounds_max_ = 0;
     // validation split: the first dma_share_ of a validating host batch is
     // copied whole by the copy engine and checked by validate_kernel while
     // host threads scan the rest; the share adapts so both finish together

@@ -1,0 +1,900 @@
+// wide_decode.cu -- see wide_decode.hpp.  Compiled with --fmad=false; every
+// value is computed with decode_body.cuh's operations in its order.
+#include <algorithm>
+
+#include "decode_body.cuh"
+#include "wide_decode.hpp"
+
+namespace msfft_b200 {
+
+namespace {
+
+constexpr int kT = 256;               // threads per CTA of the grid kernels
+constexpr int kSelBits = 12;           // radix-select digit (last digit: 4 bits)
+constexpr int kSelBins = 1 << kSelBits;
+constexpr int kChunk = 4096;          // selection compaction chunk
+constexpr int kScanT = 1024;
+constexpr int kLongSeg = 64;          // longer event segments sort with a whole CTA
+constexpr int kLongSmem = 8192;
+
+unsigned grid_of(int64_t work) {
+    return static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>((work + kT - 1) / kT, 148 * 16)));
+}
+
+__device__ __forceinline__ int64_t n_or(const int32_t* n_dev, int64_t n_max) {
+    return n_dev ? static_cast<int64_t>(*n_dev) : n_max;
+}
+
+#define GRID_LOOP(i, n) \
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < (n); \
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+
+// ---------------------------------------------------------------- scans
+// Exclusive scan of in[0..len) into out (may alias); total -> *total.
+__global__ void __launch_bounds__(kScanT)
+scan_kernel(const int32_t* in, int64_t len_max, const int32_t* len_dev, int32_t* out,
+            int32_t* total) {
+    __shared__ int32_t part[kScanT];
+    const int64_t len = n_or(len_dev, len_max);
+    const int64_t per = (len + kScanT - 1) / kScanT;
+    const int64_t lo = threadIdx.x * per, hi = std::min<int64_t>(lo + per, len);
+    int32_t s = 0;
+    for (int64_t i = lo; i < hi; ++i) s += in[i];
+    part[threadIdx.x] = s;
+    __syncthreads();
+    for (int o = 1; o < kScanT; o <<= 1) {
+        const int32_t v = threadIdx.x >= o ? part[threadIdx.x - o] : 0;
+        __syncthreads();
+        part[threadIdx.x] += v;
+        __syncthreads();
+    }
+    int32_t run = part[threadIdx.x] - s;
+    for (int64_t i = lo; i < hi; ++i) {
+        const int32_t v = in[i];
+        out[i] = run;
+        run += v;
+    }
+    if (threadIdx.x == kScanT - 1 && total) *total = part[kScanT - 1];
+}
+
+// ---------------------------------------------------------------- K3
+__global__ void k3_tones(const DevPlan* __restrict__ P, int m, const int64_t* __restrict__ sigma,
+                         const int64_t* __restrict__ AF, const double2* __restrict__ AC,
+                         const int32_t* __restrict__ acc_n, int64_t* __restrict__ tone_u,
+                         int64_t* __restrict__ tone_i, double2* __restrict__ gc,
+                         int32_t* __restrict__ cnt) {
+    const DevIter& it = P->it[m];
+    const int64_t n = acc_n[0];
+    const int64_t b = it.b, L = it.l_width, nmask = P->n - 1;
+    const double invL = 1.0 / static_cast<double>(L);
+    const int64_t sg = sigma[m];
+    GRID_LOOP(j, n) {
+        const int64_t u = (sg * AF[j]) & nmask;
+        const int64_t i = static_cast<int64_t>(floor(static_cast<double>(u) * invL + 0.5));
+        tone_u[j] = u;
+        tone_i[j] = i;
+        const double2 c = AC[j];
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            const double g = ghat_at(it, (i - 1 + d) * L - u);
+            gc[j * 3 + d] = make_double2(g * c.x, g * c.y);
+            atomicAdd(&cnt[(i - 1 + d) & (b - 1)], 1);
+        }
+    }
+}
+
+__global__ void k3_rot(const DevPlan* __restrict__ P, int m, const int32_t* __restrict__ acc_n,
+                       const int64_t* __restrict__ tone_u, double2* __restrict__ rot) {
+    const DevIter& it = P->it[m];
+    const int nr = it.nrounds;
+    const int64_t* taus = P->taus + it.tau_off;
+    const int64_t total = static_cast<int64_t>(acc_n[0]) * nr;
+    GRID_LOOP(e, total) {
+        const int64_t j = e / nr, r = e - j * nr;
+        rot[e] = unit_root(P->n, P->inv_n, taus[r] * tone_u[j]);
+    }
+}
+
+__global__ void k3_scatter(const DevPlan* __restrict__ P, int m, const int32_t* __restrict__ acc_n,
+                           const int64_t* __restrict__ tone_i, const int32_t* __restrict__ start,
+                           int32_t* __restrict__ cursor, int32_t* __restrict__ ev) {
+    const int64_t b = P->it[m].b;
+    const int64_t total = static_cast<int64_t>(acc_n[0]) * 3;
+    GRID_LOOP(e, total) {
+        const int64_t j = e / 3;
+        const int d = static_cast<int>(e - j * 3);
+        const int64_t beta = (tone_i[j] - 1 + d) & (b - 1);
+        const int32_t pos = start[beta] + atomicAdd(&cursor[beta], 1);
+        ev[pos] = static_cast<int32_t>(j * 4 + d);
+    }
+}
+
+// One warp per bucket: its events in ascending tone order (keys j*4+d are
+// unique per bucket), by rank counting.
+__global__ void k3_segsort(const DevPlan* __restrict__ P, int m, const int32_t* __restrict__ start,
+                           const int32_t* __restrict__ cnt, const int32_t* __restrict__ ev,
+                           int32_t* __restrict__ ev2) {
+    const int64_t b = P->it[m].b;
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t beta = warp; beta < b; beta += nwarps) {
+        const int32_t s0 = start[beta], len = cnt[beta];
+        if (len > kLongSeg) continue;  // k3_segsort_long
+        for (int32_t e = lane; e < len; e += 32) {
+            const int32_t key = ev[s0 + e];
+            int32_t rank = 0;
+            for (int32_t o = 0; o < len; ++o) rank += ev[s0 + o] < key;
+            ev2[s0 + rank] = key;
+        }
+    }
+}
+
+// Long segments (small b): one CTA per bucket, keys staged in shared memory.
+__global__ void __launch_bounds__(kT)
+k3_segsort_long(const DevPlan* __restrict__ P, int m, const int32_t* __restrict__ start,
+                const int32_t* __restrict__ cnt, const int32_t* __restrict__ ev,
+                int32_t* __restrict__ ev2) {
+    __shared__ int32_t ks[kLongSmem];
+    const int64_t b = P->it[m].b;
+    for (int64_t beta = blockIdx.x; beta < b; beta += gridDim.x) {
+        const int32_t s0 = start[beta], len = cnt[beta];
+        if (len <= kLongSeg) continue;
+        const bool in_smem = len <= kLongSmem;
+        __syncthreads();
+        if (in_smem)
+            for (int32_t e = threadIdx.x; e < len; e += kT) ks[e] = ev[s0 + e];
+        __syncthreads();
+        const int32_t* src = in_smem ? ks : ev + s0;
+        for (int32_t e = threadIdx.x; e < len; e += kT) {
+            const int32_t key = src[e];
+            int32_t rank = 0;
+            for (int32_t o = 0; o < len; ++o) rank += src[o] < key;
+            ev2[s0 + rank] = key;
+        }
+    }
+}
+
+// One warp per (round, bucket): the prediction summed in ascending-f order,
+// lane 0 adding 32 staged contributions at a time (decode_body.cuh K3).
+__global__ void __launch_bounds__(kT)
+k3_sum(const DevPlan* __restrict__ P, int m, const int32_t* __restrict__ start,
+       const int32_t* __restrict__ cnt, const int32_t* __restrict__ ev2,
+       const double2* __restrict__ gc, const double2* __restrict__ rot, double2* __restrict__ Y) {
+    __shared__ double2 stage[kT];
+    const DevIter& it = P->it[m];
+    const int64_t b = it.b;
+    const int nr = it.nrounds;
+    const int lane = threadIdx.x & 31;
+    const int wslot = threadIdx.x & ~31;
+    const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t e = warp; e < static_cast<int64_t>(nr) * b; e += nwarps) {
+        const int r = static_cast<int>(e / b);
+        const int64_t beta = e - static_cast<int64_t>(r) * b;
+        const int32_t s0 = start[beta], len = cnt[beta];
+        if (len == 0) continue;
+        double2 pred = make_double2(0.0, 0.0);
+        for (int32_t c0 = 0; c0 < len; c0 += 32) {
+            const int32_t take = min(32, len - c0);
+            if (lane < take) {
+                const int32_t key = ev2[s0 + c0 + lane];
+                const int64_t j = key >> 2;
+                const int d = key & 3;
+                stage[threadIdx.x] = cmul(gc[j * 3 + d], rot[j * nr + r]);
+            }
+            __syncwarp();
+            if (lane == 0)
+                for (int l = 0; l < take; ++l) {
+                    const double2 v = stage[wslot + l];
+                    pred.x += v.x;
+                    pred.y += v.y;
+                }
+            __syncwarp();
+        }
+        if (lane == 0) {
+            const double2 o = Y[e];
+            Y[e] = make_double2(o.x - pred.x, o.y - pred.y);
+        }
+    }
+}
+
+// ---------------------------------------------------------------- select
+// keys: value bits + 1 for |.| >= 0 (NaN -> 0, ranks last); larger = earlier.
+__global__ void keys_from_values(const double2* __restrict__ v, int64_t n_max,
+                                 const int32_t* __restrict__ n_dev, double* __restrict__ mag,
+                                 uint64_t* __restrict__ key) {
+    const int64_t n = n_or(n_dev, n_max);
+    GRID_LOOP(j, n) {
+        const double2 x = v[j];
+        const double mg = cabs_ref(x.x, x.y);
+        if (mag) mag[j] = mg == mg ? mg : -1.0;
+        key[j] = mg == mg ? static_cast<uint64_t>(__double_as_longlong(mg)) + 1ull : 0ull;
+    }
+}
+
+__global__ void sel_init(uint64_t* sel, int64_t kth_host, const int32_t* kth_dev,
+                         int64_t cap_kth) {
+    int64_t kth = kth_dev ? static_cast<int64_t>(*kth_dev) : kth_host;
+    if (kth > cap_kth) kth = cap_kth;
+    sel[0] = 0;
+    sel[1] = 0;
+    sel[2] = static_cast<uint64_t>(kth);
+}
+
+__global__ void __launch_bounds__(kT)
+sel_hist(const uint64_t* __restrict__ key, int64_t n_max, const int32_t* __restrict__ n_dev,
+         const uint64_t* __restrict__ sel, int shift, int width, uint32_t* __restrict__ hist) {
+    __shared__ uint32_t h[kSelBins];
+    const int64_t n = n_or(n_dev, n_max);
+    const uint64_t prefix = sel[0], mask = sel[1];
+    if (sel[2] == 0) return;
+    const uint64_t dmask = (uint64_t{1} << width) - 1;
+    for (int i = threadIdx.x; i < kSelBins; i += kT) h[i] = 0;
+    __syncthreads();
+    GRID_LOOP(j, n) {
+        const uint64_t k = key[j];
+        if ((k & mask) == prefix) atomicAdd(&h[(k >> shift) & dmask], 1u);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < kSelBins; i += kT)
+        if (h[i]) atomicAdd(&hist[i], h[i]);
+}
+
+// Digit of the kth largest among the keys matching the prefix; updates the
+// prefix and the rank remaining inside the new class.
+__global__ void __launch_bounds__(kScanT)
+sel_pick(const uint32_t* __restrict__ hist, uint64_t* sel, int shift, int width) {
+    __shared__ uint64_t part[kScanT];
+    const uint64_t remaining = sel[2];
+    if (remaining == 0) return;
+    constexpr int per = kSelBins / kScanT;
+    const int t = threadIdx.x;
+    uint32_t hv[per];
+    uint64_t s = 0;
+#pragma unroll
+    for (int i = 0; i < per; ++i) {
+        hv[i] = hist[t * per + i];
+        s += hv[i];
+    }
+    part[t] = s;
+    __syncthreads();
+    for (int o = 1; o < kScanT; o <<= 1) {  // suffix sums over threads >= t
+        const uint64_t v = t + o < kScanT ? part[t + o] : 0;
+        __syncthreads();
+        part[t] += v;
+        __syncthreads();
+    }
+    const uint64_t above = part[t] - s;  // keys in higher bins
+    if (above < remaining && remaining <= above + s) {
+        uint64_t cum = above;
+#pragma unroll
+        for (int i = per - 1; i >= 0; --i) {
+            if (cum + hv[i] >= remaining && cum < remaining) {
+                sel[0] |= static_cast<uint64_t>(t * per + i) << shift;
+                sel[1] |= ((uint64_t{1} << width) - 1) << shift;
+                sel[2] = remaining - cum;
+            }
+            cum += hv[i];
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kT)
+sel_count(const uint64_t* __restrict__ key, int64_t n_max, const int32_t* __restrict__ n_dev,
+          const uint64_t* __restrict__ sel, int32_t* __restrict__ cgt, int32_t* __restrict__ ceq) {
+    __shared__ int gt_s, eq_s;
+    const int64_t n = n_or(n_dev, n_max);
+    const uint64_t thr = sel[0];
+    if (threadIdx.x == 0) gt_s = eq_s = 0;
+    __syncthreads();
+    int gt = 0, eq = 0;
+    const int64_t base = static_cast<int64_t>(blockIdx.x) * kChunk;
+    for (int i = threadIdx.x; i < kChunk; i += kT) {
+        const int64_t j = base + i;
+        if (j >= n) break;
+        const uint64_t k = key[j];
+        gt += k > thr;
+        eq += k == thr;
+    }
+    atomicAdd(&gt_s, gt);
+    atomicAdd(&eq_s, eq);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        cgt[blockIdx.x] = gt_s;
+        ceq[blockIdx.x] = eq_s;
+    }
+}
+
+// Per chunk: selected before it = gt before + min(eq before, need_eq).
+__global__ void __launch_bounds__(kScanT)
+sel_offsets(const int32_t* __restrict__ cgt, const int32_t* __restrict__ ceq, int64_t nchunks,
+            const uint64_t* __restrict__ sel, int32_t* __restrict__ off_sel,
+            int32_t* __restrict__ off_eq) {
+    __shared__ int32_t pg[kScanT], pe[kScanT];
+    const int64_t per = (nchunks + kScanT - 1) / kScanT;
+    const int64_t lo = threadIdx.x * per, hi = std::min<int64_t>(lo + per, nchunks);
+    int32_t sg = 0, se = 0;
+    for (int64_t i = lo; i < hi; ++i) {
+        sg += cgt[i];
+        se += ceq[i];
+    }
+    pg[threadIdx.x] = sg;
+    pe[threadIdx.x] = se;
+    __syncthreads();
+    for (int o = 1; o < kScanT; o <<= 1) {
+        const int32_t a = threadIdx.x >= o ? pg[threadIdx.x - o] : 0;
+        const int32_t c = threadIdx.x >= o ? pe[threadIdx.x - o] : 0;
+        __syncthreads();
+        pg[threadIdx.x] += a;
+        pe[threadIdx.x] += c;
+        __syncthreads();
+    }
+    const int64_t need = static_cast<int64_t>(sel[2]);
+    int32_t rg = pg[threadIdx.x] - sg, re = pe[threadIdx.x] - se;
+    for (int64_t i = lo; i < hi; ++i) {
+        off_sel[i] = rg + static_cast<int32_t>(std::min<int64_t>(re, need));
+        off_eq[i] = re;
+        rg += cgt[i];
+        re += ceq[i];
+    }
+}
+
+// Ordered compaction: keys > thr, and the first need_eq keys == thr.
+__global__ void __launch_bounds__(kT)
+sel_write(const uint64_t* __restrict__ key, int64_t n_max, const int32_t* __restrict__ n_dev,
+          const uint64_t* __restrict__ sel, const int32_t* __restrict__ off_sel,
+          const int32_t* __restrict__ off_eq, int32_t* __restrict__ out_idx) {
+    __shared__ int warp_sel[kT / 32], warp_eq[kT / 32];
+    __shared__ int64_t run_sel, run_eq;
+    const int64_t n = n_or(n_dev, n_max);
+    const uint64_t thr = sel[0];
+    const int64_t need_eq = static_cast<int64_t>(sel[2]);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (threadIdx.x == 0) {
+        run_sel = off_sel[blockIdx.x];
+        run_eq = off_eq[blockIdx.x];
+    }
+    __syncthreads();
+    const int64_t base = static_cast<int64_t>(blockIdx.x) * kChunk;
+    for (int r = 0; r < kChunk / kT; ++r) {
+        const int64_t j = base + static_cast<int64_t>(r) * kT + threadIdx.x;
+        const uint64_t k = j < n ? key[j] : 0ull;
+        const bool is_eq = j < n && k == thr;
+        const bool is_gt = j < n && k > thr;
+        const unsigned eq_mask = __ballot_sync(0xffffffffu, is_eq);
+        if (lane == 0) warp_eq[wid] = __popc(eq_mask);
+        __syncthreads();
+        int eq_before = __popc(eq_mask & ((1u << lane) - 1u)), eq_total = 0;
+        for (int w = 0; w < kT / 32; ++w) {
+            if (w < wid) eq_before += warp_eq[w];
+            eq_total += warp_eq[w];
+        }
+        const bool take = is_gt || (is_eq && run_eq + eq_before < need_eq);
+        const unsigned sel_mask = __ballot_sync(0xffffffffu, take);
+        if (lane == 0) warp_sel[wid] = __popc(sel_mask);
+        __syncthreads();
+        int sel_before = __popc(sel_mask & ((1u << lane) - 1u)), sel_total = 0;
+        for (int w = 0; w < kT / 32; ++w) {
+            if (w < wid) sel_before += warp_sel[w];
+            sel_total += warp_sel[w];
+        }
+        if (take) out_idx[run_sel + sel_before] = static_cast<int32_t>(j);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            run_sel += sel_total;
+            run_eq += eq_total;
+        }
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------- K4
+// rank among the selected buckets by (|y0| desc, bucket asc): blockIdx.x
+// tiles the elements, blockIdx.y the comparison range; partial ranks add up.
+__global__ void __launch_bounds__(kT)
+k4_rank(const int32_t* __restrict__ sel_idx, int64_t budget, const double* __restrict__ mag,
+        int32_t* __restrict__ rank_out) {
+    __shared__ double tm[kT];
+    __shared__ int32_t ti[kT];
+    const int64_t e = static_cast<int64_t>(blockIdx.x) * kT + threadIdx.x;
+    const int32_t idx = e < budget ? sel_idx[e] : 0;
+    const double mj = e < budget ? mag[idx] : 0.0;
+    const int64_t span = (budget + gridDim.y - 1) / gridDim.y;
+    const int64_t c0 = blockIdx.y * span, c1 = std::min<int64_t>(c0 + span, budget);
+    int32_t rank = 0;
+    for (int64_t t0 = c0; t0 < c1; t0 += kT) {
+        __syncthreads();
+        if (t0 + threadIdx.x < c1) {
+            const int32_t o = sel_idx[t0 + threadIdx.x];
+            ti[threadIdx.x] = o;
+            tm[threadIdx.x] = mag[o];
+        }
+        __syncthreads();
+        const int lim = static_cast<int>(std::min<int64_t>(kT, c1 - t0));
+        for (int q = 0; q < lim; ++q) {
+            const double mi = tm[q];
+            rank += (mi > mj) || (mi == mj && ti[q] < idx);
+        }
+    }
+    if (e < budget && rank) atomicAdd(&rank_out[e], rank);
+}
+
+__global__ void k4_scatter(const int32_t* __restrict__ sel_idx, const int32_t* __restrict__ rank,
+                           int64_t budget, int32_t* __restrict__ order) {
+    GRID_LOOP(e, budget) order[rank[e]] = sel_idx[e];
+}
+
+__global__ void k4_thr(const int32_t* __restrict__ order, int64_t budget,
+                       const double* __restrict__ mag, double* thr) {
+    *thr = 0.2 * mag[order[budget - 1]];
+}
+
+// ---------------------------------------------------------------- K5
+__global__ void k5_stage(const DevPlan* __restrict__ P, int m, const int32_t* __restrict__ order,
+                         const double2* __restrict__ Y, double2* __restrict__ yr) {
+    const DevIter& it = P->it[m];
+    const int nr = it.nrounds;
+    const int64_t total = it.budget * nr;
+    GRID_LOOP(e, total) {
+        const int64_t rk = e / nr, st = e - rk * nr;
+        yr[e] = Y[st * it.b + order[rk]];
+    }
+}
+
+__global__ void k5_phase(const DevPlan* __restrict__ P, int m, const double2* __restrict__ yr,
+                         double* __restrict__ phi, int32_t* __restrict__ pcode) {
+    const DevIter& it = P->it[m];
+    const int nr = it.nrounds, ns = nr - 1;
+    const int64_t total = it.budget * ns;
+    GRID_LOOP(e, total) {
+        const int64_t rk = e / ns, st = e - rk * ns + 1;
+        const double2 y0e = yr[rk * nr], yt = yr[rk * nr + st];
+        int code = 0;
+        double ph = 0.0;
+        if (yt.x == 0.0 && yt.y == 0.0) {
+            code = 1;
+        } else {
+            const double2 z = cdiv_ref(y0e.x, y0e.y, yt.x, yt.y);
+            if (z.x == 0.0 && z.y == 0.0) code = 2;
+            ph = atan2(z.y, z.x);
+            if (ph < 0.0) ph += kTwoPi;
+            ph = ph + 0.0;
+        }
+        phi[e] = ph;
+        pcode[e] = code;
+    }
+}
+
+// One lane group per ranked bucket (decode_body.cuh K5 + K6 estimate).
+__global__ void __launch_bounds__(kT)
+k5_locate(const DevPlan* __restrict__ P, int m, const int64_t* __restrict__ sigma_inv,
+          const int32_t* __restrict__ order, const double* __restrict__ mag,
+          const double* __restrict__ thr_p, const double2* __restrict__ yr,
+          const double* __restrict__ phi_t, const int32_t* __restrict__ pcode,
+          int64_t* __restrict__ cand_f, double2* __restrict__ cand_v, int32_t* __restrict__ err) {
+    const DevIter& it = P->it[m];
+    const int64_t n = P->n, nmask = n - 1;
+    const double inv_n = P->inv_n;
+    const int64_t L = it.l_width;
+    const double Ld = static_cast<double>(L), invL = 1.0 / Ld;
+    const int nr = it.nrounds, ns = nr - 1;
+    const int64_t* taus = P->taus + it.tau_off;
+    const int64_t budget = it.budget;
+    const int64_t lcfg = P->l;
+    const double q = P->q;
+    const double thr = *thr_p;
+    const int64_t sgi = sigma_inv[m];
+    const int gsz = lcfg > 16 ? 32 : (lcfg > 8 ? 16 : (lcfg > 4 ? 8 : 4));
+    const int lane = threadIdx.x & 31;
+    const int glane = lane & (gsz - 1);
+    const int64_t gid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / gsz;
+    const int64_t ngroups = (static_cast<int64_t>(gridDim.x) * blockDim.x) / gsz;
+    const int64_t rounds_up = (budget + ngroups - 1) / ngroups * ngroups;
+    for (int64_t rank = gid; rank < rounds_up; rank += ngroups) {
+        // whole warp past the budget: skip (warp-uniform)
+        const int64_t warp_first = rank - (lane / gsz);
+        if (warp_first >= budget) continue;
+        const bool live = rank < budget;
+        const int64_t beta = live ? order[rank] : 0;
+        int64_t f_out = -1;
+        double2 v_out = make_double2(0.0, 0.0);
+        const double2 y0 = live ? yr[rank * nr] : make_double2(0.0, 0.0);
+        bool ok = live && mag[beta] > thr;
+        if (ok && y0.x == 0.0 && y0.y == 0.0) ok = false;
+        double u_min = (2.0 * static_cast<double>(beta) - 1.0) * Ld / 2.0;
+        double len = Ld;
+        int stage = 0;
+        const int nst = it.nstage_tab;
+        while (nst >= 0 ? stage < nst : len > 1.0 + 1e-9) {
+            ++stage;
+            if (stage >= nr) {
+                if (ok && glane == 0) atomicCAS(err, 0, kDecErrRounds);
+                ok = false;
+                break;
+            }
+            double ph = 0.0;
+            if (ok) {
+                const int64_t pe = rank * ns + (stage - 1);
+                const int code = pcode[pe];
+                if (code == 1) {
+                    ok = false;
+                } else {
+                    if (code == 2) {
+                        if (glane == 0) atomicCAS(err, 0, kDecErrPhaseZero);
+                        ok = false;
+                    }
+                    ph = phi_t[pe];
+                }
+            }
+            const int64_t tau = taus[stage];
+            const double rblk = nst >= 0 ? it.stage_blk[stage - 1] : len / static_cast<double>(lcfg);
+            double best_d = INFINITY;
+            int best_j = 0x7fffffff;
+            for (int64_t j = glane; j < lcfg; j += gsz) {
+                const double center = u_min + (static_cast<double>(j) + 0.5) * rblk;
+                const double d = circular_phase_distance(position_phase(center, tau, n, inv_n), ph);
+                if (d < best_d) {
+                    best_d = d;
+                    best_j = static_cast<int>(j);
+                }
+            }
+            for (int o = gsz >> 1; o > 0; o >>= 1) {
+                const double od = __shfl_xor_sync(0xffffffffu, best_d, o);
+                const int oj = __shfl_xor_sync(0xffffffffu, best_j, o);
+                if (od < best_d || (od == best_d && oj < best_j)) {
+                    best_d = od;
+                    best_j = oj;
+                }
+            }
+            if (best_j == 0x7fffffff) best_j = 0;
+            u_min = u_min + (static_cast<double>(best_j) - q / 2.0) * rblk;
+            len = nst >= 0 ? it.stage_len[stage] : len * (q + 1.0) / static_cast<double>(lcfg);
+        }
+        if (ok) {
+            const double lo = u_min, hi = u_min + len;
+            int64_t u = static_cast<int64_t>(ceil(lo));
+            if (!(static_cast<double>(u) < hi)) u = llround(0.5 * (lo + hi));
+            u %= n;
+            if (u < 0) u += n;
+            const int64_t i = static_cast<int64_t>(floor(static_cast<double>(u) * invL + 0.5));
+            const double g = ghat_at(it, i * L - u);
+            if (!(fabs(g) < 0.5)) {
+                v_out = make_double2(y0.x / g, y0.y / g);
+                f_out = (sgi * u) & nmask;
+            }
+        }
+        if (live && glane == 0) {
+            cand_f[rank] = f_out;
+            cand_v[rank] = v_out;
+        }
+    }
+}
+
+// ---------------------------------------------------------------- K6
+// position of each accepted candidate in (f, rank) order (2-D split as
+// k4_rank), then byf[pos] = rank.
+__global__ void __launch_bounds__(kT)
+k6_sortf(const int64_t* __restrict__ cand_f, int64_t budget, int32_t* __restrict__ pos_out) {
+    __shared__ int64_t tf[kT];
+    const int64_t r = static_cast<int64_t>(blockIdx.x) * kT + threadIdx.x;
+    const int64_t fr = r < budget ? cand_f[r] : -1;
+    const int64_t span = (budget + gridDim.y - 1) / gridDim.y;
+    const int64_t c0 = blockIdx.y * span, c1 = std::min<int64_t>(c0 + span, budget);
+    int32_t pos = 0;
+    for (int64_t t0 = c0; t0 < c1; t0 += kT) {
+        __syncthreads();
+        if (t0 + threadIdx.x < c1) tf[threadIdx.x] = cand_f[t0 + threadIdx.x];
+        __syncthreads();
+        const int lim = static_cast<int>(std::min<int64_t>(kT, c1 - t0));
+        for (int qq = 0; qq < lim; ++qq) {
+            const int64_t fo = tf[qq];
+            pos += fo >= 0 && (fo < fr || (fo == fr && t0 + qq < r));
+        }
+    }
+    if (r < budget && fr >= 0 && pos) atomicAdd(&pos_out[r], pos);
+}
+
+__global__ void k6_scatter(const int64_t* __restrict__ cand_f, const int32_t* __restrict__ pos,
+                           int64_t budget, int32_t* __restrict__ byf,
+                           int32_t* __restrict__ naccepted) {
+    GRID_LOOP(r, budget) {
+        if (cand_f[r] >= 0) {
+            byf[pos[r]] = static_cast<int32_t>(r);
+            atomicAdd(naccepted, 1);
+        }
+    }
+}
+
+// Run starts: the found-map sum in rank order, presence in the accumulated
+// list, and the "new f" flag.
+__global__ void k6_runs(const int64_t* __restrict__ cand_f, const double2* __restrict__ cand_v,
+                        const int32_t* __restrict__ byf, const int32_t* __restrict__ naccepted,
+                        const int64_t* __restrict__ AF, const int32_t* __restrict__ acc_n,
+                        double2* __restrict__ run_sum, int32_t* __restrict__ newflag) {
+    const int64_t A = naccepted[0];
+    const int an = acc_n[0];
+    GRID_LOOP(p, A) {
+        const int64_t f = cand_f[byf[p]];
+        const bool start = p == 0 || cand_f[byf[p - 1]] != f;
+        int32_t flag = 0;
+        if (start) {
+            double2 sum = make_double2(0.0, 0.0);
+            for (int64_t p2 = p; p2 < A && cand_f[byf[p2]] == f; ++p2) {
+                const double2 v = cand_v[byf[p2]];
+                sum.x += v.x;
+                sum.y += v.y;
+            }
+            run_sum[p] = sum;
+            int lo = 0, hi = an;
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (AF[mid] < f) lo = mid + 1; else hi = mid;
+            }
+            flag = (lo < an && AF[lo] == f) ? 0 : 1;
+        }
+        newflag[p] = flag;
+    }
+}
+
+__global__ void k6_newf(const int64_t* __restrict__ cand_f, const int32_t* __restrict__ byf,
+                        const int32_t* __restrict__ naccepted, const int32_t* __restrict__ newflag,
+                        const int32_t* __restrict__ newpos, int64_t* __restrict__ newf) {
+    const int64_t A = naccepted[0];
+    GRID_LOOP(p, A) {
+        if (newflag[p]) newf[newpos[p]] = cand_f[byf[p]];
+    }
+}
+
+__global__ void k6_merge_acc(const int64_t* __restrict__ AF, const double2* __restrict__ AC,
+                             const int32_t* __restrict__ acc_n, const int64_t* __restrict__ newf,
+                             const int32_t* __restrict__ nnew_p, const int64_t* __restrict__ cand_f,
+                             const int32_t* __restrict__ byf, const int32_t* __restrict__ naccepted,
+                             const double2* __restrict__ run_sum, int64_t* __restrict__ NF,
+                             double2* __restrict__ NC) {
+    const int64_t an = acc_n[0];
+    const int nnew = nnew_p[0];
+    const int A = naccepted[0];
+    GRID_LOOP(j, an) {
+        const int64_t fj = AF[j];
+        int lo = 0, hi = nnew;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (newf[mid] < fj) lo = mid + 1; else hi = mid;
+        }
+        const int before = lo;
+        int plo = 0, phi2 = A;
+        while (plo < phi2) {
+            const int mid = (plo + phi2) >> 1;
+            if (cand_f[byf[mid]] < fj) plo = mid + 1; else phi2 = mid;
+        }
+        double2 c = AC[j];
+        if (plo < A && cand_f[byf[plo]] == fj) {
+            const double2 add = run_sum[plo];
+            c = make_double2(c.x + add.x, c.y + add.y);
+        }
+        NF[j + before] = fj;
+        NC[j + before] = c;
+    }
+}
+
+__global__ void k6_merge_new(const int64_t* __restrict__ AF, const int32_t* __restrict__ acc_n,
+                             const int64_t* __restrict__ cand_f, const int32_t* __restrict__ byf,
+                             const int32_t* __restrict__ naccepted,
+                             const int32_t* __restrict__ newflag, const int32_t* __restrict__ newpos,
+                             const double2* __restrict__ run_sum, int64_t* __restrict__ NF,
+                             double2* __restrict__ NC) {
+    const int64_t A = naccepted[0];
+    const int an = acc_n[0];
+    GRID_LOOP(p, A) {
+        if (!newflag[p]) continue;
+        const int64_t fr = cand_f[byf[p]];
+        int lo = 0, hi = an;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (AF[mid] < fr) lo = mid + 1; else hi = mid;
+        }
+        const double2 sum = run_sum[p];
+        NF[lo + newpos[p]] = fr;
+        NC[lo + newpos[p]] = make_double2(0.0 + sum.x, 0.0 + sum.y);
+    }
+}
+
+__global__ void k6_count(int32_t* scal) {
+    scal[0] += scal[1];  // acc_n += new_n
+    scal[4] = 0;         // accepted counter for the next iteration
+}
+
+// ---------------------------------------------------------------- K7
+__global__ void k7_kth(int32_t* scal, int64_t K) {
+    scal[2] = static_cast<int32_t>(std::min<int64_t>(scal[0], K));
+}
+
+__global__ void k7_emit(const int32_t* __restrict__ sel_idx, const int32_t* __restrict__ scal,
+                        const int64_t* __restrict__ AF, const double2* __restrict__ AC,
+                        int64_t* __restrict__ out_f, double2* __restrict__ out_c,
+                        int64_t* __restrict__ out_count) {
+    const int64_t keep = scal[2];
+    GRID_LOOP(p, keep) {
+        const int32_t j = sel_idx[p];
+        out_f[p] = AF[j];
+        out_c[p] = AC[j];
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) *out_count = keep;
+}
+
+}  // namespace
+
+WideDecoder::WideDecoder(const DevPlan& plan, int64_t acc_cap, int64_t b_max, int64_t budget_max,
+                         int64_t rounds_max)
+    : hplan_(plan),
+      acc_cap_(std::max<int64_t>(acc_cap, 1)),
+      b_max_(b_max),
+      budget_max_(std::max<int64_t>(budget_max, 1)),
+      rounds_max_(rounds_max) {
+    dplan_.reset(1);
+    MSFFT_CUDA(cudaMemcpy(dplan_.get(), &plan, sizeof(DevPlan), cudaMemcpyHostToDevice));
+    const int64_t A = acc_cap_, B = b_max_, Q = budget_max_, R = rounds_max_;
+    for (int p = 0; p < 2; ++p) {
+        acc_f_[p].reset(A);
+        acc_c_[p].reset(A);
+    }
+    scal_.reset(8);
+    sel_.reset(4);
+    thr_.reset(1);
+    tone_u_.reset(A);
+    tone_i_.reset(A);
+    gc_.reset(3 * A);
+    rot_.reset(A * R);
+    cnt_.reset(B);
+    start_.reset(B + 1);
+    cursor_.reset(B);
+    ev_.reset(3 * A);
+    ev2_.reset(3 * A);
+    const int64_t NK = std::max(B, A);
+    key_.reset(NK);
+    mag_.reset(B);
+    hist_.reset(kSelBins);
+    const int64_t nch = (NK + kChunk - 1) / kChunk;
+    chunk_gt_.reset(nch);
+    chunk_eq_.reset(nch);
+    chunk_off_sel_.reset(nch);
+    chunk_off_eq_.reset(nch);
+    sel_idx_.reset(std::max(Q, A));
+    order_.reset(Q);
+    yr_.reset(Q * R);
+    phi_.reset(Q * R);
+    pcode_.reset(Q * R);
+    cand_f_.reset(Q);
+    cand_v_.reset(Q);
+    cand_sum_.reset(Q);
+    pos_.reset(Q);
+    byf_.reset(Q);
+    newflag_.reset(Q);
+    newpos_.reset(Q);
+    newf_.reset(Q);
+}
+
+void WideDecoder::select_kth(const uint64_t* key, int64_t n_max, const int32_t* n_dev,
+                             int64_t kth_host, const int32_t* kth_dev, cudaStream_t st) {
+    sel_init<<<1, 1, 0, st>>>(sel_.get(), kth_host, kth_dev, n_max);
+    for (int top = 64; top > 0;) {
+        const int width = std::min(kSelBits, top);
+        const int shift = top - width;
+        MSFFT_CUDA(cudaMemsetAsync(hist_.get(), 0, kSelBins * sizeof(uint32_t), st));
+        sel_hist<<<std::min<unsigned>(grid_of(n_max), 148), kT, 0, st>>>(
+            key, n_max, n_dev, sel_.get(), shift, width, hist_.get());
+        sel_pick<<<1, kScanT, 0, st>>>(hist_.get(), sel_.get(), shift, width);
+        top = shift;
+    }
+    MSFFT_LAUNCH_CHECK("wide select");
+}
+
+void WideDecoder::compact_selected(const uint64_t* key, int64_t n_max, const int32_t* n_dev,
+                                   int32_t* out_idx, cudaStream_t st) {
+    const int64_t nch = (n_max + kChunk - 1) / kChunk;
+    sel_count<<<static_cast<unsigned>(nch), kT, 0, st>>>(key, n_max, n_dev, sel_.get(),
+                                                         chunk_gt_.get(), chunk_eq_.get());
+    sel_offsets<<<1, kScanT, 0, st>>>(chunk_gt_.get(), chunk_eq_.get(), nch, sel_.get(),
+                                      chunk_off_sel_.get(), chunk_off_eq_.get());
+    sel_write<<<static_cast<unsigned>(nch), kT, 0, st>>>(key, n_max, n_dev, sel_.get(),
+                                                         chunk_off_sel_.get(), chunk_off_eq_.get(),
+                                                         out_idx);
+    MSFFT_LAUNCH_CHECK("wide compaction");
+}
+
+void WideDecoder::run(double2* y, const int64_t* sigma, const int64_t* sigma_inv, int64_t* out_f,
+                      double2* out_c, int64_t* out_count, int32_t* err, cudaStream_t st) {
+    const DevPlan& H = hplan_;
+    const DevPlan* P = dplan_.get();
+    int32_t* acc_n = scal_.get();       // [0]
+    int32_t* new_n = scal_.get() + 1;   // [1]
+    int32_t* kth = scal_.get() + 2;     // [2]
+    int32_t* naccepted = scal_.get() + 4;
+    MSFFT_CUDA(cudaMemsetAsync(scal_.get(), 0, 8 * sizeof(int32_t), st));
+    const unsigned gA = grid_of(acc_cap_ * 3);
+    for (int m = 0; m < H.iters; ++m) {
+        const DevIter& it = H.it[m];
+        const int64_t b = it.b, nr = it.nrounds, budget = it.budget;
+        double2* Y = y + it.yoff;
+        const int cur = m & 1, nxt = cur ^ 1;
+        const int64_t* AF = acc_f_[cur].get();
+        const double2* AC = acc_c_[cur].get();
+        if (m > 0) {
+            // ---- K3
+            MSFFT_CUDA(cudaMemsetAsync(cnt_.get(), 0, b * sizeof(int32_t), st));
+            MSFFT_CUDA(cudaMemsetAsync(cursor_.get(), 0, b * sizeof(int32_t), st));
+            k3_tones<<<grid_of(acc_cap_), kT, 0, st>>>(P, m, sigma, AF, AC, acc_n, tone_u_.get(),
+                                                      tone_i_.get(), gc_.get(), cnt_.get());
+            k3_rot<<<grid_of(acc_cap_ * nr), kT, 0, st>>>(P, m, acc_n, tone_u_.get(), rot_.get());
+            scan_kernel<<<1, kScanT, 0, st>>>(cnt_.get(), b, nullptr, start_.get(), nullptr);
+            k3_scatter<<<gA, kT, 0, st>>>(P, m, acc_n, tone_i_.get(), start_.get(), cursor_.get(),
+                                          ev_.get());
+            k3_segsort<<<grid_of(b * 32), kT, 0, st>>>(P, m, start_.get(), cnt_.get(), ev_.get(),
+                                                       ev2_.get());
+            k3_segsort_long<<<static_cast<unsigned>(std::min<int64_t>(b, 148 * 4)), kT, 0, st>>>(
+                P, m, start_.get(), cnt_.get(), ev_.get(), ev2_.get());
+            k3_sum<<<grid_of(nr * b * 32), kT, 0, st>>>(P, m, start_.get(), cnt_.get(), ev2_.get(),
+                                                        gc_.get(), rot_.get(), Y);
+            MSFFT_LAUNCH_CHECK("wide K3");
+        }
+        // ---- K4
+        keys_from_values<<<grid_of(b), kT, 0, st>>>(Y, b, nullptr, mag_.get(), key_.get());
+        select_kth(key_.get(), b, nullptr, budget, nullptr, st);
+        compact_selected(key_.get(), b, nullptr, sel_idx_.get(), st);
+        {
+            const unsigned tiles = static_cast<unsigned>((budget + kT - 1) / kT);
+            const unsigned split = std::max(1u, std::min(32u, 296u / tiles));
+            MSFFT_CUDA(cudaMemsetAsync(pos_.get(), 0, budget * sizeof(int32_t), st));
+            k4_rank<<<dim3(tiles, split), kT, 0, st>>>(sel_idx_.get(), budget, mag_.get(), pos_.get());
+            k4_scatter<<<grid_of(budget), kT, 0, st>>>(sel_idx_.get(), pos_.get(), budget,
+                                                       order_.get());
+        }
+        k4_thr<<<1, 1, 0, st>>>(order_.get(), budget, mag_.get(), thr_.get());
+        // ---- K5
+        k5_stage<<<grid_of(budget * nr), kT, 0, st>>>(P, m, order_.get(), Y, yr_.get());
+        k5_phase<<<grid_of(budget * nr), kT, 0, st>>>(P, m, yr_.get(), phi_.get(), pcode_.get());
+        k5_locate<<<grid_of(budget * 32), kT, 0, st>>>(P, m, sigma_inv, order_.get(), mag_.get(),
+                                                       thr_.get(), yr_.get(), phi_.get(),
+                                                       pcode_.get(), cand_f_.get(), cand_v_.get(),
+                                                       err);
+        MSFFT_LAUNCH_CHECK("wide K4/K5");
+        // ---- K6
+        {
+            const unsigned tiles = static_cast<unsigned>((budget + kT - 1) / kT);
+            const unsigned split = std::max(1u, std::min(32u, 296u / tiles));
+            MSFFT_CUDA(cudaMemsetAsync(pos_.get(), 0, budget * sizeof(int32_t), st));
+            k6_sortf<<<dim3(tiles, split), kT, 0, st>>>(cand_f_.get(), budget, pos_.get());
+            k6_scatter<<<grid_of(budget), kT, 0, st>>>(cand_f_.get(), pos_.get(), budget, byf_.get(),
+                                                       naccepted);
+        }
+        k6_runs<<<grid_of(budget), kT, 0, st>>>(cand_f_.get(), cand_v_.get(), byf_.get(),
+                                                naccepted, AF, acc_n, cand_sum_.get(),
+                                                newflag_.get());
+        scan_kernel<<<1, kScanT, 0, st>>>(newflag_.get(), budget, naccepted, newpos_.get(), new_n);
+        k6_newf<<<grid_of(budget), kT, 0, st>>>(cand_f_.get(), byf_.get(), naccepted,
+                                                newflag_.get(), newpos_.get(), newf_.get());
+        k6_merge_acc<<<grid_of(acc_cap_), kT, 0, st>>>(AF, AC, acc_n, newf_.get(), new_n,
+                                                       cand_f_.get(), byf_.get(), naccepted,
+                                                       cand_sum_.get(), acc_f_[nxt].get(),
+                                                       acc_c_[nxt].get());
+        k6_merge_new<<<grid_of(budget), kT, 0, st>>>(AF, acc_n, cand_f_.get(), byf_.get(),
+                                                     naccepted, newflag_.get(), newpos_.get(),
+                                                     cand_sum_.get(), acc_f_[nxt].get(),
+                                                     acc_c_[nxt].get());
+        k6_count<<<1, 1, 0, st>>>(scal_.get());
+        MSFFT_LAUNCH_CHECK("wide K6");
+    }
+    // ---- K7: the K largest |c| (stable over ascending f), emitted in f order
+    const int fin = H.iters & 1;
+    keys_from_values<<<grid_of(acc_cap_), kT, 0, st>>>(acc_c_[fin].get(), acc_cap_, acc_n, nullptr,
+                                                       key_.get());
+    k7_kth<<<1, 1, 0, st>>>(scal_.get(), H.k);
+    select_kth(key_.get(), acc_cap_, acc_n, 0, kth, st);
+    compact_selected(key_.get(), acc_cap_, acc_n, sel_idx_.get(), st);
+    k7_emit<<<grid_of(H.k), kT, 0, st>>>(sel_idx_.get(), scal_.get(), acc_f_[fin].get(),
+                                         acc_c_[fin].get(), out_f, out_c, out_count);
+    MSFFT_LAUNCH_CHECK("wide K7");
+}
+
+}  // namespace msfft_b200

@@ -245,3 +245,23 @@ def test_sparse_ingest_validates_every_sample():
     x[1, 12345] = 0
     f, c, cnt, _ = plan.execute(x, [1, 2, 3])
     assert list(cnt) == [0, 0, 0]
+
+
+@pytest.mark.parametrize("n,k,dtype,snr", [(1 << 20, 2000, "complex128", 20.0),
+                                           (1 << 19, 1200, "complex64", 20.0),
+                                           (1 << 18, 3000, "complex128", None)])
+def test_wide_decode_bit_identical_to_cta_decode(oracle, monkeypatch, n, k, dtype, snr):
+    """Large single signals decode with the grid-wide kernels (wide_decode.cu);
+    outputs must equal the one-CTA decode (decode_body.cuh) bit for bit."""
+    x, _, _ = __import__("paper_2011_05698_b200.workloads", fromlist=["x"]).make_signal_np(
+        n, k, 5, snr, dtype, "loguniform_0.1_10")
+    x = x.astype(dtype)
+    delta = 1e-6 if snr is not None else 1e-8
+    res = []
+    for wide in ("8", "0"):
+        monkeypatch.setenv("MSFFT_WIDE_MAX_BATCH", wide)
+        plan = M.Plan(n, k, M.MultiscaleConfig(), delta, dtype)
+        res.append(plan.execute(x[None, :], [123]))
+    (f1, c1, n1, _), (f0, c0, n0, _) = res
+    assert int(n1[0]) == int(n0[0]) > 0
+    assert np.array_equal(f1, f0) and np.array_equal(c1, c0)
