@@ -148,6 +148,8 @@ Plan::Plan(int64_t n, int64_t k, int64_t l, double q, double delta, bool c128, i
     if (const char* e = std::getenv("MSFFT_FUSED")) fused_enabled_ = std::atoi(e) != 0;
     if (const char* e = std::getenv("MSFFT_FUSED_CHUNK")) fused_chunk_ = std::max(1LL, std::atoll(e));
     if (const char* e = std::getenv("MSFFT_FUSED_LAG")) fused_lag_ = std::max(1LL, std::atoll(e));
+    if (const char* e = std::getenv("MSFFT_FUSED_TAIL")) fused_tail_ = std::max(0LL, std::atoll(e));
+    if (const char* e = std::getenv("MSFFT_ENC_SMEM_PAD")) enc_smem_pad_ = std::atoll(e);
     fused_smem_ = std::max(enc_smem_, lay_.in_smem ? static_cast<size_t>(lay_.bytes) : size_t{0});
     flags_.reset(2);
     imap_ = make_ingest_map(sched_);
@@ -226,17 +228,24 @@ const Plan::FusedSet& Plan::fused_for(int64_t batch) {
             ++need[c * iters + tasks[i].m];
         }
     }
-    // E(0) .. E(lag) D(0) E(lag+1) D(1) ...: decodes trail their encodes
+    // E(0) .. E(lag) D(0) E(lag+1) D(1) ...: decodes trail their encodes by
+    // `lag` chunks so they rarely wait.  The last `tail` chunks get lag 0:
+    // their decodes are claimed right after their encode tasks and run the
+    // early iterations (gated per iteration) while the later iterations'
+    // encodes finish, so less decode work is left after the last encode.
     std::vector<int32_t> items;
     auto decodes = [&](int64_t c) {
         for (int64_t s = c * chunk; s < std::min(batch, (c + 1) * chunk); ++s)
             items.push_back(static_cast<int32_t>(-(s + 1)));
     };
+    const int64_t tail_from = std::max<int64_t>(0, nchunks - fused_tail_);
+    int64_t next_dec = 0;
     for (int64_t c = 0; c < nchunks; ++c) {
         items.insert(items.end(), enc[c].begin(), enc[c].end());
-        if (c - fused_lag_ >= 0) decodes(c - fused_lag_);
+        const int64_t upto = c >= tail_from ? c : c - fused_lag_;  // decode chunks <= upto
+        for (; next_dec <= upto; ++next_dec) decodes(next_dec);
     }
-    for (int64_t c = std::max<int64_t>(0, nchunks - fused_lag_); c < nchunks; ++c) decodes(c);
+    for (; next_dec < nchunks; ++next_dec) decodes(next_dec);
     FusedSet fs;
     fs.tasks.reset(tasks.size());
     fs.items.reset(items.size());
@@ -396,7 +405,7 @@ void Plan::run_chunk(int64_t batch, const void* d_x, int64_t x_stride, const int
     const TaskSet& ts = tasks_for(batch);
     if (opt.stage_times) MSFFT_CUDA(cudaEventRecord(ev_stage_[0], st));
     launch_encode(P, ts.d.get(), ts.count, d_x, c128_, x_stride, batch, d_sig, y_.get(),
-                  enc_smem_, st);
+                  enc_smem_ + enc_smem_pad_, st);
     if (opt.stage_times) MSFFT_CUDA(cudaEventRecord(ev_stage_[1], st));
     for (int m : big_b_iters_) {
         const DevIter& di = dplan_.it[m];

@@ -126,7 +126,9 @@ private:
     bool fused_enabled_ = true;   // persistent encode+decode launch when all b <= 256
     int64_t fused_chunk_ = 64;    // signals per fused chunk
     int64_t fused_lag_ = 2;       // chunks a decode trails its encode by
+    int64_t fused_tail_ = 0;      // last chunks whose decodes follow their encodes at once
     size_t fused_smem_ = 0;
+    size_t enc_smem_pad_ = 0;     // diagnostics: extra encode smem (lowers occupancy)
 
     cudaStream_t own_stream_ = nullptr, copy_stream_ = nullptr;
     cudaEvent_t ev_start_ = nullptr, ev_end_ = nullptr;

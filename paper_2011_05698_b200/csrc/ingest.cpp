@@ -137,51 +137,131 @@ bool block_non_finite(const U* p, int64_t count) {
     return acc != 0;
 }
 
+// Compact samples of row s, iteration m (random reads with prefetch).
+template <class E>
+void gather_row_iteration(const IngestMap& map, int64_t n, int iterations, const void* x,
+                          int64_t x_stride, int64_t s, int m, const int64_t* sigma, void* out) {
+    const uint64_t mask = static_cast<uint64_t>(n - 1);
+    const uint64_t sg = static_cast<uint64_t>(sigma[s * iterations + m]);
+    const auto& u = map.uni[m];
+    const auto& ps = map.pos[m];
+    const E* xs = static_cast<const E*>(x) + s * x_stride;
+    E* o = static_cast<E*>(out) + s * map.per_signal;
+    for (size_t i = 0; i < u.size(); ++i)
+        gather_interval(xs, mask, sg, u[i].first, u[i].second, o + ps[i]);
+}
+
+constexpr int kFuseShift = 17;  // 2^17-sample blocks: 1 MiB (c64) / 2 MiB (c128)
+
+// Validation scan of row s fused with its gather: the row's compact entries
+// are bucketed by source block once, then each block is scanned and its
+// entries copied while it is cache-resident.  Returns true on a non-finite
+// sample.
+template <class E, class U>
+bool scan_gather_row(const IngestMap& map, int64_t n, int iterations, const void* x,
+                     int64_t x_stride, int64_t s, const int64_t* sigma, void* out) {
+    thread_local std::vector<uint32_t> src, dst;
+    thread_local std::vector<int64_t> start;
+    const uint64_t mask = static_cast<uint64_t>(n - 1);
+    const int64_t C = map.per_signal;
+    int shift = 0;
+    while ((int64_t{1} << (shift + 1)) <= n && shift < kFuseShift) ++shift;
+    const int64_t nblk = n >> shift;
+    src.resize(static_cast<size_t>(C));
+    dst.resize(static_cast<size_t>(C));
+    start.assign(static_cast<size_t>(nblk + 1), 0);
+    // counting sort of (source index, compact position) by source block
+    for (int pass = 0; pass < 2; ++pass) {
+        for (int m = 0; m < iterations; ++m) {
+            const uint64_t sg = static_cast<uint64_t>(sigma[s * iterations + m]);
+            const auto& u = map.uni[m];
+            const auto& ps = map.pos[m];
+            for (size_t i = 0; i < u.size(); ++i) {
+                uint64_t idx = (sg * static_cast<uint64_t>(u[i].first)) & mask;
+                const int64_t len = u[i].second - u[i].first + 1;
+                for (int64_t j = 0; j < len; ++j) {
+                    const int64_t bk = static_cast<int64_t>(idx >> shift);
+                    if (pass == 0) {
+                        ++start[bk + 1];
+                    } else {
+                        const int64_t at = start[bk]++;
+                        src[at] = static_cast<uint32_t>(idx);
+                        dst[at] = static_cast<uint32_t>(ps[i] + j);
+                    }
+                    idx = (idx + sg) & mask;
+                }
+            }
+        }
+        if (pass == 0) {
+            for (int64_t b = 0; b < nblk; ++b) start[b + 1] += start[b];
+        } else {  // the fill advanced start[b] to the end of block b: shift back
+            for (int64_t b = nblk; b > 0; --b) start[b] = start[b - 1];
+            start[0] = 0;
+        }
+    }
+    const E* xs = static_cast<const E*>(x) + s * x_stride;
+    E* o = static_cast<E*>(out) + s * C;
+    const int64_t bl = int64_t{1} << shift;
+    bool nf = false;
+    for (int64_t b = 0; b < nblk; ++b) {
+        nf |= block_non_finite(reinterpret_cast<const U*>(xs + b * bl), 2 * bl);
+        for (int64_t e = start[b]; e < start[b + 1]; ++e) o[dst[e]] = xs[src[e]];
+    }
+    return nf;
+}
+
 }  // namespace
 
 bool gather_compact(HostPool& pool, const IngestMap& map, int64_t n, int iterations,
                     const void* x, int64_t x_stride, int elem_bytes, int64_t count,
                     const int64_t* sigma, void* out, bool validate, int64_t scan_from) {
-    const uint64_t mask = static_cast<uint64_t>(n - 1);
-    const int64_t C = map.per_signal;
-    // work items: (signal, iteration) gathers, then validation blocks
-    constexpr int64_t kScanBlock = int64_t{1} << 20;  // samples per scan item
-    scan_from = std::min(std::max<int64_t>(scan_from, 0), count);
-    const int64_t blocks_per_sig = validate ? (n + kScanBlock - 1) / kScanBlock : 0;
-    const int64_t gather_items = count * iterations;
+    scan_from = validate ? std::min(std::max<int64_t>(scan_from, 0), count) : count;
+    static const bool fused = [] {
+        const char* e = std::getenv("MSFFT_INGEST_FUSED");
+        return !e || std::atoi(e) != 0;
+    }();
+    // Rows [0, scan_from) need only their samples: one item per (row,
+    // iteration), random reads with prefetch.  Rows [scan_from, count) are
+    // also scanned for non-finite values: fused, one item per row scans it in
+    // cache-sized blocks and copies each block's samples while it is hot;
+    // otherwise (MSFFT_INGEST_FUSED=0) gather items for every row plus
+    // separate scan items per 2^20-sample block.
+    constexpr int64_t kScanBlock = int64_t{1} << 20;
+    const int64_t blocks_per_row = (n + kScanBlock - 1) / kScanBlock;
+    const int64_t gather_rows = fused ? scan_from : count;
+    const int64_t gather_items = gather_rows * iterations;
+    const int64_t scan_items = fused ? (count - scan_from) : (count - scan_from) * blocks_per_row;
     std::atomic<int> bad{0};
     const std::function<void(int64_t)> fn = [&](int64_t item) {
         if (item < gather_items) {
             const int64_t s = item / iterations;
             const int m = static_cast<int>(item - s * iterations);
-            const uint64_t sg = static_cast<uint64_t>(sigma[s * iterations + m]);
-            const auto& u = map.uni[m];
-            const auto& ps = map.pos[m];
-            if (elem_bytes == 8) {
-                const C64* xs = static_cast<const C64*>(x) + s * x_stride;
-                C64* o = static_cast<C64*>(out) + s * C;
-                for (size_t i = 0; i < u.size(); ++i)
-                    gather_interval(xs, mask, sg, u[i].first, u[i].second, o + ps[i]);
-            } else {
-                const C128* xs = static_cast<const C128*>(x) + s * x_stride;
-                C128* o = static_cast<C128*>(out) + s * C;
-                for (size_t i = 0; i < u.size(); ++i)
-                    gather_interval(xs, mask, sg, u[i].first, u[i].second, o + ps[i]);
-            }
+            if (elem_bytes == 8)
+                gather_row_iteration<C64>(map, n, iterations, x, x_stride, s, m, sigma, out);
+            else
+                gather_row_iteration<C128>(map, n, iterations, x, x_stride, s, m, sigma, out);
             return;
         }
         const int64_t v = item - gather_items;
-        const int64_t s = scan_from + v / blocks_per_sig;
-        const int64_t b0 = (v - s * blocks_per_sig) * kScanBlock;
-        const int64_t len = std::min(kScanBlock, n - b0);
         bool nf;
-        if (elem_bytes == 8)
-            nf = block_non_finite(static_cast<const uint32_t*>(x) + 2 * (s * x_stride + b0), 2 * len);
-        else
-            nf = block_non_finite(static_cast<const uint64_t*>(x) + 2 * (s * x_stride + b0), 2 * len);
+        if (fused) {
+            const int64_t s = scan_from + v;
+            nf = elem_bytes == 8 ? scan_gather_row<C64, uint32_t>(map, n, iterations, x, x_stride,
+                                                                 s, sigma, out)
+                                 : scan_gather_row<C128, uint64_t>(map, n, iterations, x, x_stride,
+                                                                  s, sigma, out);
+        } else {
+            const int64_t r = v / blocks_per_row;
+            const int64_t s = scan_from + r;
+            const int64_t b0 = (v - r * blocks_per_row) * kScanBlock;
+            const int64_t len = std::min(kScanBlock, n - b0);
+            nf = elem_bytes == 8
+                     ? block_non_finite(static_cast<const uint32_t*>(x) + 2 * (s * x_stride + b0), 2 * len)
+                     : block_non_finite(static_cast<const uint64_t*>(x) + 2 * (s * x_stride + b0), 2 * len);
+        }
         if (nf) bad.store(1, std::memory_order_relaxed);
     };
-    pool.run(gather_items + (count - scan_from) * blocks_per_sig, fn);
+    pool.run(gather_items + scan_items, fn);
     return bad.load() != 0;
 }
 

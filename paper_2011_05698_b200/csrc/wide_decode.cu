@@ -1,6 +1,7 @@
 // wide_decode.cu -- see wide_decode.hpp.  Compiled with --fmad=false; every
 // value is computed with decode_body.cuh's operations in its order.
 #include <algorithm>
+#include <cstdlib>
 
 #include "decode_body.cuh"
 #include "wide_decode.hpp"
@@ -773,6 +774,11 @@ WideDecoder::WideDecoder(const DevPlan& plan, int64_t acc_cap, int64_t b_max, in
     newflag_.reset(Q);
     newpos_.reset(Q);
     newf_.reset(Q);
+    out_f_.reset(std::max<int64_t>(plan.k, 1));
+    out_c_.reset(std::max<int64_t>(plan.k, 1));
+    out_count_.reset(1);
+    if (const char* e = std::getenv("MSFFT_WIDE_GRAPH")) use_graphs_ = std::atoi(e) != 0;
+    // kernel attributes are set before any capture
 }
 
 void WideDecoder::select_kth(const uint64_t* key, int64_t n_max, const int32_t* n_dev,
@@ -803,8 +809,44 @@ void WideDecoder::compact_selected(const uint64_t* key, int64_t n_max, const int
     MSFFT_LAUNCH_CHECK("wide compaction");
 }
 
+WideDecoder::~WideDecoder() {
+    for (auto& kv : graphs_) cudaGraphExecDestroy(kv.second);
+}
+
 void WideDecoder::run(double2* y, const int64_t* sigma, const int64_t* sigma_inv, int64_t* out_f,
                       double2* out_c, int64_t* out_count, int32_t* err, cudaStream_t st) {
+    const int64_t K = hplan_.k;
+    if (!use_graphs_) {
+        enqueue(y, sigma, sigma_inv, err, st);
+    } else {
+        const GraphKey key{y, sigma, sigma_inv, err};
+        auto it = graphs_.find(key);
+        if (it == graphs_.end()) {
+            cudaStream_t cap = nullptr;
+            MSFFT_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+            cudaGraph_t g = nullptr;
+            MSFFT_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+            enqueue(y, sigma, sigma_inv, err, cap);
+            MSFFT_CUDA(cudaStreamEndCapture(cap, &g));
+            cudaGraphExec_t ex = nullptr;
+            MSFFT_CUDA(cudaGraphInstantiate(&ex, g, 0));
+            cudaGraphDestroy(g);
+            cudaStreamDestroy(cap);
+            it = graphs_.emplace(key, ex).first;
+        }
+        MSFFT_CUDA(cudaGraphLaunch(it->second, st));
+    }
+    MSFFT_CUDA(cudaMemcpyAsync(out_f, out_f_.get(), K * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+    MSFFT_CUDA(cudaMemcpyAsync(out_c, out_c_.get(), K * sizeof(double2), cudaMemcpyDeviceToDevice, st));
+    MSFFT_CUDA(cudaMemcpyAsync(out_count, out_count_.get(), sizeof(int64_t),
+                               cudaMemcpyDeviceToDevice, st));
+}
+
+void WideDecoder::enqueue(double2* y, const int64_t* sigma, const int64_t* sigma_inv, int32_t* err,
+                          cudaStream_t st) {
+    int64_t* out_f = out_f_.get();
+    double2* out_c = out_c_.get();
+    int64_t* out_count = out_count_.get();
     const DevPlan& H = hplan_;
     const DevPlan* P = dplan_.get();
     int32_t* acc_n = scal_.get();       // [0]

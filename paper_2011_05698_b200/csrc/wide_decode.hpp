@@ -24,6 +24,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <map>
+#include <tuple>
 
 #include "cuda_check.hpp"
 #include "plan_dev.cuh"
@@ -40,7 +42,12 @@ public:
     void run(double2* y, const int64_t* sigma, const int64_t* sigma_inv, int64_t* out_f,
              double2* out_c, int64_t* out_count, int32_t* err, cudaStream_t st);
 
+    ~WideDecoder();
+
 private:
+    // the fixed kernel sequence of one decode (outputs to internal buffers)
+    void enqueue(double2* y, const int64_t* sigma, const int64_t* sigma_inv, int32_t* err,
+                 cudaStream_t st);
     void select_kth(const uint64_t* key, int64_t n_max, const int32_t* n_dev, int64_t kth_host,
                     const int32_t* kth_dev, cudaStream_t st);
     void compact_selected(const uint64_t* key, int64_t n_max, const int32_t* n_dev,
@@ -69,6 +76,14 @@ private:
     DeviceBuffer<double> phi_;
     DeviceBuffer<int32_t> pcode_, pos_, byf_, newflag_, newpos_;
     DeviceBuffer<int64_t> cand_f_, newf_;
+    // outputs, copied to the caller's buffers after the graph
+    DeviceBuffer<int64_t> out_f_, out_count_;
+    DeviceBuffer<double2> out_c_;
+    // one instantiated CUDA graph per (y, sigma, sigma_inv, err) tuple: the
+    // ~40 launches per iteration replay without per-launch host overhead
+    using GraphKey = std::tuple<const void*, const void*, const void*, const void*>;
+    std::map<GraphKey, cudaGraphExec_t> graphs_;
+    bool use_graphs_ = true;  // MSFFT_WIDE_GRAPH=0 launches eagerly
 };
 
 }  // namespace msfft_b200

@@ -265,3 +265,31 @@ def test_wide_decode_bit_identical_to_cta_decode(oracle, monkeypatch, n, k, dtyp
     (f1, c1, n1, _), (f0, c0, n0, _) = res
     assert int(n1[0]) == int(n0[0]) > 0
     assert np.array_equal(f1, f0) and np.array_equal(c1, c0)
+
+
+def test_sparse_ingest_split_validation(oracle, monkeypatch):
+    """Pinned host batches split validation between the copy engine + device
+    check (first rows) and the host's fused scan+gather (the rest): a
+    non-finite sample anywhere in any row raises, and clean results equal the
+    device-resident path bit for bit."""
+    import torch
+    n, k = 1 << 20, 20
+    monkeypatch.setenv("MSFFT_DMA_VALIDATE_SHARE", "0.5")
+    monkeypatch.setenv("MSFFT_INGEST_CHUNK", "3")
+    plan = M.Plan(n, k, M.MultiscaleConfig(), 1e-6, "complex64")
+    assert plan.ingest_samples_per_signal > 0
+    xs = np.stack([make_signal(oracle, dict(gen="np", n=n, k=k, seed=70 + s, snr=20.0,
+                                            dtype="complex64")) for s in range(8)])
+    xh = torch.from_numpy(xs).pin_memory()
+    seeds = np.arange(900, 908, dtype=np.uint64)
+    f, c, cnt, _ = plan.execute(xh, seeds)
+    out = (torch.empty((8, k), dtype=torch.int64, device="cuda"),
+           torch.empty((8, k), dtype=torch.complex128, device="cuda"),
+           torch.empty((8,), dtype=torch.int64, device="cuda"))
+    plan.execute(xh.cuda(), seeds, out=out)
+    assert np.array_equal(f, out[0].cpu().numpy()) and np.array_equal(c, out[1].cpu().numpy())
+    for row, col in ((1, 5), (6, n - 1), (7, 0), (4, n // 2 + 3)):
+        xb = xh.clone()
+        xb[row, col] = complex(float("nan"), 0.0)
+        with pytest.raises(M.InvalidArgument, match="ComplexSignal: non-finite sample"):
+            plan.execute(xb.pin_memory(), seeds)
