@@ -146,6 +146,19 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def e2e_batch(batch: int, sig_bytes: int, local_ranks: int) -> int:
+    """Signals per rank for the e2e leg: all of them when the host can pin
+    them (half of the available memory split over the local ranks), else as
+    many as fit (at least 8)."""
+    try:
+        import psutil
+        avail = psutil.virtual_memory().available
+    except Exception:  # noqa: BLE001
+        return batch
+    fit = int(avail * 0.5 / max(local_ranks, 1) / sig_bytes)
+    return max(min(batch, fit), min(batch, 8))
+
+
 def cpu_model():
     try:
         with open("/proc/cpuinfo") as f:
@@ -307,26 +320,31 @@ def main():
     # e2e through the public API with pinned host buffers
     e2e = None
     if not args.no_e2e and args.e2e_steps > 0:
-        xh = torch.empty((B, n), dtype=torch.complex64, pin_memory=True)
-        xh.copy_(x)
+        # every rank pins a host copy of its signals: size it to the host
+        # memory actually available (all local ranks share the host)
+        be = e2e_batch(B, n * 8, int(os.environ.get("LOCAL_WORLD_SIZE", world)))
+        xh = torch.empty((be, n), dtype=torch.complex64, pin_memory=True)
+        xh.copy_(x[:be])
+        eseeds = aseeds[:be]
         for _ in range(max(1, args.e2e_warmup)):
-            plan.execute(xh, aseeds)  # warm the host path
+            plan.execute(xh, eseeds)  # warm the host path
         if world > 1:
             torch.distributed.barrier()
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
-            fh, ch, nh, _ = plan.execute(xh, aseeds)  # validating call, D2H results
+            fh, ch, nh, _ = plan.execute(xh, eseeds)  # validating call, D2H results
         et = (time.perf_counter() - t0) / args.e2e_steps
         if world > 1:
             et = max_over_ranks(et, dev)
+        etotal = sum_over_ranks(be, dev) if world > 1 else be
         ingest = plan.ingest_samples_per_signal
-        e2e = {"value": total / et, "unit": "transforms/s",
-               "h2d_bytes_per_step": int(total * (ingest or n) * 8),
+        e2e = {"value": etotal / et, "unit": "transforms/s", "signals_per_step": int(etotal),
+               "h2d_bytes_per_step": int(etotal * (ingest or n) * 8),
                "ingest": (f"sparse: host threads gather the {ingest} samples per signal the "
                           "transform reads into pinned staging (and scan all n for "
                           "non-finite values); only those are copied" if ingest else
                           "dense: whole signals copied"),
-               "d2h_bytes_per_step": int(total * k * (8 + 16) + total * 8),
+               "d2h_bytes_per_step": int(etotal * k * (8 + 16) + etotal * 8),
                "ms_per_step": et * 1e3, "timing": "wall clock around msfft_execute (blocking)"}
         del xh
 

@@ -97,7 +97,13 @@ int ingest_threads() {
         if (v > 0) return v;
     }
     const unsigned hc = std::thread::hardware_concurrency();
-    return hc ? static_cast<int>(hc) : 8;
+    int threads = hc ? static_cast<int>(hc) : 8;
+    // one process per GPU (torchrun): the local ranks share the host cores
+    if (const char* e = std::getenv("LOCAL_WORLD_SIZE")) {
+        const int ranks = std::atoi(e);
+        if (ranks > 1) threads = std::max(1, threads / ranks);
+    }
+    return threads;
 }
 
 namespace {
