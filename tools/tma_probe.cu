@@ -19,7 +19,10 @@ __device__ __forceinline__ uint32_t s32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-constexpr int U = 8;
+#ifndef PROBE_U
+#define PROBE_U 8
+#endif
+constexpr int U = PROBE_U;
 
 // MODE 0: LDG 8 B, 1: LDG 16 B, 2: cp.async 16 B, 3: cp.async.bulk 16 B (TMA)
 template <int MODE>
@@ -98,14 +101,15 @@ float run(const float4* x, uint64_t n, int blocks, int iters, float* sink) {
     return ms;
 }
 
-int main() {
+int main(int argc, char** argv) {
     const uint64_t n = 1ull << 30;  // 16 GiB of float4
     float4* x;
     CK(cudaMalloc(&x, n * sizeof(float4)));
     CK(cudaMemset(x, 0, n * sizeof(float4)));
     float* sink;
-    CK(cudaMalloc(&sink, 148ull * 8 * 256 * 8 * sizeof(float)));
-    const int blocks = 148 * 8, iters = 64;
+    CK(cudaMalloc(&sink, (size_t)(argc > 1 ? atoi(argv[1]) : 148 * 8) * 256 * sizeof(float)));
+    const int blocks = argc > 1 ? atoi(argv[1]) : 148 * 8;
+    const int iters = argc > 2 ? atoi(argv[2]) : 64;
     const double reads = (double)blocks * 256 * iters * U;
     const char* names[] = {"LDG 8B (ldcs)", "LDG 16B (ldcs)", "cp.async 16B (LDGSTS)", "cp.async.bulk 16B (TMA)"};
     float ms[4] = {run<0>(x, n, blocks, iters, sink), run<1>(x, n, blocks, iters, sink),
