@@ -57,7 +57,7 @@ def parse():
     ap.add_argument("--k", type=int, default=64)
     ap.add_argument("--snr", type=float, default=25.0)
     ap.add_argument("--e2e-steps", type=int, default=4)
-    ap.add_argument("--e2e-warmup", type=int, default=4,
+    ap.add_argument("--e2e-warmup", type=int, default=6,
                     help="untimed host-path calls first (staging buffers, the adaptive "
                          "host-scan / DMA validation split)")
     ap.add_argument("--cpu-sample", type=int, default=0,

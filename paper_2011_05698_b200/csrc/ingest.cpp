@@ -1,6 +1,8 @@
 // ingest.cpp -- see ingest.hpp.
 #include "ingest.hpp"
 
+#include <immintrin.h>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
@@ -134,13 +136,63 @@ struct C128 {
 // true iff one of the `count` IEEE values has an all-ones exponent (inf or
 // NaN); integer-only so the pass vectorizes
 template <class U>
-bool block_non_finite(const U* p, int64_t count) {
+bool block_non_finite_scalar(const U* p, int64_t count) {
     constexpr int kBits = 8 * sizeof(U);
     constexpr U kExp = sizeof(U) == 4 ? U(0x7f800000u) : U(0x7ff0000000000000ull);
     constexpr U kOne = sizeof(U) == 4 ? U(0x00800000u) : U(0x0010000000000000ull);
     U acc = 0;
     for (int64_t i = 0; i < count; ++i) acc |= ((p[i] & kExp) + kOne) >> (kBits - 1);
     return acc != 0;
+}
+
+// AVX2 version with a 4 KiB software prefetch (measured on the GPU box over
+// 16 threads, tools/host_scan_probe.cpp: 131 GB/s vs 121 without the
+// prefetch and 100-118 for the scalar loop): exponent field + 1 overflows
+// into the sign bit.
+__attribute__((target("avx2"))) bool non_finite_avx2_32(const uint32_t* p, int64_t count) {
+    const __m256i e = _mm256_set1_epi32(0x7f800000), one = _mm256_set1_epi32(0x00800000);
+    __m256i acc = _mm256_setzero_si256();
+    int64_t i = 0;
+    for (; i + 32 <= count; i += 32) {
+        __builtin_prefetch(p + i + 1024);
+        __builtin_prefetch(p + i + 1024 + 16);
+        for (int k = 0; k < 4; ++k) {
+            const __m256i v = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(p + i + 8 * k));
+            acc = _mm256_or_si256(acc, _mm256_add_epi32(_mm256_and_si256(v, e), one));
+        }
+    }
+    return _mm256_movemask_ps(_mm256_castsi256_ps(acc)) != 0 ||
+           block_non_finite_scalar(p + i, count - i);
+}
+
+__attribute__((target("avx2"))) bool non_finite_avx2_64(const uint64_t* p, int64_t count) {
+    const __m256i e = _mm256_set1_epi64x(0x7ff0000000000000ll);
+    const __m256i one = _mm256_set1_epi64x(0x0010000000000000ll);
+    __m256i acc = _mm256_setzero_si256();
+    int64_t i = 0;
+    for (; i + 16 <= count; i += 16) {
+        __builtin_prefetch(p + i + 512);
+        __builtin_prefetch(p + i + 512 + 8);
+        for (int k = 0; k < 4; ++k) {
+            const __m256i v = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(p + i + 4 * k));
+            acc = _mm256_or_si256(acc, _mm256_add_epi64(_mm256_and_si256(v, e), one));
+        }
+    }
+    return _mm256_movemask_pd(_mm256_castsi256_pd(acc)) != 0 ||
+           block_non_finite_scalar(p + i, count - i);
+}
+
+bool has_avx2() {
+    static const bool v = __builtin_cpu_supports("avx2");
+    return v;
+}
+
+bool block_non_finite(const uint32_t* p, int64_t count) {
+    return has_avx2() ? non_finite_avx2_32(p, count) : block_non_finite_scalar(p, count);
+}
+
+bool block_non_finite(const uint64_t* p, int64_t count) {
+    return has_avx2() ? non_finite_avx2_64(p, count) : block_non_finite_scalar(p, count);
 }
 
 // Compact samples of row s, iteration m (random reads with prefetch).
