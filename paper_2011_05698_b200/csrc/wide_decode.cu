@@ -426,6 +426,38 @@ __global__ void k4_scatter(const int32_t* __restrict__ sel_idx, const int32_t* _
     GRID_LOOP(e, budget) order[rank[e]] = sel_idx[e];
 }
 
+// b <= 1024: the whole selection in one CTA -- |y0| (NaN -> -1), stable rank
+// by (|y0| desc, bucket asc) of every bucket, order[rank] for the ranked
+// ones and the 0.2 * kth threshold (decode_body.cuh K4, small path).
+constexpr int kSmallK4 = 1024;
+__global__ void __launch_bounds__(kSmallK4)
+k4_small(const DevPlan* __restrict__ P, int m, const double2* __restrict__ Y,
+         double* __restrict__ mag, int32_t* __restrict__ order, double* __restrict__ thr) {
+    __shared__ double sm[kSmallK4];
+    const DevIter& it = P->it[m];
+    const int b = static_cast<int>(it.b);
+    const int64_t budget = it.budget;
+    const int j = threadIdx.x;
+    double mj = 0.0;
+    if (j < b) {
+        const double2 v = Y[j];
+        const double mg = cabs_ref(v.x, v.y);
+        mj = mg == mg ? mg : -1.0;
+        sm[j] = mj;
+        mag[j] = mj;
+    }
+    __syncthreads();
+    if (j < b) {
+        int rank = 0;
+        for (int i = 0; i < b; ++i) {
+            const double mi = sm[i];
+            rank += (mi > mj) || (mi == mj && i < j);
+        }
+        if (rank < budget) order[rank] = j;
+        if (rank == budget - 1) *thr = 0.2 * mj;
+    }
+}
+
 __global__ void k4_thr(const int32_t* __restrict__ order, int64_t budget,
                        const double* __restrict__ mag, double* thr) {
     *thr = 0.2 * mag[order[budget - 1]];
@@ -881,18 +913,22 @@ void WideDecoder::enqueue(double2* y, const int64_t* sigma, const int64_t* sigma
             MSFFT_LAUNCH_CHECK("wide K3");
         }
         // ---- K4
-        keys_from_values<<<grid_of(b), kT, 0, st>>>(Y, b, nullptr, mag_.get(), key_.get());
-        select_kth(key_.get(), b, nullptr, budget, nullptr, st);
-        compact_selected(key_.get(), b, nullptr, sel_idx_.get(), st);
-        {
-            const unsigned tiles = static_cast<unsigned>((budget + kT - 1) / kT);
-            const unsigned split = std::max(1u, std::min(32u, 296u / tiles));
-            MSFFT_CUDA(cudaMemsetAsync(pos_.get(), 0, budget * sizeof(int32_t), st));
-            k4_rank<<<dim3(tiles, split), kT, 0, st>>>(sel_idx_.get(), budget, mag_.get(), pos_.get());
-            k4_scatter<<<grid_of(budget), kT, 0, st>>>(sel_idx_.get(), pos_.get(), budget,
-                                                       order_.get());
+        if (b <= kSmallK4) {
+            k4_small<<<1, kSmallK4, 0, st>>>(P, m, Y, mag_.get(), order_.get(), thr_.get());
+        } else {
+            keys_from_values<<<grid_of(b), kT, 0, st>>>(Y, b, nullptr, mag_.get(), key_.get());
+            select_kth(key_.get(), b, nullptr, budget, nullptr, st);
+            compact_selected(key_.get(), b, nullptr, sel_idx_.get(), st);
+            {
+                const unsigned tiles = static_cast<unsigned>((budget + kT - 1) / kT);
+                const unsigned split = std::max(1u, std::min(32u, 296u / tiles));
+                MSFFT_CUDA(cudaMemsetAsync(pos_.get(), 0, budget * sizeof(int32_t), st));
+                k4_rank<<<dim3(tiles, split), kT, 0, st>>>(sel_idx_.get(), budget, mag_.get(), pos_.get());
+                k4_scatter<<<grid_of(budget), kT, 0, st>>>(sel_idx_.get(), pos_.get(), budget,
+                                                           order_.get());
+            }
+            k4_thr<<<1, 1, 0, st>>>(order_.get(), budget, mag_.get(), thr_.get());
         }
-        k4_thr<<<1, 1, 0, st>>>(order_.get(), budget, mag_.get(), thr_.get());
         // ---- K5
         k5_stage<<<grid_of(budget * nr), kT, 0, st>>>(P, m, order_.get(), Y, yr_.get());
         k5_phase<<<grid_of(budget * nr), kT, 0, st>>>(P, m, yr_.get(), phi_.get(), pcode_.get());
