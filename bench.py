@@ -159,6 +159,30 @@ def e2e_batch(batch: int, sig_bytes: int, local_ranks: int) -> int:
     return max(min(batch, fit), min(batch, 8))
 
 
+def pipe_evidence():
+    """FP64-pipe and SM utilisation of the fused launch and of the decode
+    (the FFT / locate / estimate stages) from the committed ncu captures of
+    the same workload (profiles/r02/*_ncu_summary.json), or None."""
+    out = {}
+    for key, name in (("fused_kernel", "fused_ncu_summary.json"),
+                      ("decode_kernel", "decode_c4_ncu_summary.json")):
+        path = os.path.join(REPO, "profiles", "r02", name)
+        if not os.path.exists(path):
+            continue
+        with open(path) as f:
+            d = json.load(f)
+        def num(k):
+            try:
+                return float(d.get(k)) / 100.0
+            except (TypeError, ValueError):
+                return None
+        out[key] = {"fp64_pipe_frac": num("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active"),
+                    "issue_active_frac": num("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                    "sm_throughput_frac": num("sm__throughput.avg.pct_of_peak_sustained_elapsed"),
+                    "top_stalls": d.get("stall_share"), "source": f"profiles/r02/{name}"}
+    return out or None
+
+
 def cpu_model():
     try:
         with open("/proc/cpuinfo") as f:
@@ -400,7 +424,8 @@ def main():
                                      "achieved": alg_bytes / (enc_avg / 1e3) / 1e9,
                                      "frac": alg_bytes / (enc_avg / 1e3) / 1e9 / peak,
                                      "traffic": enc_traffic},
-                     "decode_only_ms": dec_avg},
+                     "decode_only_ms": dec_avg,
+                     "pipes": pipe_evidence()},
         "e2e": e2e, "cpu_baseline": cpu, "parity_sample": parity, "clocks": clk,
         "gpu_launches": launches,
     }
