@@ -293,3 +293,39 @@ def test_sparse_ingest_split_validation(oracle, monkeypatch):
         xb[row, col] = complex(float("nan"), 0.0)
         with pytest.raises(M.InvalidArgument, match="ComplexSignal: non-finite sample"):
             plan.execute(xb.pin_memory(), seeds)
+
+
+@pytest.mark.parametrize("n,k,kind", [
+    (64, 8, "max_k"),            # K = n/8, the largest K sfft4 accepts (sfft4.cpp:135)
+    (1 << 12, 512, "max_k"),
+    (8, 1, "tiny"),              # smallest n with K >= 1
+    (16, 2, "tiny"),
+    (1 << 12, 16, "equal"),      # equal magnitudes: stable tie-breaks in selection / K-prune
+    (1 << 14, 40, "range"),      # magnitudes over 12 decades
+])
+def test_edge_cases_match_reference(oracle, n, k, kind):
+    rng = np.random.default_rng(n + k)
+    if kind == "equal":
+        f = np.sort(rng.choice(n, k, replace=False))
+        c = np.full(k, 1.0 + 0.0j)
+        x = np.zeros(n, np.complex128)
+        x[f] = c
+        x = np.fft.ifft(x) * n
+    elif kind == "range":
+        f = np.sort(rng.choice(n, k, replace=False))
+        c = 10.0 ** rng.uniform(-6, 6, k) * np.exp(2j * np.pi * rng.random(k))
+        spec = np.zeros(n, np.complex128)
+        spec[f] = c
+        x = np.fft.ifft(spec) * n
+    else:
+        x = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    for delta in (1e-8, 1e-6):
+        try:
+            ref = oracle.sfft4(x, k, 16, 1.0, 77, delta)
+        except Exception as e:  # noqa: BLE001  the GPU must raise the same error
+            with pytest.raises((M.InvalidArgument, M.DomainError)) as ours:
+                M.sfft4(x, k, M.MultiscaleConfig(), 77, delta)
+            assert str(ours.value) == str(e)
+            continue
+        r = M.sfft4(x, k, M.MultiscaleConfig(), 77, delta)
+        assert_parity(ref.f, ref.c, r.spectrum.positions, r.spectrum.coeffs, k, delta, 1e-9)
