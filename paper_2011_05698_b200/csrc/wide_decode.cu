@@ -131,8 +131,11 @@ __global__ void k3_segsort(const DevPlan* __restrict__ P, int m, const int32_t* 
     }
 }
 
-// Long segments (small b): one CTA per bucket, keys staged in shared memory.
-__global__ void __launch_bounds__(kT)
+// Long segments (small b): one CTA per bucket sorts the segment's keys in
+// shared memory with a bitonic network (keys are unique; padding sorts last);
+// segments longer than the shared buffer fall back to rank counting.
+constexpr int kLongT = 1024;
+__global__ void __launch_bounds__(kLongT)
 k3_segsort_long(const DevPlan* __restrict__ P, int m, const int32_t* __restrict__ start,
                 const int32_t* __restrict__ cnt, const int32_t* __restrict__ ev,
                 int32_t* __restrict__ ev2) {
@@ -141,18 +144,37 @@ k3_segsort_long(const DevPlan* __restrict__ P, int m, const int32_t* __restrict_
     for (int64_t beta = blockIdx.x; beta < b; beta += gridDim.x) {
         const int32_t s0 = start[beta], len = cnt[beta];
         if (len <= kLongSeg) continue;
-        const bool in_smem = len <= kLongSmem;
-        __syncthreads();
-        if (in_smem)
-            for (int32_t e = threadIdx.x; e < len; e += kT) ks[e] = ev[s0 + e];
-        __syncthreads();
-        const int32_t* src = in_smem ? ks : ev + s0;
-        for (int32_t e = threadIdx.x; e < len; e += kT) {
-            const int32_t key = src[e];
-            int32_t rank = 0;
-            for (int32_t o = 0; o < len; ++o) rank += src[o] < key;
-            ev2[s0 + rank] = key;
+        if (len > kLongSmem) {
+            for (int32_t e = threadIdx.x; e < len; e += kLongT) {
+                const int32_t key = ev[s0 + e];
+                int32_t rank = 0;
+                for (int32_t o = 0; o < len; ++o) rank += ev[s0 + o] < key;
+                ev2[s0 + rank] = key;
+            }
+            continue;
         }
+        int32_t pw = 1;
+        while (pw < len) pw <<= 1;
+        __syncthreads();
+        for (int32_t e = threadIdx.x; e < pw; e += kLongT) ks[e] = e < len ? ev[s0 + e] : 0x7fffffff;
+        __syncthreads();
+        for (int32_t k = 2; k <= pw; k <<= 1) {
+            for (int32_t j = k >> 1; j > 0; j >>= 1) {
+                for (int32_t i = threadIdx.x; i < pw; i += kLongT) {
+                    const int32_t l = i ^ j;
+                    if (l > i) {
+                        const int32_t a = ks[i], c = ks[l];
+                        const bool up = (i & k) == 0;
+                        if ((a > c) == up) {
+                            ks[i] = c;
+                            ks[l] = a;
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        for (int32_t e = threadIdx.x; e < len; e += kLongT) ev2[s0 + e] = ks[e];
     }
 }
 
@@ -906,7 +928,7 @@ void WideDecoder::enqueue(double2* y, const int64_t* sigma, const int64_t* sigma
                                           ev_.get());
             k3_segsort<<<grid_of(b * 32), kT, 0, st>>>(P, m, start_.get(), cnt_.get(), ev_.get(),
                                                        ev2_.get());
-            k3_segsort_long<<<static_cast<unsigned>(std::min<int64_t>(b, 148 * 4)), kT, 0, st>>>(
+            k3_segsort_long<<<static_cast<unsigned>(std::min<int64_t>(b, 148 * 2)), kLongT, 0, st>>>(
                 P, m, start_.get(), cnt_.get(), ev_.get(), ev2_.get());
             k3_sum<<<grid_of(nr * b * 32), kT, 0, st>>>(P, m, start_.get(), cnt_.get(), ev2_.get(),
                                                         gc_.get(), rot_.get(), Y);
