@@ -5,7 +5,11 @@
 //                    uint64_t seed, double delta = 1e-8);
 // (proj/include/msfft/sfft4.hpp:32-45, 64-65; signal.hpp:13-28;
 // locate.hpp:13-19) with the same field names, the same ascending std::map
-// result and the same exception classes/messages.  A caller of the reference
+// result and the same exception classes/messages -- and the functions its
+// callers use around the transform: signal.hpp:31-70 (dft_dense,
+// idft_dense, synthesize, generate_test_signal, add_awgn, error_metrics),
+// io.hpp:11-17 (signal files, truth CSV), phase_mc.hpp:19-56
+// (run_phase_experiment) and bench.cpp:33-46 (top_k_spectrum).  A caller of the reference
 // switches by including this header and linking libmsfft_b200.so; defining
 // MSFFT_B200_AS_MSFFT before the include also makes `msfft::` name these
 // types (only when the reference headers are not included in the same TU).
@@ -16,6 +20,7 @@
 #include <map>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "msfft_b200.h"
@@ -95,6 +100,231 @@ inline SfftResult sfft4(const ComplexSignal& x, int64_t k, const MultiscaleConfi
     r.stats.b_first = st.b_first;
     r.stats.stage_counts.assign(st.stage_counts, st.stage_counts + st.iterations);
     return r;
+}
+
+// ---- around the transform ----------------------------------------------------
+
+struct EvalMetrics {  // signal.hpp:31-38
+    int64_t l0_err = 0;
+    double l1_err = 0.0;
+    double l2_err = 0.0;
+    double runtime_ms = 0.0;
+    int64_t samples_used = 0;
+    double sample_fraction = 0.0;
+};
+
+namespace detail {
+inline void spectrum_arrays(const SparseSpectrum& s, std::vector<int64_t>& f,
+                            std::vector<double>& c) {
+    f.clear();
+    c.clear();
+    for (const auto& [pos, v] : s.entries) {
+        f.push_back(pos);
+        c.push_back(v.real());
+        c.push_back(v.imag());
+    }
+}
+inline ComplexSignal signal_of(std::vector<double>& xi, int64_t n) {
+    ComplexSignal x;
+    x.n = n;
+    x.samples.resize(static_cast<size_t>(n));
+    for (int64_t j = 0; j < n; ++j) x.samples[j] = cplx(xi[2 * j], xi[2 * j + 1]);
+    return x;
+}
+}  // namespace detail
+
+// Forward transform with the 1/n factor (bit-identical to the reference).
+inline std::vector<cplx> dft_dense(const ComplexSignal& x) {
+    if (static_cast<int64_t>(x.samples.size()) != x.n)
+        throw std::invalid_argument("ComplexSignal: sample count != n");
+    std::vector<cplx> out(x.samples.size());
+    char err[1024] = {0};
+    throw_status(msfft_dft_dense(x.samples.data(), x.n, 1, MSFFT_C128, MSFFT_HOST,
+                                 reinterpret_cast<double*>(out.data()), err, sizeof(err)),
+                 err);
+    return out;
+}
+
+inline ComplexSignal idft_dense(const std::vector<cplx>& spectrum) {
+    ComplexSignal x;
+    x.n = static_cast<int64_t>(spectrum.size());
+    x.samples.resize(spectrum.size());
+    char err[1024] = {0};
+    throw_status(msfft_idft_dense(reinterpret_cast<const double*>(spectrum.data()), x.n, 1,
+                                  MSFFT_HOST, reinterpret_cast<double*>(x.samples.data()), err,
+                                  sizeof(err)),
+                 err);
+    return x;
+}
+
+inline ComplexSignal synthesize(const SparseSpectrum& spec) {
+    std::vector<int64_t> f;
+    std::vector<double> c;
+    detail::spectrum_arrays(spec, f, c);
+    ComplexSignal x;
+    x.n = spec.n;
+    x.samples.resize(static_cast<size_t>(spec.n > 0 ? spec.n : 0));
+    char err[1024] = {0};
+    throw_status(msfft_synthesize(spec.n, f.data(), c.data(), static_cast<int64_t>(f.size()),
+                                  MSFFT_C128, MSFFT_HOST, x.samples.data(), nullptr, err,
+                                  sizeof(err)),
+                 err);
+    return x;
+}
+
+// Same truth (positions, coefficients) as the reference; samples bit-identical
+// while k * ceil(n/1024) <= 2^23.
+inline std::pair<ComplexSignal, SparseSpectrum> generate_test_signal(int64_t n, int64_t k,
+                                                                     uint64_t seed) {
+    std::vector<cplx> xs(static_cast<size_t>(n > 0 ? n : 0));
+    std::vector<int64_t> f(static_cast<size_t>(k > 0 ? k : 1));
+    std::vector<double> c(2 * f.size());
+    char err[1024] = {0};
+    throw_status(msfft_generate_test_signal(n, k, seed, MSFFT_C128, MSFFT_HOST, xs.data(),
+                                            f.data(), c.data(), nullptr, err, sizeof(err)),
+                 err);
+    std::pair<ComplexSignal, SparseSpectrum> out;
+    out.first.n = n;
+    out.first.samples = std::move(xs);
+    out.second.n = n;
+    for (int64_t i = 0; i < k; ++i) out.second.entries[f[i]] = cplx(c[2 * i], c[2 * i + 1]);
+    return out;
+}
+
+// Same validation, sentinel and realised-power scaling as the reference; the
+// Gaussian noise comes from a counter-based generator (same law, not the
+// same samples as the reference's mt19937_64 stream).
+inline ComplexSignal add_awgn(const ComplexSignal& x, double snr_db, uint64_t seed) {
+    ComplexSignal y = x;
+    char err[1024] = {0};
+    throw_status(msfft_add_awgn(y.samples.data(), y.n, MSFFT_C128, MSFFT_HOST, snr_db, seed, err,
+                                sizeof(err)),
+                 err);
+    return y;
+}
+
+inline EvalMetrics error_metrics(const SparseSpectrum& truth, const SparseSpectrum& estimate,
+                                 int64_t k) {
+    std::vector<int64_t> tf, ef;
+    std::vector<double> tc, ec;
+    detail::spectrum_arrays(truth, tf, tc);
+    detail::spectrum_arrays(estimate, ef, ec);
+    msfft_eval_metrics m{};
+    char err[1024] = {0};
+    throw_status(msfft_error_metrics(truth.n, tf.data(), tc.data(), static_cast<int64_t>(tf.size()),
+                                     estimate.n, ef.data(), ec.data(),
+                                     static_cast<int64_t>(ef.size()), k, &m, err, sizeof(err)),
+                 err);
+    EvalMetrics r;
+    r.l0_err = m.l0_err;
+    r.l1_err = m.l1_err;
+    r.l2_err = m.l2_err;
+    return r;
+}
+
+// Top-k magnitudes of a dense spectrum as a sparse estimate (bench.cpp:33-46).
+inline SparseSpectrum top_k_spectrum(const std::vector<cplx>& spectrum, int64_t n, int64_t k) {
+    const int64_t cap = k > 0 ? k : 1;
+    std::vector<int64_t> f(static_cast<size_t>(cap));
+    std::vector<double> c(static_cast<size_t>(2 * cap));
+    int64_t count = 0;
+    char err[1024] = {0};
+    throw_status(msfft_top_k_spectrum(reinterpret_cast<const double*>(spectrum.data()),
+                                      static_cast<int64_t>(spectrum.size()), k, MSFFT_HOST,
+                                      f.data(), c.data(), &count, err, sizeof(err)),
+                 err);
+    SparseSpectrum out;
+    out.n = n;
+    for (int64_t i = 0; i < count; ++i) out.entries[f[i]] = cplx(c[2 * i], c[2 * i + 1]);
+    return out;
+}
+
+inline void write_signal_file(const std::string& path, const ComplexSignal& x) {
+    char err[1024] = {0};
+    throw_status(msfft_write_signal_file(path.c_str(), x.samples.data(), x.n, MSFFT_C128,
+                                         MSFFT_HOST, err, sizeof(err)),
+                 err);
+}
+
+inline ComplexSignal read_signal_file(const std::string& path) {
+    char err[1024] = {0};
+    int64_t n = 0;
+    throw_status(msfft_signal_file_length(path.c_str(), &n, err, sizeof(err)), err);
+    ComplexSignal x;
+    x.n = n;
+    x.samples.resize(static_cast<size_t>(n));
+    int64_t got = 0;
+    throw_status(msfft_read_signal_file(path.c_str(), MSFFT_C128, MSFFT_HOST, x.samples.data(), n,
+                                        &got, err, sizeof(err)),
+                 err);
+    return x;
+}
+
+inline void write_truth_csv(const std::string& path, const SparseSpectrum& truth) {
+    std::vector<int64_t> f;
+    std::vector<double> c;
+    detail::spectrum_arrays(truth, f, c);
+    char err[1024] = {0};
+    throw_status(msfft_write_truth_csv(path.c_str(), f.data(), c.data(),
+                                       static_cast<int64_t>(f.size()), err, sizeof(err)),
+                 err);
+}
+
+inline SparseSpectrum read_truth_csv(const std::string& path, int64_t n) {
+    char err[1024] = {0};
+    int64_t count = 0;
+    std::vector<int64_t> f(1);
+    std::vector<double> c(2);
+    throw_status(msfft_read_truth_csv(path.c_str(), n, f.data(), c.data(), 0, &count, err,
+                                      sizeof(err)),
+                 err);
+    f.resize(static_cast<size_t>(count > 0 ? count : 1));
+    c.resize(2 * f.size());
+    throw_status(msfft_read_truth_csv(path.c_str(), n, f.data(), c.data(), count, &count, err,
+                                      sizeof(err)),
+                 err);
+    SparseSpectrum s;
+    s.n = n;
+    for (int64_t i = 0; i < count; ++i) s.entries[f[i]] = cplx(c[2 * i], c[2 * i + 1]);
+    return s;
+}
+
+struct PhaseErrorHistogram {  // phase_mc.hpp:19-30
+    double snr_db = 0.0;
+    int64_t n = 0, k = 0, l_width = 0;
+    int64_t trials = 0;
+    std::vector<double> bin_mass;
+    double p50 = 0.0, p99 = 0.0, max = 0.0;
+    static constexpr double kBinLo = -6.0;
+    static constexpr double kBinWidth = 0.1;
+    static constexpr int kBinCount = MSFFT_PHASE_BINS;
+    static double bin_center(int i) { return kBinLo + kBinWidth * (i + 0.5); }
+};
+
+inline std::vector<PhaseErrorHistogram> run_phase_experiment(int64_t n, int64_t k, int64_t b,
+                                                             const std::vector<double>& snr_list,
+                                                             int64_t trials, uint64_t seed) {
+    std::vector<msfft_phase_histogram> hs(snr_list.size() ? snr_list.size() : 1);
+    char err[1024] = {0};
+    throw_status(msfft_phase_experiment(n, k, b, snr_list.data(),
+                                        static_cast<int64_t>(snr_list.size()), trials, seed,
+                                        hs.data(), nullptr, err, sizeof(err)),
+                 err);
+    std::vector<PhaseErrorHistogram> out;
+    for (size_t i = 0; i < snr_list.size(); ++i) {
+        PhaseErrorHistogram h;
+        h.snr_db = hs[i].snr_db;
+        h.n = hs[i].n;
+        h.k = hs[i].k;
+        h.l_width = hs[i].l_width;
+        h.trials = hs[i].trials;
+        h.bin_mass.assign(hs[i].bin_mass, hs[i].bin_mass + MSFFT_PHASE_BINS);
+        h.p50 = hs[i].p50;
+        h.p99 = hs[i].p99;
+        h.max = hs[i].max;
+        out.push_back(std::move(h));
+    }
+    return out;
 }
 
 }  // namespace msfft_b200

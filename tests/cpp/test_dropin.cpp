@@ -68,7 +68,102 @@ int main() {
             return 1;
         }
     }
-    std::printf("dropin ok: %ld entries identical support, max rel err %.3e\n",
+    if (worst > 1e-9) return 1;
+
+    // ---- the reference's functions around the transform (signal.hpp, io.hpp,
+    // phase_mc.hpp, bench.cpp top_k_spectrum) against the reference library
+#define CHECK(cond, what)                          \
+    do {                                           \
+        if (!(cond)) {                             \
+            std::printf("FAILED: %s\n", what);     \
+            return 1;                              \
+        }                                          \
+    } while (0)
+    {
+        const int64_t n2 = 1 << 14, k2 = 30;
+        const auto [gx, gt] = msfft::generate_test_signal(n2, k2, 99);
+        std::vector<double> rx(2 * n2), rct(2 * k2);
+        std::vector<int64_t> rft(k2);
+        CHECK(orc_generate_test_signal(n2, k2, 99, rx.data(), rft.data(), rct.data(), err,
+                                       sizeof(err)) == 0, "reference generate");
+        for (int64_t j = 0; j < n2; ++j)
+            CHECK(gx.samples[j] == msfft::cplx(rx[2 * j], rx[2 * j + 1]), "generate bit-exact");
+        int64_t t = 0;
+        for (const auto& [f, c] : gt.entries) {
+            CHECK(f == rft[t] && c == msfft::cplx(rct[2 * t], rct[2 * t + 1]), "truth identical");
+            ++t;
+        }
+        const std::vector<msfft::cplx> X = msfft::dft_dense(gx);
+        std::vector<double> RX(2 * n2);
+        CHECK(orc_dft_dense(n2, rx.data(), RX.data(), err, sizeof(err)) == 0, "reference dft");
+        for (int64_t j = 0; j < n2; ++j)
+            CHECK(X[j] == msfft::cplx(RX[2 * j], RX[2 * j + 1]), "dft_dense bit-exact");
+        const msfft::ComplexSignal back = msfft::idft_dense(X);
+        std::vector<double> RB(2 * n2);
+        CHECK(orc_idft_dense(n2, RX.data(), RB.data(), err, sizeof(err)) == 0, "reference idft");
+        for (int64_t j = 0; j < n2; ++j)
+            CHECK(back.samples[j] == msfft::cplx(RB[2 * j], RB[2 * j + 1]), "idft_dense bit-exact");
+        const msfft::SparseSpectrum top = msfft::top_k_spectrum(X, n2, k2);
+        std::vector<int64_t> tf(k2);
+        std::vector<double> tc(2 * k2);
+        int64_t tcount = 0;
+        CHECK(orc_top_k_spectrum(n2, RX.data(), k2, tf.data(), tc.data(), &tcount, err,
+                                 sizeof(err)) == 0, "reference top_k");
+        t = 0;
+        for (const auto& [f, c] : top.entries) {
+            CHECK(f == tf[t] && c == msfft::cplx(tc[2 * t], tc[2 * t + 1]), "top_k identical");
+            ++t;
+        }
+        const msfft::EvalMetrics m = msfft::error_metrics(gt, top, k2);
+        int64_t l0 = 0;
+        double l1 = 0, l2 = 0;
+        CHECK(orc_error_metrics(n2, k2, rft.data(), rct.data(), tcount, tf.data(), tc.data(), k2,
+                                &l0, &l1, &l2, err, sizeof(err)) == 0, "reference metrics");
+        CHECK(m.l0_err == l0 && m.l1_err == l1 && m.l2_err == l2, "error_metrics identical");
+        // files: ours -> reference reader, byte-identical CSV
+        msfft::write_signal_file("/tmp/msfft_dropin.msft", gx);
+        std::vector<double> fx(2 * n2);
+        int64_t fn = 0;
+        CHECK(orc_read_signal_file("/tmp/msfft_dropin.msft", n2, fx.data(), &fn, err,
+                                   sizeof(err)) == 0 && fn == n2, "reference reads our file");
+        CHECK(fx == rx, "signal file round trip");
+        CHECK(msfft::read_signal_file("/tmp/msfft_dropin.msft").samples == gx.samples,
+              "our reader");
+        msfft::write_truth_csv("/tmp/msfft_dropin_a.csv", gt);
+        CHECK(orc_write_truth_csv("/tmp/msfft_dropin_b.csv", n2, k2, rft.data(), rct.data(), err,
+                                  sizeof(err)) == 0, "reference csv");
+        const msfft::SparseSpectrum ta = msfft::read_truth_csv("/tmp/msfft_dropin_a.csv", n2);
+        const msfft::SparseSpectrum tb = msfft::read_truth_csv("/tmp/msfft_dropin_b.csv", n2);
+        CHECK(ta.entries == gt.entries && tb.entries == gt.entries, "truth csv round trip");
+        try {
+            msfft::read_signal_file("/tmp/msfft_dropin_missing.msft");
+            CHECK(false, "missing file must throw");
+        } catch (const std::runtime_error& e) {
+            CHECK(std::string(e.what()).rfind("read_signal_file: cannot open", 0) == 0,
+                  "runtime_error message");
+        }
+        // noise: realised power ratio matches the request
+        const msfft::ComplexSignal noisy = msfft::add_awgn(gx, 20.0, 5);
+        double ps = 0, pn = 0;
+        for (int64_t j = 0; j < n2; ++j) {
+            ps += std::norm(gx.samples[j]);
+            pn += std::norm(noisy.samples[j] - gx.samples[j]);
+        }
+        CHECK(std::abs(pn / ps / 0.01 - 1.0) < 1e-9, "add_awgn realised SNR");
+    }
+    {
+        const std::vector<double> snr = {0.0, 20.0};
+        const auto hs = msfft::run_phase_experiment(8192, 50, 256, snr, 40, 3);
+        std::vector<double> ref(73 * snr.size());
+        CHECK(orc_phase_experiment(8192, 50, 256, snr.data(), static_cast<int64_t>(snr.size()), 40,
+                                   3, ref.data(), err, sizeof(err)) == 0, "reference phase mc");
+        for (size_t i = 0; i < snr.size(); ++i) {
+            CHECK(hs[i].trials == 40 && hs[i].l_width == 32, "histogram header");
+            CHECK(std::abs(hs[i].p50 - ref[73 * i + 70]) <= 1e-9, "phase p50");
+            CHECK(std::abs(hs[i].max - ref[73 * i + 72]) <= 1e-9, "phase max");
+        }
+    }
+    std::printf("dropin ok: %ld entries identical support, max rel err %.3e; signal/io/phase API ok\n",
                 static_cast<long>(cnt), worst);
-    return worst <= 1e-9 ? 0 : 1;
+    return 0;
 }
