@@ -59,7 +59,12 @@ enum msfft_flags {
     MSFFT_FLAG_STAGE_TIMES = 1u << 1,
     /* Run the encode and the decode as separate launches instead of the
      * persistent fused kernel (diagnostics: per-kernel rooflines). */
-    MSFFT_FLAG_SERIAL = 1u << 2
+    MSFFT_FLAG_SERIAL = 1u << 2,
+    /* msfft_execute returns once the work is enqueued on the stream (device
+     * input and output only): outputs are complete when the stream reaches
+     * them, decode errors are reported by the next msfft_plan_sync.  Calls
+     * that repeat the previous seeds reuse the σ plan on the device. */
+    MSFFT_FLAG_ASYNC = 1u << 3
 };
 
 /* TransformStats (proj/include/msfft/sfft4.hpp:32-40). */
@@ -108,6 +113,11 @@ int msfft_execute(msfft_plan plan, int64_t batch, const void* x, int64_t x_strid
                   int32_t x_location, const uint64_t* seeds, int64_t* out_f, double* out_c,
                   int64_t* out_count, int32_t out_location, uint32_t flags, void* stream,
                   double* device_ms, char* err, size_t errlen);
+
+/* Waits for the plan's work on `stream` (NULL: the plan's own stream) and
+ * returns the first error raised by asynchronous msfft_execute calls since
+ * the last sync (then clears it). */
+int msfft_plan_sync(msfft_plan plan, void* stream, char* err, size_t errlen);
 
 /* Algorithmic traffic of the fused gather for `batch` signals with these
  * seeds (host computation from the plan, data independent): *loads = samples

@@ -235,12 +235,14 @@ class Plan:
         return [float(v) for v in ms]
 
     def execute(self, x, seeds, out=None, assume_valid: bool = False, stream=None,
-                stage_times: bool = False, serial: bool = False):
+                stage_times: bool = False, serial: bool = False, async_: bool = False):
         """x: (batch, n) complex array/tensor (host or CUDA).  seeds: batch
         integers.  out: optional (f, c, count) preallocated outputs -- torch
         CUDA tensors (int64 [B,k], complex128 [B,k], int64 [B]) keep the
         results on the device; otherwise numpy arrays are returned.
-        Returns (f, c, count, device_ms)."""
+        async_=True (CUDA x and out only) returns once the work is enqueued:
+        outputs are ready when the stream reaches them and errors surface in
+        sync().  Returns (f, c, count, device_ms) (device_ms 0 when async)."""
         ptr, n, dt, loc, keep = _signal_arg(x)
         if n != self.n:
             raise InvalidArgument("ComplexSignal: sample count != n")
@@ -270,6 +272,8 @@ class Plan:
             flags |= _L.MSFFT_FLAG_SERIAL
         if stage_times:
             flags |= _L.MSFFT_FLAG_STAGE_TIMES
+        if async_:
+            flags |= _L.MSFFT_FLAG_ASYNC
         status = self._lib.msfft_execute(
             self._h, batch, ptr, n, loc, seeds.ctypes.data_as(C.POINTER(C.c_uint64)),
             C.c_void_p(fptr), C.c_void_p(cptr), C.c_void_p(nptr), oloc, flags,
@@ -282,6 +286,12 @@ class Plan:
         """Samples per signal moved host->device for host inputs (sparse
         ingest); 0 when whole signals are copied."""
         return int(self._lib.msfft_plan_ingest_samples(self._h))
+
+    def sync(self, stream=None) -> None:
+        """Wait for this plan's work on `stream` and raise the errors of
+        asynchronous execute calls since the last sync."""
+        err = C.create_string_buffer(1024)
+        _raise(self._lib.msfft_plan_sync(self._h, C.c_void_p(stream or 0), err, 1024), err)
 
     # ---- split phases: one signal sharded by index range over GPUs ----------
     @property

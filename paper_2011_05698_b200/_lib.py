@@ -17,6 +17,7 @@ MSFFT_HOST, MSFFT_DEVICE = 0, 1
 MSFFT_FLAG_ASSUME_VALID = 1
 MSFFT_FLAG_STAGE_TIMES = 2
 MSFFT_FLAG_SERIAL = 4
+MSFFT_FLAG_ASYNC = 8
 MAX_ITERATIONS = 64
 
 # Every symbol include/msfft_b200.h declares.
@@ -30,7 +31,7 @@ EXPORTED = (
     "msfft_add_awgn", "msfft_dft_dense", "msfft_idft_dense", "msfft_top_k_spectrum",
     "msfft_error_metrics", "msfft_signal_file_length", "msfft_read_signal_file",
     "msfft_write_signal_file", "msfft_write_truth_csv", "msfft_read_truth_csv",
-    "msfft_phase_experiment",
+    "msfft_phase_experiment", "msfft_plan_sync",
 )
 
 i64, u64, f64, i32, u32 = C.c_int64, C.c_uint64, C.c_double, C.c_int32, C.c_uint32
@@ -101,6 +102,9 @@ def lib() -> C.CDLL:
     L.msfft_plan_launches.restype = i64
     # split-phase / ingest entry points (absent from diagnostic builds of
     # older sources, which tools/build_variant.py can produce)
+    if hasattr(L, "msfft_plan_sync"):
+        L.msfft_plan_sync.argtypes = [VP, VP] + E
+        L.msfft_plan_sync.restype = C.c_int
     if hasattr(L, "msfft_plan_ingest_samples"):
         L.msfft_plan_ingest_samples.argtypes = [VP]
         L.msfft_plan_ingest_samples.restype = i64

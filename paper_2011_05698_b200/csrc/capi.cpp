@@ -197,8 +197,17 @@ int msfft_execute(msfft_plan plan, int64_t batch, const void* x, int64_t x_strid
         opt.assume_valid = (flags & MSFFT_FLAG_ASSUME_VALID) != 0;
         opt.stage_times = (flags & MSFFT_FLAG_STAGE_TIMES) != 0;
         opt.force_serial = (flags & MSFFT_FLAG_SERIAL) != 0;
+        opt.async_call = (flags & MSFFT_FLAG_ASYNC) != 0;
         opt.stream = static_cast<cudaStream_t>(stream);
         plan->plan->execute(batch, x, x_stride, seeds, out_f, out_c, out_count, opt, device_ms);
+    });
+}
+
+int msfft_plan_sync(msfft_plan plan, void* stream, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        if (!plan) throw std::invalid_argument("msfft_plan_sync: null plan");
+        std::lock_guard<std::mutex> lock(plan->plan->mutex());
+        plan->plan->sync(static_cast<cudaStream_t>(stream));
     });
 }
 

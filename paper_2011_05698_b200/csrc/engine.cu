@@ -152,6 +152,9 @@ Plan::Plan(int64_t n, int64_t k, int64_t l, double q, double delta, bool c128, i
     if (const char* e = std::getenv("MSFFT_ENC_SMEM_PAD")) enc_smem_pad_ = std::atoll(e);
     fused_smem_ = std::max(enc_smem_, lay_.in_smem ? static_cast<size_t>(lay_.bytes) : size_t{0});
     flags_.reset(2);
+    MSFFT_CUDA(cudaMemset(flags_.get(), 0, 2 * sizeof(int32_t)));
+    for (int i = 0; i < 2; ++i)
+        MSFFT_CUDA(cudaEventCreateWithFlags(&ev_seeds_[i], cudaEventDisableTiming));
     imap_ = make_ingest_map(sched_);
     dplan_compact_ = dplan_;
     dplan_compact_.x_compact = 1;
@@ -184,7 +187,10 @@ Plan::~Plan() {
     if (dec_stream_) cudaStreamDestroy(dec_stream_);
     if (ev_chunk_) cudaEventDestroy(ev_chunk_);
     if (ev_dec_done_) cudaEventDestroy(ev_dec_done_);
-    if (h_seeds_) cudaFreeHost(h_seeds_);
+    for (int i = 0; i < 2; ++i) {
+        if (h_seeds_[i]) cudaFreeHost(h_seeds_[i]);
+        if (ev_seeds_[i]) cudaEventDestroy(ev_seeds_[i]);
+    }
     for (int i = 0; i < 2; ++i)
         if (gstage_[i]) cudaFreeHost(gstage_[i]);
     if (vstream_) cudaStreamDestroy(vstream_);
@@ -474,6 +480,10 @@ void Plan::execute(int64_t batch, const void* x, int64_t x_stride, const uint64_
     if (x_stride < n) throw std::invalid_argument("msfft_execute: x_stride < n");
     cudaStream_t st = opt.stream ? opt.stream : own_stream_;
     const size_t elem = c128_ ? sizeof(double2) : sizeof(float2);
+    const bool async_call = opt.async_call && !opt.stage_times && !opt.pre && !opt.post &&
+                            !opt.sel_bucket;
+    if (async_call && !(opt.x_on_device && opt.out_on_device))
+        throw std::invalid_argument("msfft_execute: MSFFT_FLAG_ASYNC needs device input and output");
 
     // chunking: device inputs run as one chunk; host inputs stream through
     // two staging buffers overlapped with compute
@@ -499,7 +509,6 @@ void Plan::execute(int64_t batch, const void* x, int64_t x_stride, const uint64_
 
     stage_ms_[0] = stage_ms_[1] = stage_ms_[2] = 0.0;
     MSFFT_CUDA(cudaEventRecord(ev_start_, st));
-    MSFFT_CUDA(cudaMemsetAsync(flags_.get(), 0, 2 * sizeof(int32_t), st));
     upload_sigmas(batch, seeds, st);
     const bool validate = !opt.assume_valid;
     bool host_bad = false;
@@ -541,6 +550,10 @@ void Plan::execute(int64_t batch, const void* x, int64_t x_stride, const uint64_
                                    cudaMemcpyDeviceToHost, st));
     }
     MSFFT_CUDA(cudaEventRecord(ev_end_, st));
+    if (async_call) {
+        if (device_ms) *device_ms = 0.0;  // not measured: the call did not wait
+        return;
+    }
     if (device_ms) {
         MSFFT_CUDA(cudaEventSynchronize(ev_end_));
         float ms = 0.f;
@@ -548,6 +561,7 @@ void Plan::execute(int64_t batch, const void* x, int64_t x_stride, const uint64_
         *device_ms = ms;
     }
     if (host_bad) {
+        MSFFT_CUDA(cudaMemsetAsync(flags_.get(), 0, 2 * sizeof(int32_t), st));
         MSFFT_CUDA(cudaStreamSynchronize(st));
         throw std::invalid_argument("ComplexSignal: non-finite sample");
     }
@@ -661,26 +675,40 @@ bool Plan::execute_sparse(int64_t batch, const void* x, int64_t x_stride, const 
 void Plan::upload_sigmas(int64_t batch, const uint64_t* seeds, cudaStream_t st) {
     // sigma plan: exact mt19937_64 draws on the device, one thread per signal
     const int iters = sched_.iterations;
+    if (static_cast<int64_t>(last_seeds_.size()) == batch &&
+        std::equal(seeds, seeds + batch, last_seeds_.begin()))
+        return;  // sig_ / sig_inv_ already hold this batch's plan (stream-ordered)
     if (h_seeds_cap_ < batch) {
         MSFFT_CUDA(cudaStreamSynchronize(st));
-        if (h_seeds_) cudaFreeHost(h_seeds_);
-        h_seeds_ = nullptr;
-        MSFFT_CUDA(cudaMallocHost(&h_seeds_, sizeof(uint64_t) * batch));
+        for (int i = 0; i < 2; ++i) {
+            if (h_seeds_[i]) cudaFreeHost(h_seeds_[i]);
+            h_seeds_[i] = nullptr;
+            MSFFT_CUDA(cudaMallocHost(&h_seeds_[i], sizeof(uint64_t) * batch));
+        }
         h_seeds_cap_ = batch;
     }
     sig_.ensure(static_cast<size_t>(batch * iters));
     sig_inv_.ensure(static_cast<size_t>(batch * iters));
     seeds_.ensure(static_cast<size_t>(batch));
-    MSFFT_CUDA(cudaStreamSynchronize(st));  // previous use of the pinned seed staging
-    std::memcpy(h_seeds_, seeds, sizeof(uint64_t) * batch);
-    MSFFT_CUDA(cudaMemcpyAsync(seeds_.get(), h_seeds_, sizeof(uint64_t) * batch,
+    seed_slot_ ^= 1;
+    MSFFT_CUDA(cudaEventSynchronize(ev_seeds_[seed_slot_]));  // this slot's last copy is done
+    std::memcpy(h_seeds_[seed_slot_], seeds, sizeof(uint64_t) * batch);
+    MSFFT_CUDA(cudaMemcpyAsync(seeds_.get(), h_seeds_[seed_slot_], sizeof(uint64_t) * batch,
                                cudaMemcpyHostToDevice, st));
+    MSFFT_CUDA(cudaEventRecord(ev_seeds_[seed_slot_], st));
     launch_sigma(seeds_.get(), batch, iters, sched_.n, sig_.get(), sig_inv_.get(), st);
+    last_seeds_.assign(seeds, seeds + batch);
+}
+
+void Plan::sync(cudaStream_t stream) {
+    DeviceGuard dg(device_);
+    check_flags(stream ? stream : own_stream_);
 }
 
 void Plan::check_flags(cudaStream_t st) {
     int32_t hflags[2] = {0, 0};
     MSFFT_CUDA(cudaMemcpyAsync(hflags, flags_.get(), sizeof(hflags), cudaMemcpyDeviceToHost, st));
+    MSFFT_CUDA(cudaMemsetAsync(flags_.get(), 0, 2 * sizeof(int32_t), st));
     MSFFT_CUDA(cudaStreamSynchronize(st));
     if (hflags[1]) throw std::invalid_argument("ComplexSignal: non-finite sample");
     if (hflags[0] == kDecErrPhaseZero) throw std::domain_error("phase_of: zero value");

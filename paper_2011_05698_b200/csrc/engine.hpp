@@ -33,6 +33,9 @@ struct ExecOptions {
     bool assume_valid = false;
     bool stage_times = false;  // CUDA events around encode / fft / decode (or fused)
     bool force_serial = false; // separate encode and decode launches (diagnostics)
+    // return after enqueueing (device input and output only): outputs are
+    // complete when the stream reaches them; decode errors are raised by sync()
+    bool async_call = false;
     cudaStream_t stream = nullptr;
     double* pre = nullptr;   // trace: encode output (batch must be 1, host)
     double* post = nullptr;  // trace: post-subtract values
@@ -73,6 +76,10 @@ public:
     int64_t values_per_signal() const { return dplan_.values_per_signal; }
 
     int64_t launches(int64_t batch, bool validate, bool serial = false) const;
+
+    // Waits for the plan's work on `stream` (nullptr: its own stream) and
+    // raises the errors of asynchronous calls since the last sync.
+    void sync(cudaStream_t stream);
 
     // compact samples per signal moved by sparse host ingest (0 if the plan
     // uses the dense H2D path for host inputs)
@@ -171,8 +178,13 @@ private:
     cudaEvent_t ev_vbeg_ = nullptr, ev_vend_ = nullptr;
     DeviceBuffer<unsigned char> vstage_;
     DeviceBuffer<uint64_t> seeds_;
-    uint64_t* h_seeds_ = nullptr;  // pinned staging
+    // pinned seed staging, two slots so an asynchronous call never waits for
+    // the previous call's copy; the σ plan is reused while the seeds repeat
+    uint64_t* h_seeds_[2] = {nullptr, nullptr};
+    cudaEvent_t ev_seeds_[2] = {nullptr, nullptr};
     int64_t h_seeds_cap_ = 0;
+    int seed_slot_ = 0;
+    std::vector<uint64_t> last_seeds_;
     std::mutex mu_;
 };
 

@@ -329,3 +329,38 @@ def test_edge_cases_match_reference(oracle, n, k, kind):
             continue
         r = M.sfft4(x, k, M.MultiscaleConfig(), 77, delta)
         assert_parity(ref.f, ref.c, r.spectrum.positions, r.spectrum.coeffs, k, delta, 1e-9)
+
+
+def test_async_execute(oracle):
+    """MSFFT_FLAG_ASYNC: enqueue-only calls give the synchronous results,
+    the σ plan is reused only while the seeds repeat, decode/validation
+    errors are raised by sync() and then cleared, host inputs are refused."""
+    import torch
+    n, k = 1 << 18, 40
+    xs = np.stack([make_signal(oracle, dict(gen="np", n=n, k=k, seed=s, snr=20.0,
+                                            dtype="complex64")) for s in range(4)])
+    plan = M.Plan(n, k, M.MultiscaleConfig(), 1e-6, "complex64")
+    xd = torch.as_tensor(xs).cuda()
+    outs = []
+    for seeds in (np.arange(10, 14, dtype=np.uint64), np.arange(10, 14, dtype=np.uint64),
+                  np.arange(20, 24, dtype=np.uint64)):
+        o = (torch.empty((4, k), dtype=torch.int64, device="cuda"),
+             torch.empty((4, k), dtype=torch.complex128, device="cuda"),
+             torch.empty((4,), dtype=torch.int64, device="cuda"))
+        plan.execute(xd, seeds, out=o, async_=True)
+        outs.append((seeds, o))
+    plan.sync()
+    for seeds, o in outs:
+        f, c, cnt, _ = plan.execute(xs, seeds)
+        assert np.array_equal(cnt, o[2].cpu().numpy())
+        assert np.array_equal(f, o[0].cpu().numpy()) and np.array_equal(c, o[1].cpu().numpy())
+    assert not np.array_equal(outs[0][1][0].cpu().numpy(), outs[2][1][0].cpu().numpy())
+    bad = xd.clone()
+    bad[2, 17] = complex(float("nan"), 0)
+    plan.execute(bad, outs[0][0], out=outs[0][1], async_=True)
+    with pytest.raises(M.InvalidArgument, match="ComplexSignal: non-finite sample"):
+        plan.sync()
+    plan.execute(xd, outs[0][0], out=outs[0][1], async_=True)
+    plan.sync()  # cleared
+    with pytest.raises(M.InvalidArgument, match="MSFFT_FLAG_ASYNC needs device input and output"):
+        plan.execute(xs, outs[0][0], async_=True)
