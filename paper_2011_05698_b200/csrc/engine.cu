@@ -161,6 +161,7 @@ Plan::Plan(int64_t n, int64_t k, int64_t l, double q, double delta, bool c128, i
     if (const char* e = std::getenv("MSFFT_SPARSE_INGEST")) ingest_enabled_ = std::atoi(e) != 0;
     if (const char* e = std::getenv("MSFFT_INGEST_CHUNK")) ingest_chunk_ = std::max(1LL, std::atoll(e));
     if (const char* e = std::getenv("MSFFT_WIDE_MAX_BATCH")) wide_max_batch_ = std::atoll(e);
+    if (const char* e = std::getenv("MSFFT_PDL")) pdl_enabled_ = std::atoi(e) != 0;
     if (const char* e = std::getenv("MSFFT_DMA_VALIDATE_SHARE")) {
         dma_share_ = std::min(1.0, std::max(0.0, std::atof(e)));
         dma_share_fixed_ = true;
@@ -190,6 +191,7 @@ Plan::~Plan() {
     for (int i = 0; i < 2; ++i) {
         if (h_seeds_[i]) cudaFreeHost(h_seeds_[i]);
         if (ev_seeds_[i]) cudaEventDestroy(ev_seeds_[i]);
+        if (h_pdl_seeds_[i]) cudaFreeHost(h_pdl_seeds_[i]);
     }
     for (int i = 0; i < 2; ++i)
         if (gstage_[i]) cudaFreeHost(gstage_[i]);
@@ -212,8 +214,9 @@ const Plan::TaskSet& Plan::tasks_for(int64_t batch) {
     return tasks_.emplace(batch, std::move(ts)).first->second;
 }
 
-const Plan::FusedSet& Plan::fused_for(int64_t batch) {
-    auto it = fused_.find(batch);
+const Plan::FusedSet& Plan::fused_for(int64_t batch, int slot) {
+    const int64_t key = batch * 4 + slot;
+    auto it = fused_.find(key);
     if (it != fused_.end()) return it->second;
     // chunk: a multiple of the largest signal group of a fused encode task
     int64_t group = 1;
@@ -256,7 +259,7 @@ const Plan::FusedSet& Plan::fused_for(int64_t batch) {
     fs.tasks.reset(tasks.size());
     fs.items.reset(items.size());
     fs.need.reset(need.size());
-    fs.counters.reset(need.size() + 1);
+    fs.counters.reset(need.size() + 2);  // ticket, done[], exit count
     MSFFT_CUDA(cudaMemcpy(fs.tasks.get(), tasks.data(), tasks.size() * sizeof(EncTask),
                           cudaMemcpyHostToDevice));
     MSFFT_CUDA(cudaMemcpy(fs.items.get(), items.data(), items.size() * sizeof(int32_t),
@@ -270,8 +273,9 @@ const Plan::FusedSet& Plan::fused_for(int64_t batch) {
     fs.fw.need = fs.need.get();
     fs.fw.counters = fs.counters.get();
     fs.fw.n_chunks = nchunks;
-    fs.fw.n_counters = static_cast<int64_t>(need.size()) + 1;
-    return fused_.emplace(batch, std::move(fs)).first->second;
+    fs.fw.n_counters = static_cast<int64_t>(need.size()) + 2;
+    MSFFT_CUDA(cudaMemset(fs.counters.get(), 0, sizeof(int32_t) * fs.fw.n_counters));
+    return fused_.emplace(key, std::move(fs)).first->second;
 }
 
 void Plan::append_tasks(std::vector<EncTask>& v, int64_t s_begin, int64_t s_end) const {
@@ -484,6 +488,15 @@ void Plan::execute(int64_t batch, const void* x, int64_t x_stride, const uint64_
                             !opt.sel_bucket;
     if (async_call && !(opt.x_on_device && opt.out_on_device))
         throw std::invalid_argument("msfft_execute: MSFFT_FLAG_ASYNC needs device input and output");
+    if (async_call && pdl_enabled_ && fused_enabled_ && !opt.force_serial && big_b_iters_.empty() &&
+        !lay_.big && lay_.in_smem &&
+        fused_for(batch).fw.n_items >= fused_slots(c128_, fused_smem_)) {
+        // PDL needs a grid that fills every CTA slot (see execute_pdl)
+        execute_pdl(batch, x, x_stride, seeds, out_f, reinterpret_cast<double2*>(out_c), out_count,
+                    st);
+        if (device_ms) *device_ms = 0.0;
+        return;
+    }
 
     // chunking: device inputs run as one chunk; host inputs stream through
     // two staging buffers overlapped with compute
@@ -698,6 +711,43 @@ void Plan::upload_sigmas(int64_t batch, const uint64_t* seeds, cudaStream_t st) 
     MSFFT_CUDA(cudaEventRecord(ev_seeds_[seed_slot_], st));
     launch_sigma(seeds_.get(), batch, iters, sched_.n, sig_.get(), sig_inv_.get(), st);
     last_seeds_.assign(seeds, seeds + batch);
+}
+
+void Plan::execute_pdl(int64_t batch, const void* x, int64_t x_stride, const uint64_t* seeds,
+                       int64_t* d_of, double2* d_oc, int64_t* d_ocnt, cudaStream_t st) {
+    const int iters = sched_.iterations;
+    const int p = static_cast<int>(pdl_count_++ & 1);
+    y_pdl_[p].ensure(static_cast<size_t>(batch * dplan_.values_per_signal));
+    sig_pdl_[p].ensure(static_cast<size_t>(batch * iters));
+    sig_inv_pdl_[p].ensure(static_cast<size_t>(batch * iters));
+    if (h_pdl_cap_ < batch) {
+        MSFFT_CUDA(cudaStreamSynchronize(st));
+        for (int i = 0; i < 2; ++i) {
+            if (h_pdl_seeds_[i]) cudaFreeHost(h_pdl_seeds_[i]);
+            h_pdl_seeds_[i] = nullptr;
+            MSFFT_CUDA(cudaMallocHost(&h_pdl_seeds_[i], sizeof(uint64_t) * batch));
+            pdl_seeds_[i].clear();
+        }
+        h_pdl_cap_ = batch;
+    }
+    // set p's seed slot is rewritten only when its seeds change (and only
+    // after the work that read it is done)
+    if (static_cast<int64_t>(pdl_seeds_[p].size()) != batch ||
+        !std::equal(seeds, seeds + batch, pdl_seeds_[p].begin())) {
+        MSFFT_CUDA(cudaStreamSynchronize(st));
+        std::memcpy(h_pdl_seeds_[p], seeds, sizeof(uint64_t) * batch);
+        pdl_seeds_[p].assign(seeds, seeds + batch);
+    }
+    // Both launches may start while the previous fused launch (set p^1) is
+    // finishing.  They touch only set p, whose last user (two launches back)
+    // has exited: the previous launch fills every CTA slot and could only
+    // become fully resident after it did.
+    launch_sigma(h_pdl_seeds_[p], batch, iters, sched_.n, sig_pdl_[p].get(), sig_inv_pdl_[p].get(),
+                 st, true);
+    const FusedSet& fs = fused_for(batch, 1 + p);
+    launch_fused(dplan_, lay_, fs.fw, x, c128_, x_stride, batch, sig_pdl_[p].get(),
+                 sig_inv_pdl_[p].get(), y_pdl_[p].get(), dec_work_.get(), d_of, d_oc, d_ocnt,
+                 flags_.get(), fused_smem_, st, true);
 }
 
 void Plan::sync(cudaStream_t stream) {

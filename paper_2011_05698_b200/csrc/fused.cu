@@ -31,12 +31,19 @@ fused_kernel(const __grid_constant__ DevPlan plan, DecLayout lay, DecArgs args,
              const EncTask* __restrict__ tasks, const int32_t* __restrict__ items,
              int32_t n_items, int64_t chunk, const int32_t* __restrict__ need,
              int32_t* __restrict__ done, int32_t* __restrict__ ticket, const T* __restrict__ x,
-             int64_t x_stride, int64_t batch, unsigned char* __restrict__ work) {
+             int64_t x_stride, int64_t batch, unsigned char* __restrict__ work,
+             int64_t n_counters) {
+    int32_t* exit_count = ticket + n_counters - 1;  // the last counter slot
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t bar;
     __shared__ DecShared sh;
     __shared__ int s_item;
     static_assert(kEncThreads == kDecThreads, "fused CTA runs both bodies");
+    // programmatic dependent launch: this grid reads the σ plan of the
+    // kernel before it (wait), and the next launch may be scheduled as soon
+    // as SM slots free up (launch_dependents); it uses other buffers
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     encode_barrier_init(&bar);
     uint32_t phase = 0;
     const bool bad_input = args.err[1] != 0;  // set by the validation pass
@@ -67,6 +74,18 @@ fused_kernel(const __grid_constant__ DevPlan plan, DecLayout lay, DecArgs args,
         }
         __syncthreads();
     }
+    // the last CTA out resets this launch's counters (ticket, done, exit)
+    // for the next launch that uses them, so no memset sits between launches
+    __shared__ int s_last;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        s_last = atomicAdd(exit_count, 1) == static_cast<int>(gridDim.x) - 1;
+    }
+    __syncthreads();
+    if (s_last) {
+        for (int64_t i = threadIdx.x; i < n_counters; i += blockDim.x) ticket[i] = 0;
+        __threadfence();
+    }
 }
 
 template <class T>
@@ -74,7 +93,7 @@ void launch_t(const DevPlan& plan, const DecLayout& lay, const FusedWork& fw, co
               int64_t x_stride, int64_t batch, const int64_t* d_sigma,
               const int64_t* d_sigma_inv, double2* d_y, unsigned char* d_work, int64_t* d_out_f,
               double2* d_out_c, int64_t* d_out_count, int32_t* d_err, size_t smem,
-              cudaStream_t stream) {
+              cudaStream_t stream, bool programmatic) {
     auto k = fused_kernel<T>;
     MSFFT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(smem)));
@@ -84,31 +103,68 @@ void launch_t(const DevPlan& plan, const DecLayout& lay, const FusedWork& fw, co
     MSFFT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kEncThreads, smem));
     if (per_sm < 1) throw CudaError("fused_kernel: does not fit on an SM");
     const int64_t grid = std::min<int64_t>(static_cast<int64_t>(sms) * per_sm, fw.n_items);
-    MSFFT_CUDA(cudaMemsetAsync(fw.counters, 0, sizeof(int32_t) * fw.n_counters, stream));
+    // counters are zero: from creation, then reset by the previous launch's
+    // last CTA (a memset here would also serialise programmatic launches)
     DecArgs args{d_y, d_sigma, d_sigma_inv, d_out_f, d_out_c, d_out_count, d_err,
                  nullptr, nullptr, nullptr};
-    k<<<static_cast<unsigned>(grid), kEncThreads, smem, stream>>>(
-        plan, lay, args, fw.tasks, fw.items, fw.n_items, fw.chunk, fw.need, fw.counters + 1,
-        fw.counters, x, x_stride, batch, d_work);
+    if (programmatic) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(static_cast<unsigned>(grid));
+        cfg.blockDim = dim3(kEncThreads);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        MSFFT_CUDA(cudaLaunchKernelEx(&cfg, k, plan, lay, args, fw.tasks, fw.items, fw.n_items,
+                                      fw.chunk, fw.need, fw.counters + 1, fw.counters, x, x_stride,
+                                      batch, d_work, fw.n_counters));
+    } else {
+        k<<<static_cast<unsigned>(grid), kEncThreads, smem, stream>>>(
+            plan, lay, args, fw.tasks, fw.items, fw.n_items, fw.chunk, fw.need, fw.counters + 1,
+            fw.counters, x, x_stride, batch, d_work, fw.n_counters);
+    }
     MSFFT_LAUNCH_CHECK("fused_kernel");
 }
 
 }  // namespace
 
+int64_t fused_slots(bool x_c128, size_t smem_bytes) {
+    int dev = 0, sms = 0, per_sm = 0;
+    MSFFT_CUDA(cudaGetDevice(&dev));
+    MSFFT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    if (x_c128) {
+        MSFFT_CUDA(cudaFuncSetAttribute(fused_kernel<double2>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(smem_bytes)));
+        MSFFT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fused_kernel<double2>,
+                                                                 kEncThreads, smem_bytes));
+    } else {
+        MSFFT_CUDA(cudaFuncSetAttribute(fused_kernel<float2>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(smem_bytes)));
+        MSFFT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fused_kernel<float2>,
+                                                                 kEncThreads, smem_bytes));
+    }
+    return static_cast<int64_t>(sms) * per_sm;
+}
+
 void launch_fused(const DevPlan& plan, const DecLayout& lay, const FusedWork& fw, const void* x,
                   bool x_c128, int64_t x_stride, int64_t batch, const int64_t* d_sigma,
                   const int64_t* d_sigma_inv, double2* d_y, unsigned char* d_work,
                   int64_t* d_out_f, double2* d_out_c, int64_t* d_out_count, int32_t* d_err,
-                  size_t smem_bytes, cudaStream_t stream) {
+                  size_t smem_bytes, cudaStream_t stream, bool programmatic) {
     if (fw.n_items <= 0) return;
     if (x_c128)
         launch_t(plan, lay, fw, static_cast<const double2*>(x), x_stride, batch, d_sigma,
                  d_sigma_inv, d_y, d_work, d_out_f, d_out_c, d_out_count, d_err, smem_bytes,
-                 stream);
+                 stream, programmatic);
     else
         launch_t(plan, lay, fw, static_cast<const float2*>(x), x_stride, batch, d_sigma,
                  d_sigma_inv, d_y, d_work, d_out_f, d_out_c, d_out_count, d_err, smem_bytes,
-                 stream);
+                 stream, programmatic);
 }
 
 }  // namespace msfft_b200

@@ -18,15 +18,20 @@ struct FusedWork {
     int32_t n_items = 0;
     int64_t chunk = 0;               // signals per chunk
     const int32_t* need = nullptr;   // [chunk][iteration] encode tasks
-    int32_t* counters = nullptr;     // [0] ticket, [1 + c*iters + m] tasks done
+    // [0] ticket, [1 + c*iters + m] tasks done, [n_counters - 1] CTAs exited;
+    // zero between launches (the last CTA of each launch resets them)
+    int32_t* counters = nullptr;
     int64_t n_chunks = 0;
     int64_t n_counters = 0;
 };
+
+// CTA slots of the fused kernel on the current device (its persistent grid).
+int64_t fused_slots(bool x_c128, size_t smem_bytes);
 
 void launch_fused(const DevPlan& plan, const DecLayout& lay, const FusedWork& fw, const void* x,
                   bool x_c128, int64_t x_stride, int64_t batch, const int64_t* d_sigma,
                   const int64_t* d_sigma_inv, double2* d_y, unsigned char* d_work,
                   int64_t* d_out_f, double2* d_out_c, int64_t* d_out_count, int32_t* d_err,
-                  size_t smem_bytes, cudaStream_t stream);
+                  size_t smem_bytes, cudaStream_t stream, bool programmatic = false);
 
 }  // namespace msfft_b200

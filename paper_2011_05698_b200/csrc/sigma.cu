@@ -32,6 +32,9 @@ template <int MAXD>
 __global__ void sigma_kernel(const uint64_t* __restrict__ seeds, int64_t batch, int iters,
                              int64_t n, int64_t* __restrict__ sigma,
                              int64_t* __restrict__ sigma_inv) {
+    // programmatic dependent launch: the next kernel may be scheduled now
+    // (it waits for this grid's results with griddepcontrol.wait)
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (s >= batch) return;
     // seeded state words 0..MAXD and kMM..kMM+MAXD
@@ -67,12 +70,26 @@ __global__ void sigma_kernel(const uint64_t* __restrict__ seeds, int64_t batch, 
 }  // namespace
 
 void launch_sigma(const uint64_t* d_seeds, int64_t batch, int iters, int64_t n, int64_t* d_sigma,
-                  int64_t* d_sigma_inv, cudaStream_t stream) {
+                  int64_t* d_sigma_inv, cudaStream_t stream, bool programmatic) {
     if (batch <= 0) return;
     if (iters > kMaxSigmaIters) throw std::invalid_argument("sigma plan: too many iterations");
     const unsigned blocks = static_cast<unsigned>((batch + 127) / 128);
-    sigma_kernel<kMaxSigmaIters><<<blocks, 128, 0, stream>>>(d_seeds, batch, iters, n, d_sigma,
-                                                             d_sigma_inv);
+    if (programmatic) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(blocks);
+        cfg.blockDim = dim3(128);
+        cfg.stream = stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        MSFFT_CUDA(cudaLaunchKernelEx(&cfg, sigma_kernel<kMaxSigmaIters>, d_seeds, batch, iters, n,
+                                      d_sigma, d_sigma_inv));
+    } else {
+        sigma_kernel<kMaxSigmaIters><<<blocks, 128, 0, stream>>>(d_seeds, batch, iters, n,
+                                                                 d_sigma, d_sigma_inv);
+    }
     MSFFT_LAUNCH_CHECK("sigma_kernel");
 }
 

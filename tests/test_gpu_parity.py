@@ -364,3 +364,37 @@ def test_async_execute(oracle):
     plan.sync()  # cleared
     with pytest.raises(M.InvalidArgument, match="MSFFT_FLAG_ASYNC needs device input and output"):
         plan.execute(xs, outs[0][0], async_=True)
+
+
+def test_async_pdl_chain(oracle, monkeypatch):
+    """Batches large enough for chained programmatic launches (step i+1 starts
+    while step i's last decodes run; opt-in MSFFT_PDL=1): every step's outputs
+    equal the synchronous path's, over alternating and changing seed sets."""
+    import torch
+    monkeypatch.setenv("MSFFT_PDL", "1")
+    n, k, B = 1 << 18, 40, 320
+    rng = np.random.default_rng(5)
+    xs = (rng.standard_normal((B, n)) + 1j * rng.standard_normal((B, n))).astype(np.complex64)
+    xs[:, 0] += 50.0  # a strong tone so every signal has support
+    plan = M.Plan(n, k, M.MultiscaleConfig(), 1e-6, "complex64")
+    xd = torch.as_tensor(xs).cuda()
+    seed_sets = [np.arange(1000, 1000 + B, dtype=np.uint64) + np.uint64(7919 * i) for i in range(3)]
+    order = [0, 1, 0, 1, 2, 1, 2, 0]
+    outs = []
+    for i in order:
+        o = (torch.empty((B, k), dtype=torch.int64, device="cuda"),
+             torch.empty((B, k), dtype=torch.complex128, device="cuda"),
+             torch.empty((B,), dtype=torch.int64, device="cuda"))
+        plan.execute(xd, seed_sets[i], out=o, assume_valid=True, async_=True)
+        outs.append(o)
+    plan.sync()
+    ref = {}
+    for i in set(order):
+        o = (torch.empty((B, k), dtype=torch.int64, device="cuda"),
+             torch.empty((B, k), dtype=torch.complex128, device="cuda"),
+             torch.empty((B,), dtype=torch.int64, device="cuda"))
+        plan.execute(xd, seed_sets[i], out=o, assume_valid=True)
+        ref[i] = [t.cpu().numpy() for t in o]
+    for i, o in zip(order, outs):
+        got = [t.cpu().numpy() for t in o]
+        assert all(np.array_equal(a, b) for a, b in zip(got, ref[i]))
