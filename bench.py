@@ -162,11 +162,11 @@ def e2e_batch(batch: int, sig_bytes: int, local_ranks: int) -> int:
 def pipe_evidence():
     """FP64-pipe and SM utilisation of the fused launch and of the decode
     (the FFT / locate / estimate stages) from the committed ncu captures of
-    the same workload (profiles/r02/*_ncu_summary.json), or None."""
+    the same workload (profiles/r01_final/*_ncu_summary.json), or None."""
     out = {}
     for key, name in (("fused_kernel", "fused_ncu_summary.json"),
                       ("decode_kernel", "decode_c4_ncu_summary.json")):
-        path = os.path.join(REPO, "profiles", "r02", name)
+        path = os.path.join(REPO, "profiles", "r01_final", name)
         if not os.path.exists(path):
             continue
         with open(path) as f:
@@ -179,7 +179,7 @@ def pipe_evidence():
         out[key] = {"fp64_pipe_frac": num("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active"),
                     "issue_active_frac": num("smsp__issue_active.avg.pct_of_peak_sustained_active"),
                     "sm_throughput_frac": num("sm__throughput.avg.pct_of_peak_sustained_elapsed"),
-                    "top_stalls": d.get("stall_share"), "source": f"profiles/r02/{name}"}
+                    "top_stalls": d.get("stall_share"), "source": f"profiles/r01_final/{name}"}
     return out or None
 
 
