@@ -250,7 +250,8 @@ def main():
               -(-args.batch // world), "global_batch": args.batch * world
               if args.scaling == "weak" else args.batch, "snr_db": args.snr,
               "parallelism": f"signal-sharded x{world} (no collective on the data path)",
-              "l2_policy": "inputs (32 GiB/GPU) >> L2 (126 MB); no flush"}
+              "l2_policy": "inputs (32 GiB/GPU) >> L2 (126 MB); no flush",
+              "input_dtype": "complex64 (upcast exactly; all arithmetic in float64)"}
 
     if args.impl == "reference":
         return run_reference_arm(args, rank, world, n, k, delta, config)
@@ -419,7 +420,7 @@ def main():
         "metric": METRIC, "value": value, "unit": "transforms/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
-        "dtype": "c64->f64",
+        "dtype": "f64",
         "data": "synthetic (seeded K-sparse spectra + AWGN, BASELINE.json configs[3] law)",
         "config": config,
         "roofline": {"bound": "hbm",
@@ -467,7 +468,7 @@ def run_reference_arm(args, rank, world, n, k, delta, config):
     line = {
         "metric": METRIC, "value": rate, "unit": "transforms/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": S / rate * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c64->f64",
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (same generator as the b200 arm)", "config": config,
         "impl": "reference",
         "cpu_baseline": {"value": rate, "unit": "transforms/s", "cores": threads, "kind": kind,
