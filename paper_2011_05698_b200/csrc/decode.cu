@@ -21,8 +21,8 @@ decode_kernel(const __grid_constant__ DevPlan plan, DecLayout lay, DecArgs args,
     // err[1]: the validation pass found a non-finite sample; the call will
     // throw (ComplexSignal::validate) so there is nothing to decode.
     if (s >= batch || args.err[1] != 0) return;
-    decode_signal(plan, lay, args, s, lay.in_smem ? dsm : work + s * lay.bytes, sh,
-                  lay.big ? reinterpret_cast<int*>(dsm) : nullptr);
+    decode_signal<kDecThreads>(plan, lay, args, s, lay.in_smem ? dsm : work + s * lay.bytes, sh,
+                               lay.big ? reinterpret_cast<int*>(dsm) : nullptr);
 }
 
 }  // namespace
@@ -49,7 +49,9 @@ DecLayout make_dec_layout(int64_t acc_cap, int64_t b_max, int64_t budget_max,
     L.off_cand_v = take(budget_max * 16);
     L.off_cand_first = take(budget_max * 4);
     L.off_cand_sum = take(budget_max * 16);
-    L.off_contrib = take(cap * rounds_max * 3 * 16);
+    // rotations per (tone, round); reused for the staged rounds of the ranked
+    // buckets (budget_max <= cap)
+    L.off_rot = take(std::max(cap, budget_max) * rounds_max * 16);
     L.off_bstart = take((b_max + 1) * 4);
     L.off_blist = take(cap * 4);
     L.off_gc = take(cap * 3 * 16);

@@ -66,7 +66,7 @@ struct Scratch {
     double2* cand_v;
     int32_t* cand_first;
     double2* cand_sum;
-    double2* contrib;  // [tone][round][3] predicted contributions
+    double2* rot;      // [tone][round] e^{-2 pi i tau_r u / n}; later the staged rounds
     int32_t* bstart;   // [b + 1] per-bucket list offsets
     int32_t* blist;    // [acc] tone indices grouped by bucket
     double2* gc;       // [acc][3] G * c per tone and bucket offset
@@ -92,12 +92,27 @@ __device__ __forceinline__ double2 unit_root(int64_t n, double inv_n, int64_t e)
     return make_double2(c, s);
 }
 
-// Decodes signal s; base = this signal's scratch (shared or global memory).
+// Barrier of a decode group: the whole CTA (bar_id 0, __syncthreads) or a
+// warp-aligned group of kThreads threads on named barrier bar_id.
+template <int kThreads>
+__device__ __forceinline__ void group_sync(int bar_id) {
+    if (bar_id == 0)
+        __syncthreads();
+    else
+        asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "n"(kThreads) : "memory");
+}
+
+// Decodes signal s with the kThreads threads starting at threadIdx.x ==
+// grp_base (the whole CTA, or one half of it when a fused CTA decodes two
+// signals); base = this signal's scratch (shared or global memory).  The
+// large-size paths (cta_radix_sort) need the whole CTA.
+template <int kThreads = kDecThreads>
 __device__ __forceinline__ void decode_signal(const DevPlan& plan, const DecLayout& lay,
                                            const DecArgs& A, int64_t s, unsigned char* base,
-                                           DecShared& sh, int* sort_smem) {
-    constexpr int kThreads = kDecThreads;
-    const int tid = threadIdx.x;
+                                           DecShared& sh, int* sort_smem, int grp_base = 0,
+                                           int bar_id = 0) {
+    const int tid = static_cast<int>(threadIdx.x) - grp_base;
+    const auto gsync = [bar_id] { group_sync<kThreads>(bar_id); };
     const int lane = tid & 31;
 
     Scratch S;
@@ -113,7 +128,7 @@ __device__ __forceinline__ void decode_signal(const DevPlan& plan, const DecLayo
     S.cand_v = reinterpret_cast<double2*>(base + lay.off_cand_v);
     S.cand_first = reinterpret_cast<int32_t*>(base + lay.off_cand_first);
     S.cand_sum = reinterpret_cast<double2*>(base + lay.off_cand_sum);
-    S.contrib = reinterpret_cast<double2*>(base + lay.off_contrib);
+    S.rot = reinterpret_cast<double2*>(base + lay.off_rot);
     S.bstart = reinterpret_cast<int32_t*>(base + lay.off_bstart);
     S.blist = reinterpret_cast<int32_t*>(base + lay.off_blist);
     S.gc = reinterpret_cast<double2*>(base + lay.off_gc);
@@ -131,7 +146,7 @@ __device__ __forceinline__ void decode_signal(const DevPlan& plan, const DecLayo
         sh.acc_n = 0;
         sh.cur = 0;
     }
-    __syncthreads();
+    gsync();
 
     const int64_t n = plan.n;
     const int64_t nmask = n - 1;
@@ -148,11 +163,11 @@ __device__ __forceinline__ void decode_signal(const DevPlan& plan, const DecLayo
     for (int m = 0; m < plan.iters; ++m) {
         DEC_MARK(0);
         if (A.gate_done) {  // fused: iteration m's buckets must be encoded
-            if (threadIdx.x == 0) {
+            if (tid == 0) {
                 while (load_acquire(&A.gate_done[m]) < A.gate_need[m]) __nanosleep(64);
                 __threadfence();
             }
-            __syncthreads();
+            gsync();
         }
         const DevIter& it = plan.it[m];
         const int64_t b = it.b, L = it.l_width;
@@ -171,9 +186,10 @@ __device__ __forceinline__ void decode_signal(const DevPlan& plan, const DecLayo
         // ---- K3: subtract the prediction of everything already known.
         // predict_buckets (bucketize.cpp:84-93) adds, per known tone in
         // ascending f, (G_{jL-u} * c) * e^{-2 pi i tau u/n} into buckets
-        // j = i-1, i, i+1.  Step 1 evaluates each (tone, round) rotation and
-        // its three contributions once; step 2 sums, per (round, bucket), the
-        // contributions in ascending tone order -- the reference's order.
+        // j = i-1, i, i+1.  Step 1 evaluates G*c per (tone, offset) and the
+        // rotation per (tone, round) once; step 2 sums, per (round, bucket),
+        // the contributions (G*c) * rot in ascending tone order -- the
+        // reference's order and operands.
         if (acc_n > 0) {
             for (int j = tid; j < acc_n; j += kThreads) {
                 const int64_t u = (sg * AF[j]) & nmask;
@@ -188,14 +204,11 @@ __device__ __forceinline__ void decode_signal(const DevPlan& plan, const DecLayo
                     S.gc[j * 3 + d] = make_double2(g * c.x, g * c.y);
                 }
             }
-            __syncthreads();
+            gsync();
             DEC_MARK(1);
             for (int e = tid; e < acc_n * nr; e += kThreads) {
                 const int j = e / nr, r = e - j * nr;
-                const double2 rot = unit_root(n, inv_n, taus[r] * S.tone_u[j]);
-                double2* dst = S.contrib + static_cast<int64_t>(e) * 3;
-#pragma unroll
-                for (int d = 0; d < 3; ++d) dst[d] = cmul(S.gc[j * 3 + d], rot);
+                S.rot[e] = unit_root(n, inv_n, taus[r] * S.tone_u[j]);
             }
             // per-bucket tone lists (ascending tone index = ascending f),
             // built by warp 0 while the other warps evaluate contributions:
@@ -242,7 +255,7 @@ __device__ __forceinline__ void decode_signal(const DevPlan& plan, const DecLayo
                     __syncwarp();
                 }
             }
-            __syncthreads();
+            gsync();
             DEC_MARK(2);
             // bucket beta collects, in ascending tone order, the tones whose
             // own bucket is beta+1 (offset jj = i-1), beta (jj = i) and
@@ -270,7 +283,8 @@ __device__ __forceinline__ void decode_signal(const DevPlan& plan, const DecLayo
                         }
                     if (best < 0) break;
                     ++p[best];
-                    const double2 v = S.contrib[(static_cast<int64_t>(bj) * nr + r) * 3 + best];
+                    // the contribution G*c * rot, evaluated here (same operands)
+                    const double2 v = cmul(S.gc[bj * 3 + best], S.rot[static_cast<int64_t>(bj) * nr + r]);
                     pred.x += v.x;
                     pred.y += v.y;
                     any = true;
@@ -280,7 +294,7 @@ __device__ __forceinline__ void decode_signal(const DevPlan& plan, const DecLayo
                     Y[e] = make_double2(o.x - pred.x, o.y - pred.y);
                 }
             }
-            __syncthreads();
+            gsync();
             DEC_MARK(3);
         }
 
@@ -290,7 +304,7 @@ __device__ __forceinline__ void decode_signal(const DevPlan& plan, const DecLayo
             const double mg = cabs_ref(v.x, v.y);
             S.mag[j] = mg == mg ? mg : -1.0;  // NaN (unvalidated input) ranks last
         }
-        __syncthreads();
+        gsync();
         DEC_MARK(4);
         if (b > kSmallRank && sort_smem) {
             // stable radix sort by |y0| descending (ties: lower bucket first)
@@ -298,7 +312,7 @@ __device__ __forceinline__ void decode_signal(const DevPlan& plan, const DecLayo
                 S.sk[0][j] = desc_key(S.mag[j]);
                 S.sv[0][j] = static_cast<int32_t>(j);
             }
-            __syncthreads();
+            gsync();
             const bool fl = cta_radix_sort<kThreads>(S.sk[0], S.sv[0], S.sk[1], S.sv[1],
                                                      static_cast<int>(b), 64, sort_smem,
                                                      sort_smem + 16 * kThreads);
@@ -315,22 +329,22 @@ __device__ __forceinline__ void decode_signal(const DevPlan& plan, const DecLayo
                 S.order[rank] = static_cast<int32_t>(j);
             }
         }
-        __syncthreads();
+        gsync();
         DEC_MARK(5);
         const int64_t budget = it.budget;
         if (tid == 0) sh.thr = 0.2 * S.mag[S.order[budget - 1]];
-        __syncthreads();
+        gsync();
         DEC_MARK(6);
         const double thr = sh.thr;
         // every ranked bucket's round values, staged in shared memory in one
-        // pass (the contribution area is free after K3): the locate stages
+        // pass (the rotation area is free after K3): the locate stages
         // then never wait on L2
-        double2* yr = S.contrib;
+        double2* yr = S.rot;  // free after K3
         for (int64_t e = tid; e < budget * nr; e += kThreads) {
             const int64_t rk = e / nr, st = e - rk * nr;
             yr[e] = Y[st * b + S.order[rk]];
         }
-        __syncthreads();
+        gsync();
         DEC_MARK(11);
         // phase_of(y0 / y_tau) (locate.cpp:110) depends only on the bucket
         // values, not on the narrowing region, so every (rank, stage) pair is
@@ -354,7 +368,7 @@ __device__ __forceinline__ void decode_signal(const DevPlan& plan, const DecLayo
             S.phi[e] = ph;
             S.pcode[e] = code;
         }
-        __syncthreads();
+        gsync();
         DEC_MARK(12);
 
         // ---- K5 + K6: locate and estimate.  A group of `gsz` lanes takes one
@@ -458,7 +472,7 @@ __device__ __forceinline__ void decode_signal(const DevPlan& plan, const DecLayo
                 }
             }
         }
-        __syncthreads();
+        gsync();
         DEC_MARK(7);
 
         // ---- K6 (merge): found[f] = 0 + v_r1 + v_r2 + ... in rank order
@@ -482,7 +496,7 @@ __device__ __forceinline__ void decode_signal(const DevPlan& plan, const DecLayo
                 S.sv[0][r] = static_cast<int32_t>(r);
             }
             for (int r = tid; r < padded; r += kThreads) S.flag[r] = 0;
-            __syncthreads();
+            gsync();
             const bool fl = cta_radix_sort<kThreads>(S.sk[0], S.sv[0], S.sk[1], S.sv[1],
                                                      static_cast<int>(budget), key_bits,
                                                      sort_smem, sort_smem + 16 * kThreads);
@@ -507,18 +521,18 @@ __device__ __forceinline__ void decode_signal(const DevPlan& plan, const DecLayo
                 S.flag[p] = present ? 0 : 1;
                 S.nfs[p] = present ? -2 : -1;  // marks a run start (-1 new, -2 present)
             }
-            __syncthreads();
+            gsync();
             // flag -> index among the new f; remember which positions start runs
             for (int64_t p = tid; p < budget; p += kThreads) {
                 const uint64_t f = Ks[p];
                 const bool start = f < static_cast<uint64_t>(n) && !(p > 0 && Ks[p - 1] == f);
                 S.cand_first[p] = start ? (S.flag[p] ? 1 : 2) : 0;  // indexed by position here
             }
-            __syncthreads();
+            gsync();
             const int nnew = cta_exclusive_scan<kThreads>(S.flag, padded, sort_smem + 16 * kThreads);
             for (int64_t p = tid; p < budget; p += kThreads)
                 if (S.cand_first[p] == 1) S.nfs[S.flag[p]] = static_cast<int64_t>(Ks[p]);
-            __syncthreads();
+            gsync();
             for (int j = tid; j < acc_n; j += kThreads) {
                 const int64_t fj = AF[j];
                 int lo = 0, hi = nnew;  // new f below fj
@@ -577,7 +591,7 @@ __device__ __forceinline__ void decode_signal(const DevPlan& plan, const DecLayo
             }
             S.cand_first[r] = first;
         }
-        __syncthreads();
+        gsync();
         DEC_MARK(8);
         // acc entries move up by the number of NEW found f below them
         for (int j = tid; j < acc_n; j += kThreads) {
@@ -615,14 +629,14 @@ __device__ __forceinline__ void decode_signal(const DevPlan& plan, const DecLayo
             atomicAdd(&sh.new_n, 1);
         }
         }  // small-budget merge
-        __syncthreads();
+        gsync();
         DEC_MARK(9);
         if (tid == 0) {
             sh.acc_n = acc_n + sh.new_n;
             sh.cur = nxt;
         }
         sel_off += budget;
-        __syncthreads();
+        gsync();
         DEC_MARK(10);
 #ifdef MSFFT_DECODE_PROFILE
         if (tid == 0 && s < 2)
@@ -647,7 +661,7 @@ __device__ __forceinline__ void decode_signal(const DevPlan& plan, const DecLayo
         const double mg = cabs_ref(c.x, c.y);
         S.mag[j] = mg == mg ? mg : -1.0;
     }
-    __syncthreads();
+    gsync();
     if (acc_n > kSmallAcc && sort_smem) {
         // stable sort by |c| descending over ascending f; keep ranks < K;
         // output positions by a prefix count over f order
@@ -657,14 +671,14 @@ __device__ __forceinline__ void decode_signal(const DevPlan& plan, const DecLayo
             S.sv[0][j] = j;
         }
         for (int j = tid; j < padded; j += kThreads) S.flag[j] = 0;
-        __syncthreads();
+        gsync();
         const bool fl = cta_radix_sort<kThreads>(S.sk[0], S.sv[0], S.sk[1], S.sv[1], acc_n, 64,
                                                  sort_smem, sort_smem + 16 * kThreads);
         const int32_t* V = fl ? S.sv[1] : S.sv[0];
         for (int r = tid; r < acc_n && r < K; r += kThreads) S.flag[V[r]] = 1;
-        __syncthreads();
+        gsync();
         for (int j = tid; j < acc_n; j += kThreads) S.tone_i[j] = S.flag[j];
-        __syncthreads();
+        gsync();
         cta_exclusive_scan<kThreads>(S.flag, padded, sort_smem + 16 * kThreads);
         for (int j = tid; j < acc_n; j += kThreads) {
             if (!S.tone_i[j]) continue;
@@ -682,7 +696,7 @@ __device__ __forceinline__ void decode_signal(const DevPlan& plan, const DecLayo
             }
             S.tone_i[j] = rank < K ? 1 : 0;
         }
-        __syncthreads();
+        gsync();
         for (int j = tid; j < acc_n; j += kThreads) {
             if (!S.tone_i[j]) continue;
             int64_t pos = 0;

@@ -22,7 +22,7 @@ struct DecLayout {
     int64_t off_acc_f[2], off_acc_c[2];
     int64_t off_tone_u, off_tone_i;
     int64_t off_mag, off_order;
-    int64_t off_cand_f, off_cand_v, off_cand_first, off_cand_sum, off_contrib;
+    int64_t off_cand_f, off_cand_v, off_cand_first, off_cand_sum, off_rot;
     int64_t off_bstart, off_blist, off_gc, off_phi, off_pcode;
     // large-size scratch (radix sorts), present when big != 0
     int64_t off_sk[2], off_sv[2], off_flag, off_nfs, sort_n;

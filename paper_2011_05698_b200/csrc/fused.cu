@@ -64,13 +64,13 @@ fused_kernel(const __grid_constant__ DevPlan plan, DecLayout lay, DecArgs args,
         } else if (!bad_input) {
             // the decode waits per iteration (DecArgs::gate_*), so it can run
             // while the later iterations of its chunk are still being encoded
-            const int64_t s = -static_cast<int64_t>(code) - 1;
-            const int64_t c = s / chunk;
+            const int64_t s0 = -static_cast<int64_t>(code) - 1;
+            const int64_t c = s0 / chunk;
             DecArgs a = args;
             a.gate_done = done + c * plan.iters;
             a.gate_need = need + c * plan.iters;
-            decode_signal(plan, lay, a, s, lay.in_smem ? smem : work + s * lay.bytes, sh,
-                          nullptr);
+            decode_signal<kDecThreads>(plan, lay, a, s0, lay.in_smem ? smem : work + s0 * lay.bytes,
+                                       sh, nullptr);
         }
         __syncthreads();
     }
