@@ -59,6 +59,8 @@ Plan::Plan(int64_t n, int64_t k, int64_t l, double q, double delta, bool c128, i
     // Scatter-free L2 fills: the gather touches one 32-B sector per sample.
     cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, 32);
 
+    size_t taps_smem_max = kTapsSmemMax;  // MSFFT_TAPS_SMEM_MAX (bytes): diagnostics
+    if (const char* e = std::getenv("MSFFT_TAPS_SMEM_MAX")) taps_smem_max = std::atoll(e);
     DevPlan& P = dplan_;
     std::memset(&P, 0, sizeof(P));
     P.n = n;
@@ -108,7 +110,7 @@ Plan::Plan(int64_t n, int64_t k, int64_t l, double q, double delta, bool c128, i
             it.nstage_tab = (len > 1.0 + 1e-9) ? -1 : st;
         }
         const size_t taps_bytes = static_cast<size_t>(win->w + 1) * sizeof(double);
-        it.taps_in_smem = taps_bytes <= kTapsSmemMax ? 1 : 0;
+        it.taps_in_smem = taps_bytes <= taps_smem_max ? 1 : 0;
         if (tau_off + it.nrounds > kMaxTaus)
             throw std::invalid_argument("sfft4: tau plan exceeds the device plan limit");
         for (int r = 0; r < it.nrounds; ++r) P.taus[tau_off + r] = ip.taus[r];
