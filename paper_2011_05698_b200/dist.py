@@ -78,6 +78,12 @@ def combine_partials(y, group=None):
     import torch.distributed as dist
     if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
         return y
+    if y.is_cuda and dist.get_backend(group) != "nccl":
+        # host-side backends (gloo): reduce a host copy
+        h = torch.view_as_real(y).cpu()
+        dist.all_reduce(h, op=dist.ReduceOp.SUM, group=group)
+        torch.view_as_real(y).copy_(h)
+        return y
     dist.all_reduce(torch.view_as_real(y), op=dist.ReduceOp.SUM, group=group)
     return y
 
