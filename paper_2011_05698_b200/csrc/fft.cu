@@ -114,6 +114,45 @@ __global__ void __launch_bounds__(512) stages_kernel(double2* __restrict__ data,
     }
 }
 
+// Whole transform of one array (size <= kSmemFftMax) in shared memory: the
+// bit-reversal permutation folded into the load, then every radix-2 stage
+// with the same butterflies and twiddles as stages_kernel (bit-identical).
+constexpr int64_t kSmemFftMax = 4096;
+__global__ void __launch_bounds__(512) fft_smem_kernel(double2* __restrict__ data, int64_t size,
+                                                       int log2size, int64_t inner,
+                                                       int64_t outer_stride, int sign,
+                                                       const double2* __restrict__ tw,
+                                                       double scale) {
+    extern __shared__ double2 buf[];
+    const int64_t bi = blockIdx.x;
+    double2* a = data + (bi / inner) * outer_stride + (bi % inner) * size;
+    const int n = static_cast<int>(size);
+    for (int e = threadIdx.x; e < n; e += blockDim.x)
+        buf[bitrev_bits(static_cast<unsigned>(e), log2size)] = a[e];
+    __syncthreads();
+    for (int s = 1; s <= log2size; ++s) {
+        const int half = 1 << (s - 1);
+        const int64_t step = size >> s;
+        for (int bf = threadIdx.x; bf < n / 2; bf += blockDim.x) {
+            const int blk = bf / half, off = bf - blk * half;
+            const int e0 = blk * 2 * half + off, e1 = e0 + half;
+            double2 w = tw[static_cast<int64_t>(off) * step];
+            if (sign > 0) w.y = -w.y;
+            const double2 x0 = buf[e0];
+            const double2 t = cmul(buf[e1], w);
+            buf[e1] = make_double2(x0.x - t.x, x0.y - t.y);
+            buf[e0] = make_double2(x0.x + t.x, x0.y + t.y);
+        }
+        __syncthreads();
+    }
+    const bool do_scale = scale != 1.0;
+    for (int e = threadIdx.x; e < n; e += blockDim.x) {
+        double2 v = buf[e];
+        if (do_scale) v = make_double2(v.x * scale, v.y * scale);
+        a[e] = v;
+    }
+}
+
 }  // namespace
 
 const double* host_twiddles(int64_t n) {
@@ -149,6 +188,21 @@ void fft_radix2_batched(double2* data, int64_t size, int64_t batch, int64_t inne
     int log2size = 0;
     while ((int64_t{1} << log2size) < size) ++log2size;
     const double2* tw = device_twiddles(size);
+    if (size <= kSmemFftMax && batch <= 0x7fffffff) {
+        // one launch, one read and one write of the data
+        const size_t smem = sizeof(double2) * static_cast<size_t>(size);
+        static bool attr_set = false;
+        if (!attr_set) {
+            MSFFT_CUDA(cudaFuncSetAttribute(fft_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            static_cast<int>(sizeof(double2) * kSmemFftMax)));
+            attr_set = true;
+        }
+        const int threads = static_cast<int>(std::min<int64_t>(512, std::max<int64_t>(32, size / 2)));
+        fft_smem_kernel<<<static_cast<unsigned>(batch), threads, smem, stream>>>(
+            data, size, log2size, inner, outer_stride, sign, tw, scale);
+        MSFFT_LAUNCH_CHECK("fft_smem_kernel");
+        return;
+    }
     const int64_t total = size * batch;
     bitrev_inplace_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, stream>>>(
         data, size, log2size, inner, outer_stride, total);
