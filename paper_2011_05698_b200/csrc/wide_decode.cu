@@ -755,6 +755,129 @@ __global__ void k6_merge_new(const int64_t* __restrict__ AF, const int32_t* __re
     }
 }
 
+// budget <= 1024: the whole found-map merge in one CTA (same ordering rules
+// and arithmetic as k6_sortf .. k6_count): accepted candidates ranked by
+// (f, rank) in shared memory, run sums in rank order, block scan of the "new
+// f" flags, then the merge into the ascending accumulated list.
+constexpr int kSmallK6 = 1024;
+constexpr int64_t kSmallK6Acc = 16384;  // accumulated-list cap for the one-CTA merge
+__global__ void __launch_bounds__(kSmallK6)
+k6_small(const DevPlan* __restrict__ P, int m, const int64_t* __restrict__ cand_f,
+         const double2* __restrict__ cand_v, const int64_t* __restrict__ AF,
+         const double2* __restrict__ AC, int32_t* __restrict__ scal, int64_t* __restrict__ NF,
+         double2* __restrict__ NC) {
+    __shared__ int64_t sf[kSmallK6];     // f by rank, then f at sorted position
+    __shared__ int32_t byf[kSmallK6];    // rank at sorted position
+    __shared__ double2 rsum[kSmallK6];   // run sums at run starts
+    __shared__ int32_t nflag[kSmallK6];  // new-f flag -> exclusive prefix
+    __shared__ int64_t newf[kSmallK6];
+    __shared__ int32_t wsum[kSmallK6 / 32];
+    __shared__ int32_t s_acc, s_A;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t budget = P->it[m].budget;
+    if (tid == 0) {
+        s_acc = scal[0];
+        s_A = 0;
+    }
+    const int64_t fr = tid < budget ? cand_f[tid] : -1;
+    sf[tid] = fr;
+    __syncthreads();
+    const int an = s_acc;
+    if (fr >= 0) {
+        int pos = 0;
+        for (int o = 0; o < budget; ++o) {
+            const int64_t fo = sf[o];
+            pos += fo >= 0 && (fo < fr || (fo == fr && o < tid));
+        }
+        byf[pos] = tid;
+        atomicAdd(&s_A, 1);
+    }
+    __syncthreads();
+    const int A = s_A;
+    const int64_t fsorted = tid < A ? sf[byf[tid]] : -1;
+    __syncthreads();
+    sf[tid] = fsorted;
+    __syncthreads();
+    int flag = 0;
+    if (tid < A) {
+        const int64_t f = sf[tid];
+        if (tid == 0 || sf[tid - 1] != f) {
+            double2 sum = make_double2(0.0, 0.0);
+            for (int p2 = tid; p2 < A && sf[p2] == f; ++p2) {
+                const double2 v = cand_v[byf[p2]];
+                sum.x += v.x;
+                sum.y += v.y;
+            }
+            rsum[tid] = sum;
+            int lo = 0, hi = an;
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (AF[mid] < f) lo = mid + 1; else hi = mid;
+            }
+            flag = (lo < an && AF[lo] == f) ? 0 : 1;
+        }
+    }
+    // exclusive scan of the flags over the block
+    int v = flag;
+    for (int o = 1; o < 32; o <<= 1) {
+        const int w = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += w;
+    }
+    if (lane == 31) wsum[warp] = v;
+    __syncthreads();
+    if (warp == 0) {
+        int wv = wsum[lane];
+        for (int o = 1; o < 32; o <<= 1) {
+            const int w = __shfl_up_sync(0xffffffffu, wv, o);
+            if (lane >= o) wv += w;
+        }
+        wsum[lane] = wv;
+    }
+    __syncthreads();
+    const int npos = v - flag + (warp ? wsum[warp - 1] : 0);
+    const int nnew = wsum[kSmallK6 / 32 - 1];
+    nflag[tid] = flag;
+    if (flag) newf[npos] = sf[tid];
+    __syncthreads();
+    for (int j = tid; j < an; j += kSmallK6) {
+        const int64_t fj = AF[j];
+        int lo = 0, hi = nnew;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (newf[mid] < fj) lo = mid + 1; else hi = mid;
+        }
+        const int before = lo;
+        int plo = 0, phi2 = A;
+        while (plo < phi2) {
+            const int mid = (plo + phi2) >> 1;
+            if (sf[mid] < fj) plo = mid + 1; else phi2 = mid;
+        }
+        double2 c = AC[j];
+        if (plo < A && sf[plo] == fj) {
+            const double2 add = rsum[plo];
+            c = make_double2(c.x + add.x, c.y + add.y);
+        }
+        NF[j + before] = fj;
+        NC[j + before] = c;
+    }
+    if (tid < A && nflag[tid]) {
+        const int64_t f = sf[tid];
+        int lo = 0, hi = an;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (AF[mid] < f) lo = mid + 1; else hi = mid;
+        }
+        const double2 sum = rsum[tid];
+        NF[lo + npos] = f;
+        NC[lo + npos] = make_double2(0.0 + sum.x, 0.0 + sum.y);
+    }
+    __syncthreads();
+    if (tid == 0) {
+        scal[0] = an + nnew;
+        scal[4] = 0;
+    }
+}
+
 __global__ void k6_count(int32_t* scal) {
     scal[0] += scal[1];  // acc_n += new_n
     scal[4] = 0;         // accepted counter for the next iteration
@@ -960,29 +1083,34 @@ void WideDecoder::enqueue(double2* y, const int64_t* sigma, const int64_t* sigma
                                                        err);
         MSFFT_LAUNCH_CHECK("wide K4/K5");
         // ---- K6
-        {
-            const unsigned tiles = static_cast<unsigned>((budget + kT - 1) / kT);
-            const unsigned split = std::max(1u, std::min(32u, 296u / tiles));
-            MSFFT_CUDA(cudaMemsetAsync(pos_.get(), 0, budget * sizeof(int32_t), st));
-            k6_sortf<<<dim3(tiles, split), kT, 0, st>>>(cand_f_.get(), budget, pos_.get());
-            k6_scatter<<<grid_of(budget), kT, 0, st>>>(cand_f_.get(), pos_.get(), budget, byf_.get(),
-                                                       naccepted);
+        if (budget <= kSmallK6 && acc_cap_ <= kSmallK6Acc) {
+            k6_small<<<1, kSmallK6, 0, st>>>(P, m, cand_f_.get(), cand_v_.get(), AF, AC, scal_.get(),
+                                             acc_f_[nxt].get(), acc_c_[nxt].get());
+        } else {
+            {
+                const unsigned tiles = static_cast<unsigned>((budget + kT - 1) / kT);
+                const unsigned split = std::max(1u, std::min(32u, 296u / tiles));
+                MSFFT_CUDA(cudaMemsetAsync(pos_.get(), 0, budget * sizeof(int32_t), st));
+                k6_sortf<<<dim3(tiles, split), kT, 0, st>>>(cand_f_.get(), budget, pos_.get());
+                k6_scatter<<<grid_of(budget), kT, 0, st>>>(cand_f_.get(), pos_.get(), budget, byf_.get(),
+                                                           naccepted);
+            }
+            k6_runs<<<grid_of(budget), kT, 0, st>>>(cand_f_.get(), cand_v_.get(), byf_.get(),
+                                                    naccepted, AF, acc_n, cand_sum_.get(),
+                                                    newflag_.get());
+            scan_kernel<<<1, kScanT, 0, st>>>(newflag_.get(), budget, naccepted, newpos_.get(), new_n);
+            k6_newf<<<grid_of(budget), kT, 0, st>>>(cand_f_.get(), byf_.get(), naccepted,
+                                                    newflag_.get(), newpos_.get(), newf_.get());
+            k6_merge_acc<<<grid_of(acc_cap_), kT, 0, st>>>(AF, AC, acc_n, newf_.get(), new_n,
+                                                           cand_f_.get(), byf_.get(), naccepted,
+                                                           cand_sum_.get(), acc_f_[nxt].get(),
+                                                           acc_c_[nxt].get());
+            k6_merge_new<<<grid_of(budget), kT, 0, st>>>(AF, acc_n, cand_f_.get(), byf_.get(),
+                                                         naccepted, newflag_.get(), newpos_.get(),
+                                                         cand_sum_.get(), acc_f_[nxt].get(),
+                                                         acc_c_[nxt].get());
+            k6_count<<<1, 1, 0, st>>>(scal_.get());
         }
-        k6_runs<<<grid_of(budget), kT, 0, st>>>(cand_f_.get(), cand_v_.get(), byf_.get(),
-                                                naccepted, AF, acc_n, cand_sum_.get(),
-                                                newflag_.get());
-        scan_kernel<<<1, kScanT, 0, st>>>(newflag_.get(), budget, naccepted, newpos_.get(), new_n);
-        k6_newf<<<grid_of(budget), kT, 0, st>>>(cand_f_.get(), byf_.get(), naccepted,
-                                                newflag_.get(), newpos_.get(), newf_.get());
-        k6_merge_acc<<<grid_of(acc_cap_), kT, 0, st>>>(AF, AC, acc_n, newf_.get(), new_n,
-                                                       cand_f_.get(), byf_.get(), naccepted,
-                                                       cand_sum_.get(), acc_f_[nxt].get(),
-                                                       acc_c_[nxt].get());
-        k6_merge_new<<<grid_of(budget), kT, 0, st>>>(AF, acc_n, cand_f_.get(), byf_.get(),
-                                                     naccepted, newflag_.get(), newpos_.get(),
-                                                     cand_sum_.get(), acc_f_[nxt].get(),
-                                                     acc_c_[nxt].get());
-        k6_count<<<1, 1, 0, st>>>(scal_.get());
         MSFFT_LAUNCH_CHECK("wide K6");
     }
     // ---- K7: the K largest |c| (stable over ascending f), emitted in f order
