@@ -3,6 +3,7 @@
 #include <map>
 #include <memory>
 #include <mutex>
+#include <set>
 #include <thread>
 #include <vector>
 
@@ -191,11 +192,19 @@ void fft_radix2_batched(double2* data, int64_t size, int64_t batch, int64_t inne
     if (size <= kSmemFftMax && batch <= 0x7fffffff) {
         // one launch, one read and one write of the data
         const size_t smem = sizeof(double2) * static_cast<size_t>(size);
-        static bool attr_set = false;
-        if (!attr_set) {
-            MSFFT_CUDA(cudaFuncSetAttribute(fft_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            static_cast<int>(sizeof(double2) * kSmemFftMax)));
-            attr_set = true;
+        {
+            // the attribute is per device
+            static std::mutex mu;
+            static std::set<int> ready;
+            int dev = 0;
+            MSFFT_CUDA(cudaGetDevice(&dev));
+            std::lock_guard<std::mutex> lock(mu);
+            if (!ready.count(dev)) {
+                MSFFT_CUDA(cudaFuncSetAttribute(fft_smem_kernel,
+                                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                static_cast<int>(sizeof(double2) * kSmemFftMax)));
+                ready.insert(dev);
+            }
         }
         const int threads = static_cast<int>(std::min<int64_t>(512, std::max<int64_t>(32, size / 2)));
         fft_smem_kernel<<<static_cast<unsigned>(batch), threads, smem, stream>>>(
