@@ -30,6 +30,12 @@ namespace {
 struct DecShared {
     int acc_n, new_n, cur;
     double thr;
+    // the iteration's locate stage table and first taus, copied from the
+    // (grid-constant) plan at the top of each iteration: the stage chain of
+    // K5 then reads shared memory instead of missing the constant cache once
+    // per stage
+    double st_len[kMaxStageTable], st_blk[kMaxStageTable];
+    int64_t st_tau[kMaxStageTable];
 };
 
 struct DecArgs {
@@ -175,6 +181,12 @@ __device__ __forceinline__ void decode_signal(const DevPlan& plan, const DecLayo
         const double invL = 1.0 / Ld;  // exact: L is a power of two
         const int nr = it.nrounds;
         const int64_t* taus = plan.taus + it.tau_off;
+        if (tid < kMaxStageTable) {  // read after the next group barrier (K3 or K4)
+            sh.st_len[tid] = it.stage_len[tid];
+            sh.st_blk[tid] = it.stage_blk[tid];
+            sh.st_tau[tid] = tid < nr ? taus[tid] : 0;
+        }
+        const auto tau_at = [&](int r) { return r < kMaxStageTable ? sh.st_tau[r] : taus[r]; };
         double2* Y = ysig + it.yoff;
         const int64_t sg = A.sigma[s * plan.iters + m];
         const int64_t sgi = A.sigma_inv[s * plan.iters + m];
@@ -208,7 +220,7 @@ __device__ __forceinline__ void decode_signal(const DevPlan& plan, const DecLayo
             DEC_MARK(1);
             for (int e = tid; e < acc_n * nr; e += kThreads) {
                 const int j = e / nr, r = e - j * nr;
-                S.rot[e] = unit_root(n, inv_n, taus[r] * S.tone_u[j]);
+                S.rot[e] = unit_root(n, inv_n, tau_at(r) * S.tone_u[j]);
             }
             // per-bucket tone lists (ascending tone index = ascending f),
             // built by warp 0 while the other warps evaluate contributions:
@@ -422,9 +434,9 @@ __device__ __forceinline__ void decode_signal(const DevPlan& plan, const DecLayo
                         phi = S.phi[pe];
                     }
                 }
-                const int64_t tau = taus[stage];
+                const int64_t tau = tau_at(stage);
                 const double rblk =
-                    nst >= 0 ? it.stage_blk[stage - 1] : len / static_cast<double>(lcfg);
+                    nst >= 0 ? sh.st_blk[stage - 1] : len / static_cast<double>(lcfg);
                 double best_d = INFINITY;
                 int best_j = 0x7fffffff;
                 for (int64_t j = glane; j < lcfg; j += gsz) {
@@ -447,7 +459,7 @@ __device__ __forceinline__ void decode_signal(const DevPlan& plan, const DecLayo
                 }
                 if (best_j == 0x7fffffff) best_j = 0;  // all distances NaN: reference keeps 0
                 u_min = u_min + (static_cast<double>(best_j) - q / 2.0) * rblk;
-                len = nst >= 0 ? it.stage_len[stage] : len * (q + 1.0) / static_cast<double>(lcfg);
+                len = nst >= 0 ? sh.st_len[stage] : len * (q + 1.0) / static_cast<double>(lcfg);
             }
             if (ok) {
                 const double lo = u_min, hi = u_min + len;
