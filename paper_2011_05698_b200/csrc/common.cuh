@@ -9,9 +9,54 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdio>
 #include <cuda_runtime.h>
 
 namespace msfft_b200 {
+
+// Checked build (-DMSFFT_CHECKED, tools/build_variant.py checked ...): every
+// scratch array the kernels index through dptr<T> carries its capacity and
+// traps with the file, line and thread on an out-of-range index; MSFFT_DCHECK
+// guards the remaining computed indices.  Normal builds: dptr<T> is T* and
+// the checks compile to nothing.
+#ifdef MSFFT_CHECKED
+#define MSFFT_DCHECK(c)                                                                   \
+    do {                                                                                  \
+        if (!(c)) {                                                                       \
+            printf("MSFFT_DCHECK %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #c, \
+                   static_cast<int>(blockIdx.x), static_cast<int>(threadIdx.x));          \
+            __trap();                                                                     \
+        }                                                                                 \
+    } while (0)
+template <class T>
+struct CheckedPtr {
+    T* p = nullptr;
+    int64_t n = 0;
+    CheckedPtr() = default;
+    __host__ __device__ CheckedPtr(T* p_, int64_t n_) : p(p_), n(n_) {}
+    __device__ T& operator[](int64_t i) const {
+        MSFFT_DCHECK(p != nullptr && i >= 0 && i < n);
+        return p[i];
+    }
+    __device__ operator T*() const { return p; }
+};
+template <class T>
+using dptr = CheckedPtr<T>;
+template <class T>
+__device__ inline dptr<T> make_dptr(T* p, int64_t n) {
+    return dptr<T>(p, n);
+}
+#else
+#define MSFFT_DCHECK(c) \
+    do {                \
+    } while (0)
+template <class T>
+using dptr = T*;
+template <class T>
+__device__ __forceinline__ T* make_dptr(T* p, int64_t) {
+    return p;
+}
+#endif
 
 // 2*pi as in proj/src/locate.cpp:10 / window.cpp:15 (2.0 * std::numbers::pi).
 constexpr double kTwoPi = 6.283185307179586476925286766559;

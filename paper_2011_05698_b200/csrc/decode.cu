@@ -37,6 +37,10 @@ DecLayout make_dec_layout(int64_t acc_cap, int64_t b_max, int64_t budget_max,
         return o;
     };
     const int64_t cap = std::max<int64_t>(acc_cap, 1);
+    L.cap = cap;
+    L.b_max = b_max;
+    L.budget_max = budget_max;
+    L.rounds_max = rounds_max;
     for (int p = 0; p < 2; ++p) {
         L.off_acc_f[p] = take(cap * 8);
         L.off_acc_c[p] = take(cap * 16);

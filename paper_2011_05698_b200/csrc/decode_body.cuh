@@ -62,26 +62,26 @@ __device__ __forceinline__ int32_t load_acquire(const int32_t* p) {
 }
 
 struct Scratch {
-    int64_t* acc_f[2];
-    double2* acc_c[2];
-    int64_t* tone_u;
-    int64_t* tone_i;
-    double* mag;
-    int32_t* order;
-    int64_t* cand_f;
-    double2* cand_v;
-    int32_t* cand_first;
-    double2* cand_sum;
-    double2* rot;      // [tone][round] e^{-2 pi i tau_r u / n}; later the staged rounds
-    int32_t* bstart;   // [b + 1] per-bucket list offsets
-    int32_t* blist;    // [acc] tone indices grouped by bucket
-    double2* gc;       // [acc][3] G * c per tone and bucket offset
-    double* phi;       // [budget][stages] phase of y0 / y_tau
-    int32_t* pcode;    // [budget][stages] 0 ok, 1 y_tau == 0, 2 quotient == 0
-    uint64_t* sk[2];   // large sizes: radix-sort keys (ping-pong)
-    int32_t* sv[2];    //              and values
-    int32_t* flag;     //              scan flags
-    int64_t* nfs;      //              new found frequencies
+    dptr<int64_t> acc_f[2];
+    dptr<double2> acc_c[2];
+    dptr<int64_t> tone_u;
+    dptr<int64_t> tone_i;
+    dptr<double> mag;
+    dptr<int32_t> order;
+    dptr<int64_t> cand_f;
+    dptr<double2> cand_v;
+    dptr<int32_t> cand_first;
+    dptr<double2> cand_sum;
+    dptr<double2> rot;      // [tone][round] e^{-2 pi i tau_r u / n}; later the staged rounds
+    dptr<int32_t> bstart;   // [b + 1] per-bucket list offsets
+    dptr<int32_t> blist;    // [acc] tone indices grouped by bucket
+    dptr<double2> gc;       // [acc][3] G * c per tone and bucket offset
+    dptr<double> phi;       // [budget][stages] phase of y0 / y_tau
+    dptr<int32_t> pcode;    // [budget][stages] 0 ok, 1 y_tau == 0, 2 quotient == 0
+    dptr<uint64_t> sk[2];   // large sizes: radix-sort keys (ping-pong)
+    dptr<int32_t> sv[2];    //              and values
+    dptr<int32_t> flag;     //              scan flags
+    dptr<int64_t> nfs;      //              new found frequencies
 };
 
 __device__ __forceinline__ double ghat_at(const DevIter& it, int64_t d) {
@@ -122,30 +122,35 @@ __device__ __forceinline__ void decode_signal(const DevPlan& plan, const DecLayo
     const int lane = tid & 31;
 
     Scratch S;
+    const int64_t cap = lay.cap, capb = cap > lay.b_max ? cap : lay.b_max;
+    const int64_t bud = lay.budget_max, rmax = lay.rounds_max;
+    const auto at = [base](int64_t off) { return base + off; };
     for (int p = 0; p < 2; ++p) {
-        S.acc_f[p] = reinterpret_cast<int64_t*>(base + lay.off_acc_f[p]);
-        S.acc_c[p] = reinterpret_cast<double2*>(base + lay.off_acc_c[p]);
+        S.acc_f[p] = make_dptr(reinterpret_cast<int64_t*>(at(lay.off_acc_f[p])), cap);
+        S.acc_c[p] = make_dptr(reinterpret_cast<double2*>(at(lay.off_acc_c[p])), cap);
     }
-    S.tone_u = reinterpret_cast<int64_t*>(base + lay.off_tone_u);
-    S.tone_i = reinterpret_cast<int64_t*>(base + lay.off_tone_i);
-    S.mag = reinterpret_cast<double*>(base + lay.off_mag);
-    S.order = reinterpret_cast<int32_t*>(base + lay.off_order);
-    S.cand_f = reinterpret_cast<int64_t*>(base + lay.off_cand_f);
-    S.cand_v = reinterpret_cast<double2*>(base + lay.off_cand_v);
-    S.cand_first = reinterpret_cast<int32_t*>(base + lay.off_cand_first);
-    S.cand_sum = reinterpret_cast<double2*>(base + lay.off_cand_sum);
-    S.rot = reinterpret_cast<double2*>(base + lay.off_rot);
-    S.bstart = reinterpret_cast<int32_t*>(base + lay.off_bstart);
-    S.blist = reinterpret_cast<int32_t*>(base + lay.off_blist);
-    S.gc = reinterpret_cast<double2*>(base + lay.off_gc);
-    S.phi = reinterpret_cast<double*>(base + lay.off_phi);
-    S.pcode = reinterpret_cast<int32_t*>(base + lay.off_pcode);
+    S.tone_u = make_dptr(reinterpret_cast<int64_t*>(at(lay.off_tone_u)), cap);
+    S.tone_i = make_dptr(reinterpret_cast<int64_t*>(at(lay.off_tone_i)), capb);
+    S.mag = make_dptr(reinterpret_cast<double*>(at(lay.off_mag)), capb);
+    S.order = make_dptr(reinterpret_cast<int32_t*>(at(lay.off_order)), lay.b_max);
+    S.cand_f = make_dptr(reinterpret_cast<int64_t*>(at(lay.off_cand_f)), bud);
+    S.cand_v = make_dptr(reinterpret_cast<double2*>(at(lay.off_cand_v)), bud);
+    S.cand_first = make_dptr(reinterpret_cast<int32_t*>(at(lay.off_cand_first)), bud);
+    S.cand_sum = make_dptr(reinterpret_cast<double2*>(at(lay.off_cand_sum)), bud);
+    S.rot = make_dptr(reinterpret_cast<double2*>(at(lay.off_rot)), (cap > bud ? cap : bud) * rmax);
+    S.bstart = make_dptr(reinterpret_cast<int32_t*>(at(lay.off_bstart)), lay.b_max + 1);
+    S.blist = make_dptr(reinterpret_cast<int32_t*>(at(lay.off_blist)), cap);
+    S.gc = make_dptr(reinterpret_cast<double2*>(at(lay.off_gc)), cap * 3);
+    S.phi = make_dptr(reinterpret_cast<double*>(at(lay.off_phi)), bud * rmax);
+    S.pcode = make_dptr(reinterpret_cast<int32_t*>(at(lay.off_pcode)), bud * rmax);
+    const int64_t nsort = lay.big ? lay.sort_n : 0;
     for (int p = 0; p < 2; ++p) {
-        S.sk[p] = lay.big ? reinterpret_cast<uint64_t*>(base + lay.off_sk[p]) : nullptr;
-        S.sv[p] = lay.big ? reinterpret_cast<int32_t*>(base + lay.off_sv[p]) : nullptr;
+        S.sk[p] = make_dptr(lay.big ? reinterpret_cast<uint64_t*>(at(lay.off_sk[p])) : nullptr, nsort);
+        S.sv[p] = make_dptr(lay.big ? reinterpret_cast<int32_t*>(at(lay.off_sv[p])) : nullptr, nsort);
     }
-    S.flag = lay.big ? reinterpret_cast<int32_t*>(base + lay.off_flag) : nullptr;
-    S.nfs = lay.big ? reinterpret_cast<int64_t*>(base + lay.off_nfs) : nullptr;
+    S.flag = make_dptr(lay.big ? reinterpret_cast<int32_t*>(at(lay.off_flag)) : nullptr,
+                       lay.big ? nsort + kThreads : 0);
+    S.nfs = make_dptr(lay.big ? reinterpret_cast<int64_t*>(at(lay.off_nfs)) : nullptr, nsort);
     if (!lay.big) sort_smem = nullptr;
 
     if (tid == 0) {
@@ -187,13 +192,13 @@ __device__ __forceinline__ void decode_signal(const DevPlan& plan, const DecLayo
             sh.st_tau[tid] = tid < nr ? taus[tid] : 0;
         }
         const auto tau_at = [&](int r) { return r < kMaxStageTable ? sh.st_tau[r] : taus[r]; };
-        double2* Y = ysig + it.yoff;
+        const auto Y = make_dptr(ysig + it.yoff, static_cast<int64_t>(nr) * b);
         const int64_t sg = A.sigma[s * plan.iters + m];
         const int64_t sgi = A.sigma_inv[s * plan.iters + m];
         const int acc_n = sh.acc_n;
         const int cur = sh.cur;
-        const int64_t* AF = cur ? S.acc_f[1] : S.acc_f[0];
-        const double2* AC = cur ? S.acc_c[1] : S.acc_c[0];
+        const auto AF = cur ? S.acc_f[1] : S.acc_f[0];
+        const auto AC = cur ? S.acc_c[1] : S.acc_c[0];
 
         // ---- K3: subtract the prediction of everything already known.
         // predict_buckets (bucketize.cpp:84-93) adds, per known tone in
@@ -227,7 +232,7 @@ __device__ __forceinline__ void decode_signal(const DevPlan& plan, const DecLayo
             // counts, a scan, then a stable fill; lanes of a 32-tone chunk
             // that share a bucket are ranked with __match_any_sync.
             if (tid < 32) {
-                int32_t* cnt = S.order;  // free until K4
+                const auto cnt = S.order;  // free until K4
                 for (int64_t bk = tid; bk < b; bk += 32) cnt[bk] = 0;
                 __syncwarp();
                 for (int j0 = 0; j0 < acc_n; j0 += 32) {
@@ -328,7 +333,7 @@ __device__ __forceinline__ void decode_signal(const DevPlan& plan, const DecLayo
             const bool fl = cta_radix_sort<kThreads>(S.sk[0], S.sv[0], S.sk[1], S.sv[1],
                                                      static_cast<int>(b), 64, sort_smem,
                                                      sort_smem + 16 * kThreads);
-            const int32_t* V = fl ? S.sv[1] : S.sv[0];
+            const auto V = fl ? S.sv[1] : S.sv[0];
             for (int64_t j = tid; j < b; j += kThreads) S.order[j] = V[j];
         } else {
             for (int64_t j = tid; j < b; j += kThreads) {
@@ -351,7 +356,7 @@ __device__ __forceinline__ void decode_signal(const DevPlan& plan, const DecLayo
         // every ranked bucket's round values, staged in shared memory in one
         // pass (the rotation area is free after K3): the locate stages
         // then never wait on L2
-        double2* yr = S.rot;  // free after K3
+        const auto yr = S.rot;  // free after K3
         for (int64_t e = tid; e < budget * nr; e += kThreads) {
             const int64_t rk = e / nr, st = e - rk * nr;
             yr[e] = Y[st * b + S.order[rk]];
@@ -492,8 +497,8 @@ __device__ __forceinline__ void decode_signal(const DevPlan& plan, const DecLayo
         // accepted rank of each f carries the sum; the found set is merged
         // into the ascending acc list (ping-pong buffers).
         const int nxt = cur ^ 1;
-        int64_t* NF = nxt ? S.acc_f[1] : S.acc_f[0];
-        double2* NC = nxt ? S.acc_c[1] : S.acc_c[0];
+        const auto NF = nxt ? S.acc_f[1] : S.acc_f[0];
+        const auto NC = nxt ? S.acc_c[1] : S.acc_c[0];
         if (tid == 0) sh.new_n = 0;
         if (budget > kSmallBudget && sort_smem) {
             // large budgets: stable sort of the accepted ranks by f (equal f
@@ -512,8 +517,8 @@ __device__ __forceinline__ void decode_signal(const DevPlan& plan, const DecLayo
             const bool fl = cta_radix_sort<kThreads>(S.sk[0], S.sv[0], S.sk[1], S.sv[1],
                                                      static_cast<int>(budget), key_bits,
                                                      sort_smem, sort_smem + 16 * kThreads);
-            const uint64_t* Ks = fl ? S.sk[1] : S.sk[0];
-            const int32_t* Vs = fl ? S.sv[1] : S.sv[0];
+            const auto Ks = fl ? S.sk[1] : S.sk[0];
+            const auto Vs = fl ? S.sv[1] : S.sv[0];
             for (int64_t p = tid; p < budget; p += kThreads) {
                 const uint64_t f = Ks[p];
                 if (f >= static_cast<uint64_t>(n) || (p > 0 && Ks[p - 1] == f)) continue;
@@ -665,8 +670,8 @@ __device__ __forceinline__ void decode_signal(const DevPlan& plan, const DecLayo
     // ---- K7: keep the K largest |c| (stable over ascending f), emit in f order
     const int acc_n = sh.acc_n;
     const int cur = sh.cur;
-    const int64_t* AF = cur ? S.acc_f[1] : S.acc_f[0];
-    const double2* AC = cur ? S.acc_c[1] : S.acc_c[0];
+    const auto AF = cur ? S.acc_f[1] : S.acc_f[0];
+    const auto AC = cur ? S.acc_c[1] : S.acc_c[0];
     const int64_t K = plan.k;
     for (int j = tid; j < acc_n; j += kThreads) {
         const double2 c = AC[j];
@@ -686,7 +691,7 @@ __device__ __forceinline__ void decode_signal(const DevPlan& plan, const DecLayo
         gsync();
         const bool fl = cta_radix_sort<kThreads>(S.sk[0], S.sv[0], S.sk[1], S.sv[1], acc_n, 64,
                                                  sort_smem, sort_smem + 16 * kThreads);
-        const int32_t* V = fl ? S.sv[1] : S.sv[0];
+        const auto V = fl ? S.sv[1] : S.sv[0];
         for (int r = tid; r < acc_n && r < K; r += kThreads) S.flag[V[r]] = 1;
         gsync();
         for (int j = tid; j < acc_n; j += kThreads) S.tone_i[j] = S.flag[j];
@@ -695,6 +700,7 @@ __device__ __forceinline__ void decode_signal(const DevPlan& plan, const DecLayo
         for (int j = tid; j < acc_n; j += kThreads) {
             if (!S.tone_i[j]) continue;
             const int64_t pos = S.flag[j];
+            MSFFT_DCHECK(pos >= 0 && pos < K);
             A.out_f[s * K + pos] = AF[j];
             A.out_c[s * K + pos] = AC[j];
         }
@@ -713,6 +719,7 @@ __device__ __forceinline__ void decode_signal(const DevPlan& plan, const DecLayo
             if (!S.tone_i[j]) continue;
             int64_t pos = 0;
             for (int i = 0; i < j; ++i) pos += S.tone_i[i];
+            MSFFT_DCHECK(pos >= 0 && pos < K);
             A.out_f[s * K + pos] = AF[j];
             A.out_c[s * K + pos] = AC[j];
         }

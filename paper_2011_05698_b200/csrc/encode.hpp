@@ -27,6 +27,7 @@ struct DecLayout {
     // large-size scratch (radix sorts), present when big != 0
     int64_t off_sk[2], off_sv[2], off_flag, off_nfs, sort_n;
     int64_t bytes;      // per signal
+    int64_t cap, b_max, budget_max, rounds_max;  // the sizes above (checked builds)
     int32_t in_smem;
     int32_t big;        // large-size paths: sort counters live in shared memory
 };

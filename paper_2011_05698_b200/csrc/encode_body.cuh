@@ -83,6 +83,8 @@ __device__ __forceinline__ void gather_accumulate(const DevPlan& plan, const Enc
                 const int64_t tt = t + u * stride;
                 if (tt <= B) {
                     if (kMode == kLoadCompact) {
+                        MSFFT_DCHECK(task.seg_cpos[sgi] + (tt - A) >= 0 &&
+                                     task.seg_cpos[sgi] + (tt - A) < plan.x_row);
                         v[u] = ld_sample(cbase + tt);
                     } else {
                         const uint32_t src = (sg * static_cast<uint32_t>(tt)) & mask;
@@ -203,7 +205,10 @@ __device__ __forceinline__ void encode_task(const DevPlan& plan, const EncTask& 
             double2* ys = y + s * vps + it.yoff + static_cast<int64_t>(task.r0) * b;
 #pragma unroll
             for (int r = 0; r < kEncRounds; ++r)
-                if (r < nr) ys[static_cast<int64_t>(r) * b + ((c + taus[r]) & (b - 1))] = acc[r];
+                if (r < nr) {
+                    MSFFT_DCHECK(it.yoff + (task.r0 + r + 1) * b <= vps);
+                    ys[static_cast<int64_t>(r) * b + ((c + taus[r]) & (b - 1))] = acc[r];
+                }
         }
         return;
     }

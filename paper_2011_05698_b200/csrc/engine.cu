@@ -160,6 +160,7 @@ Plan::Plan(int64_t n, int64_t k, int64_t l, double q, double delta, bool c128, i
     imap_ = make_ingest_map(sched_);
     dplan_compact_ = dplan_;
     dplan_compact_.x_compact = 1;
+    dplan_compact_.x_row = imap_.per_signal;
     if (const char* e = std::getenv("MSFFT_SPARSE_INGEST")) ingest_enabled_ = std::atoi(e) != 0;
     if (const char* e = std::getenv("MSFFT_INGEST_CHUNK")) ingest_chunk_ = std::max(1LL, std::atoll(e));
     if (const char* e = std::getenv("MSFFT_WIDE_MAX_BATCH")) wide_max_batch_ = std::atoll(e);

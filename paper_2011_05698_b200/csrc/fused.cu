@@ -59,6 +59,8 @@ fused_kernel(const __grid_constant__ DevPlan plan, DecLayout lay, DecArgs args,
             __syncthreads();
             if (threadIdx.x == 0) {
                 __threadfence();
+                // done = counters + 1; the last counter is the exit count
+                MSFFT_DCHECK((t.sig0 / chunk) * plan.iters + t.m + 2 < n_counters);
                 atomicAdd(&done[(t.sig0 / chunk) * plan.iters + t.m], 1);
             }
         } else if (!bad_input) {
@@ -66,6 +68,7 @@ fused_kernel(const __grid_constant__ DevPlan plan, DecLayout lay, DecArgs args,
             // while the later iterations of its chunk are still being encoded
             const int64_t s0 = -static_cast<int64_t>(code) - 1;
             const int64_t c = s0 / chunk;
+            MSFFT_DCHECK(s0 < batch && (c + 1) * plan.iters + 2 <= n_counters);
             DecArgs a = args;
             a.gate_done = done + c * plan.iters;
             a.gate_need = need + c * plan.iters;

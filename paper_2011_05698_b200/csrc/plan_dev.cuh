@@ -50,6 +50,7 @@ struct DevPlan {
     // 1: x rows hold the compact samples of sparse host ingest (ingest.hpp):
     // the sample of t' is x[task.seg_cpos[seg] + (t' - seg_lo[seg])]
     int32_t x_compact;
+    int64_t x_row;  // compact mode: samples per compact row (bounds checks)
     DevIter it[kMaxIters];
     int64_t taus[kMaxTaus];
 };

@@ -106,6 +106,7 @@ __global__ void k3_scatter(const DevPlan* __restrict__ P, int m, const int32_t* 
         const int d = static_cast<int>(e - j * 3);
         const int64_t beta = (tone_i[j] - 1 + d) & (b - 1);
         const int32_t pos = start[beta] + atomicAdd(&cursor[beta], 1);
+        MSFFT_DCHECK(pos >= 0 && pos < total && total <= 3 * P->acc_cap);
         ev[pos] = static_cast<int32_t>(j * 4 + d);
     }
 }
@@ -445,7 +446,10 @@ k4_rank(const int32_t* __restrict__ sel_idx, int64_t budget, const double* __res
 
 __global__ void k4_scatter(const int32_t* __restrict__ sel_idx, const int32_t* __restrict__ rank,
                            int64_t budget, int32_t* __restrict__ order) {
-    GRID_LOOP(e, budget) order[rank[e]] = sel_idx[e];
+    GRID_LOOP(e, budget) {
+        MSFFT_DCHECK(rank[e] >= 0 && rank[e] < budget);
+        order[rank[e]] = sel_idx[e];
+    }
 }
 
 // b <= 1024: the whole selection in one CTA -- |y0| (NaN -> -1), stable rank
@@ -873,12 +877,14 @@ k6_small(const DevPlan* __restrict__ P, int m, const int64_t* __restrict__ cand_
     }
     __syncthreads();
     if (tid == 0) {
+        MSFFT_DCHECK(an + nnew <= P->acc_cap);
         scal[0] = an + nnew;
         scal[4] = 0;
     }
 }
 
-__global__ void k6_count(int32_t* scal) {
+__global__ void k6_count(int32_t* scal, int64_t acc_cap) {
+    MSFFT_DCHECK(scal[0] + scal[1] <= acc_cap);
     scal[0] += scal[1];  // acc_n += new_n
     scal[4] = 0;         // accepted counter for the next iteration
 }
@@ -895,6 +901,7 @@ __global__ void k7_emit(const int32_t* __restrict__ sel_idx, const int32_t* __re
     const int64_t keep = scal[2];
     GRID_LOOP(p, keep) {
         const int32_t j = sel_idx[p];
+        MSFFT_DCHECK(j >= 0 && j < scal[0]);
         out_f[p] = AF[j];
         out_c[p] = AC[j];
     }
@@ -1109,7 +1116,7 @@ void WideDecoder::enqueue(double2* y, const int64_t* sigma, const int64_t* sigma
                                                          naccepted, newflag_.get(), newpos_.get(),
                                                          cand_sum_.get(), acc_f_[nxt].get(),
                                                          acc_c_[nxt].get());
-            k6_count<<<1, 1, 0, st>>>(scal_.get());
+            k6_count<<<1, 1, 0, st>>>(scal_.get(), acc_cap_);
         }
         MSFFT_LAUNCH_CHECK("wide K6");
     }

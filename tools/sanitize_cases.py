@@ -1,13 +1,13 @@
-"""Small cases that drive every kernel path once, for compute-sanitizer:
+"""Small cases that drive every kernel path once, for the checked build
+(compute-sanitizer is closed on the GPU pool):
 
-    compute-sanitizer --tool memcheck|racecheck|synccheck|initcheck \
-        --error-exitcode 9 python tools/sanitize_cases.py [case ...]
+    python tools/build_variant.py checked -DMSFFT_CHECKED
+    MSFFT_B200_LIB=tools/variants/lib_checked.so python tools/sanitize_cases.py [case ...]
 
 Cases (all by default): fused batch, serial encode/decode, one-CTA large-size
 decode, wide decode, sparse host ingest, async + PDL chain, window designer,
-signal helpers, phase Monte Carlo.  Sizes are chosen so each case needs
-seconds of GPU work natively (sanitizers run 10-100x slower) while still
-reaching the code path named (large-size layout, shared-memory FFT, ...).
+signal helpers, phase Monte Carlo.  Sizes are small (the whole run takes
+seconds) while still reaching the code path named.
 """
 import os
 import sys
