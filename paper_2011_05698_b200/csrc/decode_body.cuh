@@ -416,55 +416,109 @@ __device__ __forceinline__ void decode_signal(const DevPlan& plan, const DecLayo
             if (ok && y0.x == 0.0 && y0.y == 0.0) ok = false;
             double u_min = (2.0 * static_cast<double>(beta) - 1.0) * Ld / 2.0;
             double len = Ld;
-            int stage = 0;
             const int nst = it.nstage_tab;  // host-precomputed stage lengths (or -1)
-            while (nst >= 0 ? stage < nst : len > 1.0 + 1e-9) {
-                ++stage;
-                if (stage >= nr) {  // cannot happen for sfft4's own tau plans
-                    if (ok && glane == 0) atomicCAS(A.err, 0, kDecErrRounds);
-                    ok = false;
-                    break;  // uniform: every group sees the same stage count
-                }
-                double phi = 0.0;
-                if (ok) {
-                    const int64_t pe = rank * ns + (stage - 1);
-                    const int code = S.pcode[pe];
-                    if (code == 1) {
-                        ok = false;  // locate_frequency returns nullopt
-                    } else {
-                        if (code == 2) {  // phase_of throws
-                            if (glane == 0) atomicCAS(A.err, 0, kDecErrPhaseZero);
-                            ok = false;
+            if (nst >= 0 && nst < nr) {
+                // the usual case: the stage count and every stage's operands
+                // are known up front, so the next stage's phase code, phase,
+                // tau, block width and length load while this stage runs;
+                // only center -> phase -> distance -> argmin -> u_min stays
+                // on the dependent chain.  Same operations as the loop below.
+                const int64_t pe0 = rank * ns;
+                int code_n = live && nst > 0 ? S.pcode[pe0] : 1;
+                double phi_n = live && nst > 0 ? S.phi[pe0] : 0.0;
+                double rblk_n = sh.st_blk[0], len_n = sh.st_len[1];
+                int64_t tau_n = tau_at(1);
+                for (int stage = 1; stage <= nst; ++stage) {
+                    const int code = code_n;
+                    const double phi = phi_n, rblk = rblk_n, nlen = len_n;
+                    const int64_t tau = tau_n;
+                    if (stage < nst) {
+                        if (live) {
+                            code_n = S.pcode[pe0 + stage];
+                            phi_n = S.phi[pe0 + stage];
                         }
-                        phi = S.phi[pe];
+                        rblk_n = sh.st_blk[stage];
+                        len_n = sh.st_len[stage + 1];
+                        tau_n = tau_at(stage + 1);
                     }
-                }
-                const int64_t tau = tau_at(stage);
-                const double rblk =
-                    nst >= 0 ? sh.st_blk[stage - 1] : len / static_cast<double>(lcfg);
-                double best_d = INFINITY;
-                int best_j = 0x7fffffff;
-                for (int64_t j = glane; j < lcfg; j += gsz) {
-                    const double center = u_min + (static_cast<double>(j) + 0.5) * rblk;
-                    const double d = circular_phase_distance(
-                        position_phase(center, tau, n, inv_n), phi);
-                    if (d < best_d) {
-                        best_d = d;
-                        best_j = static_cast<int>(j);
+                    if (ok && code != 0) {
+                        // 1: locate_frequency returns nullopt; 2: phase_of throws
+                        if (code == 2 && glane == 0) atomicCAS(A.err, 0, kDecErrPhaseZero);
+                        ok = false;
                     }
-                }
-                // lowest block index wins ties (strict < in ascending order)
-                for (int o = gsz >> 1; o > 0; o >>= 1) {
-                    const double od = __shfl_xor_sync(0xffffffffu, best_d, o);
-                    const int oj = __shfl_xor_sync(0xffffffffu, best_j, o);
-                    if (od < best_d || (od == best_d && oj < best_j)) {
-                        best_d = od;
-                        best_j = oj;
+                    double best_d = INFINITY;
+                    int best_j = 0x7fffffff;
+                    for (int64_t j = glane; j < lcfg; j += gsz) {
+                        const double center = u_min + (static_cast<double>(j) + 0.5) * rblk;
+                        const double d = circular_phase_distance(
+                            position_phase(center, tau, n, inv_n), phi);
+                        if (d < best_d) {
+                            best_d = d;
+                            best_j = static_cast<int>(j);
+                        }
                     }
+                    for (int o = gsz >> 1; o > 0; o >>= 1) {
+                        const double od = __shfl_xor_sync(0xffffffffu, best_d, o);
+                        const int oj = __shfl_xor_sync(0xffffffffu, best_j, o);
+                        if (od < best_d || (od == best_d && oj < best_j)) {
+                            best_d = od;
+                            best_j = oj;
+                        }
+                    }
+                    if (best_j == 0x7fffffff) best_j = 0;
+                    u_min = u_min + (static_cast<double>(best_j) - q / 2.0) * rblk;
+                    len = nlen;
                 }
-                if (best_j == 0x7fffffff) best_j = 0;  // all distances NaN: reference keeps 0
-                u_min = u_min + (static_cast<double>(best_j) - q / 2.0) * rblk;
-                len = nst >= 0 ? sh.st_len[stage] : len * (q + 1.0) / static_cast<double>(lcfg);
+            } else {
+                int stage = 0;
+                while (nst >= 0 ? stage < nst : len > 1.0 + 1e-9) {
+                    ++stage;
+                    if (stage >= nr) {  // cannot happen for sfft4's own tau plans
+                        if (ok && glane == 0) atomicCAS(A.err, 0, kDecErrRounds);
+                        ok = false;
+                        break;  // uniform: every group sees the same stage count
+                    }
+                    double phi = 0.0;
+                    if (ok) {
+                        const int64_t pe = rank * ns + (stage - 1);
+                        const int code = S.pcode[pe];
+                        if (code == 1) {
+                            ok = false;  // locate_frequency returns nullopt
+                        } else {
+                            if (code == 2) {  // phase_of throws
+                                if (glane == 0) atomicCAS(A.err, 0, kDecErrPhaseZero);
+                                ok = false;
+                            }
+                            phi = S.phi[pe];
+                        }
+                    }
+                    const int64_t tau = tau_at(stage);
+                    const double rblk =
+                        nst >= 0 ? sh.st_blk[stage - 1] : len / static_cast<double>(lcfg);
+                    double best_d = INFINITY;
+                    int best_j = 0x7fffffff;
+                    for (int64_t j = glane; j < lcfg; j += gsz) {
+                        const double center = u_min + (static_cast<double>(j) + 0.5) * rblk;
+                        const double d = circular_phase_distance(
+                            position_phase(center, tau, n, inv_n), phi);
+                        if (d < best_d) {
+                            best_d = d;
+                            best_j = static_cast<int>(j);
+                        }
+                    }
+                    // lowest block index wins ties (strict < in ascending order)
+                    for (int o = gsz >> 1; o > 0; o >>= 1) {
+                        const double od = __shfl_xor_sync(0xffffffffu, best_d, o);
+                        const int oj = __shfl_xor_sync(0xffffffffu, best_j, o);
+                        if (od < best_d || (od == best_d && oj < best_j)) {
+                            best_d = od;
+                            best_j = oj;
+                        }
+                    }
+                    if (best_j == 0x7fffffff) best_j = 0;  // all distances NaN: reference keeps 0
+                    u_min = u_min + (static_cast<double>(best_j) - q / 2.0) * rblk;
+                    len = nst >= 0 ? sh.st_len[stage] : len * (q + 1.0) / static_cast<double>(lcfg);
+                }
             }
             if (ok) {
                 const double lo = u_min, hi = u_min + len;
