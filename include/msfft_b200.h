@@ -293,6 +293,45 @@ int msfft_trace(const void* x, int64_t n, int32_t dtype, int64_t k, int64_t l, d
                 int64_t* sel_f, double* sel_value, int64_t cap, int64_t* out_f, double* out_c,
                 int64_t* out_count, char* err, size_t errlen);
 
+/* ---- the reference's component API on the path --------------
+ * Batched device versions of the functions the reference's own tests call
+ * directly.  `location` flags say where each array lives (MSFFT_HOST or
+ * MSFFT_DEVICE); complex arrays are interleaved (re, im) doubles.
+ *
+ * bucketize (proj/src/bucketize.cpp:50-61, bucketize.hpp:63-86) of one
+ * signal x (n samples, dtype) under `rounds` permutations (sigma[r], tau[r])
+ * (host arrays) with the window (n, b, delta): values [rounds][b], bit-equal
+ * to the reference; *samples_read = w. */
+int msfft_bucketize(const void* x, int64_t n, int32_t dtype, int32_t x_location, int64_t b,
+                    double delta, const int64_t* sigma, const int64_t* tau, int64_t rounds,
+                    double* values, int32_t values_location, int64_t* samples_read, char* err,
+                    size_t errlen);
+/* predict_buckets (bucketize.cpp:70-95) of `count` known tones (f strictly
+ * ascending in [0, n), c) for each (sigma[r], tau[r]): values [rounds][b].
+ * f, c and values are in `location`. */
+int msfft_predict_buckets(int64_t n, int64_t b, double delta, const int64_t* f, const double* c,
+                          int64_t count, const int64_t* sigma, const int64_t* tau,
+                          int64_t rounds, double* values, int32_t location, char* err,
+                          size_t errlen);
+/* locate_frequency (proj/src/locate.cpp:83-123) of `count` buckets against
+ * one round set: rounds [nrounds][b] (round r bucketized with tau[r], host
+ * array; tau[0] must be 0), config (l, q).  Per bucket: u, stages and status
+ * (0 located, 1 nullopt: a needed bucket value is exactly zero).  A zero
+ * quotient raises MSFFT_ERR_DOMAIN "phase_of: zero value" as the
+ * reference's phase_of throws.  buckets/rounds/u/stages/status in
+ * `location`. */
+int msfft_locate_frequency(int64_t n, int64_t b, int64_t l, double q, const int64_t* buckets,
+                           int64_t count, const double* rounds, const int64_t* tau,
+                           int64_t nrounds, int64_t* u, int32_t* stages, int32_t* status,
+                           int32_t location, char* err, size_t errlen);
+/* estimate_value (proj/src/sfft4.cpp:27-36) of `count` (y0, u) pairs with the
+ * window (n, b, delta): out = y0 / G_{iL-u}; status 1 where |G| < 0.5 (the
+ * reference throws std::domain_error "estimate_value: located position
+ * outside the pass region").  y0/u/out/status in `location`. */
+int msfft_estimate_values(int64_t n, int64_t b, double delta, const double* y0, const int64_t* u,
+                          int64_t count, double* out, int32_t* status, int32_t location,
+                          char* err, size_t errlen);
+
 #ifdef __cplusplus
 }
 #endif

@@ -9,7 +9,9 @@
 // callers use around the transform: signal.hpp:31-70 (dft_dense,
 // idft_dense, synthesize, generate_test_signal, add_awgn, error_metrics),
 // io.hpp:11-17 (signal files, truth CSV), phase_mc.hpp:19-56
-// (run_phase_experiment) and bench.cpp:33-46 (top_k_spectrum).  A caller of the reference
+// (run_phase_experiment) and bench.cpp:33-46 (top_k_spectrum) -- and the
+// component API on the path (get_flat_window, bucketize, predict_buckets,
+// subtract, locate_frequency, estimate_value).  A caller of the reference
 // switches by including this header and linking libmsfft_b200.so; defining
 // MSFFT_B200_AS_MSFFT before the include also makes `msfft::` name these
 // types (only when the reference headers are not included in the same TU).
@@ -18,6 +20,8 @@
 #include <complex>
 #include <cstdint>
 #include <map>
+#include <memory>
+#include <optional>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -325,6 +329,155 @@ inline std::vector<PhaseErrorHistogram> run_phase_experiment(int64_t n, int64_t 
         out.push_back(std::move(h));
     }
     return out;
+}
+
+// ---- component API on the path (bucketize.hpp:56-95, locate.hpp:75-78,
+// sfft4.hpp:50): the functions the reference's own tests call directly ------
+
+struct FlatWindow {  // window.hpp:16-30 (taps as designed; G_d lives on the device)
+    int64_t n = 0, b = 0, l_width = 0, w = 0;
+    double delta = 0.0;
+    std::vector<double> g_time;
+};
+
+struct PermutationParams {  // bucketize.hpp:16-20
+    int64_t sigma = 1, sigma_inv = 1, tau = 0;
+};
+
+struct BucketSet {  // bucketize.hpp:24-30
+    int64_t n = 0, b = 0;
+    std::vector<cplx> values;
+    PermutationParams params;
+    int64_t samples_read = 0;
+};
+
+struct LocateOutcome {  // locate.hpp:42-45
+    int64_t u = 0;
+    int stages = 0;
+};
+
+// get_flat_window (window.cpp:179-193): designed on the GPU, bit-identical taps.
+inline std::shared_ptr<const FlatWindow> get_flat_window(int64_t n, int64_t b, double delta) {
+    auto win = std::make_shared<FlatWindow>();
+    char err[1024] = {0};
+    int64_t w = 0;
+    throw_status(msfft_window(n, b, delta, -1, &w, nullptr, 0, err, sizeof(err)), err);
+    win->g_time.resize(static_cast<size_t>(w));
+    throw_status(msfft_window(n, b, delta, -1, &w, win->g_time.data(), w, err, sizeof(err)), err);
+    win->n = n;
+    win->b = b;
+    win->l_width = n / b;
+    win->w = w;
+    win->delta = delta;
+    return win;
+}
+
+// bucketize of one signal under several permutations in one launch.
+inline std::vector<BucketSet> bucketize_rounds(const ComplexSignal& x, const FlatWindow& win,
+                                               const std::vector<PermutationParams>& params) {
+    if (x.n != win.n) throw std::invalid_argument("bucketize: signal/window size mismatch");
+    std::vector<int64_t> sg, tu;
+    for (const auto& p : params) {
+        sg.push_back(p.sigma);
+        tu.push_back(p.tau);
+    }
+    std::vector<cplx> vals(params.size() * static_cast<size_t>(win.b));
+    int64_t w = 0;
+    char err[1024] = {0};
+    throw_status(msfft_bucketize(x.samples.data(), x.n, MSFFT_C128, MSFFT_HOST, win.b, win.delta,
+                                 sg.data(), tu.data(), static_cast<int64_t>(params.size()),
+                                 reinterpret_cast<double*>(vals.data()), MSFFT_HOST, &w, err,
+                                 sizeof(err)),
+                 err);
+    std::vector<BucketSet> out(params.size());
+    for (size_t r = 0; r < params.size(); ++r) {
+        out[r].n = x.n;
+        out[r].b = win.b;
+        out[r].values.assign(vals.begin() + r * win.b, vals.begin() + (r + 1) * win.b);
+        out[r].params = params[r];
+        out[r].samples_read = w;
+    }
+    return out;
+}
+
+inline BucketSet bucketize(const ComplexSignal& x, const FlatWindow& win,
+                           const PermutationParams& params) {
+    return bucketize_rounds(x, win, {params})[0];
+}
+
+inline BucketSet predict_buckets(const SparseSpectrum& known, const FlatWindow& win,
+                                 const PermutationParams& params) {
+    if (known.n != win.n) throw std::invalid_argument("predict_buckets: size mismatch");
+    std::vector<int64_t> f;
+    std::vector<double> c;
+    detail::spectrum_arrays(known, f, c);
+    BucketSet out;
+    out.n = win.n;
+    out.b = win.b;
+    out.values.resize(static_cast<size_t>(win.b));
+    out.params = params;
+    char err[1024] = {0};
+    throw_status(msfft_predict_buckets(win.n, win.b, win.delta, f.data(), c.data(),
+                                       static_cast<int64_t>(f.size()), &params.sigma,
+                                       &params.tau, 1, reinterpret_cast<double*>(out.values.data()),
+                                       MSFFT_HOST, err, sizeof(err)),
+                 err);
+    return out;
+}
+
+inline BucketSet subtract(const BucketSet& a, const BucketSet& b_set) {  // bucketize.cpp:97-104
+    if (a.b != b_set.b || a.n != b_set.n || a.params.sigma != b_set.params.sigma ||
+        a.params.tau != b_set.params.tau)
+        throw std::invalid_argument("subtract: bucket sets are not from the same round");
+    BucketSet out = a;
+    for (size_t i = 0; i < out.values.size(); ++i) out.values[i] -= b_set.values[i];
+    return out;
+}
+
+// locate_frequency for many buckets against one round set (one launch).
+inline std::vector<std::optional<LocateOutcome>> locate_frequencies(
+    const std::vector<int64_t>& buckets, const std::vector<BucketSet>& rounds,
+    const MultiscaleConfig& cfg, const FlatWindow& win) {
+    if (rounds.empty()) throw std::invalid_argument("locate_frequency: no rounds");
+    std::vector<cplx> vals;
+    std::vector<int64_t> tau;
+    for (const auto& r : rounds) {
+        vals.insert(vals.end(), r.values.begin(), r.values.end());
+        tau.push_back(r.params.tau);
+    }
+    std::vector<int64_t> u(buckets.size());
+    std::vector<int32_t> st(buckets.size()), status(buckets.size());
+    char err[1024] = {0};
+    throw_status(msfft_locate_frequency(win.n, win.b, cfg.l, cfg.q, buckets.data(),
+                                        static_cast<int64_t>(buckets.size()),
+                                        reinterpret_cast<const double*>(vals.data()), tau.data(),
+                                        static_cast<int64_t>(rounds.size()), u.data(), st.data(),
+                                        status.data(), MSFFT_HOST, err, sizeof(err)),
+                 err);
+    std::vector<std::optional<LocateOutcome>> out(buckets.size());
+    for (size_t i = 0; i < buckets.size(); ++i)
+        if (status[i] == 0) out[i] = LocateOutcome{u[i], st[i]};
+    return out;
+}
+
+inline std::optional<LocateOutcome> locate_frequency(int64_t bucket,
+                                                     const std::vector<BucketSet>& rounds,
+                                                     const MultiscaleConfig& cfg,
+                                                     const FlatWindow& win) {
+    return locate_frequencies({bucket}, rounds, cfg, win)[0];
+}
+
+inline cplx estimate_value(cplx y0_bucket, int64_t u, const FlatWindow& win) {
+    double out[2] = {0.0, 0.0};
+    int32_t status = 0;
+    char err[1024] = {0};
+    throw_status(msfft_estimate_values(win.n, win.b, win.delta,
+                                       reinterpret_cast<const double*>(&y0_bucket), &u, 1, out,
+                                       &status, MSFFT_HOST, err, sizeof(err)),
+                 err);
+    if (status != 0)
+        throw std::domain_error("estimate_value: located position outside the pass region");
+    return cplx(out[0], out[1]);
 }
 
 }  // namespace msfft_b200

@@ -31,7 +31,8 @@ EXPORTED = (
     "msfft_add_awgn", "msfft_dft_dense", "msfft_idft_dense", "msfft_top_k_spectrum",
     "msfft_error_metrics", "msfft_signal_file_length", "msfft_read_signal_file",
     "msfft_write_signal_file", "msfft_write_truth_csv", "msfft_read_truth_csv",
-    "msfft_phase_experiment", "msfft_plan_sync",
+    "msfft_phase_experiment", "msfft_plan_sync", "msfft_bucketize", "msfft_predict_buckets",
+    "msfft_locate_frequency", "msfft_estimate_values",
 )
 
 i64, u64, f64, i32, u32 = C.c_int64, C.c_uint64, C.c_double, C.c_int32, C.c_uint32
@@ -139,6 +140,16 @@ def lib() -> C.CDLL:
                    "msfft_dft_dense", "msfft_idft_dense", "msfft_top_k_spectrum",
                    "msfft_error_metrics", "msfft_signal_file_length", "msfft_read_signal_file",
                    "msfft_write_signal_file", "msfft_write_truth_csv", "msfft_read_truth_csv"):
+            getattr(L, fn).restype = C.c_int
+    if hasattr(L, "msfft_bucketize"):  # component API
+        L.msfft_bucketize.argtypes = [VP, i64, i32, i32, i64, f64, VP, VP, i64, VP, i32,
+                                      P(i64)] + E
+        L.msfft_predict_buckets.argtypes = [i64, i64, f64, VP, VP, i64, VP, VP, i64, VP, i32] + E
+        L.msfft_locate_frequency.argtypes = [i64, i64, i64, f64, VP, i64, VP, VP, i64, VP, VP,
+                                             VP, i32] + E
+        L.msfft_estimate_values.argtypes = [i64, i64, f64, VP, VP, i64, VP, VP, i32] + E
+        for fn in ("msfft_bucketize", "msfft_predict_buckets", "msfft_locate_frequency",
+                   "msfft_estimate_values"):
             getattr(L, fn).restype = C.c_int
     L.msfft_window.argtypes = [i64, i64, f64, i32, P(i64), P(f64), i64] + E
     L.msfft_window_response.argtypes = [i64, i64, f64, i32, P(i64), i64, P(f64)] + E

@@ -21,7 +21,7 @@ LIB = os.path.join(HERE, "libmsfft_b200.so")
 CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
 CU_SOURCES = ["fft.cu", "window.cu", "sigma.cu", "encode.cu", "decode.cu", "fused.cu", "engine.cu",
-              "signal_ops.cu", "phase_mc.cu", "wide_decode.cu"]
+              "signal_ops.cu", "phase_mc.cu", "wide_decode.cu", "components.cu"]
 CXX_SOURCES = ["host_plan.cpp", "ingest.cpp", "signal_io.cpp", "capi.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC",

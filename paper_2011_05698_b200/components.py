@@ -1,0 +1,215 @@
+"""The reference's component API on the sfft4 path: the
+functions its own tests call directly, each on the GPU through the C ABI.
+
+    bucketize         proj/src/bucketize.cpp:50-61 (bucketize.hpp:63-86)
+    predict_buckets   proj/src/bucketize.cpp:70-95
+    subtract          proj/src/bucketize.cpp:97-104 (host, elementwise)
+    locate_frequency  proj/src/locate.cpp:83-123
+    estimate_value    proj/src/sfft4.cpp:27-36
+
+Types mirror the reference: PermutationParams (bucketize.hpp:16-20),
+BucketSet (:24-30), LocateOutcome (locate.hpp:42-45), and FlatWindow as a
+handle on the device window cache (n, b, delta; window.hpp:16-30).  The
+batched forms (bucketize_rounds, locate_frequencies, estimate_values) are the
+same functions over many rounds / buckets in one launch.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import DomainError, InvalidArgument, MultiscaleConfig, SparseSpectrum, _raise
+from . import _lib as _L
+from .signal import _buf
+
+__all__ = ["FlatWindow", "PermutationParams", "BucketSet", "LocateOutcome", "flat_window",
+           "bucketize", "bucketize_rounds", "predict_buckets", "subtract", "locate_frequency",
+           "locate_frequencies", "estimate_value", "estimate_values", "tau_plan", "sigma_plan"]
+
+
+def _err():
+    return C.create_string_buffer(1024)
+
+
+@dataclass(frozen=True)
+class FlatWindow:
+    """Handle on the designed window (n, b, delta); w = support."""
+    n: int
+    b: int
+    delta: float
+    w: int
+
+    @property
+    def l_width(self) -> int:
+        return self.n // self.b
+
+
+def flat_window(n: int, b: int, delta: float) -> FlatWindow:
+    """get_flat_window (window.cpp:179-193): designs (or reuses) the window on
+    the current device; infeasible parameters raise the reference's errors."""
+    from . import window
+    w, _ = window(n, b, delta)
+    return FlatWindow(int(n), int(b), float(delta), int(w))
+
+
+@dataclass(frozen=True)
+class PermutationParams:
+    sigma: int
+    sigma_inv: int = 0
+    tau: int = 0
+
+
+@dataclass
+class BucketSet:
+    n: int
+    b: int
+    values: np.ndarray                 # complex128 [b]
+    params: PermutationParams = field(default_factory=PermutationParams)
+    samples_read: int = 0
+
+
+@dataclass(frozen=True)
+class LocateOutcome:
+    u: int
+    stages: int
+
+
+def _cx_host(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.complex128))
+
+
+def bucketize_rounds(x, win: FlatWindow, params) -> list[BucketSet]:
+    """bucketize of one signal x (numpy or CUDA torch, complex64/128, n
+    samples) under every PermutationParams in `params`, in one launch."""
+    params = list(params)
+    ptr, loc, code, keep = _buf(x)
+    if code is None:
+        raise InvalidArgument("bucketize: x must be complex")
+    n = int(keep.shape[-1])
+    if n != win.n:
+        raise InvalidArgument("bucketize: signal/window size mismatch")
+    sig = np.array([p.sigma for p in params], np.int64)
+    tau = np.array([p.tau for p in params], np.int64)
+    out = np.zeros((len(params), win.b), np.complex128)
+    w = C.c_int64()
+    e = _err()
+    _raise(_L.lib().msfft_bucketize(ptr, n, code, loc, win.b, win.delta,
+                                    C.c_void_p(sig.ctypes.data), C.c_void_p(tau.ctypes.data),
+                                    len(params), C.c_void_p(out.ctypes.data), _L.MSFFT_HOST,
+                                    C.byref(w), e, 1024), e)
+    return [BucketSet(n, win.b, out[r], p, int(w.value)) for r, p in enumerate(params)]
+
+
+def bucketize(x, win: FlatWindow, params: PermutationParams) -> BucketSet:
+    return bucketize_rounds(x, win, [params])[0]
+
+
+def predict_buckets(known: SparseSpectrum, win: FlatWindow, params) -> BucketSet | list:
+    """predict_buckets for one PermutationParams (-> BucketSet) or a list of
+    them (-> list, one launch)."""
+    if known.n != win.n:
+        raise InvalidArgument("predict_buckets: size mismatch")
+    many = isinstance(params, (list, tuple))
+    plist = list(params) if many else [params]
+    f = np.ascontiguousarray(np.asarray(known.positions, np.int64))
+    c = _cx_host(known.coeffs)
+    sig = np.array([p.sigma for p in plist], np.int64)
+    tau = np.array([p.tau for p in plist], np.int64)
+    out = np.zeros((len(plist), win.b), np.complex128)
+    e = _err()
+    _raise(_L.lib().msfft_predict_buckets(win.n, win.b, win.delta, C.c_void_p(f.ctypes.data),
+                                          C.c_void_p(c.ctypes.data), f.size,
+                                          C.c_void_p(sig.ctypes.data),
+                                          C.c_void_p(tau.ctypes.data), len(plist),
+                                          C.c_void_p(out.ctypes.data), _L.MSFFT_HOST, e, 1024), e)
+    sets = [BucketSet(win.n, win.b, out[r], p, 0) for r, p in enumerate(plist)]
+    return sets if many else sets[0]
+
+
+def subtract(a: BucketSet, b_set: BucketSet) -> BucketSet:
+    """bucketize.cpp:97-104."""
+    if (a.b != b_set.b or a.n != b_set.n or a.params.sigma != b_set.params.sigma or
+            a.params.tau != b_set.params.tau):
+        raise InvalidArgument("subtract: bucket sets are not from the same round")
+    return BucketSet(a.n, a.b, np.asarray(a.values) - np.asarray(b_set.values), a.params,
+                     a.samples_read)
+
+
+def locate_frequencies(buckets, rounds: list[BucketSet], cfg: MultiscaleConfig,
+                       win: FlatWindow) -> list:
+    """locate_frequency for every bucket in `buckets` against one round set
+    (one launch): a LocateOutcome or None (nullopt) per bucket."""
+    cfg = cfg or MultiscaleConfig()
+    bk = np.ascontiguousarray(np.asarray(list(buckets), np.int64))
+    if not rounds:
+        raise InvalidArgument("locate_frequency: no rounds")
+    vals = np.ascontiguousarray(np.stack([_cx_host(r.values) for r in rounds]))
+    tau = np.array([r.params.tau for r in rounds], np.int64)
+    u = np.zeros(bk.size, np.int64)
+    st = np.zeros(bk.size, np.int32)
+    status = np.zeros(bk.size, np.int32)
+    e = _err()
+    _raise(_L.lib().msfft_locate_frequency(win.n, win.b, int(cfg.l), float(cfg.q),
+                                           C.c_void_p(bk.ctypes.data), bk.size,
+                                           C.c_void_p(vals.ctypes.data),
+                                           C.c_void_p(tau.ctypes.data), len(rounds),
+                                           C.c_void_p(u.ctypes.data), C.c_void_p(st.ctypes.data),
+                                           C.c_void_p(status.ctypes.data), _L.MSFFT_HOST, e,
+                                           1024), e)
+    return [LocateOutcome(int(u[i]), int(st[i])) if status[i] == 0 else None
+            for i in range(bk.size)]
+
+
+def locate_frequency(bucket: int, rounds: list[BucketSet], cfg: MultiscaleConfig,
+                     win: FlatWindow):
+    return locate_frequencies([bucket], rounds, cfg, win)[0]
+
+
+def estimate_values(y0, u, win: FlatWindow):
+    """estimate_value over arrays: (values, ok) with ok False where the
+    reference throws (|G| < 0.5)."""
+    y = _cx_host(np.atleast_1d(y0))
+    uu = np.ascontiguousarray(np.atleast_1d(np.asarray(u, np.int64)))
+    out = np.zeros(y.size, np.complex128)
+    status = np.zeros(y.size, np.int32)
+    e = _err()
+    _raise(_L.lib().msfft_estimate_values(win.n, win.b, win.delta, C.c_void_p(y.ctypes.data),
+                                          C.c_void_p(uu.ctypes.data), y.size,
+                                          C.c_void_p(out.ctypes.data),
+                                          C.c_void_p(status.ctypes.data), _L.MSFFT_HOST, e,
+                                          1024), e)
+    return out, status == 0
+
+
+def estimate_value(y0: complex, u: int, win: FlatWindow) -> complex:
+    v, ok = estimate_values([y0], [u], win)
+    if not ok[0]:
+        raise DomainError("estimate_value: located position outside the pass region")
+    return complex(v[0])
+
+
+def tau_plan(l_width: int, n: int, cfg: MultiscaleConfig | None = None) -> list[int]:
+    """{0, tau_1..tau_R} of an iteration (stage_count + tau_schedule,
+    sfft4.cpp:49-55), host-side like the reference."""
+    cfg = cfg or MultiscaleConfig()
+    taus = np.zeros(64, np.int64)
+    rounds = C.c_int32()
+    e = _err()
+    _raise(_L.lib().msfft_tau_plan(float(l_width), int(n), int(cfg.l), float(cfg.q),
+                                   taus.ctypes.data_as(C.POINTER(C.c_int64)), taus.size,
+                                   C.byref(rounds), e, 1024), e)
+    return [int(t) for t in taus[:rounds.value]]
+
+
+def sigma_plan(seed: int, n: int, iterations: int) -> list[PermutationParams]:
+    """random_params(n, Rng(seed), 0) for the first `iterations` iterations
+    of a transform seeded `seed` (bucketize.cpp:39-48, sfft4.cpp:48)."""
+    s = np.zeros(iterations, np.int64)
+    si = np.zeros(iterations, np.int64)
+    e = _err()
+    _raise(_L.lib().msfft_sigma_plan(int(seed) & (2**64 - 1), int(n), int(iterations),
+                                     s.ctypes.data_as(C.POINTER(C.c_int64)),
+                                     si.ctypes.data_as(C.POINTER(C.c_int64)), e, 1024), e)
+    return [PermutationParams(int(a), int(b), 0) for a, b in zip(s, si)]

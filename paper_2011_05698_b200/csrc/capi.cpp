@@ -10,6 +10,7 @@
 #include <vector>
 
 #include "../../include/msfft_b200.h"
+#include "components.hpp"
 #include "engine.hpp"
 #include "host_plan.hpp"
 #include "phase_mc.hpp"
@@ -559,6 +560,117 @@ int msfft_phase_experiment(int64_t n, int64_t k, int64_t b, const double* snr_li
                     d.true_phi = a.true_phi;
                 }
         }
+    });
+}
+
+
+int msfft_bucketize(const void* x, int64_t n, int32_t dtype, int32_t x_location, int64_t b,
+                    double delta, const int64_t* sigma, const int64_t* tau, int64_t rounds,
+                    double* values, int32_t values_location, int64_t* samples_read, char* err,
+                    size_t errlen) {
+    return guarded(err, errlen, [&] {
+        require_device();
+        const size_t esz = elem_of(dtype);
+        if (n < 4 || !is_pow2_u(static_cast<uint64_t>(n)))
+            throw std::invalid_argument("ComplexSignal: n must be a power of two >= 4");
+        if (rounds < 1) throw std::invalid_argument("bucketize: rounds must be >= 1");
+        DeviceView in(const_cast<void*>(x), static_cast<size_t>(n) * esz,
+                      x_location == MSFFT_DEVICE, true);
+        DeviceView out(values, static_cast<size_t>(rounds * b) * 16,
+                       values_location == MSFFT_DEVICE, false);
+        const int64_t w = bucketize_device(in.dev, dtype == MSFFT_C128, n, b, delta, sigma, tau,
+                                           rounds, static_cast<double2*>(out.dev), nullptr);
+        out.write_back();
+        if (samples_read) *samples_read = w;
+    });
+}
+
+int msfft_predict_buckets(int64_t n, int64_t b, double delta, const int64_t* f, const double* c,
+                          int64_t count, const int64_t* sigma, const int64_t* tau,
+                          int64_t rounds, double* values, int32_t location, char* err,
+                          size_t errlen) {
+    return guarded(err, errlen, [&] {
+        require_device();
+        if (rounds < 1) throw std::invalid_argument("predict_buckets: rounds must be >= 1");
+        if (count < 0) throw std::invalid_argument("predict_buckets: negative tone count");
+        const bool dev = location == MSFFT_DEVICE;
+        if (!dev) {  // SparseSpectrum is a std::map: ascending, unique positions
+            for (int64_t i = 0; i < count; ++i)
+                if (f[i] < 0 || f[i] >= n || (i > 0 && f[i] <= f[i - 1]))
+                    throw std::invalid_argument(
+                        "predict_buckets: positions must be strictly ascending in [0, n)");
+        }
+        DeviceView df(const_cast<int64_t*>(f), static_cast<size_t>(count) * 8, dev, true);
+        DeviceView dc(const_cast<double*>(c), static_cast<size_t>(count) * 16, dev, true);
+        DeviceView out(values, static_cast<size_t>(rounds * b) * 16, dev, false);
+        predict_buckets_device(n, b, delta, static_cast<const int64_t*>(df.dev),
+                               static_cast<const double2*>(dc.dev), count, sigma, tau, rounds,
+                               static_cast<double2*>(out.dev), nullptr);
+        out.write_back();
+    });
+}
+
+int msfft_locate_frequency(int64_t n, int64_t b, int64_t l, double q, const int64_t* buckets,
+                           int64_t count, const double* rounds, const int64_t* tau,
+                           int64_t nrounds, int64_t* u, int32_t* stages, int32_t* status,
+                           int32_t location, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        require_device();
+        validate_cfg(l, q);
+        if (nrounds < 1) throw std::invalid_argument("locate_frequency: no rounds");
+        if (tau[0] != 0) throw std::invalid_argument("locate_frequency: round 0 must have tau = 0");
+        if (n < 4 || !is_pow2_u(static_cast<uint64_t>(n)) || b < 1 ||
+            !is_pow2_u(static_cast<uint64_t>(b)) || b > n)
+            throw std::invalid_argument("locate_frequency: n and b must be powers of two, b <= n");
+        const int needed = stage_count(static_cast<double>(n / b), l, q);
+        if (nrounds < needed + 1)
+            throw std::invalid_argument("locate_frequency: not enough rounds for the schedule");
+        const bool dev = location == MSFFT_DEVICE;
+        DeviceView db(const_cast<int64_t*>(buckets), static_cast<size_t>(count) * 8, dev, true);
+        if (!dev)
+            for (int64_t i = 0; i < count; ++i)
+                if (buckets[i] < 0 || buckets[i] >= b)
+                    throw std::invalid_argument("locate_frequency: bucket out of range");
+        DeviceView dr(const_cast<double*>(rounds), static_cast<size_t>(nrounds * b) * 16, dev,
+                      true);
+        DeviceView du(u, static_cast<size_t>(count) * 8, dev, false);
+        DeviceView ds(stages, static_cast<size_t>(count) * 4, dev, false);
+        DeviceView dst(status, static_cast<size_t>(count) * 4, dev, false);
+        locate_frequency_device(n, b, l, q, static_cast<const int64_t*>(db.dev), count,
+                                static_cast<const double2*>(dr.dev), tau, nrounds,
+                                static_cast<int64_t*>(du.dev), static_cast<int32_t*>(ds.dev),
+                                static_cast<int32_t*>(dst.dev), nullptr);
+        du.write_back();
+        ds.write_back();
+        dst.write_back();
+        std::vector<int32_t> st(static_cast<size_t>(count));
+        if (count)
+            MSFFT_CUDA(cudaMemcpy(st.data(), dst.dev, st.size() * 4, cudaMemcpyDeviceToHost));
+        for (const int32_t code : st) {  // first failing bucket in input order
+            if (code == 2) throw std::domain_error("phase_of: zero value");
+            if (code == 3)
+                throw std::invalid_argument("locate_frequency: not enough rounds for the schedule");
+            if (code == 4) throw std::invalid_argument("locate_frequency: bucket out of range");
+        }
+    });
+}
+
+int msfft_estimate_values(int64_t n, int64_t b, double delta, const double* y0, const int64_t* u,
+                          int64_t count, double* out, int32_t* status, int32_t location,
+                          char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        require_device();
+        const bool dev = location == MSFFT_DEVICE;
+        DeviceView dy(const_cast<double*>(y0), static_cast<size_t>(count) * 16, dev, true);
+        DeviceView du(const_cast<int64_t*>(u), static_cast<size_t>(count) * 8, dev, true);
+        DeviceView dout(out, static_cast<size_t>(count) * 16, dev, false);
+        DeviceView dst(status, static_cast<size_t>(count) * 4, dev, false);
+        estimate_values_device(n, b, delta, static_cast<const double2*>(dy.dev),
+                               static_cast<const int64_t*>(du.dev), count,
+                               static_cast<double2*>(dout.dev), static_cast<int32_t*>(dst.dev),
+                               nullptr);
+        dout.write_back();
+        dst.write_back();
     });
 }
 

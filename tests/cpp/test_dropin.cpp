@@ -163,7 +163,89 @@ int main() {
             CHECK(std::abs(hs[i].max - ref[73 * i + 72]) <= 1e-9, "phase max");
         }
     }
-    std::printf("dropin ok: %ld entries identical support, max rel err %.3e; signal/io/phase API ok\n",
+    // ---- component API on the path (bucketize.hpp, locate.hpp, sfft4.hpp:50)
+    {
+        const int64_t n3 = 1 << 14, b3 = 64;
+        const double d3 = 1e-8;
+        const auto win = msfft::get_flat_window(n3, b3, d3);
+        int64_t wref = 0;
+        CHECK(orc_window(n3, b3, d3, &wref, nullptr, 0, err, sizeof(err)) == 0, "reference window");
+        CHECK(win->w == wref && win->l_width == n3 / b3, "window support");
+        const auto [sx, st] = msfft::generate_test_signal(n3, 12, 5);
+        std::vector<double> sxi(2 * n3);
+        for (int64_t j = 0; j < n3; ++j) {
+            sxi[2 * j] = sx.samples[j].real();
+            sxi[2 * j + 1] = sx.samples[j].imag();
+        }
+        // taus of one iteration (sfft4.cpp:49-55) and a sigma
+        int32_t nr = 0;
+        std::vector<int64_t> taus(32);
+        CHECK(msfft_tau_plan(static_cast<double>(n3 / b3), n3, 16, 1.0, taus.data(), 32, &nr, err,
+                             sizeof(err)) == 0, "tau plan");
+        std::vector<msfft::PermutationParams> ps;
+        for (int r = 0; r < nr; ++r) ps.push_back({4097, 0, taus[r]});
+        const auto rounds = msfft::bucketize_rounds(sx, *win, ps);
+        std::vector<double> rv(2 * b3 * nr);
+        for (int r = 0; r < nr; ++r) {
+            std::vector<double> one(2 * b3);
+            CHECK(orc_bucketize(n3, sxi.data(), b3, d3, ps[r].sigma, ps[r].tau, one.data(), err,
+                                sizeof(err)) == 0, "reference bucketize");
+            for (int64_t j = 0; j < b3; ++j)
+                CHECK(rounds[r].values[j] == msfft::cplx(one[2 * j], one[2 * j + 1]),
+                      "bucketize bit-exact");
+            std::copy(one.begin(), one.end(), rv.begin() + 2 * b3 * r);
+        }
+        const msfft::BucketSet pred = msfft::predict_buckets(st, *win, ps[1]);
+        std::vector<int64_t> pf;
+        std::vector<double> pc, pref(2 * b3);
+        for (const auto& [f, c] : st.entries) {
+            pf.push_back(f);
+            pc.push_back(c.real());
+            pc.push_back(c.imag());
+        }
+        CHECK(orc_predict(n3, b3, d3, static_cast<int64_t>(pf.size()), pf.data(), pc.data(),
+                          ps[1].sigma, ps[1].tau, pref.data(), err, sizeof(err)) == 0,
+              "reference predict");
+        double pmax = 0.0, perr = 0.0;
+        for (int64_t j = 0; j < b3; ++j) {
+            const msfft::cplx r(pref[2 * j], pref[2 * j + 1]);
+            pmax = std::max(pmax, std::abs(r));
+            perr = std::max(perr, std::abs(pred.values[j] - r));
+        }
+        CHECK(perr <= 1e-13 * pmax, "predict_buckets within ulps");
+        const msfft::BucketSet resid = msfft::subtract(rounds[1], pred);
+        CHECK(std::abs(resid.values[0] - (rounds[1].values[0] - pred.values[0])) == 0.0,
+              "subtract");
+        bool threw = false;
+        try {
+            msfft::subtract(rounds[0], rounds[1]);
+        } catch (const std::invalid_argument& e) {
+            threw = std::string(e.what()) == "subtract: bucket sets are not from the same round";
+        }
+        CHECK(threw, "subtract geometry check");
+        std::vector<int64_t> all(b3);
+        for (int64_t j = 0; j < b3; ++j) all[j] = j;
+        const auto loc = msfft::locate_frequencies(all, rounds, msfft::MultiscaleConfig{16, 1.0},
+                                                   *win);
+        for (int64_t j = 0; j < b3; ++j) {
+            int64_t u = -1;
+            int stg = 0;
+            CHECK(orc_locate(n3, b3, d3, 16, 1.0, j, nr, taus.data(), rv.data(), &u, &stg, err,
+                             sizeof(err)) == 0, "reference locate");
+            CHECK(u < 0 ? !loc[j] : (loc[j] && loc[j]->u == u && loc[j]->stages == stg),
+                  "locate_frequency identical");
+            if (loc[j]) {
+                double ev[2];
+                CHECK(orc_estimate_value(n3, b3, d3, rounds[0].values[j].real(),
+                                         rounds[0].values[j].imag(), u, ev, err,
+                                         sizeof(err)) == 0, "reference estimate");
+                const msfft::cplx e = msfft::estimate_value(rounds[0].values[j], u, *win);
+                CHECK(std::abs(e - msfft::cplx(ev[0], ev[1])) <= 1e-13 * std::abs(e),
+                      "estimate_value");
+            }
+        }
+    }
+    std::printf("dropin ok: %ld entries identical support, max rel err %.3e; signal/io/phase/component API ok\n",
                 static_cast<long>(cnt), worst);
     return 0;
 }
