@@ -6,6 +6,7 @@ functions its own tests call directly, each on the GPU through the C ABI.
     subtract          proj/src/bucketize.cpp:97-104 (host, elementwise)
     locate_frequency  proj/src/locate.cpp:83-123
     estimate_value    proj/src/sfft4.cpp:27-36
+    run_iteration     proj/src/sfft4.cpp:38-113 (composed from the above)
 
 Types mirror the reference: PermutationParams (bucketize.hpp:16-20),
 BucketSet (:24-30), LocateOutcome (locate.hpp:42-45), and FlatWindow as a
@@ -26,7 +27,8 @@ from .signal import _buf
 
 __all__ = ["FlatWindow", "PermutationParams", "BucketSet", "LocateOutcome", "flat_window",
            "bucketize", "bucketize_rounds", "predict_buckets", "subtract", "locate_frequency",
-           "locate_frequencies", "estimate_value", "estimate_values", "tau_plan", "sigma_plan"]
+           "locate_frequencies", "estimate_value", "estimate_values", "tau_plan", "sigma_plan",
+           "Rng", "IterationState", "run_iteration"]
 
 
 def _err():
@@ -213,3 +215,76 @@ def sigma_plan(seed: int, n: int, iterations: int) -> list[PermutationParams]:
                                      s.ctypes.data_as(C.POINTER(C.c_int64)),
                                      si.ctypes.data_as(C.POINTER(C.c_int64)), e, 1024), e)
     return [PermutationParams(int(a), int(b), 0) for a, b in zip(s, si)]
+
+
+class Rng:
+    """The draws sfft4 makes from its Rng (rng.hpp:19-59): one
+    random_params(n, rng, 0) per iteration (sfft4.cpp:48), reproduced from
+    the seed by the host σ plan."""
+
+    def __init__(self, seed: int):
+        self.seed = int(seed)
+        self.draws = 0
+
+    def random_params(self, n: int) -> PermutationParams:
+        p = sigma_plan(self.seed, n, self.draws + 1)[self.draws]
+        self.draws += 1
+        return p
+
+
+@dataclass
+class IterationState:
+    """sfft4.hpp:14-30; `accumulated` maps f -> c (ascending on read)."""
+    m: int = 1
+    k_m: int = 0
+    b_m: int = 0
+    delta: float = 1e-8
+    accumulated: dict = field(default_factory=dict)
+    sigma_m: int = 1
+    tau_plan: list = field(default_factory=list)
+    w_m: int = 0
+    stages_m: int = 0
+    samples_round_sum: int = 0
+
+
+def run_iteration(x, state: IterationState, cfg: MultiscaleConfig, rng: Rng) -> SparseSpectrum:
+    """run_iteration (sfft4.cpp:38-113) composed from the component API:
+    encode every round, subtract the prediction of the accumulated tones,
+    rank |y0|, locate and estimate the buckets above the threshold, fold the
+    found tones into state.accumulated, halve k_m / b_m.  Returns the tones
+    found this iteration.  Each step is one GPU launch over all rounds or
+    all candidate buckets."""
+    n = int(x.shape[-1])
+    win = flat_window(n, state.b_m, state.delta)
+    base = rng.random_params(n)
+    taus = tau_plan(win.l_width, n, cfg)
+    state.sigma_m, state.tau_plan, state.w_m, state.stages_m = base.sigma, taus, win.w, len(taus) - 1
+    params = [PermutationParams(base.sigma, base.sigma_inv, t) for t in taus]
+    rounds = bucketize_rounds(x, win, params)
+    if state.accumulated:
+        fs = np.array(sorted(state.accumulated), np.int64)
+        known = SparseSpectrum(n, fs, np.array([state.accumulated[f] for f in fs]))
+        rounds = [subtract(r, p) for r, p in zip(rounds, predict_buckets(known, win, params))]
+    state.samples_round_sum += len(taus) * win.w
+    budget = min(state.k_m, state.b_m)
+    y0 = rounds[0].values
+    mag = np.abs(y0)  # hypot, as std::abs(cplx)
+    order = np.argsort(-mag, kind="stable")
+    threshold = 0.2 * mag[order[budget - 1]]
+    cand = [int(order[r]) for r in range(budget) if mag[order[r]] > threshold]
+    found = {}
+    outs = locate_frequencies(cand, rounds, cfg, win) if cand else []
+    located = [(bk, o) for bk, o in zip(cand, outs) if o is not None]
+    if located:
+        vals, ok = estimate_values([y0[bk] for bk, _ in located], [o.u for _, o in located], win)
+        for (bk, o), v, good in zip(located, vals, ok):  # rank order
+            if good:
+                f = (base.sigma_inv * o.u) % n
+                found[f] = found.get(f, 0j) + complex(v)
+    for f in sorted(found):
+        state.accumulated[f] = state.accumulated.get(f, 0j) + found[f]
+    state.k_m = (state.k_m + 1) // 2
+    state.b_m = state.b_m // 2 if state.b_m > 32 else state.b_m
+    state.m += 1
+    fs = sorted(found)
+    return SparseSpectrum(n, np.array(fs, np.int64), np.array([found[f] for f in fs], np.complex128))

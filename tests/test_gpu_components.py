@@ -151,47 +151,23 @@ def test_estimate_value_matches_reference(oracle):
 
 
 def sfft4_from_components(x, k, cfg, seed, delta):
-    """run_iteration + sfft4 (sfft4.cpp:38-187) written with the component API."""
+    """sfft4 (sfft4.cpp:131-187) over components.run_iteration."""
     n = x.shape[-1]
     iter_cap = int(math.ceil(math.log2(k))) + 2 if k > 1 else 2
-    k_m, b_m = k, M.Plan(n, k, cfg, delta, "complex128").stats().b_first
-    perms = CMP.sigma_plan(seed, n, iter_cap)
-    acc = {}
-    for m in range(iter_cap):
-        if k_m < 1:
+    state = CMP.IterationState(k_m=k, b_m=M.Plan(n, k, cfg, delta, "complex128").stats().b_first,
+                               delta=delta)
+    rng = CMP.Rng(seed)
+    stages = []
+    for _ in range(iter_cap):
+        if state.k_m < 1:
             break
-        win = CMP.flat_window(n, b_m, delta)
-        taus = CMP.tau_plan(n // b_m, n, cfg)
-        params = [CMP.PermutationParams(perms[m].sigma, perms[m].sigma_inv, t) for t in taus]
-        rounds = CMP.bucketize_rounds(x, win, params)
-        if acc:
-            fs = np.array(sorted(acc), np.int64)
-            known = M.SparseSpectrum(n, fs, np.array([acc[f] for f in fs]))
-            rounds = [CMP.subtract(r, p) for r, p in
-                      zip(rounds, CMP.predict_buckets(known, win, params))]
-        budget = min(k_m, b_m)
-        y0 = rounds[0].values
-        mag = np.abs(y0)
-        order = np.argsort(-mag, kind="stable")
-        thr = 0.2 * mag[order[budget - 1]]
-        cand = [int(order[r]) for r in range(budget) if mag[order[r]] > thr]
-        found = {}
-        for bucket, out in zip(cand, CMP.locate_frequencies(cand, rounds, cfg, win)):
-            if out is None:
-                continue
-            v, ok = CMP.estimate_values([y0[bucket]], [out.u], win)
-            if not ok[0]:
-                continue
-            f = (perms[m].sigma_inv * out.u) % n
-            found[f] = found.get(f, 0j) + complex(v[0])
-        for f in sorted(found):
-            acc[f] = acc.get(f, 0j) + found[f]
-        k_m = (k_m + 1) // 2
-        b_m = b_m // 2 if b_m > 32 else b_m
+        CMP.run_iteration(x, state, cfg, rng)
+        stages.append(state.stages_m)
+    acc = state.accumulated
     fs = sorted(acc)
     keep = sorted(sorted(range(len(fs)), key=lambda i: -abs(acc[fs[i]]))[:k])
     return (np.array([fs[i] for i in keep], np.int64),
-            np.array([acc[fs[i]] for i in keep], np.complex128))
+            np.array([acc[fs[i]] for i in keep], np.complex128), stages, state.samples_round_sum)
 
 
 @pytest.mark.parametrize("n,k,snr,seed", [(1 << 14, 20, None, 3), (1 << 16, 50, 20.0, 7)])
@@ -202,8 +178,9 @@ def test_components_compose_to_sfft4(oracle, n, k, snr, seed):
     x = make_signal(oracle, dict(gen="np", n=n, k=k, seed=seed, snr=snr))
     delta = 1e-8 if snr is None else 1e-6
     cfg = M.MultiscaleConfig()
-    f, c = sfft4_from_components(x, k, cfg, 1000 + seed, delta)
+    f, c, stages, round_sum = sfft4_from_components(x, k, cfg, 1000 + seed, delta)
     r = M.sfft4(x, k, cfg, 1000 + seed, delta)
+    assert stages == r.stats.stage_counts and round_sum == r.stats.samples_round_sum
     assert np.array_equal(f, r.spectrum.positions)
     assert np.array_equal(c, r.spectrum.coeffs)
     ref = oracle.sfft4(x, k, 16, 1.0, 1000 + seed, delta)
