@@ -223,7 +223,9 @@ __device__ __forceinline__ void decode_signal(const DevPlan& plan, const DecLayo
             }
             gsync();
             DEC_MARK(1);
-            for (int e = tid; e < acc_n * nr; e += kThreads) {
+            // warps 1.. evaluate the rotations while warp 0 builds the lists
+            static_assert(kThreads > 32, "the rotation loop needs warps besides warp 0");
+            for (int e = tid - 32; e >= 0 && e < acc_n * nr; e += kThreads - 32) {
                 const int j = e / nr, r = e - j * nr;
                 S.rot[e] = unit_root(n, inv_n, tau_at(r) * S.tone_u[j]);
             }
@@ -288,6 +290,7 @@ __device__ __forceinline__ void decode_signal(const DevPlan& plan, const DecLayo
                     p[d] = S.bstart[bk];
                     q3[d] = S.bstart[bk + 1];
                 }
+                const double2 o = Y[e];  // issued before the merge walk
                 double2 pred = make_double2(0.0, 0.0);
                 bool any = false;
                 for (;;) {
@@ -306,10 +309,7 @@ __device__ __forceinline__ void decode_signal(const DevPlan& plan, const DecLayo
                     pred.y += v.y;
                     any = true;
                 }
-                if (any) {
-                    const double2 o = Y[e];
-                    Y[e] = make_double2(o.x - pred.x, o.y - pred.y);
-                }
+                if (any) Y[e] = make_double2(o.x - pred.x, o.y - pred.y);
             }
             gsync();
             DEC_MARK(3);
