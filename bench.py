@@ -171,14 +171,18 @@ def pipe_evidence():
             continue
         with open(path) as f:
             d = json.load(f)
-        def num(k):
+        def num(raw, short):  # raw ncu metric names or tools/ncu_summary.py keys
+            v = d.get(raw, d.get(short))
             try:
-                return float(d.get(k)) / 100.0
+                return float(v) / 100.0
             except (TypeError, ValueError):
                 return None
-        out[key] = {"fp64_pipe_frac": num("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active"),
-                    "issue_active_frac": num("smsp__issue_active.avg.pct_of_peak_sustained_active"),
-                    "sm_throughput_frac": num("sm__throughput.avg.pct_of_peak_sustained_elapsed"),
+        out[key] = {"fp64_pipe_frac": num("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
+                                          "fp64_pipe_pct"),
+                    "issue_active_frac": num("smsp__issue_active.avg.pct_of_peak_sustained_active",
+                                             "issue_active_pct"),
+                    "sm_throughput_frac": num("sm__throughput.avg.pct_of_peak_sustained_elapsed",
+                                              "sm_throughput_pct"),
                     "top_stalls": d.get("stall_share"), "source": f"profiles/r01_final/{name}"}
     return out or None
 
