@@ -21,6 +21,20 @@
 #define MSFFT_FUSED_MINB 2
 #endif
 
+#ifdef MSFFT_TIMELINE
+// diagnostic build only: per item {start ns, end ns, smid << 48 | m << 40 | code}
+__device__ unsigned long long g_timeline[1 << 16][3];
+__device__ __forceinline__ unsigned long long tl_now() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+extern "C" int msfft_debug_timeline(void* dst, long long n_items) {
+    if (n_items > (1 << 16)) n_items = 1 << 16;
+    return static_cast<int>(cudaMemcpyFromSymbol(dst, g_timeline, n_items * 24));
+}
+#endif
+
 namespace msfft_b200 {
 
 namespace {
@@ -53,6 +67,9 @@ fused_kernel(const __grid_constant__ DevPlan plan, DecLayout lay, DecArgs args,
         const int item = s_item;
         if (item >= n_items) break;
         const int32_t code = items[item];
+#ifdef MSFFT_TIMELINE
+        const unsigned long long tl_start = tl_now();
+#endif
         if (code >= 0) {
             const EncTask& t = tasks[code];
             encode_task(plan, t, x, x_stride, batch, args.sigma, args.y, smem, &bar, phase);
@@ -76,6 +93,18 @@ fused_kernel(const __grid_constant__ DevPlan plan, DecLayout lay, DecArgs args,
                                        sh, nullptr);
         }
         __syncthreads();
+#ifdef MSFFT_TIMELINE
+        if (threadIdx.x == 0 && item < (1 << 16)) {
+            unsigned smid;
+            asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+            g_timeline[item][0] = tl_start;
+            g_timeline[item][1] = tl_now();
+            const unsigned m = code >= 0 ? static_cast<unsigned>(tasks[code].m) : 0xffu;
+            g_timeline[item][2] = (static_cast<unsigned long long>(smid) << 48) |
+                                  (static_cast<unsigned long long>(m) << 40) |
+                                  static_cast<unsigned>(code);
+        }
+#endif
     }
     // the last CTA out resets this launch's counters (ticket, done, exit)
     // for the next launch that uses them, so no memset sits between launches
