@@ -153,6 +153,8 @@ Plan::Plan(int64_t n, int64_t k, int64_t l, double q, double delta, bool c128, i
     if (const char* e = std::getenv("MSFFT_FUSED_TAIL")) fused_tail_ = std::max(0LL, std::atoll(e));
     if (const char* e = std::getenv("MSFFT_ENC_SMEM_PAD")) enc_smem_pad_ = std::atoll(e);
     fused_smem_ = std::max(enc_smem_, lay_.in_smem ? static_cast<size_t>(lay_.bytes) : size_t{0});
+    if (const char* e = std::getenv("MSFFT_FUSED_SMEM_PAD"))  // diagnostic: L1 carve-out experiments
+        fused_smem_ += static_cast<size_t>(std::max(0LL, std::atoll(e)));
     flags_.reset(2);
     MSFFT_CUDA(cudaMemset(flags_.get(), 0, 2 * sizeof(int32_t)));
     for (int i = 0; i < 2; ++i)
