@@ -153,6 +153,7 @@ Plan::Plan(int64_t n, int64_t k, int64_t l, double q, double delta, bool c128, i
     if (const char* e = std::getenv("MSFFT_FUSED_TAIL")) fused_tail_ = std::max(0LL, std::atoll(e));
     if (const char* e = std::getenv("MSFFT_ENC_SMEM_PAD")) enc_smem_pad_ = std::atoll(e);
     fused_smem_ = std::max(enc_smem_, lay_.in_smem ? static_cast<size_t>(lay_.bytes) : size_t{0});
+    if (const char* e = std::getenv("MSFFT_ENC_SPLIT")) split_enabled_ = std::atoi(e) != 0;
     if (const char* e = std::getenv("MSFFT_FUSED_SMEM_PAD"))  // diagnostic: L1 carve-out experiments
         fused_smem_ += static_cast<size_t>(std::max(0LL, std::atoll(e)));
     flags_.reset(2);
@@ -210,7 +211,11 @@ const Plan::TaskSet& Plan::tasks_for(int64_t batch) {
     auto it = tasks_.find(batch);
     if (it != tasks_.end()) return it->second;
     std::vector<EncTask> v;
-    append_tasks(v, 0, batch);
+    append_tasks(v, 0, batch, false);
+    if (split_tasks(static_cast<int64_t>(v.size()))) {
+        v.clear();
+        append_tasks(v, 0, batch, true);
+    }
     TaskSet ts;
     ts.count = static_cast<int64_t>(v.size());
     ts.d.reset(v.size());
@@ -230,13 +235,16 @@ const Plan::FusedSet& Plan::fused_for(int64_t batch, int slot) {
     const int64_t chunk = std::max<int64_t>(group, (fused_chunk_ + group - 1) / group * group);
     const int64_t nchunks = (batch + chunk - 1) / chunk;
     std::vector<EncTask> tasks;
+    append_tasks(tasks, 0, batch, false);
+    const bool split = split_tasks(static_cast<int64_t>(tasks.size()));
+    tasks.clear();
     std::vector<std::vector<int32_t>> enc(nchunks);
     // need[c * iters + m]: encode tasks of chunk c and iteration m
     const int iters = sched_.iterations;
     std::vector<int32_t> need(static_cast<size_t>(nchunks * iters), 0);
     for (int64_t c = 0; c < nchunks; ++c) {
         const size_t before = tasks.size();
-        append_tasks(tasks, c * chunk, std::min(batch, (c + 1) * chunk));
+        append_tasks(tasks, c * chunk, std::min(batch, (c + 1) * chunk), split);
         for (size_t i = before; i < tasks.size(); ++i) {
             enc[c].push_back(static_cast<int32_t>(i));
             ++need[c * iters + tasks[i].m];
@@ -283,7 +291,19 @@ const Plan::FusedSet& Plan::fused_for(int64_t batch, int slot) {
     return fused_.emplace(key, std::move(fs)).first->second;
 }
 
-void Plan::append_tasks(std::vector<EncTask>& v, int64_t s_begin, int64_t s_end) const {
+bool Plan::split_tasks(int64_t n_tasks) const {
+    static const int sms = [] {
+        int dev = 0, v = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess ||
+            cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+            return 0;
+        return v;
+    }();
+    return split_enabled_ && n_tasks < 2 * static_cast<int64_t>(sms);
+}
+
+void Plan::append_tasks(std::vector<EncTask>& v, int64_t s_begin, int64_t s_end,
+                        bool split) const {
     for (int m = 0; m < sched_.iterations; ++m) {
         const DevIter& di = dplan_.it[m];
         const IterationPlan& ip = sched_.iters[m];
@@ -303,29 +323,53 @@ void Plan::append_tasks(std::vector<EncTask>& v, int64_t s_begin, int64_t s_end)
                 else
                     merged.push_back(s);
             }
-            t.nseg = static_cast<int32_t>(merged.size());
-            for (size_t i = 0; i < merged.size(); ++i) {
-                t.seg_lo[i] = static_cast<int32_t>(merged[i].first);
-                t.seg_hi[i] = static_cast<int32_t>(merged[i].second);
-                t.seg_cpos[i] = static_cast<int32_t>(imap_.position(m, merged[i].first));
-            }
-            if (di.b <= kEncThreads) {
-                t.fused = 1;
-                t.nsig = static_cast<int32_t>(kEncThreads / di.b);
-                t.lane0 = 0;
-                for (int64_t s0 = s_begin; s0 < s_end; s0 += t.nsig) {
-                    t.sig0 = s0;
-                    v.push_back(t);
-                }
-            } else {
-                t.fused = 0;
-                t.nsig = 1;
-                for (int64_t s0 = s_begin; s0 < s_end; ++s0)
-                    for (int64_t lane0 = 0; lane0 < di.b; lane0 += kEncThreads) {
+            const auto emit = [&](EncTask t) {
+                if (di.b <= kEncThreads) {
+                    t.fused = 1;
+                    t.nsig = static_cast<int32_t>(kEncThreads / di.b);
+                    t.lane0 = 0;
+                    for (int64_t s0 = s_begin; s0 < s_end; s0 += t.nsig) {
                         t.sig0 = s0;
-                        t.lane0 = static_cast<int32_t>(lane0);
                         v.push_back(t);
                     }
+                } else {
+                    t.fused = 0;
+                    t.nsig = 1;
+                    for (int64_t s0 = s_begin; s0 < s_end; ++s0)
+                        for (int64_t lane0 = 0; lane0 < di.b; lane0 += kEncThreads) {
+                            t.sig0 = s0;
+                            t.lane0 = static_cast<int32_t>(lane0);
+                            v.push_back(t);
+                        }
+                }
+            };
+            const auto seg = [&](EncTask& t, int i, size_t j) {
+                t.seg_lo[i] = static_cast<int32_t>(merged[j].first);
+                t.seg_hi[i] = static_cast<int32_t>(merged[j].second);
+                t.seg_cpos[i] = static_cast<int32_t>(imap_.position(m, merged[j].first));
+            };
+            if (!split) {
+                t.nseg = static_cast<int32_t>(merged.size());
+                for (size_t i = 0; i < merged.size(); ++i) seg(t, static_cast<int>(i), i);
+                emit(t);
+            } else {
+                // small launches: one task per merged segment, which covers
+                // a contiguous run of rounds (the intervals shift with tau,
+                // which grows with r), so no sample is loaded twice
+                for (size_t j = 0; j < merged.size(); ++j) {
+                    EncTask ts = t;
+                    int ra = t.r0 + t.nr, rb = t.r0 - 1;
+                    for (int r = t.r0; r < t.r0 + t.nr; ++r)
+                        if (-di.h - ip.taus[r] >= merged[j].first && di.h - ip.taus[r] <= merged[j].second) {
+                            ra = std::min(ra, r);
+                            rb = std::max(rb, r);
+                        }
+                    ts.r0 = ra;
+                    ts.nr = rb - ra + 1;
+                    ts.nseg = 1;
+                    seg(ts, 0, j);
+                    emit(ts);
+                }
             }
         }
     }

@@ -107,7 +107,9 @@ private:
     // slot 0: synchronous launches; 1, 2: the two alternating buffer sets of
     // programmatic (PDL) asynchronous launches
     const FusedSet& fused_for(int64_t batch, int slot = 0);
-    void append_tasks(std::vector<EncTask>& v, int64_t s_begin, int64_t s_end) const;
+    // split: one task per merged t' segment (more CTAs for small batches)
+    void append_tasks(std::vector<EncTask>& v, int64_t s_begin, int64_t s_end, bool split) const;
+    bool split_tasks(int64_t n_tasks) const;
     void upload_sigmas(int64_t batch, const uint64_t* seeds, cudaStream_t st);
     void check_flags(cudaStream_t st);
     void run_chunk(int64_t batch, const void* d_x, int64_t x_stride, const int64_t* d_sig,
@@ -141,6 +143,7 @@ private:
     int64_t fused_chunk_ = 64;    // signals per fused chunk
     int64_t fused_lag_ = 2;       // chunks a decode trails its encode by
     int64_t fused_tail_ = 0;      // last chunks whose decodes follow their encodes at once
+    bool split_enabled_ = true;   // split encode tasks per segment when a launch is small
     size_t fused_smem_ = 0;
     size_t enc_smem_pad_ = 0;     // diagnostics: extra encode smem (lowers occupancy)
 

@@ -6,7 +6,9 @@ timer, TransformStats::runtime_ms, one thread) on the same input, with the
 parity check.  C5's reference run takes hours (window design alone > 22 min
 per window) and is skipped.  Prints one JSON line per config and a summary.
 
-    python tools/configs_table.py [C1 C2 C3 C4 C5]
+    python tools/configs_table.py [--no-ref] [C1 C2 C3 C4 C5]
+
+--no-ref times the GPU side only (parity is then not checked here).
 """
 import json
 import math
@@ -50,7 +52,11 @@ def gpu_time(x_host, k, l, q, seed, delta, dtype, reps=7):
     return statistics.median(ms), stages, f[0, :cnt], c[0, :cnt]
 
 
+NO_REF = "--no-ref" in sys.argv
+
+
 def cell(name, x, k, l, q, seed, delta, dtype, ref=True):
+    ref = ref and not NO_REF
     row = {"config": name, "n": int(x.shape[-1]), "k": k, "l": l, "q": q, "dtype": dtype}
     try:
         g_ms, stages, f, c = gpu_time(x, k, l, q, seed, delta, dtype)
@@ -112,4 +118,4 @@ def main(names):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1:] or ["C1", "C2", "C3", "C4", "C5"])
+    main([a for a in sys.argv[1:] if not a.startswith("--")] or ["C1", "C2", "C3", "C4", "C5"])
