@@ -291,6 +291,21 @@ const Plan::FusedSet& Plan::fused_for(int64_t batch, int slot) {
     return fused_.emplace(key, std::move(fs)).first->second;
 }
 
+// K2 for the iterations with b > 256 (the encode's fused epilogue does the
+// rest): their b-point transforms and the 1/n scale, as few launches as the
+// sizes allow.
+void Plan::bucket_ffts(double2* y, int64_t batch, cudaStream_t st) const {
+    std::vector<FftSet> sets;
+    for (int m : big_b_iters_) {
+        const DevIter& di = dplan_.it[m];
+        sets.push_back(FftSet{di.yoff, di.b, di.nrounds});
+    }
+    for (size_t i = 0; i < sets.size(); i += kMaxFftSets)
+        fft_radix2_sets(y, sets.data() + i,
+                        static_cast<int>(std::min<size_t>(kMaxFftSets, sets.size() - i)), batch,
+                        dplan_.values_per_signal, -1, dplan_.inv_n, st);
+}
+
 bool Plan::split_tasks(int64_t n_tasks) const {
     static const int sms = [] {
         int dev = 0, v = 0;
@@ -445,11 +460,7 @@ void Plan::run_chunk(int64_t batch, const void* d_x, int64_t x_stride, const int
             double2* yc = y_.get() + c0 * vps;
             launch_encode(P, tsc.d.get(), tsc.count, xc, c128_, x_stride, cb,
                           d_sig + c0 * iters, yc, enc_smem_, st);
-            for (int m : big_b_iters_) {
-                const DevIter& di = dplan_.it[m];
-                fft_radix2_batched(yc + di.yoff, di.b, cb * di.nrounds, di.nrounds, vps, -1,
-                                   dplan_.inv_n, st);
-            }
+            bucket_ffts(yc, cb, st);
             MSFFT_CUDA(cudaEventRecord(ev_chunk_, st));
             MSFFT_CUDA(cudaStreamWaitEvent(dec_stream_, ev_chunk_, 0));
             launch_decode(dplan_, lay_, yc, d_sig + c0 * iters, d_sig_inv + c0 * iters, cb,
@@ -466,11 +477,7 @@ void Plan::run_chunk(int64_t batch, const void* d_x, int64_t x_stride, const int
     launch_encode(P, ts.d.get(), ts.count, d_x, c128_, x_stride, batch, d_sig, y_.get(),
                   enc_smem_ + enc_smem_pad_, st);
     if (opt.stage_times) MSFFT_CUDA(cudaEventRecord(ev_stage_[1], st));
-    for (int m : big_b_iters_) {
-        const DevIter& di = dplan_.it[m];
-        fft_radix2_batched(y_.get() + di.yoff, di.b, batch * di.nrounds, di.nrounds,
-                           dplan_.values_per_signal, -1, dplan_.inv_n, st);
-    }
+    bucket_ffts(y_.get(), batch, st);
     if (opt.stage_times) MSFFT_CUDA(cudaEventRecord(ev_stage_[2], st));
     const size_t ybytes = sizeof(double2) * static_cast<size_t>(dplan_.values_per_signal);
     if (opt.pre) {
@@ -845,11 +852,7 @@ void Plan::encode_values(int64_t batch, const void* d_x, int64_t x_stride, int64
     const TaskSet& ts = tasks_for(batch);
     launch_encode(p, ts.d.get(), ts.count, d_x, c128_, x_stride, batch, sig_.get(), d_y,
                   enc_smem_, st);
-    for (int m : big_b_iters_) {
-        const DevIter& di = dplan_.it[m];
-        fft_radix2_batched(d_y + di.yoff, di.b, batch * di.nrounds, di.nrounds,
-                           dplan_.values_per_signal, -1, dplan_.inv_n, st);
-    }
+    bucket_ffts(d_y, batch, st);
     check_flags(st);
 }
 

@@ -110,6 +110,7 @@ private:
     // split: one task per merged t' segment (more CTAs for small batches)
     void append_tasks(std::vector<EncTask>& v, int64_t s_begin, int64_t s_end, bool split) const;
     bool split_tasks(int64_t n_tasks) const;
+    void bucket_ffts(double2* y, int64_t batch, cudaStream_t st) const;
     void upload_sigmas(int64_t batch, const uint64_t* seeds, cudaStream_t st);
     void check_flags(cudaStream_t st);
     void run_chunk(int64_t batch, const void* d_x, int64_t x_stride, const int64_t* d_sig,

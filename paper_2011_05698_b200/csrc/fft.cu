@@ -154,7 +154,107 @@ __global__ void __launch_bounds__(512) fft_smem_kernel(double2* __restrict__ dat
     }
 }
 
+// fft_smem_kernel over several array sets of different sizes in one launch
+// (the bucket vectors of every iteration with 256 < b <= kSmemFftMax): the
+// CTA's set is found from the cumulative block counts, then the transform is
+// fft_smem_kernel's, operation for operation.
+struct SmemFftSets {
+    int nsets;
+    int64_t first[kMaxFftSets + 1];  // first block of each set
+    int64_t off[kMaxFftSets], size[kMaxFftSets], inner[kMaxFftSets];
+    int log2size[kMaxFftSets];
+    const double2* tw[kMaxFftSets];
+};
+
+__global__ void __launch_bounds__(512) fft_smem_sets_kernel(double2* __restrict__ data,
+                                                            const __grid_constant__ SmemFftSets S,
+                                                            int64_t outer_stride, int sign,
+                                                            double scale) {
+    extern __shared__ double2 buf[];
+    int si = 0;
+    while (si + 1 < S.nsets && static_cast<int64_t>(blockIdx.x) >= S.first[si + 1]) ++si;
+    const int64_t bi = static_cast<int64_t>(blockIdx.x) - S.first[si];
+    const int64_t size = S.size[si];
+    const int log2size = S.log2size[si];
+    const double2* __restrict__ tw = S.tw[si];
+    double2* a = data + S.off[si] + (bi / S.inner[si]) * outer_stride + (bi % S.inner[si]) * size;
+    const int n = static_cast<int>(size);
+    for (int e = threadIdx.x; e < n; e += blockDim.x)
+        buf[bitrev_bits(static_cast<unsigned>(e), log2size)] = a[e];
+    __syncthreads();
+    for (int s = 1; s <= log2size; ++s) {
+        const int half = 1 << (s - 1);
+        const int64_t step = size >> s;
+        for (int bf = threadIdx.x; bf < n / 2; bf += blockDim.x) {
+            const int blk = bf / half, off = bf - blk * half;
+            const int e0 = blk * 2 * half + off, e1 = e0 + half;
+            double2 w = tw[static_cast<int64_t>(off) * step];
+            if (sign > 0) w.y = -w.y;
+            const double2 x0 = buf[e0];
+            const double2 t = cmul(buf[e1], w);
+            buf[e1] = make_double2(x0.x - t.x, x0.y - t.y);
+            buf[e0] = make_double2(x0.x + t.x, x0.y + t.y);
+        }
+        __syncthreads();
+    }
+    const bool do_scale = scale != 1.0;
+    for (int e = threadIdx.x; e < n; e += blockDim.x) {
+        double2 v = buf[e];
+        if (do_scale) v = make_double2(v.x * scale, v.y * scale);
+        a[e] = v;
+    }
+}
+
+void smem_fft_attribute(const void* fn) {
+    // the attribute is per device
+    static std::mutex mu;
+    static std::set<std::pair<int, const void*>> ready;
+    int dev = 0;
+    MSFFT_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(mu);
+    if (!ready.count({dev, fn})) {
+        MSFFT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(sizeof(double2) * kSmemFftMax)));
+        ready.insert({dev, fn});
+    }
+}
+
 }  // namespace
+
+void fft_radix2_sets(double2* data, const FftSet* sets, int nsets, int64_t batch,
+                     int64_t outer_stride, int sign, double scale, cudaStream_t stream) {
+    SmemFftSets S{};
+    int64_t blocks = 0, max_size = 0;
+    for (int i = 0; i < nsets; ++i) {
+        const FftSet& f = sets[i];
+        if (f.size <= 1 || batch <= 0) continue;
+        if (f.size > kSmemFftMax || S.nsets == kMaxFftSets) {
+            fft_radix2_batched(data + f.off, f.size, batch * f.inner, f.inner, outer_stride, sign,
+                               scale, stream);
+            continue;
+        }
+        int lg = 0;
+        while ((int64_t{1} << lg) < f.size) ++lg;
+        S.first[S.nsets] = blocks;
+        S.off[S.nsets] = f.off;
+        S.size[S.nsets] = f.size;
+        S.inner[S.nsets] = f.inner;
+        S.log2size[S.nsets] = lg;
+        S.tw[S.nsets] = device_twiddles(f.size);
+        ++S.nsets;
+        blocks += batch * f.inner;
+        max_size = std::max(max_size, f.size);
+    }
+    if (S.nsets == 0) return;
+    S.first[S.nsets] = blocks;
+    if (blocks > 0x7fffffff) throw CudaError("fft_radix2_sets: too many arrays");
+    smem_fft_attribute(reinterpret_cast<const void*>(fft_smem_sets_kernel));
+    const int threads = static_cast<int>(std::min<int64_t>(512, std::max<int64_t>(32, max_size / 2)));
+    fft_smem_sets_kernel<<<static_cast<unsigned>(blocks), threads,
+                           sizeof(double2) * static_cast<size_t>(max_size), stream>>>(
+        data, S, outer_stride, sign, scale);
+    MSFFT_LAUNCH_CHECK("fft_smem_sets_kernel");
+}
 
 const double* host_twiddles(int64_t n) {
     std::lock_guard<std::mutex> lock(g_tw_mu);
@@ -192,20 +292,7 @@ void fft_radix2_batched(double2* data, int64_t size, int64_t batch, int64_t inne
     if (size <= kSmemFftMax && batch <= 0x7fffffff) {
         // one launch, one read and one write of the data
         const size_t smem = sizeof(double2) * static_cast<size_t>(size);
-        {
-            // the attribute is per device
-            static std::mutex mu;
-            static std::set<int> ready;
-            int dev = 0;
-            MSFFT_CUDA(cudaGetDevice(&dev));
-            std::lock_guard<std::mutex> lock(mu);
-            if (!ready.count(dev)) {
-                MSFFT_CUDA(cudaFuncSetAttribute(fft_smem_kernel,
-                                                cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                static_cast<int>(sizeof(double2) * kSmemFftMax)));
-                ready.insert(dev);
-            }
-        }
+        smem_fft_attribute(reinterpret_cast<const void*>(fft_smem_kernel));
         const int threads = static_cast<int>(std::min<int64_t>(512, std::max<int64_t>(32, size / 2)));
         fft_smem_kernel<<<static_cast<unsigned>(batch), threads, smem, stream>>>(
             data, size, log2size, inner, outer_stride, sign, tw, scale);

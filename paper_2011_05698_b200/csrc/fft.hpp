@@ -27,4 +27,18 @@ const double* host_twiddles(int64_t n);
 void fft_radix2_batched(double2* data, int64_t size, int64_t batch, int64_t inner,
                         int64_t outer_stride, int sign, double scale, cudaStream_t stream);
 
+// One set of equally sized arrays for fft_radix2_sets: for each of `batch`
+// rows (row stride outer_stride), `inner` arrays of `size` starting at
+// data + off + row * outer_stride.
+struct FftSet {
+    int64_t off, size, inner;
+};
+constexpr int kMaxFftSets = 16;
+
+// fft_radix2_batched of several sets: the sets with size <= 4096 go into ONE
+// launch (one CTA per array, shared memory), larger ones through the
+// multi-pass path.  Bit-identical to transforming each set separately.
+void fft_radix2_sets(double2* data, const FftSet* sets, int nsets, int64_t batch,
+                     int64_t outer_stride, int sign, double scale, cudaStream_t stream);
+
 }  // namespace msfft_b200
