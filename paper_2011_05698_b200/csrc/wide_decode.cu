@@ -2,6 +2,7 @@
 // value is computed with decode_body.cuh's operations in its order.
 #include <algorithm>
 #include <cstdlib>
+#include <utility>
 
 #include "decode_body.cuh"
 #include "wide_decode.hpp"
@@ -18,6 +19,14 @@ constexpr int kScanT = 1024;
 constexpr int kLongSeg = 64;          // longer event segments sort with a whole CTA
 constexpr int kLongSmem = 8192;
 
+bool pdl_enabled() {
+    static const bool v = [] {
+        const char* e = std::getenv("MSFFT_WIDE_PDL");
+        return !e || std::atoi(e) != 0;
+    }();
+    return v;
+}
+
 unsigned grid_of(int64_t work) {
     return static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>((work + kT - 1) / kT, 148 * 16)));
 }
@@ -26,15 +35,53 @@ __device__ __forceinline__ int64_t n_or(const int32_t* n_dev, int64_t n_max) {
     return n_dev ? static_cast<int64_t>(*n_dev) : n_max;
 }
 
+// Programmatic dependent launch: every kernel of the decode sequence waits
+// for its predecessor's completion (and memory) before touching anything,
+// then lets its successor be scheduled, so a kernel's launch overlaps the
+// one before it instead of following its completion -- in the stream and in
+// the captured graph (programmatic edges).
+__device__ __forceinline__ void pdl_entry() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+template <class... KArgs, class... Args>
+void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    MSFFT_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+}
+
 #define GRID_LOOP(i, n) \
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < (n); \
          i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+
+__global__ void zero_words(uint32_t* p, int64_t n) {
+    pdl_entry();
+    GRID_LOOP(i, n) p[i] = 0u;
+}
+
+// cudaMemsetAsync(p, 0, bytes) as a kernel of the programmatic chain
+void zero_async(void* p, size_t bytes, cudaStream_t st) {
+    const int64_t words = static_cast<int64_t>(bytes / 4);
+    launch_pdl(zero_words, grid_of(words), kT, 0, st, static_cast<uint32_t*>(p), words);
+}
 
 // ---------------------------------------------------------------- scans
 // Exclusive scan of in[0..len) into out (may alias); total -> *total.
 __global__ void __launch_bounds__(kScanT)
 scan_kernel(const int32_t* in, int64_t len_max, const int32_t* len_dev, int32_t* out,
             int32_t* total) {
+    pdl_entry();
     __shared__ int32_t part[kScanT];
     const int64_t len = n_or(len_dev, len_max);
     const int64_t per = (len + kScanT - 1) / kScanT;
@@ -64,6 +111,7 @@ __global__ void k3_tones(const DevPlan* __restrict__ P, int m, const int64_t* __
                          const int32_t* __restrict__ acc_n, int64_t* __restrict__ tone_u,
                          int64_t* __restrict__ tone_i, double2* __restrict__ gc,
                          int32_t* __restrict__ cnt) {
+    pdl_entry();
     const DevIter& it = P->it[m];
     const int64_t n = acc_n[0];
     const int64_t b = it.b, L = it.l_width, nmask = P->n - 1;
@@ -86,6 +134,7 @@ __global__ void k3_tones(const DevPlan* __restrict__ P, int m, const int64_t* __
 
 __global__ void k3_rot(const DevPlan* __restrict__ P, int m, const int32_t* __restrict__ acc_n,
                        const int64_t* __restrict__ tone_u, double2* __restrict__ rot) {
+    pdl_entry();
     const DevIter& it = P->it[m];
     const int nr = it.nrounds;
     const int64_t* taus = P->taus + it.tau_off;
@@ -99,6 +148,7 @@ __global__ void k3_rot(const DevPlan* __restrict__ P, int m, const int32_t* __re
 __global__ void k3_scatter(const DevPlan* __restrict__ P, int m, const int32_t* __restrict__ acc_n,
                            const int64_t* __restrict__ tone_i, const int32_t* __restrict__ start,
                            int32_t* __restrict__ cursor, int32_t* __restrict__ ev) {
+    pdl_entry();
     const int64_t b = P->it[m].b;
     const int64_t total = static_cast<int64_t>(acc_n[0]) * 3;
     GRID_LOOP(e, total) {
@@ -116,6 +166,7 @@ __global__ void k3_scatter(const DevPlan* __restrict__ P, int m, const int32_t* 
 __global__ void k3_segsort(const DevPlan* __restrict__ P, int m, const int32_t* __restrict__ start,
                            const int32_t* __restrict__ cnt, const int32_t* __restrict__ ev,
                            int32_t* __restrict__ ev2) {
+    pdl_entry();
     const int64_t b = P->it[m].b;
     const int lane = threadIdx.x & 31;
     const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -140,6 +191,7 @@ __global__ void __launch_bounds__(kLongT)
 k3_segsort_long(const DevPlan* __restrict__ P, int m, const int32_t* __restrict__ start,
                 const int32_t* __restrict__ cnt, const int32_t* __restrict__ ev,
                 int32_t* __restrict__ ev2) {
+    pdl_entry();
     __shared__ int32_t ks[kLongSmem];
     const int64_t b = P->it[m].b;
     for (int64_t beta = blockIdx.x; beta < b; beta += gridDim.x) {
@@ -185,6 +237,7 @@ __global__ void __launch_bounds__(kT)
 k3_sum(const DevPlan* __restrict__ P, int m, const int32_t* __restrict__ start,
        const int32_t* __restrict__ cnt, const int32_t* __restrict__ ev2,
        const double2* __restrict__ gc, const double2* __restrict__ rot, double2* __restrict__ Y) {
+    pdl_entry();
     __shared__ double2 stage[kT];
     const DevIter& it = P->it[m];
     const int64_t b = it.b;
@@ -228,6 +281,7 @@ k3_sum(const DevPlan* __restrict__ P, int m, const int32_t* __restrict__ start,
 __global__ void keys_from_values(const double2* __restrict__ v, int64_t n_max,
                                  const int32_t* __restrict__ n_dev, double* __restrict__ mag,
                                  uint64_t* __restrict__ key) {
+    pdl_entry();
     const int64_t n = n_or(n_dev, n_max);
     GRID_LOOP(j, n) {
         const double2 x = v[j];
@@ -239,6 +293,7 @@ __global__ void keys_from_values(const double2* __restrict__ v, int64_t n_max,
 
 __global__ void sel_init(uint64_t* sel, int64_t kth_host, const int32_t* kth_dev,
                          int64_t cap_kth) {
+    pdl_entry();
     int64_t kth = kth_dev ? static_cast<int64_t>(*kth_dev) : kth_host;
     if (kth > cap_kth) kth = cap_kth;
     sel[0] = 0;
@@ -249,6 +304,7 @@ __global__ void sel_init(uint64_t* sel, int64_t kth_host, const int32_t* kth_dev
 __global__ void __launch_bounds__(kT)
 sel_hist(const uint64_t* __restrict__ key, int64_t n_max, const int32_t* __restrict__ n_dev,
          const uint64_t* __restrict__ sel, int shift, int width, uint32_t* __restrict__ hist) {
+    pdl_entry();
     __shared__ uint32_t h[kSelBins];
     const int64_t n = n_or(n_dev, n_max);
     const uint64_t prefix = sel[0], mask = sel[1];
@@ -269,6 +325,7 @@ sel_hist(const uint64_t* __restrict__ key, int64_t n_max, const int32_t* __restr
 // prefix and the rank remaining inside the new class.
 __global__ void __launch_bounds__(kScanT)
 sel_pick(const uint32_t* __restrict__ hist, uint64_t* sel, int shift, int width) {
+    pdl_entry();
     __shared__ uint64_t part[kScanT];
     const uint64_t remaining = sel[2];
     if (remaining == 0) return;
@@ -307,6 +364,7 @@ sel_pick(const uint32_t* __restrict__ hist, uint64_t* sel, int shift, int width)
 __global__ void __launch_bounds__(kT)
 sel_count(const uint64_t* __restrict__ key, int64_t n_max, const int32_t* __restrict__ n_dev,
           const uint64_t* __restrict__ sel, int32_t* __restrict__ cgt, int32_t* __restrict__ ceq) {
+    pdl_entry();
     __shared__ int gt_s, eq_s;
     const int64_t n = n_or(n_dev, n_max);
     const uint64_t thr = sel[0];
@@ -335,6 +393,7 @@ __global__ void __launch_bounds__(kScanT)
 sel_offsets(const int32_t* __restrict__ cgt, const int32_t* __restrict__ ceq, int64_t nchunks,
             const uint64_t* __restrict__ sel, int32_t* __restrict__ off_sel,
             int32_t* __restrict__ off_eq) {
+    pdl_entry();
     __shared__ int32_t pg[kScanT], pe[kScanT];
     const int64_t per = (nchunks + kScanT - 1) / kScanT;
     const int64_t lo = threadIdx.x * per, hi = std::min<int64_t>(lo + per, nchunks);
@@ -369,6 +428,7 @@ __global__ void __launch_bounds__(kT)
 sel_write(const uint64_t* __restrict__ key, int64_t n_max, const int32_t* __restrict__ n_dev,
           const uint64_t* __restrict__ sel, const int32_t* __restrict__ off_sel,
           const int32_t* __restrict__ off_eq, int32_t* __restrict__ out_idx) {
+    pdl_entry();
     __shared__ int warp_sel[kT / 32], warp_eq[kT / 32];
     __shared__ int64_t run_sel, run_eq;
     const int64_t n = n_or(n_dev, n_max);
@@ -419,6 +479,7 @@ sel_write(const uint64_t* __restrict__ key, int64_t n_max, const int32_t* __rest
 __global__ void __launch_bounds__(kT)
 k4_rank(const int32_t* __restrict__ sel_idx, int64_t budget, const double* __restrict__ mag,
         int32_t* __restrict__ rank_out) {
+    pdl_entry();
     __shared__ double tm[kT];
     __shared__ int32_t ti[kT];
     const int64_t e = static_cast<int64_t>(blockIdx.x) * kT + threadIdx.x;
@@ -446,6 +507,7 @@ k4_rank(const int32_t* __restrict__ sel_idx, int64_t budget, const double* __res
 
 __global__ void k4_scatter(const int32_t* __restrict__ sel_idx, const int32_t* __restrict__ rank,
                            int64_t budget, int32_t* __restrict__ order) {
+    pdl_entry();
     GRID_LOOP(e, budget) {
         MSFFT_DCHECK(rank[e] >= 0 && rank[e] < budget);
         order[rank[e]] = sel_idx[e];
@@ -459,6 +521,7 @@ constexpr int kSmallK4 = 1024;
 __global__ void __launch_bounds__(kSmallK4)
 k4_small(const DevPlan* __restrict__ P, int m, const double2* __restrict__ Y,
          double* __restrict__ mag, int32_t* __restrict__ order, double* __restrict__ thr) {
+    pdl_entry();
     __shared__ double sm[kSmallK4];
     const DevIter& it = P->it[m];
     const int b = static_cast<int>(it.b);
@@ -486,12 +549,14 @@ k4_small(const DevPlan* __restrict__ P, int m, const double2* __restrict__ Y,
 
 __global__ void k4_thr(const int32_t* __restrict__ order, int64_t budget,
                        const double* __restrict__ mag, double* thr) {
+    pdl_entry();
     *thr = 0.2 * mag[order[budget - 1]];
 }
 
 // ---------------------------------------------------------------- K5
 __global__ void k5_stage(const DevPlan* __restrict__ P, int m, const int32_t* __restrict__ order,
                          const double2* __restrict__ Y, double2* __restrict__ yr) {
+    pdl_entry();
     const DevIter& it = P->it[m];
     const int nr = it.nrounds;
     const int64_t total = it.budget * nr;
@@ -503,6 +568,7 @@ __global__ void k5_stage(const DevPlan* __restrict__ P, int m, const int32_t* __
 
 __global__ void k5_phase(const DevPlan* __restrict__ P, int m, const double2* __restrict__ yr,
                          double* __restrict__ phi, int32_t* __restrict__ pcode) {
+    pdl_entry();
     const DevIter& it = P->it[m];
     const int nr = it.nrounds, ns = nr - 1;
     const int64_t total = it.budget * ns;
@@ -532,6 +598,7 @@ k5_locate(const DevPlan* __restrict__ P, int m, const int64_t* __restrict__ sigm
           const double* __restrict__ thr_p, const double2* __restrict__ yr,
           const double* __restrict__ phi_t, const int32_t* __restrict__ pcode,
           int64_t* __restrict__ cand_f, double2* __restrict__ cand_v, int32_t* __restrict__ err) {
+    pdl_entry();
     const DevIter& it = P->it[m];
     const int64_t n = P->n, nmask = n - 1;
     const double inv_n = P->inv_n;
@@ -635,6 +702,7 @@ k5_locate(const DevPlan* __restrict__ P, int m, const int64_t* __restrict__ sigm
 // k4_rank), then byf[pos] = rank.
 __global__ void __launch_bounds__(kT)
 k6_sortf(const int64_t* __restrict__ cand_f, int64_t budget, int32_t* __restrict__ pos_out) {
+    pdl_entry();
     __shared__ int64_t tf[kT];
     const int64_t r = static_cast<int64_t>(blockIdx.x) * kT + threadIdx.x;
     const int64_t fr = r < budget ? cand_f[r] : -1;
@@ -657,6 +725,7 @@ k6_sortf(const int64_t* __restrict__ cand_f, int64_t budget, int32_t* __restrict
 __global__ void k6_scatter(const int64_t* __restrict__ cand_f, const int32_t* __restrict__ pos,
                            int64_t budget, int32_t* __restrict__ byf,
                            int32_t* __restrict__ naccepted) {
+    pdl_entry();
     GRID_LOOP(r, budget) {
         if (cand_f[r] >= 0) {
             byf[pos[r]] = static_cast<int32_t>(r);
@@ -671,6 +740,7 @@ __global__ void k6_runs(const int64_t* __restrict__ cand_f, const double2* __res
                         const int32_t* __restrict__ byf, const int32_t* __restrict__ naccepted,
                         const int64_t* __restrict__ AF, const int32_t* __restrict__ acc_n,
                         double2* __restrict__ run_sum, int32_t* __restrict__ newflag) {
+    pdl_entry();
     const int64_t A = naccepted[0];
     const int an = acc_n[0];
     GRID_LOOP(p, A) {
@@ -699,6 +769,7 @@ __global__ void k6_runs(const int64_t* __restrict__ cand_f, const double2* __res
 __global__ void k6_newf(const int64_t* __restrict__ cand_f, const int32_t* __restrict__ byf,
                         const int32_t* __restrict__ naccepted, const int32_t* __restrict__ newflag,
                         const int32_t* __restrict__ newpos, int64_t* __restrict__ newf) {
+    pdl_entry();
     const int64_t A = naccepted[0];
     GRID_LOOP(p, A) {
         if (newflag[p]) newf[newpos[p]] = cand_f[byf[p]];
@@ -711,6 +782,7 @@ __global__ void k6_merge_acc(const int64_t* __restrict__ AF, const double2* __re
                              const int32_t* __restrict__ byf, const int32_t* __restrict__ naccepted,
                              const double2* __restrict__ run_sum, int64_t* __restrict__ NF,
                              double2* __restrict__ NC) {
+    pdl_entry();
     const int64_t an = acc_n[0];
     const int nnew = nnew_p[0];
     const int A = naccepted[0];
@@ -743,6 +815,7 @@ __global__ void k6_merge_new(const int64_t* __restrict__ AF, const int32_t* __re
                              const int32_t* __restrict__ newflag, const int32_t* __restrict__ newpos,
                              const double2* __restrict__ run_sum, int64_t* __restrict__ NF,
                              double2* __restrict__ NC) {
+    pdl_entry();
     const int64_t A = naccepted[0];
     const int an = acc_n[0];
     GRID_LOOP(p, A) {
@@ -770,6 +843,7 @@ k6_small(const DevPlan* __restrict__ P, int m, const int64_t* __restrict__ cand_
          const double2* __restrict__ cand_v, const int64_t* __restrict__ AF,
          const double2* __restrict__ AC, int32_t* __restrict__ scal, int64_t* __restrict__ NF,
          double2* __restrict__ NC) {
+    pdl_entry();
     __shared__ int64_t sf[kSmallK6];     // f by rank, then f at sorted position
     __shared__ int32_t byf[kSmallK6];    // rank at sorted position
     __shared__ double2 rsum[kSmallK6];   // run sums at run starts
@@ -884,6 +958,7 @@ k6_small(const DevPlan* __restrict__ P, int m, const int64_t* __restrict__ cand_
 }
 
 __global__ void k6_count(int32_t* scal, int64_t acc_cap) {
+    pdl_entry();
     MSFFT_DCHECK(scal[0] + scal[1] <= acc_cap);
     scal[0] += scal[1];  // acc_n += new_n
     scal[4] = 0;         // accepted counter for the next iteration
@@ -891,6 +966,7 @@ __global__ void k6_count(int32_t* scal, int64_t acc_cap) {
 
 // ---------------------------------------------------------------- K7
 __global__ void k7_kth(int32_t* scal, int64_t K) {
+    pdl_entry();
     scal[2] = static_cast<int32_t>(std::min<int64_t>(scal[0], K));
 }
 
@@ -898,6 +974,7 @@ __global__ void k7_emit(const int32_t* __restrict__ sel_idx, const int32_t* __re
                         const int64_t* __restrict__ AF, const double2* __restrict__ AC,
                         int64_t* __restrict__ out_f, double2* __restrict__ out_c,
                         int64_t* __restrict__ out_count) {
+    pdl_entry();
     const int64_t keep = scal[2];
     GRID_LOOP(p, keep) {
         const int32_t j = sel_idx[p];
@@ -967,14 +1044,14 @@ WideDecoder::WideDecoder(const DevPlan& plan, int64_t acc_cap, int64_t b_max, in
 
 void WideDecoder::select_kth(const uint64_t* key, int64_t n_max, const int32_t* n_dev,
                              int64_t kth_host, const int32_t* kth_dev, cudaStream_t st) {
-    sel_init<<<1, 1, 0, st>>>(sel_.get(), kth_host, kth_dev, n_max);
+    launch_pdl(sel_init, 1, 1, 0, st, sel_.get(), kth_host, kth_dev, n_max);
     for (int top = 64; top > 0;) {
         const int width = std::min(kSelBits, top);
         const int shift = top - width;
-        MSFFT_CUDA(cudaMemsetAsync(hist_.get(), 0, kSelBins * sizeof(uint32_t), st));
-        sel_hist<<<std::min<unsigned>(grid_of(n_max), 148), kT, 0, st>>>(
+        zero_async(hist_.get(), kSelBins * sizeof(uint32_t), st);
+        launch_pdl(sel_hist, std::min<unsigned>(grid_of(n_max), 148), kT, 0, st, 
             key, n_max, n_dev, sel_.get(), shift, width, hist_.get());
-        sel_pick<<<1, kScanT, 0, st>>>(hist_.get(), sel_.get(), shift, width);
+        launch_pdl(sel_pick, 1, kScanT, 0, st, hist_.get(), sel_.get(), shift, width);
         top = shift;
     }
     MSFFT_LAUNCH_CHECK("wide select");
@@ -983,11 +1060,11 @@ void WideDecoder::select_kth(const uint64_t* key, int64_t n_max, const int32_t* 
 void WideDecoder::compact_selected(const uint64_t* key, int64_t n_max, const int32_t* n_dev,
                                    int32_t* out_idx, cudaStream_t st) {
     const int64_t nch = (n_max + kChunk - 1) / kChunk;
-    sel_count<<<static_cast<unsigned>(nch), kT, 0, st>>>(key, n_max, n_dev, sel_.get(),
+    launch_pdl(sel_count, static_cast<unsigned>(nch), kT, 0, st, key, n_max, n_dev, sel_.get(),
                                                          chunk_gt_.get(), chunk_eq_.get());
-    sel_offsets<<<1, kScanT, 0, st>>>(chunk_gt_.get(), chunk_eq_.get(), nch, sel_.get(),
+    launch_pdl(sel_offsets, 1, kScanT, 0, st, chunk_gt_.get(), chunk_eq_.get(), nch, sel_.get(),
                                       chunk_off_sel_.get(), chunk_off_eq_.get());
-    sel_write<<<static_cast<unsigned>(nch), kT, 0, st>>>(key, n_max, n_dev, sel_.get(),
+    launch_pdl(sel_write, static_cast<unsigned>(nch), kT, 0, st, key, n_max, n_dev, sel_.get(),
                                                          chunk_off_sel_.get(), chunk_off_eq_.get(),
                                                          out_idx);
     MSFFT_LAUNCH_CHECK("wide compaction");
@@ -1037,7 +1114,7 @@ void WideDecoder::enqueue(double2* y, const int64_t* sigma, const int64_t* sigma
     int32_t* new_n = scal_.get() + 1;   // [1]
     int32_t* kth = scal_.get() + 2;     // [2]
     int32_t* naccepted = scal_.get() + 4;
-    MSFFT_CUDA(cudaMemsetAsync(scal_.get(), 0, 8 * sizeof(int32_t), st));
+    zero_async(scal_.get(), 8 * sizeof(int32_t), st);
     const unsigned gA = grid_of(acc_cap_ * 3);
     for (int m = 0; m < H.iters; ++m) {
         const DevIter& it = H.it[m];
@@ -1048,86 +1125,86 @@ void WideDecoder::enqueue(double2* y, const int64_t* sigma, const int64_t* sigma
         const double2* AC = acc_c_[cur].get();
         if (m > 0) {
             // ---- K3
-            MSFFT_CUDA(cudaMemsetAsync(cnt_.get(), 0, b * sizeof(int32_t), st));
-            MSFFT_CUDA(cudaMemsetAsync(cursor_.get(), 0, b * sizeof(int32_t), st));
-            k3_tones<<<grid_of(acc_cap_), kT, 0, st>>>(P, m, sigma, AF, AC, acc_n, tone_u_.get(),
+            zero_async(cnt_.get(), b * sizeof(int32_t), st);
+            zero_async(cursor_.get(), b * sizeof(int32_t), st);
+            launch_pdl(k3_tones, grid_of(acc_cap_), kT, 0, st, P, m, sigma, AF, AC, acc_n, tone_u_.get(),
                                                       tone_i_.get(), gc_.get(), cnt_.get());
-            k3_rot<<<grid_of(acc_cap_ * nr), kT, 0, st>>>(P, m, acc_n, tone_u_.get(), rot_.get());
-            scan_kernel<<<1, kScanT, 0, st>>>(cnt_.get(), b, nullptr, start_.get(), nullptr);
-            k3_scatter<<<gA, kT, 0, st>>>(P, m, acc_n, tone_i_.get(), start_.get(), cursor_.get(),
+            launch_pdl(k3_rot, grid_of(acc_cap_ * nr), kT, 0, st, P, m, acc_n, tone_u_.get(), rot_.get());
+            launch_pdl(scan_kernel, 1, kScanT, 0, st, cnt_.get(), b, nullptr, start_.get(), nullptr);
+            launch_pdl(k3_scatter, gA, kT, 0, st, P, m, acc_n, tone_i_.get(), start_.get(), cursor_.get(),
                                           ev_.get());
-            k3_segsort<<<grid_of(b * 32), kT, 0, st>>>(P, m, start_.get(), cnt_.get(), ev_.get(),
+            launch_pdl(k3_segsort, grid_of(b * 32), kT, 0, st, P, m, start_.get(), cnt_.get(), ev_.get(),
                                                        ev2_.get());
-            k3_segsort_long<<<static_cast<unsigned>(std::min<int64_t>(b, 148 * 2)), kLongT, 0, st>>>(
+            launch_pdl(k3_segsort_long, static_cast<unsigned>(std::min<int64_t>(b, 148 * 2)), kLongT, 0, st, 
                 P, m, start_.get(), cnt_.get(), ev_.get(), ev2_.get());
-            k3_sum<<<grid_of(nr * b * 32), kT, 0, st>>>(P, m, start_.get(), cnt_.get(), ev2_.get(),
+            launch_pdl(k3_sum, grid_of(nr * b * 32), kT, 0, st, P, m, start_.get(), cnt_.get(), ev2_.get(),
                                                         gc_.get(), rot_.get(), Y);
             MSFFT_LAUNCH_CHECK("wide K3");
         }
         // ---- K4
         if (b <= kSmallK4) {
-            k4_small<<<1, kSmallK4, 0, st>>>(P, m, Y, mag_.get(), order_.get(), thr_.get());
+            launch_pdl(k4_small, 1, kSmallK4, 0, st, P, m, Y, mag_.get(), order_.get(), thr_.get());
         } else {
-            keys_from_values<<<grid_of(b), kT, 0, st>>>(Y, b, nullptr, mag_.get(), key_.get());
+            launch_pdl(keys_from_values, grid_of(b), kT, 0, st, Y, b, nullptr, mag_.get(), key_.get());
             select_kth(key_.get(), b, nullptr, budget, nullptr, st);
             compact_selected(key_.get(), b, nullptr, sel_idx_.get(), st);
             {
                 const unsigned tiles = static_cast<unsigned>((budget + kT - 1) / kT);
                 const unsigned split = std::max(1u, std::min(32u, 296u / tiles));
-                MSFFT_CUDA(cudaMemsetAsync(pos_.get(), 0, budget * sizeof(int32_t), st));
-                k4_rank<<<dim3(tiles, split), kT, 0, st>>>(sel_idx_.get(), budget, mag_.get(), pos_.get());
-                k4_scatter<<<grid_of(budget), kT, 0, st>>>(sel_idx_.get(), pos_.get(), budget,
+                zero_async(pos_.get(), budget * sizeof(int32_t), st);
+                launch_pdl(k4_rank, dim3(tiles, split), kT, 0, st, sel_idx_.get(), budget, mag_.get(), pos_.get());
+                launch_pdl(k4_scatter, grid_of(budget), kT, 0, st, sel_idx_.get(), pos_.get(), budget,
                                                            order_.get());
             }
-            k4_thr<<<1, 1, 0, st>>>(order_.get(), budget, mag_.get(), thr_.get());
+            launch_pdl(k4_thr, 1, 1, 0, st, order_.get(), budget, mag_.get(), thr_.get());
         }
         // ---- K5
-        k5_stage<<<grid_of(budget * nr), kT, 0, st>>>(P, m, order_.get(), Y, yr_.get());
-        k5_phase<<<grid_of(budget * nr), kT, 0, st>>>(P, m, yr_.get(), phi_.get(), pcode_.get());
-        k5_locate<<<grid_of(budget * 32), kT, 0, st>>>(P, m, sigma_inv, order_.get(), mag_.get(),
+        launch_pdl(k5_stage, grid_of(budget * nr), kT, 0, st, P, m, order_.get(), Y, yr_.get());
+        launch_pdl(k5_phase, grid_of(budget * nr), kT, 0, st, P, m, yr_.get(), phi_.get(), pcode_.get());
+        launch_pdl(k5_locate, grid_of(budget * 32), kT, 0, st, P, m, sigma_inv, order_.get(), mag_.get(),
                                                        thr_.get(), yr_.get(), phi_.get(),
                                                        pcode_.get(), cand_f_.get(), cand_v_.get(),
                                                        err);
         MSFFT_LAUNCH_CHECK("wide K4/K5");
         // ---- K6
         if (budget <= kSmallK6 && acc_cap_ <= kSmallK6Acc) {
-            k6_small<<<1, kSmallK6, 0, st>>>(P, m, cand_f_.get(), cand_v_.get(), AF, AC, scal_.get(),
+            launch_pdl(k6_small, 1, kSmallK6, 0, st, P, m, cand_f_.get(), cand_v_.get(), AF, AC, scal_.get(),
                                              acc_f_[nxt].get(), acc_c_[nxt].get());
         } else {
             {
                 const unsigned tiles = static_cast<unsigned>((budget + kT - 1) / kT);
                 const unsigned split = std::max(1u, std::min(32u, 296u / tiles));
-                MSFFT_CUDA(cudaMemsetAsync(pos_.get(), 0, budget * sizeof(int32_t), st));
-                k6_sortf<<<dim3(tiles, split), kT, 0, st>>>(cand_f_.get(), budget, pos_.get());
-                k6_scatter<<<grid_of(budget), kT, 0, st>>>(cand_f_.get(), pos_.get(), budget, byf_.get(),
+                zero_async(pos_.get(), budget * sizeof(int32_t), st);
+                launch_pdl(k6_sortf, dim3(tiles, split), kT, 0, st, cand_f_.get(), budget, pos_.get());
+                launch_pdl(k6_scatter, grid_of(budget), kT, 0, st, cand_f_.get(), pos_.get(), budget, byf_.get(),
                                                            naccepted);
             }
-            k6_runs<<<grid_of(budget), kT, 0, st>>>(cand_f_.get(), cand_v_.get(), byf_.get(),
+            launch_pdl(k6_runs, grid_of(budget), kT, 0, st, cand_f_.get(), cand_v_.get(), byf_.get(),
                                                     naccepted, AF, acc_n, cand_sum_.get(),
                                                     newflag_.get());
-            scan_kernel<<<1, kScanT, 0, st>>>(newflag_.get(), budget, naccepted, newpos_.get(), new_n);
-            k6_newf<<<grid_of(budget), kT, 0, st>>>(cand_f_.get(), byf_.get(), naccepted,
+            launch_pdl(scan_kernel, 1, kScanT, 0, st, newflag_.get(), budget, naccepted, newpos_.get(), new_n);
+            launch_pdl(k6_newf, grid_of(budget), kT, 0, st, cand_f_.get(), byf_.get(), naccepted,
                                                     newflag_.get(), newpos_.get(), newf_.get());
-            k6_merge_acc<<<grid_of(acc_cap_), kT, 0, st>>>(AF, AC, acc_n, newf_.get(), new_n,
+            launch_pdl(k6_merge_acc, grid_of(acc_cap_), kT, 0, st, AF, AC, acc_n, newf_.get(), new_n,
                                                            cand_f_.get(), byf_.get(), naccepted,
                                                            cand_sum_.get(), acc_f_[nxt].get(),
                                                            acc_c_[nxt].get());
-            k6_merge_new<<<grid_of(budget), kT, 0, st>>>(AF, acc_n, cand_f_.get(), byf_.get(),
+            launch_pdl(k6_merge_new, grid_of(budget), kT, 0, st, AF, acc_n, cand_f_.get(), byf_.get(),
                                                          naccepted, newflag_.get(), newpos_.get(),
                                                          cand_sum_.get(), acc_f_[nxt].get(),
                                                          acc_c_[nxt].get());
-            k6_count<<<1, 1, 0, st>>>(scal_.get(), acc_cap_);
+            launch_pdl(k6_count, 1, 1, 0, st, scal_.get(), acc_cap_);
         }
         MSFFT_LAUNCH_CHECK("wide K6");
     }
     // ---- K7: the K largest |c| (stable over ascending f), emitted in f order
     const int fin = H.iters & 1;
-    keys_from_values<<<grid_of(acc_cap_), kT, 0, st>>>(acc_c_[fin].get(), acc_cap_, acc_n, nullptr,
+    launch_pdl(keys_from_values, grid_of(acc_cap_), kT, 0, st, acc_c_[fin].get(), acc_cap_, acc_n, nullptr,
                                                        key_.get());
-    k7_kth<<<1, 1, 0, st>>>(scal_.get(), H.k);
+    launch_pdl(k7_kth, 1, 1, 0, st, scal_.get(), H.k);
     select_kth(key_.get(), acc_cap_, acc_n, 0, kth, st);
     compact_selected(key_.get(), acc_cap_, acc_n, sel_idx_.get(), st);
-    k7_emit<<<grid_of(H.k), kT, 0, st>>>(sel_idx_.get(), scal_.get(), acc_f_[fin].get(),
+    launch_pdl(k7_emit, grid_of(H.k), kT, 0, st, sel_idx_.get(), scal_.get(), acc_f_[fin].get(),
                                          acc_c_[fin].get(), out_f, out_c, out_count);
     MSFFT_LAUNCH_CHECK("wide K7");
 }
