@@ -291,24 +291,37 @@ __global__ void keys_from_values(const double2* __restrict__ v, int64_t n_max,
     }
 }
 
+// sel = {prefix, prefix mask, rank remaining, blocks done}; also clears the
+// digit histogram for the first pass (each pass's last block clears it for
+// the next).
 __global__ void sel_init(uint64_t* sel, int64_t kth_host, const int32_t* kth_dev,
-                         int64_t cap_kth) {
+                         int64_t cap_kth, uint32_t* hist) {
     pdl_entry();
-    int64_t kth = kth_dev ? static_cast<int64_t>(*kth_dev) : kth_host;
-    if (kth > cap_kth) kth = cap_kth;
-    sel[0] = 0;
-    sel[1] = 0;
-    sel[2] = static_cast<uint64_t>(kth);
+    for (int i = threadIdx.x; i < kSelBins; i += blockDim.x) hist[i] = 0u;
+    if (threadIdx.x == 0) {
+        int64_t kth = kth_dev ? static_cast<int64_t>(*kth_dev) : kth_host;
+        if (kth > cap_kth) kth = cap_kth;
+        sel[0] = 0;
+        sel[1] = 0;
+        sel[2] = static_cast<uint64_t>(kth);
+        sel[3] = 0;
+    }
 }
 
+// One radix-select digit in one launch: every block histograms its keys
+// (those matching the prefix) into the global histogram; the last block to
+// finish picks the digit of the kth largest (suffix counts over the bins), updates sel,
+// and clears the histogram and the block count for the next digit.
 __global__ void __launch_bounds__(kT)
-sel_hist(const uint64_t* __restrict__ key, int64_t n_max, const int32_t* __restrict__ n_dev,
-         const uint64_t* __restrict__ sel, int shift, int width, uint32_t* __restrict__ hist) {
+sel_digit(const uint64_t* __restrict__ key, int64_t n_max, const int32_t* __restrict__ n_dev,
+          uint64_t* sel, int shift, int width, uint32_t* hist) {
     pdl_entry();
     __shared__ uint32_t h[kSelBins];
+    __shared__ uint64_t part[kT];
+    __shared__ int last;
     const int64_t n = n_or(n_dev, n_max);
-    const uint64_t prefix = sel[0], mask = sel[1];
-    if (sel[2] == 0) return;
+    const uint64_t prefix = sel[0], mask = sel[1], remaining = sel[2];
+    if (remaining == 0) return;  // uniform: every block returns, hist stays clear
     const uint64_t dmask = (uint64_t{1} << width) - 1;
     for (int i = threadIdx.x; i < kSelBins; i += kT) h[i] = 0;
     __syncthreads();
@@ -319,29 +332,28 @@ sel_hist(const uint64_t* __restrict__ key, int64_t n_max, const int32_t* __restr
     __syncthreads();
     for (int i = threadIdx.x; i < kSelBins; i += kT)
         if (h[i]) atomicAdd(&hist[i], h[i]);
-}
-
-// Digit of the kth largest among the keys matching the prefix; updates the
-// prefix and the rank remaining inside the new class.
-__global__ void __launch_bounds__(kScanT)
-sel_pick(const uint32_t* __restrict__ hist, uint64_t* sel, int shift, int width) {
-    pdl_entry();
-    __shared__ uint64_t part[kScanT];
-    const uint64_t remaining = sel[2];
-    if (remaining == 0) return;
-    constexpr int per = kSelBins / kScanT;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(reinterpret_cast<unsigned long long*>(&sel[3]), 1ull) ==
+               static_cast<unsigned long long>(gridDim.x) - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    constexpr int per = kSelBins / kT;
     const int t = threadIdx.x;
     uint32_t hv[per];
     uint64_t s = 0;
 #pragma unroll
     for (int i = 0; i < per; ++i) {
-        hv[i] = hist[t * per + i];
+        hv[i] = __ldcg(&hist[t * per + i]);
         s += hv[i];
     }
     part[t] = s;
     __syncthreads();
-    for (int o = 1; o < kScanT; o <<= 1) {  // suffix sums over threads >= t
-        const uint64_t v = t + o < kScanT ? part[t + o] : 0;
+    for (int o = 1; o < kT; o <<= 1) {  // suffix sums over threads >= t
+        const uint64_t v = t + o < kT ? part[t + o] : 0;
         __syncthreads();
         part[t] += v;
         __syncthreads();
@@ -352,13 +364,15 @@ sel_pick(const uint32_t* __restrict__ hist, uint64_t* sel, int shift, int width)
 #pragma unroll
         for (int i = per - 1; i >= 0; --i) {
             if (cum + hv[i] >= remaining && cum < remaining) {
-                sel[0] |= static_cast<uint64_t>(t * per + i) << shift;
-                sel[1] |= ((uint64_t{1} << width) - 1) << shift;
+                sel[0] = prefix | static_cast<uint64_t>(t * per + i) << shift;
+                sel[1] = mask | ((uint64_t{1} << width) - 1) << shift;
                 sel[2] = remaining - cum;
             }
             cum += hv[i];
         }
     }
+    for (int i = t; i < kSelBins; i += kT) hist[i] = 0u;
+    if (t == 0) sel[3] = 0;
 }
 
 __global__ void __launch_bounds__(kT)
@@ -1044,14 +1058,12 @@ WideDecoder::WideDecoder(const DevPlan& plan, int64_t acc_cap, int64_t b_max, in
 
 void WideDecoder::select_kth(const uint64_t* key, int64_t n_max, const int32_t* n_dev,
                              int64_t kth_host, const int32_t* kth_dev, cudaStream_t st) {
-    launch_pdl(sel_init, 1, 1, 0, st, sel_.get(), kth_host, kth_dev, n_max);
+    launch_pdl(sel_init, 1, kT, 0, st, sel_.get(), kth_host, kth_dev, n_max, hist_.get());
     for (int top = 64; top > 0;) {
         const int width = std::min(kSelBits, top);
         const int shift = top - width;
-        zero_async(hist_.get(), kSelBins * sizeof(uint32_t), st);
-        launch_pdl(sel_hist, std::min<unsigned>(grid_of(n_max), 148), kT, 0, st, 
-            key, n_max, n_dev, sel_.get(), shift, width, hist_.get());
-        launch_pdl(sel_pick, 1, kScanT, 0, st, hist_.get(), sel_.get(), shift, width);
+        launch_pdl(sel_digit, std::min<unsigned>(grid_of(n_max), 148), kT, 0, st, key, n_max, n_dev,
+                   sel_.get(), shift, width, hist_.get());
         top = shift;
     }
     MSFFT_LAUNCH_CHECK("wide select");
