@@ -19,14 +19,6 @@ constexpr int kScanT = 1024;
 constexpr int kLongSeg = 64;          // longer event segments sort with a whole CTA
 constexpr int kLongSmem = 8192;
 
-bool pdl_enabled() {
-    static const bool v = [] {
-        const char* e = std::getenv("MSFFT_WIDE_PDL");
-        return !e || std::atoi(e) != 0;
-    }();
-    return v;
-}
-
 unsigned grid_of(int64_t work) {
     return static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>((work + kT - 1) / kT, 148 * 16)));
 }
@@ -46,8 +38,8 @@ __device__ __forceinline__ void pdl_entry() {
 }
 
 template <class... KArgs, class... Args>
-void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
-                Args&&... args) {
+void launch_pdl(bool pdl, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                cudaStream_t st, Args&&... args) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
     cfg.blockDim = block;
@@ -55,7 +47,7 @@ void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cu
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     MSFFT_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
@@ -71,9 +63,9 @@ __global__ void zero_words(uint32_t* p, int64_t n) {
 }
 
 // cudaMemsetAsync(p, 0, bytes) as a kernel of the programmatic chain
-void zero_async(void* p, size_t bytes, cudaStream_t st) {
+void zero_async(bool pdl, void* p, size_t bytes, cudaStream_t st) {
     const int64_t words = static_cast<int64_t>(bytes / 4);
-    launch_pdl(zero_words, grid_of(words), kT, 0, st, static_cast<uint32_t*>(p), words);
+    launch_pdl(pdl, zero_words, grid_of(words), kT, 0, st, static_cast<uint32_t*>(p), words);
 }
 
 // ---------------------------------------------------------------- scans
@@ -1053,16 +1045,17 @@ WideDecoder::WideDecoder(const DevPlan& plan, int64_t acc_cap, int64_t b_max, in
     out_c_.reset(std::max<int64_t>(plan.k, 1));
     out_count_.reset(1);
     if (const char* e = std::getenv("MSFFT_WIDE_GRAPH")) use_graphs_ = std::atoi(e) != 0;
+    if (const char* e = std::getenv("MSFFT_WIDE_PDL")) pdl_ = std::atoi(e) != 0;
     // kernel attributes are set before any capture
 }
 
 void WideDecoder::select_kth(const uint64_t* key, int64_t n_max, const int32_t* n_dev,
                              int64_t kth_host, const int32_t* kth_dev, cudaStream_t st) {
-    launch_pdl(sel_init, 1, kT, 0, st, sel_.get(), kth_host, kth_dev, n_max, hist_.get());
+    launch_pdl(pdl_, sel_init, 1, kT, 0, st, sel_.get(), kth_host, kth_dev, n_max, hist_.get());
     for (int top = 64; top > 0;) {
         const int width = std::min(kSelBits, top);
         const int shift = top - width;
-        launch_pdl(sel_digit, std::min<unsigned>(grid_of(n_max), 148), kT, 0, st, key, n_max, n_dev,
+        launch_pdl(pdl_, sel_digit, std::min<unsigned>(grid_of(n_max), 148), kT, 0, st, key, n_max, n_dev,
                    sel_.get(), shift, width, hist_.get());
         top = shift;
     }
@@ -1072,11 +1065,11 @@ void WideDecoder::select_kth(const uint64_t* key, int64_t n_max, const int32_t* 
 void WideDecoder::compact_selected(const uint64_t* key, int64_t n_max, const int32_t* n_dev,
                                    int32_t* out_idx, cudaStream_t st) {
     const int64_t nch = (n_max + kChunk - 1) / kChunk;
-    launch_pdl(sel_count, static_cast<unsigned>(nch), kT, 0, st, key, n_max, n_dev, sel_.get(),
+    launch_pdl(pdl_, sel_count, static_cast<unsigned>(nch), kT, 0, st, key, n_max, n_dev, sel_.get(),
                                                          chunk_gt_.get(), chunk_eq_.get());
-    launch_pdl(sel_offsets, 1, kScanT, 0, st, chunk_gt_.get(), chunk_eq_.get(), nch, sel_.get(),
+    launch_pdl(pdl_, sel_offsets, 1, kScanT, 0, st, chunk_gt_.get(), chunk_eq_.get(), nch, sel_.get(),
                                       chunk_off_sel_.get(), chunk_off_eq_.get());
-    launch_pdl(sel_write, static_cast<unsigned>(nch), kT, 0, st, key, n_max, n_dev, sel_.get(),
+    launch_pdl(pdl_, sel_write, static_cast<unsigned>(nch), kT, 0, st, key, n_max, n_dev, sel_.get(),
                                                          chunk_off_sel_.get(), chunk_off_eq_.get(),
                                                          out_idx);
     MSFFT_LAUNCH_CHECK("wide compaction");
@@ -1126,7 +1119,7 @@ void WideDecoder::enqueue(double2* y, const int64_t* sigma, const int64_t* sigma
     int32_t* new_n = scal_.get() + 1;   // [1]
     int32_t* kth = scal_.get() + 2;     // [2]
     int32_t* naccepted = scal_.get() + 4;
-    zero_async(scal_.get(), 8 * sizeof(int32_t), st);
+    zero_async(pdl_, scal_.get(), 8 * sizeof(int32_t), st);
     const unsigned gA = grid_of(acc_cap_ * 3);
     for (int m = 0; m < H.iters; ++m) {
         const DevIter& it = H.it[m];
@@ -1137,86 +1130,86 @@ void WideDecoder::enqueue(double2* y, const int64_t* sigma, const int64_t* sigma
         const double2* AC = acc_c_[cur].get();
         if (m > 0) {
             // ---- K3
-            zero_async(cnt_.get(), b * sizeof(int32_t), st);
-            zero_async(cursor_.get(), b * sizeof(int32_t), st);
-            launch_pdl(k3_tones, grid_of(acc_cap_), kT, 0, st, P, m, sigma, AF, AC, acc_n, tone_u_.get(),
+            zero_async(pdl_, cnt_.get(), b * sizeof(int32_t), st);
+            zero_async(pdl_, cursor_.get(), b * sizeof(int32_t), st);
+            launch_pdl(pdl_, k3_tones, grid_of(acc_cap_), kT, 0, st, P, m, sigma, AF, AC, acc_n, tone_u_.get(),
                                                       tone_i_.get(), gc_.get(), cnt_.get());
-            launch_pdl(k3_rot, grid_of(acc_cap_ * nr), kT, 0, st, P, m, acc_n, tone_u_.get(), rot_.get());
-            launch_pdl(scan_kernel, 1, kScanT, 0, st, cnt_.get(), b, nullptr, start_.get(), nullptr);
-            launch_pdl(k3_scatter, gA, kT, 0, st, P, m, acc_n, tone_i_.get(), start_.get(), cursor_.get(),
+            launch_pdl(pdl_, k3_rot, grid_of(acc_cap_ * nr), kT, 0, st, P, m, acc_n, tone_u_.get(), rot_.get());
+            launch_pdl(pdl_, scan_kernel, 1, kScanT, 0, st, cnt_.get(), b, nullptr, start_.get(), nullptr);
+            launch_pdl(pdl_, k3_scatter, gA, kT, 0, st, P, m, acc_n, tone_i_.get(), start_.get(), cursor_.get(),
                                           ev_.get());
-            launch_pdl(k3_segsort, grid_of(b * 32), kT, 0, st, P, m, start_.get(), cnt_.get(), ev_.get(),
+            launch_pdl(pdl_, k3_segsort, grid_of(b * 32), kT, 0, st, P, m, start_.get(), cnt_.get(), ev_.get(),
                                                        ev2_.get());
-            launch_pdl(k3_segsort_long, static_cast<unsigned>(std::min<int64_t>(b, 148 * 2)), kLongT, 0, st, 
+            launch_pdl(pdl_, k3_segsort_long, static_cast<unsigned>(std::min<int64_t>(b, 148 * 2)), kLongT, 0, st, 
                 P, m, start_.get(), cnt_.get(), ev_.get(), ev2_.get());
-            launch_pdl(k3_sum, grid_of(nr * b * 32), kT, 0, st, P, m, start_.get(), cnt_.get(), ev2_.get(),
+            launch_pdl(pdl_, k3_sum, grid_of(nr * b * 32), kT, 0, st, P, m, start_.get(), cnt_.get(), ev2_.get(),
                                                         gc_.get(), rot_.get(), Y);
             MSFFT_LAUNCH_CHECK("wide K3");
         }
         // ---- K4
         if (b <= kSmallK4) {
-            launch_pdl(k4_small, 1, kSmallK4, 0, st, P, m, Y, mag_.get(), order_.get(), thr_.get());
+            launch_pdl(pdl_, k4_small, 1, kSmallK4, 0, st, P, m, Y, mag_.get(), order_.get(), thr_.get());
         } else {
-            launch_pdl(keys_from_values, grid_of(b), kT, 0, st, Y, b, nullptr, mag_.get(), key_.get());
+            launch_pdl(pdl_, keys_from_values, grid_of(b), kT, 0, st, Y, b, nullptr, mag_.get(), key_.get());
             select_kth(key_.get(), b, nullptr, budget, nullptr, st);
             compact_selected(key_.get(), b, nullptr, sel_idx_.get(), st);
             {
                 const unsigned tiles = static_cast<unsigned>((budget + kT - 1) / kT);
                 const unsigned split = std::max(1u, std::min(32u, 296u / tiles));
-                zero_async(pos_.get(), budget * sizeof(int32_t), st);
-                launch_pdl(k4_rank, dim3(tiles, split), kT, 0, st, sel_idx_.get(), budget, mag_.get(), pos_.get());
-                launch_pdl(k4_scatter, grid_of(budget), kT, 0, st, sel_idx_.get(), pos_.get(), budget,
+                zero_async(pdl_, pos_.get(), budget * sizeof(int32_t), st);
+                launch_pdl(pdl_, k4_rank, dim3(tiles, split), kT, 0, st, sel_idx_.get(), budget, mag_.get(), pos_.get());
+                launch_pdl(pdl_, k4_scatter, grid_of(budget), kT, 0, st, sel_idx_.get(), pos_.get(), budget,
                                                            order_.get());
             }
-            launch_pdl(k4_thr, 1, 1, 0, st, order_.get(), budget, mag_.get(), thr_.get());
+            launch_pdl(pdl_, k4_thr, 1, 1, 0, st, order_.get(), budget, mag_.get(), thr_.get());
         }
         // ---- K5
-        launch_pdl(k5_stage, grid_of(budget * nr), kT, 0, st, P, m, order_.get(), Y, yr_.get());
-        launch_pdl(k5_phase, grid_of(budget * nr), kT, 0, st, P, m, yr_.get(), phi_.get(), pcode_.get());
-        launch_pdl(k5_locate, grid_of(budget * 32), kT, 0, st, P, m, sigma_inv, order_.get(), mag_.get(),
+        launch_pdl(pdl_, k5_stage, grid_of(budget * nr), kT, 0, st, P, m, order_.get(), Y, yr_.get());
+        launch_pdl(pdl_, k5_phase, grid_of(budget * nr), kT, 0, st, P, m, yr_.get(), phi_.get(), pcode_.get());
+        launch_pdl(pdl_, k5_locate, grid_of(budget * 32), kT, 0, st, P, m, sigma_inv, order_.get(), mag_.get(),
                                                        thr_.get(), yr_.get(), phi_.get(),
                                                        pcode_.get(), cand_f_.get(), cand_v_.get(),
                                                        err);
         MSFFT_LAUNCH_CHECK("wide K4/K5");
         // ---- K6
         if (budget <= kSmallK6 && acc_cap_ <= kSmallK6Acc) {
-            launch_pdl(k6_small, 1, kSmallK6, 0, st, P, m, cand_f_.get(), cand_v_.get(), AF, AC, scal_.get(),
+            launch_pdl(pdl_, k6_small, 1, kSmallK6, 0, st, P, m, cand_f_.get(), cand_v_.get(), AF, AC, scal_.get(),
                                              acc_f_[nxt].get(), acc_c_[nxt].get());
         } else {
             {
                 const unsigned tiles = static_cast<unsigned>((budget + kT - 1) / kT);
                 const unsigned split = std::max(1u, std::min(32u, 296u / tiles));
-                zero_async(pos_.get(), budget * sizeof(int32_t), st);
-                launch_pdl(k6_sortf, dim3(tiles, split), kT, 0, st, cand_f_.get(), budget, pos_.get());
-                launch_pdl(k6_scatter, grid_of(budget), kT, 0, st, cand_f_.get(), pos_.get(), budget, byf_.get(),
+                zero_async(pdl_, pos_.get(), budget * sizeof(int32_t), st);
+                launch_pdl(pdl_, k6_sortf, dim3(tiles, split), kT, 0, st, cand_f_.get(), budget, pos_.get());
+                launch_pdl(pdl_, k6_scatter, grid_of(budget), kT, 0, st, cand_f_.get(), pos_.get(), budget, byf_.get(),
                                                            naccepted);
             }
-            launch_pdl(k6_runs, grid_of(budget), kT, 0, st, cand_f_.get(), cand_v_.get(), byf_.get(),
+            launch_pdl(pdl_, k6_runs, grid_of(budget), kT, 0, st, cand_f_.get(), cand_v_.get(), byf_.get(),
                                                     naccepted, AF, acc_n, cand_sum_.get(),
                                                     newflag_.get());
-            launch_pdl(scan_kernel, 1, kScanT, 0, st, newflag_.get(), budget, naccepted, newpos_.get(), new_n);
-            launch_pdl(k6_newf, grid_of(budget), kT, 0, st, cand_f_.get(), byf_.get(), naccepted,
+            launch_pdl(pdl_, scan_kernel, 1, kScanT, 0, st, newflag_.get(), budget, naccepted, newpos_.get(), new_n);
+            launch_pdl(pdl_, k6_newf, grid_of(budget), kT, 0, st, cand_f_.get(), byf_.get(), naccepted,
                                                     newflag_.get(), newpos_.get(), newf_.get());
-            launch_pdl(k6_merge_acc, grid_of(acc_cap_), kT, 0, st, AF, AC, acc_n, newf_.get(), new_n,
+            launch_pdl(pdl_, k6_merge_acc, grid_of(acc_cap_), kT, 0, st, AF, AC, acc_n, newf_.get(), new_n,
                                                            cand_f_.get(), byf_.get(), naccepted,
                                                            cand_sum_.get(), acc_f_[nxt].get(),
                                                            acc_c_[nxt].get());
-            launch_pdl(k6_merge_new, grid_of(budget), kT, 0, st, AF, acc_n, cand_f_.get(), byf_.get(),
+            launch_pdl(pdl_, k6_merge_new, grid_of(budget), kT, 0, st, AF, acc_n, cand_f_.get(), byf_.get(),
                                                          naccepted, newflag_.get(), newpos_.get(),
                                                          cand_sum_.get(), acc_f_[nxt].get(),
                                                          acc_c_[nxt].get());
-            launch_pdl(k6_count, 1, 1, 0, st, scal_.get(), acc_cap_);
+            launch_pdl(pdl_, k6_count, 1, 1, 0, st, scal_.get(), acc_cap_);
         }
         MSFFT_LAUNCH_CHECK("wide K6");
     }
     // ---- K7: the K largest |c| (stable over ascending f), emitted in f order
     const int fin = H.iters & 1;
-    launch_pdl(keys_from_values, grid_of(acc_cap_), kT, 0, st, acc_c_[fin].get(), acc_cap_, acc_n, nullptr,
+    launch_pdl(pdl_, keys_from_values, grid_of(acc_cap_), kT, 0, st, acc_c_[fin].get(), acc_cap_, acc_n, nullptr,
                                                        key_.get());
-    launch_pdl(k7_kth, 1, 1, 0, st, scal_.get(), H.k);
+    launch_pdl(pdl_, k7_kth, 1, 1, 0, st, scal_.get(), H.k);
     select_kth(key_.get(), acc_cap_, acc_n, 0, kth, st);
     compact_selected(key_.get(), acc_cap_, acc_n, sel_idx_.get(), st);
-    launch_pdl(k7_emit, grid_of(H.k), kT, 0, st, sel_idx_.get(), scal_.get(), acc_f_[fin].get(),
+    launch_pdl(pdl_, k7_emit, grid_of(H.k), kT, 0, st, sel_idx_.get(), scal_.get(), acc_f_[fin].get(),
                                          acc_c_[fin].get(), out_f, out_c, out_count);
     MSFFT_LAUNCH_CHECK("wide K7");
 }

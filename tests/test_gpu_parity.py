@@ -267,6 +267,29 @@ def test_wide_decode_bit_identical_to_cta_decode(oracle, monkeypatch, n, k, dtyp
     assert np.array_equal(f1, f0) and np.array_equal(c1, c0)
 
 
+@pytest.mark.parametrize("knob,values", [("MSFFT_ENC_SPLIT", ("1", "0")),
+                                         ("MSFFT_WIDE_PDL", ("1", "0")),
+                                         ("MSFFT_WIDE_GRAPH", ("1", "0"))])
+def test_launch_knobs_bit_identical(oracle, monkeypatch, knob, values):
+    """Launch-shape knobs change only how the work is spread over CTAs and
+    launches: per-segment encode tasks (small launches), programmatic edges
+    and the CUDA graph of the wide decode.  Results are bit-identical."""
+    n, k = 1 << 19, 1200
+    x, _, _ = __import__("paper_2011_05698_b200.workloads", fromlist=["x"]).make_signal_np(
+        n, k, 9, 20.0, "complex128", "loguniform_0.1_10")
+    res = []
+    for v in values:
+        monkeypatch.setenv(knob, v)
+        plan = M.Plan(n, k, M.MultiscaleConfig(), 1e-6, "complex128")
+        res.append(plan.execute(x[None, :], [321]))
+        res.append(plan.execute(x[None, :], [321], assume_valid=True))  # graph replay
+    f0, c0, n0, _ = res[0]
+    assert int(n0[0]) > 0
+    for f, c, cnt, _ in res[1:]:
+        assert int(cnt[0]) == int(n0[0])
+        assert np.array_equal(f, f0) and np.array_equal(c, c0)
+
+
 def test_sparse_ingest_split_validation(oracle, monkeypatch):
     """Pinned host batches split validation between the copy engine + device
     check (first rows) and the host's fused scan+gather (the rest): a
