@@ -165,6 +165,15 @@ __host__ __device__ inline double position_phase(double u, int64_t tau, int64_t 
     return x * kTwoPi * inv_n;
 }
 
+// The same with n and tau already converted to double (the decode's stage
+// chain keeps them in registers).
+__host__ __device__ inline double position_phase_d(double u, double tau, double nd, double inv_n) {
+    const double p = u * tau;
+    double x = p - trunc(p * inv_n) * nd;  // fmod(p, n), exact
+    if (x < 0) x += nd;
+    return x * kTwoPi * inv_n;
+}
+
 // circular_phase_distance (proj/src/locate.cpp:14-17).  Both phases lie in
 // [0, 2pi], so |a-b| <= 2pi and fmod reduces to one exact subtraction.
 __host__ __device__ inline double circular_phase_distance(double a, double b) {

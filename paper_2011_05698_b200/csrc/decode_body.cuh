@@ -392,8 +392,10 @@ __device__ __forceinline__ void decode_signal(const DevPlan& plan, const DecLayo
         // ranked bucket; the region length evolves identically for every
         // bucket, so all groups run the same number of stages and the
         // shuffles stay convergent.
+        // stage-chain operands converted once: q/2, n and the taus as doubles
         const int64_t lcfg = plan.l;
-        const double q = plan.q;
+        const double q = plan.q, hq = plan.q / 2.0, nd_r = static_cast<double>(n), inv_n_r = inv_n;
+        const int nst_r = it.nstage_tab;
         // group size: enough lanes for the l blocks, shrunk (each lane then
         // scans several blocks) until every ranked bucket fits in one pass
         int gsz = lcfg > 16 ? 32 : (lcfg > 8 ? 16 : (lcfg > 4 ? 8 : 4));
@@ -416,7 +418,7 @@ __device__ __forceinline__ void decode_signal(const DevPlan& plan, const DecLayo
             if (ok && y0.x == 0.0 && y0.y == 0.0) ok = false;
             double u_min = (2.0 * static_cast<double>(beta) - 1.0) * Ld / 2.0;
             double len = Ld;
-            const int nst = it.nstage_tab;  // host-precomputed stage lengths (or -1)
+            const int nst = nst_r;  // host-precomputed stage lengths (or -1)
             if (nst >= 0 && nst < nr) {
                 // the usual case: the stage count and every stage's operands
                 // are known up front, so the next stage's phase code, phase,
@@ -427,11 +429,11 @@ __device__ __forceinline__ void decode_signal(const DevPlan& plan, const DecLayo
                 int code_n = live && nst > 0 ? S.pcode[pe0] : 1;
                 double phi_n = live && nst > 0 ? S.phi[pe0] : 0.0;
                 double rblk_n = sh.st_blk[0], len_n = sh.st_len[1];
-                int64_t tau_n = tau_at(1);
+                double tau_n = static_cast<double>(tau_at(1));
                 for (int stage = 1; stage <= nst; ++stage) {
                     const int code = code_n;
                     const double phi = phi_n, rblk = rblk_n, nlen = len_n;
-                    const int64_t tau = tau_n;
+                    const double tau = tau_n;
                     if (stage < nst) {
                         if (live) {
                             code_n = S.pcode[pe0 + stage];
@@ -439,7 +441,7 @@ __device__ __forceinline__ void decode_signal(const DevPlan& plan, const DecLayo
                         }
                         rblk_n = sh.st_blk[stage];
                         len_n = sh.st_len[stage + 1];
-                        tau_n = tau_at(stage + 1);
+                        tau_n = static_cast<double>(tau_at(stage + 1));
                     }
                     if (ok && code != 0) {
                         // 1: locate_frequency returns nullopt; 2: phase_of throws
@@ -451,7 +453,7 @@ __device__ __forceinline__ void decode_signal(const DevPlan& plan, const DecLayo
                     for (int64_t j = glane; j < lcfg; j += gsz) {
                         const double center = u_min + (static_cast<double>(j) + 0.5) * rblk;
                         const double d = circular_phase_distance(
-                            position_phase(center, tau, n, inv_n), phi);
+                            position_phase_d(center, tau, nd_r, inv_n_r), phi);
                         if (d < best_d) {
                             best_d = d;
                             best_j = static_cast<int>(j);
@@ -466,7 +468,7 @@ __device__ __forceinline__ void decode_signal(const DevPlan& plan, const DecLayo
                         }
                     }
                     if (best_j == 0x7fffffff) best_j = 0;
-                    u_min = u_min + (static_cast<double>(best_j) - q / 2.0) * rblk;
+                    u_min = u_min + (static_cast<double>(best_j) - hq) * rblk;
                     len = nlen;
                 }
             } else {
@@ -524,8 +526,7 @@ __device__ __forceinline__ void decode_signal(const DevPlan& plan, const DecLayo
                 const double lo = u_min, hi = u_min + len;
                 int64_t u = static_cast<int64_t>(ceil(lo));
                 if (!(static_cast<double>(u) < hi)) u = llround(0.5 * (lo + hi));
-                u %= n;
-                if (u < 0) u += n;
+                u &= nmask;  // u mod n (n is a power of two): locate.cpp:120-121
                 const int64_t i = static_cast<int64_t>(floor(static_cast<double>(u) * invL + 0.5));
                 const double g = ghat_at(it, i * L - u);
                 if (!(fabs(g) < 0.5)) {

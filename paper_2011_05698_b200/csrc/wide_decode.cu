@@ -687,8 +687,7 @@ k5_locate(const DevPlan* __restrict__ P, int m, const int64_t* __restrict__ sigm
             const double lo = u_min, hi = u_min + len;
             int64_t u = static_cast<int64_t>(ceil(lo));
             if (!(static_cast<double>(u) < hi)) u = llround(0.5 * (lo + hi));
-            u %= n;
-            if (u < 0) u += n;
+            u &= nmask;  // u mod n (n is a power of two): locate.cpp:120-121
             const int64_t i = static_cast<int64_t>(floor(static_cast<double>(u) * invL + 0.5));
             const double g = ghat_at(it, i * L - u);
             if (!(fabs(g) < 0.5)) {
