@@ -264,11 +264,19 @@ def main():
     import paper_2011_05698_b200 as M
     from paper_2011_05698_b200.workloads import algo_seed, make_batch, signal_seed
 
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # one GPU per local rank; the modulo only matters for the functional
+    # multi-rank check on a one-GPU box (tools/bench_ranks_check.sh), whose
+    # ranks share the device and use gloo (MSFFT_BENCH_DIST_BACKEND)
+    gpu = local % max(torch.cuda.device_count(), 1)
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("MSFFT_BENCH_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     from paper_2011_05698_b200.dist import max_over_ranks, rank_seeds, sum_over_ranks
     seeds = rank_seeds(SIG_BASE, args.batch, rank, world, args.scaling)
@@ -276,7 +284,7 @@ def main():
     x, _ = make_batch(n, k, seeds, args.snr, dev, "complex64")
     torch.cuda.synchronize()
 
-    plan = M.Plan(n, k, M.MultiscaleConfig(16, 1.0), delta, "complex64", local)
+    plan = M.Plan(n, k, M.MultiscaleConfig(16, 1.0), delta, "complex64", gpu)
     B = len(seeds)  # this rank's signals
     total = sum_over_ranks(B, dev) if world > 1 else B
     out_f = torch.empty((B, k), dtype=torch.int64, device=dev)
@@ -295,7 +303,7 @@ def main():
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(gpu)
     if not args.no_clocks:
         clocks.start()
     ev0 = torch.cuda.Event(enable_timing=True)

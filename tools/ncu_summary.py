@@ -1,11 +1,13 @@
 """Key counters of one kernel launch from an ncu report:
 
-    python tools/ncu_summary.py report.ncu-rep [--workload TEXT] [--traffic out.json]
+    python tools/ncu_summary.py report.ncu-rep [--workload TEXT] [--traffic out.json
+                                [--batch B --n N]]
 
 Reads `ncu -i report --page raw --csv` (first launch in the report) and prints a
 JSON summary: duration, DRAM bytes, occupancy, issue activity, FP64 pipe,
 and the share of each warp-stall reason.  --traffic also writes the
-DRAM-bytes record bench.py reads for roofline.traffic."""
+DRAM-bytes record bench.py reads for roofline.traffic (bench.py uses it only
+when its batch and n match the run, so pass --batch and --n)."""
 import argparse
 import csv
 import io
@@ -79,6 +81,8 @@ if __name__ == "__main__":
     ap.add_argument("report")
     ap.add_argument("--workload", default="")
     ap.add_argument("--traffic")
+    ap.add_argument("--batch", type=int)
+    ap.add_argument("--n", type=int)
     a = ap.parse_args()
     s = summarize(a.report)
     if a.workload:
@@ -90,7 +94,10 @@ if __name__ == "__main__":
         dur = s.get("duration")
         dur_ms = dur / 1e6 if s.get("duration_unit") == "nsecond" else (
             dur / 1e3 if s.get("duration_unit") == "usecond" else dur)
-        rec = {"kernel": s["kernel"], "dram_bytes_per_launch": int(rd + wr),
+        if a.batch is None or a.n is None:
+            raise SystemExit("--traffic needs --batch and --n (bench.py matches them)")
+        rec = {"kernel": s["kernel"], "batch": a.batch, "n": a.n,
+               "dram_bytes_per_launch": int(rd + wr),
                "dram_bytes_read": int(rd), "dram_bytes_write": int(wr),
                "duration_ms_under_ncu": dur_ms,
                "source": f"{a.report} (ncu --set full --clock-control none)"}
