@@ -244,14 +244,29 @@ k3_sum(const DevPlan* __restrict__ P, int m, const int32_t* __restrict__ start,
         const int32_t s0 = start[beta], len = cnt[beta];
         if (len == 0) continue;
         double2 pred = make_double2(0.0, 0.0);
+        // software-pipelined: while lane 0 adds chunk c, the lanes' loads of
+        // chunk c+1's operands and chunk c+2's event keys are in flight
+        const auto key_at = [&](int32_t c) { return c + lane < len ? ev2[s0 + c + lane] : -1; };
+        int32_t key1 = key_at(32), key2 = -1;
+        double2 g = make_double2(0.0, 0.0), rr = g;
+        {
+            const int32_t key0 = key_at(0);
+            if (key0 >= 0) {
+                g = gc[(key0 >> 2) * 3 + (key0 & 3)];
+                rr = rot[static_cast<int64_t>(key0 >> 2) * nr + r];
+            }
+        }
         for (int32_t c0 = 0; c0 < len; c0 += 32) {
             const int32_t take = min(32, len - c0);
-            if (lane < take) {
-                const int32_t key = ev2[s0 + c0 + lane];
-                const int64_t j = key >> 2;
-                const int d = key & 3;
-                stage[threadIdx.x] = cmul(gc[j * 3 + d], rot[j * nr + r]);
+            double2 g_n = make_double2(0.0, 0.0), r_n = g_n;
+            if (c0 + 32 < len) {
+                key2 = key_at(c0 + 64);
+                if (key1 >= 0) {
+                    g_n = gc[(key1 >> 2) * 3 + (key1 & 3)];
+                    r_n = rot[static_cast<int64_t>(key1 >> 2) * nr + r];
+                }
             }
+            if (lane < take) stage[threadIdx.x] = cmul(g, rr);
             __syncwarp();
             if (lane == 0)
                 for (int l = 0; l < take; ++l) {
@@ -260,6 +275,9 @@ k3_sum(const DevPlan* __restrict__ P, int m, const int32_t* __restrict__ start,
                     pred.y += v.y;
                 }
             __syncwarp();
+            g = g_n;
+            rr = r_n;
+            key1 = key2;
         }
         if (lane == 0) {
             const double2 o = Y[e];
