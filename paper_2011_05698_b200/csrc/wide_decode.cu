@@ -385,6 +385,87 @@ sel_digit(const uint64_t* __restrict__ key, int64_t n_max, const int32_t* __rest
     if (t == 0) sel[3] = 0;
 }
 
+// The low 40 bits of the selection in one CTA: the keys matching the
+// 24-bit prefix of the first two digits are gathered into shared memory
+// (read from global memory each pass if they do not fit), then four 10-bit
+// digits are picked with sel_digit's rule.  The final sel (full key, full
+// mask, rank among equal keys) is the one the remaining 12-bit digits give.
+constexpr int kFinT = 1024;
+constexpr int kFinCap = 4096;
+__global__ void __launch_bounds__(kFinT)
+sel_finish(const uint64_t* __restrict__ key, int64_t n_max, const int32_t* __restrict__ n_dev,
+           uint64_t* sel) {
+    pdl_entry();
+    __shared__ uint64_t cand[kFinCap];
+    __shared__ uint32_t hist[kFinT];
+    __shared__ uint32_t part[kFinT];
+    __shared__ int cnt;
+    __shared__ uint64_t s_prefix, s_mask, s_rem;
+    const int t = threadIdx.x;
+    if (t == 0) {
+        cnt = 0;
+        s_prefix = sel[0];
+        s_mask = sel[1];
+        s_rem = sel[2];
+    }
+    __syncthreads();
+    if (s_rem == 0) return;  // uniform
+    const int64_t n = n_or(n_dev, n_max);
+    {
+        const uint64_t pf = s_prefix, mk = s_mask;
+        for (int64_t j = t; j < n; j += kFinT) {
+            const uint64_t k = key[j];
+            if ((k & mk) == pf) {
+                const int p = atomicAdd(&cnt, 1);
+                if (p < kFinCap) cand[p] = k;
+            }
+        }
+    }
+    __syncthreads();
+    const int c = cnt;
+    const bool in_smem = c <= kFinCap;
+    for (int shift = 30; shift >= 0; shift -= 10) {
+        hist[t] = 0;
+        __syncthreads();
+        const uint64_t pf = s_prefix, mk = s_mask;
+        if (in_smem) {
+            for (int i = t; i < c; i += kFinT) {
+                const uint64_t k = cand[i];
+                if ((k & mk) == pf) atomicAdd(&hist[(k >> shift) & 1023u], 1u);
+            }
+        } else {
+            for (int64_t j = t; j < n; j += kFinT) {
+                const uint64_t k = key[j];
+                if ((k & mk) == pf) atomicAdd(&hist[(k >> shift) & 1023u], 1u);
+            }
+        }
+        __syncthreads();
+        const uint32_t hv = hist[t];
+        part[t] = hv;
+        __syncthreads();
+        for (int o = 1; o < kFinT; o <<= 1) {  // suffix sums over bins >= t
+            const uint32_t v = t + o < kFinT ? part[t + o] : 0u;
+            __syncthreads();
+            part[t] += v;
+            __syncthreads();
+        }
+        const uint64_t above = part[t] - hv;  // keys in higher bins
+        const uint64_t rem = s_rem;
+        __syncthreads();  // every thread has read s_rem before it changes
+        if (above < rem && rem <= above + hv) {
+            s_prefix = pf | static_cast<uint64_t>(t) << shift;
+            s_mask = mk | uint64_t{1023} << shift;
+            s_rem = rem - above;
+        }
+        __syncthreads();
+    }
+    if (t == 0) {
+        sel[0] = s_prefix;
+        sel[1] = s_mask;
+        sel[2] = s_rem;
+    }
+}
+
 __global__ void __launch_bounds__(kT)
 sel_count(const uint64_t* __restrict__ key, int64_t n_max, const int32_t* __restrict__ n_dev,
           const uint64_t* __restrict__ sel, int32_t* __restrict__ cgt, int32_t* __restrict__ ceq) {
@@ -1069,13 +1150,15 @@ WideDecoder::WideDecoder(const DevPlan& plan, int64_t acc_cap, int64_t b_max, in
 void WideDecoder::select_kth(const uint64_t* key, int64_t n_max, const int32_t* n_dev,
                              int64_t kth_host, const int32_t* kth_dev, cudaStream_t st) {
     launch_pdl(pdl_, sel_init, 1, kT, 0, st, sel_.get(), kth_host, kth_dev, n_max, hist_.get());
-    for (int top = 64; top > 0;) {
+    // the top 24 bits over the whole grid, the low 40 in one CTA
+    for (int top = 64; top > 40;) {
         const int width = std::min(kSelBits, top);
         const int shift = top - width;
         launch_pdl(pdl_, sel_digit, std::min<unsigned>(grid_of(n_max), 148), kT, 0, st, key, n_max, n_dev,
                    sel_.get(), shift, width, hist_.get());
         top = shift;
     }
+    launch_pdl(pdl_, sel_finish, 1, kFinT, 0, st, key, n_max, n_dev, sel_.get());
     MSFFT_LAUNCH_CHECK("wide select");
 }
 
