@@ -70,31 +70,48 @@ void zero_async(bool pdl, void* p, size_t bytes, cudaStream_t st) {
 
 // ---------------------------------------------------------------- scans
 // Exclusive scan of in[0..len) into out (may alias); total -> *total.
+// Each warp owns a contiguous segment and walks it in coalesced 32-element
+// tiles (warp shuffles scan a tile); a block scan of the warp totals gives
+// each segment its offset.
 __global__ void __launch_bounds__(kScanT)
 scan_kernel(const int32_t* in, int64_t len_max, const int32_t* len_dev, int32_t* out,
             int32_t* total) {
     pdl_entry();
-    __shared__ int32_t part[kScanT];
+    constexpr int kWarps = kScanT / 32;
+    __shared__ int32_t wsum[kWarps];
     const int64_t len = n_or(len_dev, len_max);
-    const int64_t per = (len + kScanT - 1) / kScanT;
-    const int64_t lo = threadIdx.x * per, hi = std::min<int64_t>(lo + per, len);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t seg = (len + kWarps - 1) / kWarps;
+    const int64_t lo = w * seg, hi = std::min<int64_t>(lo + seg, len);
     int32_t s = 0;
-    for (int64_t i = lo; i < hi; ++i) s += in[i];
-    part[threadIdx.x] = s;
+#pragma unroll 8
+    for (int64_t i = lo + lane; i < hi; i += 32) s += in[i];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) wsum[w] = s;
     __syncthreads();
-    for (int o = 1; o < kScanT; o <<= 1) {
-        const int32_t v = threadIdx.x >= o ? part[threadIdx.x - o] : 0;
-        __syncthreads();
-        part[threadIdx.x] += v;
-        __syncthreads();
+    if (w == 0) {
+        const int32_t v = wsum[lane];
+        int32_t x = v;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        wsum[lane] = x - v;  // exclusive
+        if (lane == 31 && total) *total = x;
     }
-    int32_t run = part[threadIdx.x] - s;
-    for (int64_t i = lo; i < hi; ++i) {
-        const int32_t v = in[i];
-        out[i] = run;
-        run += v;
+    __syncthreads();
+    int32_t carry = wsum[w];
+    for (int64_t t0 = lo; t0 < hi; t0 += 32) {
+        const int64_t i = t0 + lane;
+        const int32_t v = i < hi ? in[i] : 0;
+        int32_t x = v;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (i < hi) out[i] = carry + x - v;
+        carry += __shfl_sync(0xffffffffu, x, 31);
     }
-    if (threadIdx.x == kScanT - 1 && total) *total = part[kScanT - 1];
 }
 
 // ---------------------------------------------------------------- K3
@@ -157,7 +174,7 @@ __global__ void k3_scatter(const DevPlan* __restrict__ P, int m, const int32_t* 
 // unique per bucket), by rank counting.
 __global__ void k3_segsort(const DevPlan* __restrict__ P, int m, const int32_t* __restrict__ start,
                            const int32_t* __restrict__ cnt, const int32_t* __restrict__ ev,
-                           int32_t* __restrict__ ev2) {
+                           int32_t* __restrict__ ev2, int32_t* __restrict__ long_list) {
     pdl_entry();
     const int64_t b = P->it[m].b;
     const int lane = threadIdx.x & 31;
@@ -165,7 +182,10 @@ __global__ void k3_segsort(const DevPlan* __restrict__ P, int m, const int32_t* 
     const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
     for (int64_t beta = warp; beta < b; beta += nwarps) {
         const int32_t s0 = start[beta], len = cnt[beta];
-        if (len > kLongSeg) continue;  // k3_segsort_long
+        if (len > kLongSeg) {  // k3_segsort_long takes it: long_list = {count, buckets...}
+            if (lane == 0) long_list[1 + atomicAdd(&long_list[0], 1)] = static_cast<int32_t>(beta);
+            continue;
+        }
         for (int32_t e = lane; e < len; e += 32) {
             const int32_t key = ev[s0 + e];
             int32_t rank = 0;
@@ -182,13 +202,13 @@ constexpr int kLongT = 1024;
 __global__ void __launch_bounds__(kLongT)
 k3_segsort_long(const DevPlan* __restrict__ P, int m, const int32_t* __restrict__ start,
                 const int32_t* __restrict__ cnt, const int32_t* __restrict__ ev,
-                int32_t* __restrict__ ev2) {
+                int32_t* __restrict__ ev2, const int32_t* __restrict__ long_list) {
     pdl_entry();
     __shared__ int32_t ks[kLongSmem];
-    const int64_t b = P->it[m].b;
-    for (int64_t beta = blockIdx.x; beta < b; beta += gridDim.x) {
+    const int32_t nlong = long_list[0];
+    for (int32_t li = blockIdx.x; li < nlong; li += gridDim.x) {
+        const int64_t beta = long_list[1 + li];
         const int32_t s0 = start[beta], len = cnt[beta];
-        if (len <= kLongSeg) continue;
         if (len > kLongSmem) {
             for (int32_t e = threadIdx.x; e < len; e += kLongT) {
                 const int32_t key = ev[s0 + e];
@@ -1115,6 +1135,7 @@ WideDecoder::WideDecoder(const DevPlan& plan, int64_t acc_cap, int64_t b_max, in
     cnt_.reset(B);
     start_.reset(B + 1);
     cursor_.reset(B);
+    long_.reset(B + 1);
     ev_.reset(3 * A);
     ev2_.reset(3 * A);
     const int64_t NK = std::max(B, A);
@@ -1238,10 +1259,11 @@ void WideDecoder::enqueue(double2* y, const int64_t* sigma, const int64_t* sigma
             launch_pdl(pdl_, scan_kernel, 1, kScanT, 0, st, cnt_.get(), b, nullptr, start_.get(), nullptr);
             launch_pdl(pdl_, k3_scatter, gA, kT, 0, st, P, m, acc_n, tone_i_.get(), start_.get(), cursor_.get(),
                                           ev_.get());
+            zero_async(pdl_, long_.get(), sizeof(int32_t), st);
             launch_pdl(pdl_, k3_segsort, grid_of(b * 32), kT, 0, st, P, m, start_.get(), cnt_.get(), ev_.get(),
-                                                       ev2_.get());
-            launch_pdl(pdl_, k3_segsort_long, static_cast<unsigned>(std::min<int64_t>(b, 148 * 2)), kLongT, 0, st, 
-                P, m, start_.get(), cnt_.get(), ev_.get(), ev2_.get());
+                                                       ev2_.get(), long_.get());
+            launch_pdl(pdl_, k3_segsort_long, static_cast<unsigned>(std::min<int64_t>(b, 148 * 2)), kLongT, 0, st,
+                P, m, start_.get(), cnt_.get(), ev_.get(), ev2_.get(), long_.get());
             launch_pdl(pdl_, k3_sum, grid_of(nr * b * 32), kT, 0, st, P, m, start_.get(), cnt_.get(), ev2_.get(),
                                                         gc_.get(), rot_.get(), Y);
             MSFFT_LAUNCH_CHECK("wide K3");

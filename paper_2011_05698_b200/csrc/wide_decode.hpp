@@ -66,6 +66,7 @@ private:
     DeviceBuffer<int64_t> tone_u_, tone_i_;
     DeviceBuffer<double2> gc_, rot_;
     DeviceBuffer<int32_t> cnt_, start_, cursor_, ev_, ev2_;
+    DeviceBuffer<int32_t> long_;  // {count, buckets...} of event segments > kLongSeg
     // K4 / K7
     DeviceBuffer<uint64_t> key_;
     DeviceBuffer<uint32_t> hist_;

@@ -249,7 +249,9 @@ def test_sparse_ingest_validates_every_sample():
 
 @pytest.mark.parametrize("n,k,dtype,snr", [(1 << 20, 2000, "complex128", 20.0),
                                            (1 << 19, 1200, "complex64", 20.0),
-                                           (1 << 18, 3000, "complex128", None)])
+                                           (1 << 18, 3000, "complex128", None),
+                                           # budgets >= 4096: K4/K6 orders by radix sort
+                                           (1 << 21, 6000, "complex128", 20.0)])
 def test_wide_decode_bit_identical_to_cta_decode(oracle, monkeypatch, n, k, dtype, snr):
     """Large single signals decode with the grid-wide kernels (wide_decode.cu);
     outputs must equal the one-CTA decode (decode_body.cuh) bit for bit."""
