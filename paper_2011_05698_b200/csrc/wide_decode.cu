@@ -132,11 +132,17 @@ __global__ void k3_tones(const DevPlan* __restrict__ P, int m, const int64_t* __
         tone_u[j] = u;
         tone_i[j] = i;
         const double2 c = AC[j];
+        const unsigned act = __activemask();
+        const int lane = threadIdx.x & 31;
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
             const double g = ghat_at(it, (i - 1 + d) * L - u);
             gc[j * 3 + d] = make_double2(g * c.x, g * c.y);
-            atomicAdd(&cnt[(i - 1 + d) & (b - 1)], 1);
+            // lanes with the same target bucket add once (small b: every
+            // tone of the warp hits one of a few counters)
+            const int bk = static_cast<int>((i - 1 + d) & (b - 1));
+            const unsigned same = __match_any_sync(act, bk);
+            if ((same & ((1u << lane) - 1u)) == 0) atomicAdd(&cnt[bk], __popc(same));
         }
     }
 }
@@ -164,7 +170,16 @@ __global__ void k3_scatter(const DevPlan* __restrict__ P, int m, const int32_t* 
         const int64_t j = e / 3;
         const int d = static_cast<int>(e - j * 3);
         const int64_t beta = (tone_i[j] - 1 + d) & (b - 1);
-        const int32_t pos = start[beta] + atomicAdd(&cursor[beta], 1);
+        // one atomic per distinct bucket of the warp (the in-bucket order is
+        // irrelevant: k3_segsort orders each bucket's events by key)
+        const unsigned act = __activemask();
+        const int lane = threadIdx.x & 31;
+        const unsigned same = __match_any_sync(act, static_cast<int>(beta));
+        const int leader = __ffs(same) - 1;
+        int32_t base = 0;
+        if (lane == leader) base = atomicAdd(&cursor[beta], __popc(same));
+        base = __shfl_sync(same, base, leader);
+        const int32_t pos = start[beta] + base + __popc(same & ((1u << lane) - 1u));
         MSFFT_DCHECK(pos >= 0 && pos < total && total <= 3 * P->acc_cap);
         ev[pos] = static_cast<int32_t>(j * 4 + d);
     }
