@@ -675,16 +675,35 @@ k4_small(const DevPlan* __restrict__ P, int m, const double2* __restrict__ Y,
         sm[j] = mj;
         mag[j] = mj;
     }
+    // rank order (|y0| desc, bucket asc) by a bitonic sort of (magnitude,
+    // bucket) pairs; padding (-2 < every magnitude and the NaN sentinel -1)
+    // sorts last
+    static_assert((kSmallK4 & (kSmallK4 - 1)) == 0, "bitonic size");
+    __shared__ int32_t si[kSmallK4];
+    if (j >= b) sm[j] = -2.0;
+    si[j] = j;
     __syncthreads();
-    if (j < b) {
-        int rank = 0;
-        for (int i = 0; i < b; ++i) {
-            const double mi = sm[i];
-            rank += (mi > mj) || (mi == mj && i < j);
+    int pw = 2;
+    while (pw < b) pw <<= 1;
+    for (int k = 2; k <= pw; k <<= 1) {
+        for (int h = k >> 1; h > 0; h >>= 1) {
+            const int p = j ^ h;
+            if (p > j && p < pw) {
+                const double ma = sm[j], mb = sm[p];
+                const int ia = si[j], ib = si[p];
+                const bool p_first = (mb > ma) || (mb == ma && ib < ia);
+                if (p_first == ((j & k) == 0)) {
+                    sm[j] = mb;
+                    sm[p] = ma;
+                    si[j] = ib;
+                    si[p] = ia;
+                }
+            }
+            __syncthreads();
         }
-        if (rank < budget) order[rank] = j;
-        if (rank == budget - 1) *thr = 0.2 * mj;
     }
+    if (j < budget) order[j] = si[j];
+    if (j == budget - 1) *thr = 0.2 * sm[j];
 }
 
 __global__ void k4_thr(const int32_t* __restrict__ order, int64_t budget,
@@ -989,31 +1008,37 @@ k6_small(const DevPlan* __restrict__ P, int m, const int64_t* __restrict__ cand_
     __shared__ int32_t nflag[kSmallK6];  // new-f flag -> exclusive prefix
     __shared__ int64_t newf[kSmallK6];
     __shared__ int32_t wsum[kSmallK6 / 32];
-    __shared__ int32_t s_acc, s_A;
+    __shared__ int32_t s_acc;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t budget = P->it[m].budget;
-    if (tid == 0) {
-        s_acc = scal[0];
-        s_A = 0;
-    }
+    if (tid == 0) s_acc = scal[0];
     const int64_t fr = tid < budget ? cand_f[tid] : -1;
-    sf[tid] = fr;
     __syncthreads();
     const int an = s_acc;
-    if (fr >= 0) {
-        int pos = 0;
-        for (int o = 0; o < budget; ++o) {
-            const int64_t fo = sf[o];
-            pos += fo >= 0 && (fo < fr || (fo == fr && o < tid));
+    // accepted ranks in (f, rank) order: a bitonic sort of the unique keys
+    // f * 1024 + rank (rejected ranks sort last); newf is free until later
+    static_assert(kSmallK6 == 1024, "one key per thread, rank in 10 bits");
+    uint64_t* key = reinterpret_cast<uint64_t*>(newf);
+    key[tid] = fr >= 0 ? (static_cast<uint64_t>(fr) << 10) | static_cast<uint64_t>(tid)
+                       : ~uint64_t{0};
+    const int A = __syncthreads_count(fr >= 0);
+    int pw = 2;
+    while (pw < budget) pw <<= 1;
+    for (int k = 2; k <= pw; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            const int p = tid ^ j;
+            if (p > tid && p < pw) {
+                const uint64_t a = key[tid], c = key[p];
+                if ((a > c) == ((tid & k) == 0)) {
+                    key[tid] = c;
+                    key[p] = a;
+                }
+            }
+            __syncthreads();
         }
-        byf[pos] = tid;
-        atomicAdd(&s_A, 1);
     }
-    __syncthreads();
-    const int A = s_A;
-    const int64_t fsorted = tid < A ? sf[byf[tid]] : -1;
-    __syncthreads();
-    sf[tid] = fsorted;
+    if (tid < A) byf[tid] = static_cast<int32_t>(key[tid] & 1023u);
+    sf[tid] = tid < A ? static_cast<int64_t>(key[tid] >> 10) : -1;
     __syncthreads();
     int flag = 0;
     if (tid < A) {
