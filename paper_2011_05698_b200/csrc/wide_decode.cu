@@ -119,11 +119,15 @@ __global__ void k3_tones(const DevPlan* __restrict__ P, int m, const int64_t* __
                          const int64_t* __restrict__ AF, const double2* __restrict__ AC,
                          const int32_t* __restrict__ acc_n, int64_t* __restrict__ tone_u,
                          int64_t* __restrict__ tone_i, double2* __restrict__ gc,
-                         int32_t* __restrict__ cnt) {
+                         int32_t* __restrict__ cnt, int32_t* __restrict__ cursor,
+                         int32_t* __restrict__ long_list, double2* __restrict__ rot) {
     pdl_entry();
     const DevIter& it = P->it[m];
     const int64_t n = acc_n[0];
     const int64_t b = it.b, L = it.l_width, nmask = P->n - 1;
+    // clear what k3_scatter / k3_segsort count into (not used before them)
+    GRID_LOOP(z, b) cursor[z] = 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) long_list[0] = 0;
     const double invL = 1.0 / static_cast<double>(L);
     const int64_t sg = sigma[m];
     GRID_LOOP(j, n) {
@@ -145,18 +149,13 @@ __global__ void k3_tones(const DevPlan* __restrict__ P, int m, const int64_t* __
             if ((same & ((1u << lane) - 1u)) == 0) atomicAdd(&cnt[bk], __popc(same));
         }
     }
-}
-
-__global__ void k3_rot(const DevPlan* __restrict__ P, int m, const int32_t* __restrict__ acc_n,
-                       const int64_t* __restrict__ tone_u, double2* __restrict__ rot) {
-    pdl_entry();
-    const DevIter& it = P->it[m];
+    // the rotation per (tone, round), u recomputed (k3_rot's values)
     const int nr = it.nrounds;
     const int64_t* taus = P->taus + it.tau_off;
-    const int64_t total = static_cast<int64_t>(acc_n[0]) * nr;
-    GRID_LOOP(e, total) {
+    GRID_LOOP(e, n * nr) {
         const int64_t j = e / nr, r = e - j * nr;
-        rot[e] = unit_root(P->n, P->inv_n, taus[r] * tone_u[j]);
+        const int64_t u = (sg * AF[j]) & nmask;
+        rot[e] = unit_root(P->n, P->inv_n, taus[r] * u);
     }
 }
 
@@ -713,27 +712,23 @@ __global__ void k4_thr(const int32_t* __restrict__ order, int64_t budget,
 }
 
 // ---------------------------------------------------------------- K5
-__global__ void k5_stage(const DevPlan* __restrict__ P, int m, const int32_t* __restrict__ order,
-                         const double2* __restrict__ Y, double2* __restrict__ yr) {
-    pdl_entry();
-    const DevIter& it = P->it[m];
-    const int nr = it.nrounds;
-    const int64_t total = it.budget * nr;
-    GRID_LOOP(e, total) {
-        const int64_t rk = e / nr, st = e - rk * nr;
-        yr[e] = Y[st * it.b + order[rk]];
-    }
-}
-
-__global__ void k5_phase(const DevPlan* __restrict__ P, int m, const double2* __restrict__ yr,
-                         double* __restrict__ phi, int32_t* __restrict__ pcode) {
+// Every ranked bucket's round values staged in rank order, and the phases
+// of y0 / y_tau per (rank, stage) -- both read Y directly, so one launch.
+__global__ void k5_stage_phase(const DevPlan* __restrict__ P, int m,
+                               const int32_t* __restrict__ order, const double2* __restrict__ Y,
+                               double2* __restrict__ yr, double* __restrict__ phi,
+                               int32_t* __restrict__ pcode) {
     pdl_entry();
     const DevIter& it = P->it[m];
     const int nr = it.nrounds, ns = nr - 1;
-    const int64_t total = it.budget * ns;
+    const int64_t total = it.budget * nr;
     GRID_LOOP(e, total) {
-        const int64_t rk = e / ns, st = e - rk * ns + 1;
-        const double2 y0e = yr[rk * nr], yt = yr[rk * nr + st];
+        const int64_t rk = e / nr, st = e - rk * nr;
+        const int64_t beta = order[rk];
+        const double2 yt = Y[st * it.b + beta];
+        yr[e] = yt;
+        if (st == 0) continue;
+        const double2 y0e = Y[beta];
         int code = 0;
         double ph = 0.0;
         if (yt.x == 0.0 && yt.y == 0.0) {
@@ -745,8 +740,9 @@ __global__ void k5_phase(const DevPlan* __restrict__ P, int m, const double2* __
             if (ph < 0.0) ph += kTwoPi;
             ph = ph + 0.0;
         }
-        phi[e] = ph;
-        pcode[e] = code;
+        const int64_t pe = rk * ns + (st - 1);
+        phi[pe] = ph;
+        pcode[pe] = code;
     }
 }
 
@@ -1292,14 +1288,12 @@ void WideDecoder::enqueue(double2* y, const int64_t* sigma, const int64_t* sigma
         if (m > 0) {
             // ---- K3
             zero_async(pdl_, cnt_.get(), b * sizeof(int32_t), st);
-            zero_async(pdl_, cursor_.get(), b * sizeof(int32_t), st);
             launch_pdl(pdl_, k3_tones, grid_of(acc_cap_), kT, 0, st, P, m, sigma, AF, AC, acc_n, tone_u_.get(),
-                                                      tone_i_.get(), gc_.get(), cnt_.get());
-            launch_pdl(pdl_, k3_rot, grid_of(acc_cap_ * nr), kT, 0, st, P, m, acc_n, tone_u_.get(), rot_.get());
+                                                      tone_i_.get(), gc_.get(), cnt_.get(), cursor_.get(),
+                                                      long_.get(), rot_.get());
             launch_pdl(pdl_, scan_kernel, 1, kScanT, 0, st, cnt_.get(), b, nullptr, start_.get(), nullptr);
             launch_pdl(pdl_, k3_scatter, gA, kT, 0, st, P, m, acc_n, tone_i_.get(), start_.get(), cursor_.get(),
                                           ev_.get());
-            zero_async(pdl_, long_.get(), sizeof(int32_t), st);
             launch_pdl(pdl_, k3_segsort, grid_of(b * 32), kT, 0, st, P, m, start_.get(), cnt_.get(), ev_.get(),
                                                        ev2_.get(), long_.get());
             launch_pdl(pdl_, k3_segsort_long, static_cast<unsigned>(std::min<int64_t>(b, 148 * 2)), kLongT, 0, st,
@@ -1326,8 +1320,8 @@ void WideDecoder::enqueue(double2* y, const int64_t* sigma, const int64_t* sigma
             launch_pdl(pdl_, k4_thr, 1, 1, 0, st, order_.get(), budget, mag_.get(), thr_.get());
         }
         // ---- K5
-        launch_pdl(pdl_, k5_stage, grid_of(budget * nr), kT, 0, st, P, m, order_.get(), Y, yr_.get());
-        launch_pdl(pdl_, k5_phase, grid_of(budget * nr), kT, 0, st, P, m, yr_.get(), phi_.get(), pcode_.get());
+        launch_pdl(pdl_, k5_stage_phase, grid_of(budget * nr), kT, 0, st, P, m, order_.get(), Y, yr_.get(),
+                   phi_.get(), pcode_.get());
         launch_pdl(pdl_, k5_locate, grid_of(budget * 32), kT, 0, st, P, m, sigma_inv, order_.get(), mag_.get(),
                                                        thr_.get(), yr_.get(), phi_.get(),
                                                        pcode_.get(), cand_f_.get(), cand_v_.get(),
