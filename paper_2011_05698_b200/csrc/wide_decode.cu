@@ -1311,7 +1311,7 @@ void WideDecoder::enqueue(double2* y, const int64_t* sigma, const int64_t* sigma
             compact_selected(key_.get(), b, nullptr, sel_idx_.get(), st);
             {
                 const unsigned tiles = static_cast<unsigned>((budget + kT - 1) / kT);
-                const unsigned split = std::max(1u, std::min(32u, 296u / tiles));
+                const unsigned split = std::max(1u, std::min(64u, 1184u / tiles));
                 zero_async(pdl_, pos_.get(), budget * sizeof(int32_t), st);
                 launch_pdl(pdl_, k4_rank, dim3(tiles, split), kT, 0, st, sel_idx_.get(), budget, mag_.get(), pos_.get());
                 launch_pdl(pdl_, k4_scatter, grid_of(budget), kT, 0, st, sel_idx_.get(), pos_.get(), budget,
@@ -1334,7 +1334,7 @@ void WideDecoder::enqueue(double2* y, const int64_t* sigma, const int64_t* sigma
         } else {
             {
                 const unsigned tiles = static_cast<unsigned>((budget + kT - 1) / kT);
-                const unsigned split = std::max(1u, std::min(32u, 296u / tiles));
+                const unsigned split = std::max(1u, std::min(64u, 1184u / tiles));
                 zero_async(pdl_, pos_.get(), budget * sizeof(int32_t), st);
                 launch_pdl(pdl_, k6_sortf, dim3(tiles, split), kT, 0, st, cand_f_.get(), budget, pos_.get());
                 launch_pdl(pdl_, k6_scatter, grid_of(budget), kT, 0, st, cand_f_.get(), pos_.get(), budget, byf_.get(),
