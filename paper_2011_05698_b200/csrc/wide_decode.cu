@@ -257,8 +257,13 @@ k3_segsort_long(const DevPlan* __restrict__ P, int m, const int32_t* __restrict_
     }
 }
 
-// One warp per (round, bucket): the prediction summed in ascending-f order,
-// lane 0 adding 32 staged contributions at a time (decode_body.cuh K3).
+// The prediction of every (round, bucket), summed in ascending-f order
+// (decode_body.cuh K3).  A warp takes up to 32 consecutive (round, bucket)
+// pairs, one per lane: a lane sums a short event list (<= kK3Short events, the
+// sparse iterations) by itself; the long lists (small b) are then summed by
+// the whole warp one after another -- lanes stage 32 contributions at a time,
+// lane 0 adds them in order, and the next chunk's operands load meanwhile.
+constexpr int kK3Short = 8;
 __global__ void __launch_bounds__(kT)
 k3_sum(const DevPlan* __restrict__ P, int m, const int32_t* __restrict__ start,
        const int32_t* __restrict__ cnt, const int32_t* __restrict__ ev2,
@@ -268,54 +273,84 @@ k3_sum(const DevPlan* __restrict__ P, int m, const int32_t* __restrict__ start,
     const DevIter& it = P->it[m];
     const int64_t b = it.b;
     const int nr = it.nrounds;
+    const int64_t total = static_cast<int64_t>(nr) * b;
     const int lane = threadIdx.x & 31;
     const int wslot = threadIdx.x & ~31;
     const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-    for (int64_t e = warp; e < static_cast<int64_t>(nr) * b; e += nwarps) {
-        const int r = static_cast<int>(e / b);
-        const int64_t beta = e - static_cast<int64_t>(r) * b;
-        const int32_t s0 = start[beta], len = cnt[beta];
-        if (len == 0) continue;
-        double2 pred = make_double2(0.0, 0.0);
-        // software-pipelined: while lane 0 adds chunk c, the lanes' loads of
-        // chunk c+1's operands and chunk c+2's event keys are in flight
-        const auto key_at = [&](int32_t c) { return c + lane < len ? ev2[s0 + c + lane] : -1; };
-        int32_t key1 = key_at(32), key2 = -1;
-        double2 g = make_double2(0.0, 0.0), rr = g;
-        {
-            const int32_t key0 = key_at(0);
-            if (key0 >= 0) {
-                g = gc[(key0 >> 2) * 3 + (key0 & 3)];
-                rr = rot[static_cast<int64_t>(key0 >> 2) * nr + r];
-            }
+    // pairs per warp: as few as the grid allows (one when warps >= pairs,
+    // so the long lists of small b run one per warp in parallel)
+    const int64_t per = std::min<int64_t>(32, (total + nwarps - 1) / nwarps);
+    for (int64_t base = warp * per; base < total; base += nwarps * per) {
+        const int64_t e = base + lane;
+        int32_t s0 = 0, len = 0;
+        int r = 0;
+        if (lane < per && e < total) {
+            r = static_cast<int>(e / b);
+            const int64_t beta = e - static_cast<int64_t>(r) * b;
+            s0 = start[beta];
+            len = cnt[beta];
         }
-        for (int32_t c0 = 0; c0 < len; c0 += 32) {
-            const int32_t take = min(32, len - c0);
-            double2 g_n = make_double2(0.0, 0.0), r_n = g_n;
-            if (c0 + 32 < len) {
-                key2 = key_at(c0 + 64);
-                if (key1 >= 0) {
-                    g_n = gc[(key1 >> 2) * 3 + (key1 & 3)];
-                    r_n = rot[static_cast<int64_t>(key1 >> 2) * nr + r];
-                }
+        if (len > 0 && len <= kK3Short) {
+            double2 pred = make_double2(0.0, 0.0);
+            for (int32_t q = 0; q < len; ++q) {
+                const int32_t key = ev2[s0 + q];
+                const double2 v = cmul(gc[(key >> 2) * 3 + (key & 3)],
+                                       rot[static_cast<int64_t>(key >> 2) * nr + r]);
+                pred.x += v.x;
+                pred.y += v.y;
             }
-            if (lane < take) stage[threadIdx.x] = cmul(g, rr);
-            __syncwarp();
-            if (lane == 0)
-                for (int l = 0; l < take; ++l) {
-                    const double2 v = stage[wslot + l];
-                    pred.x += v.x;
-                    pred.y += v.y;
-                }
-            __syncwarp();
-            g = g_n;
-            rr = r_n;
-            key1 = key2;
-        }
-        if (lane == 0) {
             const double2 o = Y[e];
             Y[e] = make_double2(o.x - pred.x, o.y - pred.y);
+        }
+        unsigned long_mask = __ballot_sync(0xffffffffu, len > kK3Short);
+        while (long_mask) {
+            const int src = __ffs(long_mask) - 1;
+            long_mask &= long_mask - 1;
+            const int32_t ls0 = __shfl_sync(0xffffffffu, s0, src);
+            const int32_t llen = __shfl_sync(0xffffffffu, len, src);
+            const int lr = __shfl_sync(0xffffffffu, r, src);
+            double2 pred = make_double2(0.0, 0.0);
+            // software-pipelined: while lane 0 adds chunk c, the lanes' loads of
+            // chunk c+1's operands and chunk c+2's event keys are in flight
+            const auto key_at = [&](int32_t c) { return c + lane < llen ? ev2[ls0 + c + lane] : -1; };
+            int32_t key1 = key_at(32), key2 = -1;
+            double2 g = make_double2(0.0, 0.0), rr = g;
+            {
+                const int32_t key0 = key_at(0);
+                if (key0 >= 0) {
+                    g = gc[(key0 >> 2) * 3 + (key0 & 3)];
+                    rr = rot[static_cast<int64_t>(key0 >> 2) * nr + lr];
+                }
+            }
+            for (int32_t c0 = 0; c0 < llen; c0 += 32) {
+                const int32_t take = min(32, llen - c0);
+                double2 g_n = make_double2(0.0, 0.0), r_n = g_n;
+                if (c0 + 32 < llen) {
+                    key2 = key_at(c0 + 64);
+                    if (key1 >= 0) {
+                        g_n = gc[(key1 >> 2) * 3 + (key1 & 3)];
+                        r_n = rot[static_cast<int64_t>(key1 >> 2) * nr + lr];
+                    }
+                }
+                if (lane < take) stage[threadIdx.x] = cmul(g, rr);
+                __syncwarp();
+                if (lane == 0)
+                    for (int l = 0; l < take; ++l) {
+                        const double2 v = stage[wslot + l];
+                        pred.x += v.x;
+                        pred.y += v.y;
+                    }
+                __syncwarp();
+                g = g_n;
+                rr = r_n;
+                key1 = key2;
+            }
+            if (lane == 0) {
+                const int64_t le = base + src;
+                const double2 o = Y[le];
+                Y[le] = make_double2(o.x - pred.x, o.y - pred.y);
+            }
         }
     }
 }
