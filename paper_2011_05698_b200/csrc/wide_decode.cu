@@ -1323,7 +1323,7 @@ void WideDecoder::enqueue(double2* y, const int64_t* sigma, const int64_t* sigma
         if (m > 0) {
             // ---- K3
             zero_async(pdl_, cnt_.get(), b * sizeof(int32_t), st);
-            launch_pdl(pdl_, k3_tones, grid_of(acc_cap_), kT, 0, st, P, m, sigma, AF, AC, acc_n, tone_u_.get(),
+            launch_pdl(pdl_, k3_tones, grid_of(acc_cap_ * nr), kT, 0, st, P, m, sigma, AF, AC, acc_n, tone_u_.get(),
                                                       tone_i_.get(), gc_.get(), cnt_.get(), cursor_.get(),
                                                       long_.get(), rot_.get());
             launch_pdl(pdl_, scan_kernel, 1, kScanT, 0, st, cnt_.get(), b, nullptr, start_.get(), nullptr);
