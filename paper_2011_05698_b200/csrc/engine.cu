@@ -307,14 +307,10 @@ void Plan::bucket_ffts(double2* y, int64_t batch, cudaStream_t st) const {
 }
 
 bool Plan::split_tasks(int64_t n_tasks) const {
-    static const int sms = [] {
-        int dev = 0, v = 0;
-        if (cudaGetDevice(&dev) != cudaSuccess ||
-            cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
-            return 0;
-        return v;
-    }();
-    return split_enabled_ && n_tasks < 2 * static_cast<int64_t>(sms);
+    if (!split_enabled_) return false;
+    int sms = 0;  // this plan's device (called once per new batch size)
+    MSFFT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_));
+    return n_tasks < 2 * static_cast<int64_t>(sms);
 }
 
 void Plan::append_tasks(std::vector<EncTask>& v, int64_t s_begin, int64_t s_end,
