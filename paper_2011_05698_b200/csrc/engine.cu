@@ -310,7 +310,7 @@ bool Plan::split_tasks(int64_t n_tasks) const {
     if (!split_enabled_) return false;
     int sms = 0;  // this plan's device (called once per new batch size)
     MSFFT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_));
-    return n_tasks < 2 * static_cast<int64_t>(sms);
+    return n_tasks < 8 * static_cast<int64_t>(sms);
 }
 
 void Plan::append_tasks(std::vector<EncTask>& v, int64_t s_begin, int64_t s_end,
