@@ -15,6 +15,7 @@ namespace msfft_b200 {
 namespace {
 
 constexpr size_t kTapsSmemMax = 96 * 1024;
+constexpr size_t kTapsSmemMaxWide = 128 * 1024;
 constexpr size_t kChunkBytes = size_t{1} << 30;  // host-input pipeline chunk
 
 struct DeviceGuard {
@@ -110,7 +111,11 @@ Plan::Plan(int64_t n, int64_t k, int64_t l, double q, double delta, bool c128, i
             it.nstage_tab = (len > 1.0 + 1e-9) ? -1 : st;
         }
         const size_t taps_bytes = static_cast<size_t>(win->w + 1) * sizeof(double);
-        it.taps_in_smem = taps_bytes <= taps_smem_max ? 1 : 0;
+        // iterations with b > 256 run only in the serial encode kernel (never
+        // fused), which can stage a larger window (C2's b = 512: 110 KB)
+        const size_t cap = ip.b > kEncThreads ? std::max(taps_smem_max, kTapsSmemMaxWide)
+                                              : taps_smem_max;
+        it.taps_in_smem = taps_bytes <= cap ? 1 : 0;
         if (tau_off + it.nrounds > kMaxTaus)
             throw std::invalid_argument("sfft4: tau plan exceeds the device plan limit");
         for (int r = 0; r < it.nrounds; ++r) P.taus[tau_off + r] = ip.taus[r];
