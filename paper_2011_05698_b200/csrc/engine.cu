@@ -15,7 +15,7 @@ namespace msfft_b200 {
 namespace {
 
 constexpr size_t kTapsSmemMax = 96 * 1024;
-constexpr size_t kTapsSmemMaxWide = 128 * 1024;
+constexpr int64_t kDecSmemMax = 200 * 1024;
 constexpr size_t kChunkBytes = size_t{1} << 30;  // host-input pipeline chunk
 
 struct DeviceGuard {
@@ -111,11 +111,7 @@ Plan::Plan(int64_t n, int64_t k, int64_t l, double q, double delta, bool c128, i
             it.nstage_tab = (len > 1.0 + 1e-9) ? -1 : st;
         }
         const size_t taps_bytes = static_cast<size_t>(win->w + 1) * sizeof(double);
-        // iterations with b > 256 run only in the serial encode kernel (never
-        // fused), which can stage a larger window (C2's b = 512: 110 KB)
-        const size_t cap = ip.b > kEncThreads ? std::max(taps_smem_max, kTapsSmemMaxWide)
-                                              : taps_smem_max;
-        it.taps_in_smem = taps_bytes <= cap ? 1 : 0;
+        it.taps_in_smem = taps_bytes <= taps_smem_max ? 1 : 0;
         if (tau_off + it.nrounds > kMaxTaus)
             throw std::invalid_argument("sfft4: tau plan exceeds the device plan limit");
         for (int r = 0; r < it.nrounds; ++r) P.taus[tau_off + r] = ip.taus[r];
@@ -134,6 +130,11 @@ Plan::Plan(int64_t n, int64_t k, int64_t l, double q, double delta, bool c128, i
     for (const auto& ip : sched_.iters)
         rounds_max = std::max<int64_t>(rounds_max, static_cast<int64_t>(ip.taus.size()));
     lay_ = make_dec_layout(sched_.acc_cap, b_max_, budget_max_, rounds_max);
+    // the standalone decode kernel may keep a larger scratch in shared
+    // memory than the fused kernel (which must keep 2 CTAs per SM): up to
+    // kDecSmemMax, one CTA per SM, instead of L2 round trips per access
+    lay_dec_ = lay_;
+    if (!lay_dec_.big && lay_dec_.bytes <= kDecSmemMax) lay_dec_.in_smem = 1;
     rounds_max_ = rounds_max;
     // Blocking streams: ordered after work on the legacy default stream, so
     // callers that pass no stream (e.g. torch default-stream producers) are safe.
@@ -464,7 +465,7 @@ void Plan::run_chunk(int64_t batch, const void* d_x, int64_t x_stride, const int
             bucket_ffts(yc, cb, st);
             MSFFT_CUDA(cudaEventRecord(ev_chunk_, st));
             MSFFT_CUDA(cudaStreamWaitEvent(dec_stream_, ev_chunk_, 0));
-            launch_decode(dplan_, lay_, yc, d_sig + c0 * iters, d_sig_inv + c0 * iters, cb,
+            launch_decode(dplan_, lay_dec_, yc, d_sig + c0 * iters, d_sig_inv + c0 * iters, cb,
                           lay_.in_smem ? nullptr : dec_work_.get() + c0 * lay_.bytes,
                           d_out_f + c0 * k, d_out_c + c0 * k, d_out_count + c0, flags_.get(),
                           dec_stream_);
@@ -507,7 +508,7 @@ void Plan::run_chunk(int64_t batch, const void* d_x, int64_t x_stride, const int
                            d_out_f + s * k, d_out_c + s * k, d_out_count + s, flags_.get(), st);
         }
     } else {
-        launch_decode(dplan_, lay_, y_.get(), d_sig, d_sig_inv, batch, dec_work_.get(), d_out_f,
+        launch_decode(dplan_, lay_dec_, y_.get(), d_sig, d_sig_inv, batch, dec_work_.get(), d_out_f,
                       d_out_c, d_out_count, flags_.get(), st, tb.get(), tf.get(), tv.get());
     }
     if (opt.stage_times) {
@@ -875,7 +876,7 @@ void Plan::decode_values(int64_t batch, double2* d_y, const uint64_t* seeds, int
             wide_->run(d_y + s * vps, sig_.get() + s * iters, sig_inv_.get() + s * iters,
                        d_out_f + s * k, d_out_c + s * k, d_out_count + s, flags_.get(), st);
     } else {
-        launch_decode(dplan_, lay_, d_y, sig_.get(), sig_inv_.get(), batch, dec_work_.get(),
+        launch_decode(dplan_, lay_dec_, d_y, sig_.get(), sig_inv_.get(), batch, dec_work_.get(),
                       d_out_f, d_out_c, d_out_count, flags_.get(), st);
     }
     check_flags(st);

@@ -135,6 +135,7 @@ private:
     DevPlan dplan_{};
     DevPlan dplan_compact_{};  // dplan_ with x_compact = 1
     DecLayout lay_{};
+    DecLayout lay_dec_{};  // the standalone decode kernel's (larger shared-memory cap)
     size_t enc_smem_ = 0;
     int64_t b_max_ = 0, budget_max_ = 0;
     std::vector<int> big_b_iters_;  // iterations needing the separate FFT
