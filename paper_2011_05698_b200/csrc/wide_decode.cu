@@ -239,15 +239,15 @@ k3_segsort_long(const DevPlan* __restrict__ P, int m, const int32_t* __restrict_
         __syncthreads();
         for (int32_t k = 2; k <= pw; k <<= 1) {
             for (int32_t j = k >> 1; j > 0; j >>= 1) {
-                for (int32_t i = threadIdx.x; i < pw; i += kLongT) {
-                    const int32_t l = i ^ j;
-                    if (l > i) {
-                        const int32_t a = ks[i], c = ks[l];
-                        const bool up = (i & k) == 0;
-                        if ((a > c) == up) {
-                            ks[i] = c;
-                            ks[l] = a;
-                        }
+                // one compare-exchange pair (i, i + j), bit j of i clear, per thread
+                for (int32_t t = threadIdx.x; t < (pw >> 1); t += kLongT) {
+                    const int32_t i = ((t & ~(j - 1)) << 1) | (t & (j - 1));
+                    const int32_t l = i + j;
+                    const int32_t a = ks[i], c = ks[l];
+                    const bool up = (i & k) == 0;
+                    if ((a > c) == up) {
+                        ks[i] = c;
+                        ks[l] = a;
                     }
                 }
                 __syncthreads();
