@@ -911,6 +911,61 @@ k6_sortf(const int64_t* __restrict__ cand_f, int64_t budget, int32_t* __restrict
     if (r < budget && fr >= 0 && pos) atomicAdd(&pos_out[r], pos);
 }
 
+// Large budgets: (f, rank) order by a bucket sort on the top 12 bits of f
+// (the f are near-uniform on [0, n)): counts, a scan, a scatter, then each
+// bucket's few entries ranked by (f, rank).  Buckets ascend in f, so byf is
+// exactly the order k6_sortf + k6_scatter give.
+constexpr int kF6B = 4096;
+constexpr int64_t kF6BucketMin = 2048;  // budgets from here use the bucket sort
+
+__global__ void k6b_count(const int64_t* __restrict__ cand_f, int64_t budget, int shift,
+                          int32_t* __restrict__ cnt, int32_t* __restrict__ cursor,
+                          int32_t* __restrict__ naccepted) {
+    pdl_entry();
+    GRID_LOOP(z, kF6B) cursor[z] = 0;  // used from k6b_scatter on
+    GRID_LOOP(r, budget) {
+        const int64_t f = cand_f[r];
+        const unsigned act = __activemask();
+        const unsigned acc = __ballot_sync(act, f >= 0);
+        if (f >= 0) atomicAdd(&cnt[f >> shift], 1);
+        if ((threadIdx.x & 31) == __ffs(act) - 1 && acc) atomicAdd(naccepted, __popc(acc));
+    }
+}
+
+__global__ void k6b_scatter(const int64_t* __restrict__ cand_f, int64_t budget, int shift,
+                            const int32_t* __restrict__ start, int32_t* __restrict__ cursor,
+                            int32_t* __restrict__ tmp) {
+    pdl_entry();
+    GRID_LOOP(r, budget) {
+        const int64_t f = cand_f[r];
+        if (f < 0) continue;
+        const int64_t bk = f >> shift;
+        tmp[start[bk] + atomicAdd(&cursor[bk], 1)] = static_cast<int32_t>(r);
+    }
+}
+
+__global__ void k6b_sort(const int64_t* __restrict__ cand_f, int64_t budget, int shift,
+                         const int32_t* __restrict__ start, const int32_t* __restrict__ cnt,
+                         const int32_t* __restrict__ tmp, int32_t* __restrict__ byf) {
+    pdl_entry();
+    // one thread per accepted entry (start[kF6B] of them), ranked within its
+    // bucket: a dense cluster of f costs O(len) per entry, not O(len^2)
+    // in one thread
+    GRID_LOOP(p, static_cast<int64_t>(start[kF6B])) {
+        const int32_t ri = tmp[p];
+        const int64_t fi = cand_f[ri];
+        const int64_t bk = fi >> shift;
+        const int32_t s0 = start[bk], len = cnt[bk];
+        int32_t rank = 0;
+        for (int32_t j = 0; j < len; ++j) {
+            const int32_t rj = tmp[s0 + j];
+            const int64_t fj = cand_f[rj];
+            rank += fj < fi || (fj == fi && rj < ri);
+        }
+        byf[s0 + rank] = ri;
+    }
+}
+
 __global__ void k6_scatter(const int64_t* __restrict__ cand_f, const int32_t* __restrict__ pos,
                            int64_t budget, int32_t* __restrict__ byf,
                            int32_t* __restrict__ naccepted) {
@@ -1228,6 +1283,9 @@ WideDecoder::WideDecoder(const DevPlan& plan, int64_t acc_cap, int64_t b_max, in
     cand_sum_.reset(Q);
     pos_.reset(Q);
     byf_.reset(Q);
+    f6cnt_.reset(kF6B);
+    f6cur_.reset(kF6B);
+    f6start_.reset(kF6B + 1);
     newflag_.reset(Q);
     newpos_.reset(Q);
     newf_.reset(Q);
@@ -1367,7 +1425,20 @@ void WideDecoder::enqueue(double2* y, const int64_t* sigma, const int64_t* sigma
             launch_pdl(pdl_, k6_small, 1, kSmallK6, 0, st, P, m, cand_f_.get(), cand_v_.get(), AF, AC, scal_.get(),
                                              acc_f_[nxt].get(), acc_c_[nxt].get());
         } else {
-            {
+            if (budget >= kF6BucketMin) {
+                int nbits = 0;
+                while ((int64_t{1} << nbits) < H.n) ++nbits;
+                const int shift = std::max(0, nbits - 12);  // f >> shift < 4096
+                zero_async(pdl_, f6cnt_.get(), kF6B * sizeof(int32_t), st);
+                launch_pdl(pdl_, k6b_count, grid_of(std::max<int64_t>(budget, kF6B)), kT, 0, st,
+                           cand_f_.get(), budget, shift, f6cnt_.get(), f6cur_.get(), naccepted);
+                launch_pdl(pdl_, scan_kernel, 1, kScanT, 0, st, f6cnt_.get(), int64_t{kF6B}, nullptr,
+                           f6start_.get(), f6start_.get() + kF6B);
+                launch_pdl(pdl_, k6b_scatter, grid_of(budget), kT, 0, st, cand_f_.get(), budget, shift,
+                           f6start_.get(), f6cur_.get(), pos_.get());
+                launch_pdl(pdl_, k6b_sort, grid_of(budget), kT, 0, st, cand_f_.get(), budget, shift,
+                           f6start_.get(), f6cnt_.get(), pos_.get(), byf_.get());
+            } else {
                 const unsigned tiles = static_cast<unsigned>((budget + kT - 1) / kT);
                 const unsigned split = std::max(1u, std::min(64u, 1184u / tiles));
                 zero_async(pdl_, pos_.get(), budget * sizeof(int32_t), st);

@@ -77,6 +77,7 @@ private:
     DeviceBuffer<double> phi_;
     DeviceBuffer<int32_t> pcode_, pos_, byf_, newflag_, newpos_;
     DeviceBuffer<int64_t> cand_f_, newf_;
+    DeviceBuffer<int32_t> f6cnt_, f6cur_, f6start_;  // K6 bucket sort of large budgets
     // outputs, copied to the caller's buffers after the graph
     DeviceBuffer<int64_t> out_f_, out_count_;
     DeviceBuffer<double2> out_c_;
