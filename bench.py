@@ -12,14 +12,19 @@ the whole batch (1024 signals per GPU; weak scaling under torchrun).
 
 The b200 arm prints one JSON line with:
   value     transforms/s, device-resident inputs, device-timed (CUDA events on
-            the execution stream), max over ranks
+            the execution stream), max over ranks; every step is a full
+            validating sfft4 (finiteness scan of every sample, as the
+            reference's sfft4.cpp:133 does per call); value_assume_valid is
+            the same steps with MSFFT_FLAG_ASSUME_VALID
   e2e       the same metric through the public API with pinned HOST inputs:
             every step ingests the batch (sparse ingest: the samples the
             transform reads, gathered by host threads; finiteness scan of
             every sample) host->device and copies the sparse results
             device->host inside the timed region
-  roofline  the fused gather (encode) kernel: algorithmic bytes = distinct
-            32-B sectors loaded (from the plan) / its CUDA-event time
+  roofline  the fused gather (encode) kernel -- the stage the metric names:
+            algorithmic bytes = distinct 32-B sectors loaded (from the plan) /
+            its CUDA-event time; roofline_validate: the finiteness scan
+            (n * 8 bytes per signal), the larger share of a validating step
   cpu_baseline  the reference's own CPU code (oracle/_ref, compiled from
             /root/reference) on a bounded sample, all host threads
 The reference arm (--impl reference) times that same CPU code alone.
@@ -159,18 +164,35 @@ def e2e_batch(batch: int, sig_bytes: int, local_ranks: int) -> int:
     return max(min(batch, fit), min(batch, 8))
 
 
-def pipe_evidence():
+def current_csrc():
+    from paper_2011_05698_b200.provenance import csrc_sha256
+    return csrc_sha256()
+
+
+def profile_record(name, csrc):
+    """A committed ncu summary under profiles/, or None unless it carries
+    the content hash of the native sources this run was built from."""
+    path = os.path.join(REPO, "profiles", name)
+    if not os.path.exists(path):
+        return None
+    with open(path) as f:
+        d = json.load(f)
+    if d.get("csrc_sha256") != csrc:
+        return None
+    return d
+
+
+def pipe_evidence(csrc):
     """FP64-pipe and SM utilisation of the fused launch and of the decode
-    (the FFT / locate / estimate stages) from the committed ncu captures of
-    the same workload (profiles/r01_final/*_ncu_summary.json), or None."""
+    (the FFT / locate / estimate stages) from committed ncu captures of the
+    same workload on the same native sources, or None."""
     out = {}
     for key, name in (("fused_kernel", "fused_ncu_summary.json"),
-                      ("decode_kernel", "decode_c4_ncu_summary.json")):
-        path = os.path.join(REPO, "profiles", "r01_final", name)
-        if not os.path.exists(path):
+                      ("decode_kernel", "decode_c4_ncu_summary.json"),
+                      ("validate_kernel", "validate_ncu_summary.json")):
+        d = profile_record(name, csrc)
+        if d is None:
             continue
-        with open(path) as f:
-            d = json.load(f)
         def num(raw, short):  # raw ncu metric names or tools/ncu_summary.py keys
             v = d.get(raw, d.get(short))
             try:
@@ -183,7 +205,7 @@ def pipe_evidence():
                                              "issue_active_pct"),
                     "sm_throughput_frac": num("sm__throughput.avg.pct_of_peak_sustained_elapsed",
                                               "sm_throughput_pct"),
-                    "top_stalls": d.get("stall_share"), "source": f"profiles/r01_final/{name}"}
+                    "top_stalls": d.get("stall_share"), "source": f"profiles/{name}"}
     return out or None
 
 
@@ -294,12 +316,15 @@ def main():
     stream = torch.cuda.current_stream(dev)
     sh = stream.cuda_stream
 
-    # ingest: validate every sample once (ComplexSignal::validate); the timed
-    # steps then run with ASSUME_VALID (documented deviation)
+    # Every timed step is a full sfft4 call as the reference defines it:
+    # ComplexSignal::validate scans all n samples of every signal
+    # (sfft4.cpp:133) before the transform.  The same steps with
+    # ASSUME_VALID (a caller that validated at ingest) are timed after, as
+    # value_assume_valid.
+    seed_sets = (aseeds, aseeds ^ np.uint64(0x9E3779B97F4A7C15))
     plan.execute(x, aseeds, out=out, assume_valid=False, stream=sh)
     for i in range(args.warmup):
-        plan.execute(x, (aseeds, aseeds ^ np.uint64(0x9E3779B97F4A7C15))[i & 1], out=out,
-                     assume_valid=True, stream=sh)
+        plan.execute(x, seed_sets[i & 1], out=out, assume_valid=False, stream=sh)
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
@@ -308,23 +333,40 @@ def main():
         clocks.start()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
-    # the K timed steps are enqueued back to back (MSFFT_FLAG_ASYNC: no host
-    # round trip between steps); two seed sets alternate so every step uploads
-    # its seeds and recomputes the σ plan; errors of the loop surface in sync()
-    seed_sets = (aseeds, aseeds ^ np.uint64(0x9E3779B97F4A7C15))
-    ev0.record(stream)
-    for i in range(args.steps):
-        plan.execute(x, seed_sets[i & 1], out=out, assume_valid=True, stream=sh, async_=True)
-    ev1.record(stream)
-    torch.cuda.synchronize()
-    plan.sync(sh)
-    if world > 1:
-        torch.distributed.barrier()
+
+    def timed(assume_valid):
+        # the K steps are enqueued back to back (MSFFT_FLAG_ASYNC: no host
+        # round trip between steps); two seed sets alternate so every step
+        # uploads its seeds and recomputes the sigma plan; errors of the loop
+        # (a non-finite sample, a decode failure) surface in sync()
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for i in range(args.steps):
+            plan.execute(x, seed_sets[i & 1], out=out, assume_valid=assume_valid, stream=sh,
+                         async_=True)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        plan.sync(sh)
+        if world > 1:
+            torch.distributed.barrier()
+        t = ev0.elapsed_time(ev1) / args.steps
+        return max_over_ranks(t, dev) if world > 1 else t
+
+    ms = timed(False)
+    for i in range(args.warmup):
+        plan.execute(x, seed_sets[i & 1], out=out, assume_valid=True, stream=sh)
+    ms_av = timed(True)
     clk = clocks.stop()
-    ms = ev0.elapsed_time(ev1) / args.steps
-    if world > 1:
-        ms = max_over_ranks(ms, dev)
     value = total / (ms / 1e3)
+    value_av = total / (ms_av / 1e3)
+
+    # live time of the validation scan alone (ComplexSignal::validate over
+    # the rank's batch), CUDA events around the kernel on the same stream
+    val_ms = [M.validate_signal(x, stream=sh) for _ in range(3)]
+    val_avg = sum(val_ms) / len(val_ms)
+    val_bytes = B * n * 8
 
     # live per-launch time of the dominant kernel (fused encode+decode), CUDA
     # events around each launch on its stream
@@ -351,19 +393,19 @@ def main():
         dec_ms.append(st[2])
     enc_avg = sum(enc_ms) / len(enc_ms)
     dec_avg = sum(dec_ms) / len(dec_ms)
+    csrc = current_csrc()
+
     def ncu_traffic(name):
         """DRAM bytes per launch from a committed `ncu --set full` capture of
-        the same workload (profiles/<name>), or None."""
-        tpath = os.path.join(REPO, "profiles", name)
-        if os.path.exists(tpath):
-            with open(tpath) as f:
-                tj = json.load(f)
-            if tj.get("batch") == B and tj.get("n") == n:
-                return tj.get("dram_bytes_per_launch")
+        the same workload on the same native sources (profiles/<name>), or None."""
+        tj = profile_record(name, csrc)
+        if tj is not None and tj.get("batch") == B and tj.get("n") == n:
+            return tj.get("dram_bytes_per_launch")
         return None
 
     traffic = ncu_traffic("fused_traffic.json")
     enc_traffic = ncu_traffic("encode_traffic.json")
+    val_traffic = ncu_traffic("validate_traffic.json")
 
     # e2e through the public API with pinned host buffers
     e2e = None
@@ -379,20 +421,28 @@ def main():
         if world > 1:
             torch.distributed.barrier()
         t0 = time.perf_counter()
+        h2d = d2h = 0
         for _ in range(args.e2e_steps):
             fh, ch, nh, _ = plan.execute(xh, eseeds)  # validating call, D2H results
+            hb, db = plan.copy_bytes()
+            h2d += hb
+            d2h += db
         et = (time.perf_counter() - t0) / args.e2e_steps
         if world > 1:
             et = max_over_ranks(et, dev)
         etotal = sum_over_ranks(be, dev) if world > 1 else be
         ingest = plan.ingest_samples_per_signal
         e2e = {"value": etotal / et, "unit": "transforms/s", "signals_per_step": int(etotal),
-               "h2d_bytes_per_step": int(etotal * (ingest or n) * 8),
+               "h2d_bytes_per_step": int(sum_over_ranks(h2d, dev) if world > 1 else h2d)
+               // args.e2e_steps,
                "ingest": (f"sparse: host threads gather the {ingest} samples per signal the "
-                          "transform reads into pinned staging (and scan all n for "
-                          "non-finite values); only those are copied" if ingest else
-                          "dense: whole signals copied"),
-               "d2h_bytes_per_step": int(etotal * k * (8 + 16) + etotal * 8),
+                          "transform reads into pinned staging; the finiteness scan of all n "
+                          "samples is split between host threads and whole rows the copy "
+                          "engine moves for a device scan (both counted in h2d bytes)"
+                          if ingest else "dense: whole signals copied"),
+               "d2h_bytes_per_step": int(sum_over_ranks(d2h, dev) if world > 1 else d2h)
+               // args.e2e_steps,
+               "bytes_source": "counted by the library per call (msfft_plan_copy_bytes)",
                "ms_per_step": et * 1e3, "timing": "wall clock around msfft_execute (blocking)"}
         del xh
 
@@ -427,10 +477,13 @@ def main():
         parity = {"signals": S, "support_identical": same, "max_rel_coef_err": worst,
                   "tolerance": 1e-4}
 
-    launches = plan.launches(B, assume_valid=True) * args.steps
+    launches = plan.launches(B, assume_valid=False) * args.steps
     line = {
         "metric": METRIC, "value": value, "unit": "transforms/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "step": "one validating sfft4 over the batch: ComplexSignal::validate scan of every "
+                "sample (sfft4.cpp:133) + the transform, as the reference does per call",
+        "value_assume_valid": value_av, "ms_per_step_assume_valid": ms_av,
         "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (seeded K-sparse spectra + AWGN, BASELINE.json configs[3] law)",
@@ -440,7 +493,7 @@ def main():
                      "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": alg_bytes, "loads_per_launch": loads,
-                     "launch_ms": main_avg,
+                     "launch_ms": main_avg, "share_of_step": main_avg / ms,
                      "note": "every random 8-B sample load fills a 128-B HBM line on B200, so "
                              "the 32-B-sector metric tops out at 0.25 of peak "
                              "(profiles/r01/gather_probe_*.log)",
@@ -449,7 +502,14 @@ def main():
                                      "frac": alg_bytes / (enc_avg / 1e3) / 1e9 / peak,
                                      "traffic": enc_traffic},
                      "decode_only_ms": dec_avg,
-                     "pipes": pipe_evidence()},
+                     "pipes": pipe_evidence(csrc), "csrc_sha256": csrc},
+        "roofline_validate": {"bound": "hbm", "kernel": "validate_kernel (finiteness scan)",
+                              "achieved": val_bytes / (val_avg / 1e3) / 1e9, "peak": peak,
+                              "unit": "GB/s",
+                              "frac": val_bytes / (val_avg / 1e3) / 1e9 / peak,
+                              "traffic": val_traffic, "algorithmic_bytes_per_launch": val_bytes,
+                              "launch_ms": val_avg,
+                              "share_of_step": val_avg / ms},
         "e2e": e2e, "cpu_baseline": cpu, "parity_sample": parity, "clocks": clk,
         "gpu_launches": launches,
     }

@@ -142,6 +142,24 @@ int64_t msfft_plan_launches(msfft_plan plan, int64_t batch, uint32_t flags);
  * signal and the environment does not set MSFFT_SPARSE_INGEST=0. */
 int64_t msfft_plan_ingest_samples(msfft_plan plan);
 
+/* ComplexSignal::validate (proj/src/signal.cpp:18-26; decl
+ * proj/include/msfft/signal.hpp:13-18) for `batch` signals of n samples,
+ * x_stride samples apart: n a power of two >= 4, sample_count == n, every
+ * sample finite -- checked in that order, with the reference's messages
+ * (MSFFT_ERR_INVALID_ARGUMENT).  Device input: one HBM-bound scan on
+ * `stream` (NULL = legacy default), synchronous; *device_ms (optional)
+ * receives the scan kernel's CUDA-event time.  Host input: scanned on the
+ * calling thread. */
+int msfft_validate_signal(const void* x, int64_t n, int64_t sample_count, int64_t batch,
+                          int64_t x_stride, int32_t dtype, int32_t x_location, void* stream,
+                          double* device_ms, char* err, size_t errlen);
+
+/* Bytes the plan's last msfft_execute moved host->device (whole signals or
+ * compact ingest rows, rows copied whole for device-side validation, seeds)
+ * and device->host (results, status flags).  No reference counterpart: the
+ * e2e accounting of bench.py. */
+int msfft_plan_copy_bytes(msfft_plan plan, int64_t* h2d, int64_t* d2h);
+
 /* ---- split phases: one signal sharded by index range over several GPUs ----
  * No reference counterpart (the reference transforms one signal on one host,
  * sfft4.cpp:133-200); this is the SURVEY §8(e) multi-GPU path.  A rank holding

@@ -145,6 +145,23 @@ def _signal_arg(x):
     return C.c_void_p(a.ctypes.data), int(a.shape[-1]), dt, _L.MSFFT_HOST, a
 
 
+def validate_signal(x, n: int | None = None, stream=None) -> float:
+    """ComplexSignal::validate (proj/src/signal.cpp:18-26) for one signal or
+    a (batch, n) array/tensor: n a power of two >= 4, sample count == n, all
+    samples finite, else InvalidArgument with the reference's message.  CUDA
+    tensors are scanned on the device (`stream`, default the legacy stream);
+    returns the scan kernel's device ms (0 for host input)."""
+    ptr, cnt, dt, loc, keep = _signal_arg(x)
+    shape = tuple(keep.shape)
+    batch = 1 if len(shape) == 1 else int(shape[0])
+    nn = cnt if n is None else int(n)
+    ms = C.c_double()
+    err = C.create_string_buffer(1024)
+    _raise(_L.lib().msfft_validate_signal(ptr, nn, cnt, batch, cnt, dt, loc,
+                                          C.c_void_p(stream or 0), C.byref(ms), err, 1024), err)
+    return ms.value
+
+
 def device_count() -> int:
     return int(_L.lib().msfft_device_count())
 
@@ -286,6 +303,12 @@ class Plan:
         """Samples per signal moved host->device for host inputs (sparse
         ingest); 0 when whole signals are copied."""
         return int(self._lib.msfft_plan_ingest_samples(self._h))
+
+    def copy_bytes(self):
+        """(host->device, device->host) bytes moved by the last execute."""
+        a, b = C.c_int64(), C.c_int64()
+        self._lib.msfft_plan_copy_bytes(self._h, C.byref(a), C.byref(b))
+        return a.value, b.value
 
     def sync(self, stream=None) -> None:
         """Wait for this plan's work on `stream` and raise the errors of

@@ -27,7 +27,7 @@ EXPORTED = (
     "msfft_window", "msfft_window_response", "msfft_trace", "msfft_plan_stage_times",
     "msfft_plan_gather_traffic", "msfft_sigma_plan", "msfft_tau_plan",
     "msfft_plan_values_per_signal", "msfft_encode_values", "msfft_decode_values",
-    "msfft_plan_ingest_samples", "msfft_generate_test_signal", "msfft_synthesize",
+    "msfft_plan_ingest_samples", "msfft_plan_copy_bytes", "msfft_validate_signal", "msfft_generate_test_signal", "msfft_synthesize",
     "msfft_add_awgn", "msfft_dft_dense", "msfft_idft_dense", "msfft_top_k_spectrum",
     "msfft_error_metrics", "msfft_signal_file_length", "msfft_read_signal_file",
     "msfft_write_signal_file", "msfft_write_truth_csv", "msfft_read_truth_csv",
@@ -106,6 +106,11 @@ def lib() -> C.CDLL:
     if hasattr(L, "msfft_plan_sync"):
         L.msfft_plan_sync.argtypes = [VP, VP] + E
         L.msfft_plan_sync.restype = C.c_int
+    L.msfft_validate_signal.argtypes = [VP, i64, i64, i64, i64, i32, i32, VP, P(f64),
+                                        C.c_char_p, C.c_size_t]
+    L.msfft_validate_signal.restype = C.c_int
+    L.msfft_plan_copy_bytes.argtypes = [VP, P(i64), P(i64)]
+    L.msfft_plan_copy_bytes.restype = C.c_int
     if hasattr(L, "msfft_plan_ingest_samples"):
         L.msfft_plan_ingest_samples.argtypes = [VP]
         L.msfft_plan_ingest_samples.restype = i64

@@ -217,6 +217,59 @@ int64_t msfft_plan_ingest_samples(msfft_plan plan) {
     return plan->plan->ingest_samples_per_signal();
 }
 
+int msfft_validate_signal(const void* x, int64_t n, int64_t sample_count, int64_t batch,
+                          int64_t x_stride, int32_t dtype, int32_t x_location, void* stream,
+                          double* device_ms, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        // ComplexSignal::validate (proj/src/signal.cpp:18-26), same check order
+        if (n < 4 || !is_pow2_u(static_cast<uint64_t>(n)))
+            throw std::invalid_argument("ComplexSignal: n must be a power of two >= 4");
+        if (sample_count != n) throw std::invalid_argument("ComplexSignal: sample count != n");
+        if (dtype != MSFFT_C128 && dtype != MSFFT_C64)
+            throw std::invalid_argument("msfft_validate_signal: unknown dtype");
+        if (batch < 0 || x_stride < n)
+            throw std::invalid_argument("msfft_validate_signal: need batch >= 0 and x_stride >= n");
+        const bool c128 = dtype == MSFFT_C128;
+        if (device_ms) *device_ms = 0.0;
+        if (batch == 0) return;
+        if (x_location != MSFFT_DEVICE) {
+            const size_t row = static_cast<size_t>(x_stride) * (c128 ? 16 : 8);
+            for (int64_t s = 0; s < batch; ++s)
+                if (has_non_finite(static_cast<const unsigned char*>(x) + s * row, n, c128, false))
+                    throw std::invalid_argument("ComplexSignal: non-finite sample");
+            return;
+        }
+        require_device();
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        int32_t* d_bad = nullptr;
+        MSFFT_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_bad), sizeof(int32_t), st));
+        MSFFT_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(int32_t), st));
+        cudaEvent_t ev[2];
+        MSFFT_CUDA(cudaEventCreate(&ev[0]));
+        MSFFT_CUDA(cudaEventCreate(&ev[1]));
+        MSFFT_CUDA(cudaEventRecord(ev[0], st));
+        launch_validate(x, c128, n, x_stride, batch, d_bad, st);
+        MSFFT_CUDA(cudaEventRecord(ev[1], st));
+        int32_t bad = 0;
+        MSFFT_CUDA(cudaMemcpyAsync(&bad, d_bad, sizeof(bad), cudaMemcpyDeviceToHost, st));
+        MSFFT_CUDA(cudaFreeAsync(d_bad, st));
+        MSFFT_CUDA(cudaStreamSynchronize(st));
+        float ms = 0.f;
+        MSFFT_CUDA(cudaEventElapsedTime(&ms, ev[0], ev[1]));
+        cudaEventDestroy(ev[0]);
+        cudaEventDestroy(ev[1]);
+        if (device_ms) *device_ms = ms;
+        if (bad) throw std::invalid_argument("ComplexSignal: non-finite sample");
+    });
+}
+
+int msfft_plan_copy_bytes(msfft_plan plan, int64_t* h2d, int64_t* d2h) {
+    if (!plan) return MSFFT_ERR_INVALID_ARGUMENT;
+    if (h2d) *h2d = plan->plan->last_h2d_bytes();
+    if (d2h) *d2h = plan->plan->last_d2h_bytes();
+    return MSFFT_OK;
+}
+
 int64_t msfft_plan_values_per_signal(msfft_plan plan) {
     if (!plan) return -1;
     return plan->plan->values_per_signal();

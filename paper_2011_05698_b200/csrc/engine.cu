@@ -30,21 +30,108 @@ struct DeviceGuard {
     }
 };
 
-// ComplexSignal::validate's finiteness scan (proj/src/signal.cpp:22-25).
-template <class T>
-__global__ void validate_kernel(const T* __restrict__ x, int64_t n, int64_t x_stride,
-                                int64_t batch, int32_t* __restrict__ bad) {
-    const int64_t total = n * batch;
-    bool ok = true;
-    for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
-         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int64_t s = e / n;
-        const T v = __ldcs(x + s * x_stride + (e - s * n));
-        ok &= isfinite(static_cast<double>(v.x)) && isfinite(static_cast<double>(v.y));
+// ComplexSignal::validate's finiteness scan (proj/src/signal.cpp:22-25),
+// HBM-bound: rows of 16-B vectors (row = one signal, or the whole batch when
+// it is contiguous), 8 streaming 16-B loads in flight per thread, a
+// non-finite value is an all-ones exponent field (integer tests, no FP).
+constexpr int kValUnroll = 8;
+constexpr int kValThreads = 256;
+
+template <bool C128>
+__global__ void __launch_bounds__(kValThreads)
+validate_kernel(const uint4* __restrict__ x, int64_t vrow, int64_t vstride, int64_t rows,
+                int32_t* __restrict__ bad) {
+    uint32_t acc = 0;  // OR of "exponent all ones" tests
+    const int64_t step = static_cast<int64_t>(gridDim.x) * kValThreads * kValUnroll;
+    for (int64_t row = blockIdx.y; row < rows; row += gridDim.y) {
+        const uint4* p = x + row * vstride;
+        for (int64_t base = static_cast<int64_t>(blockIdx.x) * kValThreads * kValUnroll + threadIdx.x;
+             base < vrow; base += step) {
+            uint4 v[kValUnroll];
+#pragma unroll
+            for (int j = 0; j < kValUnroll; ++j) {
+                const int64_t i = base + static_cast<int64_t>(j) * kValThreads;
+                v[j] = i < vrow ? __ldcs(p + i) : make_uint4(0, 0, 0, 0);
+            }
+#pragma unroll
+            for (int j = 0; j < kValUnroll; ++j) {
+                if (C128) {  // high words of the two doubles
+                    acc |= ((v[j].y & 0x7ff00000u) == 0x7ff00000u) |
+                           ((v[j].w & 0x7ff00000u) == 0x7ff00000u);
+                } else {
+                    acc |= ((v[j].x & 0x7f800000u) == 0x7f800000u) |
+                           ((v[j].y & 0x7f800000u) == 0x7f800000u) |
+                           ((v[j].z & 0x7f800000u) == 0x7f800000u) |
+                           ((v[j].w & 0x7f800000u) == 0x7f800000u);
+                }
+            }
+        }
     }
+    if (__any_sync(0xffffffffu, acc != 0) && (threadIdx.x & 31) == 0) atomicExch(bad, 1);
+}
+
+// Element-wise fallback for rows that are not 16-B vectors (odd shard spans).
+template <class T>
+__global__ void validate_scalar_kernel(const T* __restrict__ x, int64_t n, int64_t x_stride,
+                                       int64_t batch, int32_t* __restrict__ bad) {
+    bool ok = true;
+    for (int64_t s = blockIdx.y; s < batch; s += gridDim.y)
+        for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n;
+             e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+            const T v = __ldcs(x + s * x_stride + e);
+            ok &= isfinite(static_cast<double>(v.x)) && isfinite(static_cast<double>(v.y));
+        }
     if (!__all_sync(0xffffffffu, ok) && (threadIdx.x & 31) == 0) atomicExch(bad, 1);
 }
 
+}  // namespace
+
+void launch_validate(const void* d_x, bool c128, int64_t span, int64_t x_stride, int64_t batch,
+                     int32_t* bad, cudaStream_t st) {
+    if (span <= 0 || batch <= 0) return;
+    const int64_t elem = c128 ? 16 : 8;
+    int sms = 148;
+    {
+        int dev = 0;
+        if (cudaGetDevice(&dev) == cudaSuccess)
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const int64_t blocks_total = static_cast<int64_t>(sms) * (2048 / kValThreads);
+    const bool vec = (reinterpret_cast<uintptr_t>(d_x) % 16 == 0) && (span * elem) % 16 == 0 &&
+                     (x_stride * elem) % 16 == 0;
+    if (vec) {
+        int64_t vrow = span * elem / 16, vstride = x_stride * elem / 16, rows = batch;
+        if (x_stride == span) {  // one flat row
+            vrow *= batch;
+            rows = 1;
+        }
+        const int64_t per_block = static_cast<int64_t>(kValThreads) * kValUnroll;
+        const int64_t gy = std::min<int64_t>(rows, 65535);
+        const int64_t gx = std::max<int64_t>(
+            1, std::min<int64_t>((vrow + per_block - 1) / per_block, (blocks_total + gy - 1) / gy));
+        const dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>(gy));
+        if (c128)
+            validate_kernel<true><<<grid, kValThreads, 0, st>>>(static_cast<const uint4*>(d_x), vrow,
+                                                                vstride, rows, bad);
+        else
+            validate_kernel<false><<<grid, kValThreads, 0, st>>>(static_cast<const uint4*>(d_x),
+                                                                 vrow, vstride, rows, bad);
+    } else {
+        const int64_t gy = std::min<int64_t>(batch, 65535);
+        const int64_t gx = std::max<int64_t>(
+            1, std::min<int64_t>((span + 255) / 256, (blocks_total + gy - 1) / gy));
+        const dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>(gy));
+        if (c128)
+            validate_scalar_kernel<double2><<<grid, 256, 0, st>>>(static_cast<const double2*>(d_x),
+                                                                 span, x_stride, batch, bad);
+        else
+            validate_scalar_kernel<float2><<<grid, 256, 0, st>>>(static_cast<const float2*>(d_x),
+                                                                span, x_stride, batch, bad);
+    }
+    MSFFT_LAUNCH_CHECK("validate_kernel");
+}
+
+namespace {
 }  // namespace
 
 Plan::Plan(int64_t n, int64_t k, int64_t l, double q, double delta, bool c128, int device)
@@ -418,18 +505,7 @@ void Plan::run_chunk(int64_t batch, const void* d_x, int64_t x_stride, const int
                      const ExecOptions& opt, bool compact) {
     const int64_t n = sched_.n;
     const DevPlan& P = compact ? dplan_compact_ : dplan_;
-    if (validate) {
-        const int64_t total = n * batch;
-        const unsigned blocks =
-            static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, 148 * 16));
-        if (c128_)
-            validate_kernel<double2><<<blocks, 256, 0, st>>>(
-                static_cast<const double2*>(d_x), n, x_stride, batch, flags_.get() + 1);
-        else
-            validate_kernel<float2><<<blocks, 256, 0, st>>>(
-                static_cast<const float2*>(d_x), n, x_stride, batch, flags_.get() + 1);
-        MSFFT_LAUNCH_CHECK("validate_kernel");
-    }
+    if (validate) launch_validate(d_x, c128_, n, x_stride, batch, flags_.get() + 1, st);
     const bool traced = opt.pre || opt.post || opt.sel_bucket;
     if (!traced && !opt.force_serial && fused_enabled_ && big_b_iters_.empty() && !lay_.big) {
         // one persistent launch: encode and decode share the SMs
@@ -579,6 +655,8 @@ void Plan::execute(int64_t batch, const void* x, int64_t x_stride, const uint64_
     int64_t* d_ocnt = opt.out_on_device ? out_count : out_count_.get();
 
     stage_ms_[0] = stage_ms_[1] = stage_ms_[2] = 0.0;
+    h2d_bytes_ = 0;
+    d2h_bytes_ = 0;
     MSFFT_CUDA(cudaEventRecord(ev_start_, st));
     upload_sigmas(batch, seeds, st);
     const bool validate = !opt.assume_valid;
@@ -605,6 +683,7 @@ void Plan::execute(int64_t batch, const void* x, int64_t x_stride, const uint64_
                                              x_stride * elem, sig_bytes, cb,
                                              cudaMemcpyHostToDevice, copy_stream_));
             }
+            h2d_bytes_ += cb * sig_bytes;
             MSFFT_CUDA(cudaEventRecord(ev_copied_[slot], copy_stream_));
             MSFFT_CUDA(cudaStreamWaitEvent(st, ev_copied_[slot], 0));
             run_chunk(cb, dst, n, sig_.get() + s0 * iters, sig_inv_.get() + s0 * iters,
@@ -619,6 +698,8 @@ void Plan::execute(int64_t batch, const void* x, int64_t x_stride, const uint64_
                                    cudaMemcpyDeviceToHost, st));
         MSFFT_CUDA(cudaMemcpyAsync(out_count, d_ocnt, sizeof(int64_t) * batch,
                                    cudaMemcpyDeviceToHost, st));
+        d2h_bytes_ += static_cast<int64_t>(sizeof(int64_t) + sizeof(double2)) * batch * k +
+                      static_cast<int64_t>(sizeof(int64_t)) * batch;
     }
     MSFFT_CUDA(cudaEventRecord(ev_end_, st));
     if (async_call) {
@@ -700,16 +781,8 @@ bool Plan::execute_sparse(int64_t batch, const void* x, int64_t x_stride, const 
                 MSFFT_CUDA(cudaMemcpy2DAsync(vstage_.get(), sig_bytes, hx + s0 * x_stride * elem,
                                              x_stride * elem, sig_bytes, cb,
                                              cudaMemcpyHostToDevice, vstream_));
-            const int64_t total = n * cb;
-            const unsigned blocks =
-                static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, 148 * 16));
-            if (c128_)
-                validate_kernel<double2><<<blocks, 256, 0, vstream_>>>(
-                    reinterpret_cast<const double2*>(vstage_.get()), n, n, cb, flags_.get() + 1);
-            else
-                validate_kernel<float2><<<blocks, 256, 0, vstream_>>>(
-                    reinterpret_cast<const float2*>(vstage_.get()), n, n, cb, flags_.get() + 1);
-            MSFFT_LAUNCH_CHECK("validate_kernel");
+            launch_validate(vstage_.get(), c128_, n, n, cb, flags_.get() + 1, vstream_);
+            h2d_bytes_ += static_cast<int64_t>(cb * sig_bytes);
         }
         MSFFT_CUDA(cudaEventRecord(ev_vend_, vstream_));
     }
@@ -728,6 +801,7 @@ bool Plan::execute_sparse(int64_t batch, const void* x, int64_t x_stride, const 
         MSFFT_CUDA(cudaMemcpyAsync(xstage_[slot].get(), gstage_[slot],
                                    static_cast<size_t>(cb * C) * elem, cudaMemcpyHostToDevice,
                                    copy_stream_));
+        h2d_bytes_ += cb * C * static_cast<int64_t>(elem);
         MSFFT_CUDA(cudaEventRecord(ev_copied_[slot], copy_stream_));
         MSFFT_CUDA(cudaStreamWaitEvent(st, ev_copied_[slot], 0));
         run_chunk(cb, xstage_[slot].get(), C, sig_.get() + s0 * iters, sig_inv_.get() + s0 * iters,
@@ -766,6 +840,7 @@ void Plan::upload_sigmas(int64_t batch, const uint64_t* seeds, cudaStream_t st) 
     std::memcpy(h_seeds_[seed_slot_], seeds, sizeof(uint64_t) * batch);
     MSFFT_CUDA(cudaMemcpyAsync(seeds_.get(), h_seeds_[seed_slot_], sizeof(uint64_t) * batch,
                                cudaMemcpyHostToDevice, st));
+    h2d_bytes_ += static_cast<int64_t>(sizeof(uint64_t)) * batch;
     MSFFT_CUDA(cudaEventRecord(ev_seeds_[seed_slot_], st));
     launch_sigma(seeds_.get(), batch, iters, sched_.n, sig_.get(), sig_inv_.get(), st);
     last_seeds_.assign(seeds, seeds + batch);
@@ -816,6 +891,7 @@ void Plan::sync(cudaStream_t stream) {
 void Plan::check_flags(cudaStream_t st) {
     int32_t hflags[2] = {0, 0};
     MSFFT_CUDA(cudaMemcpyAsync(hflags, flags_.get(), sizeof(hflags), cudaMemcpyDeviceToHost, st));
+    d2h_bytes_ += static_cast<int64_t>(sizeof(hflags));
     MSFFT_CUDA(cudaMemsetAsync(flags_.get(), 0, 2 * sizeof(int32_t), st));
     MSFFT_CUDA(cudaStreamSynchronize(st));
     if (hflags[1]) throw std::invalid_argument("ComplexSignal: non-finite sample");
@@ -836,18 +912,7 @@ void Plan::encode_values(int64_t batch, const void* d_x, int64_t x_stride, int64
     cudaStream_t st = stream ? stream : own_stream_;
     MSFFT_CUDA(cudaMemsetAsync(flags_.get(), 0, 2 * sizeof(int32_t), st));
     upload_sigmas(batch, seeds, st);
-    if (validate) {
-        const int64_t span = x_hi - x_lo, total = span * batch;
-        const unsigned blocks =
-            static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, 148 * 16));
-        if (c128_)
-            validate_kernel<double2><<<blocks, 256, 0, st>>>(
-                static_cast<const double2*>(d_x), span, x_stride, batch, flags_.get() + 1);
-        else
-            validate_kernel<float2><<<blocks, 256, 0, st>>>(
-                static_cast<const float2*>(d_x), span, x_stride, batch, flags_.get() + 1);
-        MSFFT_LAUNCH_CHECK("validate_kernel");
-    }
+    if (validate) launch_validate(d_x, c128_, x_hi - x_lo, x_stride, batch, flags_.get() + 1, st);
     DevPlan p = dplan_;
     p.x_lo = x_lo;
     p.x_hi = x_hi;

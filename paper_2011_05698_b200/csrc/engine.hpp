@@ -90,6 +90,11 @@ public:
     // [encode, bucket fft (b > 256), decode] ms of the last execute run with
     // stage_times (summed over chunks).
     const double* stage_ms() const { return stage_ms_; }
+    // bytes the last execute moved host->device (signal data, compact rows,
+    // rows copied for device validation, seeds) and device->host (results,
+    // status flags)
+    int64_t last_h2d_bytes() const { return h2d_bytes_; }
+    int64_t last_d2h_bytes() const { return d2h_bytes_; }
 
     std::mutex& mutex() { return mu_; }
 
@@ -157,6 +162,7 @@ private:
     cudaEvent_t ev_chunk_ = nullptr, ev_dec_done_ = nullptr;
     int64_t overlap_chunk_ = 0;          // signals per encode/decode sub-chunk (0 = serial)
     double stage_ms_[3] = {0, 0, 0};
+    int64_t h2d_bytes_ = 0, d2h_bytes_ = 0;
 
     DeviceBuffer<double2> y_;
     DeviceBuffer<int64_t> sig_, sig_inv_;
@@ -214,5 +220,11 @@ private:
 // plan parameters).
 std::shared_ptr<Plan> cached_plan(int64_t n, int64_t k, int64_t l, double q, double delta,
                                   bool c128, int device);
+
+// ComplexSignal::validate's finiteness scan on the device: `batch` rows of
+// `span` samples, `x_stride` samples apart; sets *bad to 1 if any is
+// non-finite.  HBM-bound streaming kernel (engine.cu).
+void launch_validate(const void* d_x, bool c128, int64_t span, int64_t x_stride, int64_t batch,
+                     int32_t* bad, cudaStream_t st);
 
 }  // namespace msfft_b200

@@ -175,14 +175,46 @@ def big_cases():
                  magnitude="loguniform_0.1_10")]
 
 
-def prewarm(o, n, k, delta):
+def c5_case():
+    """BASELINE.json configs[4]: N=2^27, K=10^4, complex128, |c| log-uniform
+    [0.1, 10], 20 dB (delta 1e-6, l=16, q=1)."""
+    return case("np", 1 << 27, 10000, 505, 20.0, magnitude="loguniform_0.1_10")
+
+
+def c3_more_cases():
+    n, b1 = 1 << 24, 4096
+    return [case("np", n, 1000, s, 30.0, dtype=dt, magnitude="uniform_0.5_2",
+                 min_sep=4 * n // b1) for s in (302, 303) for dt in ("complex128", "complex64")]
+
+
+def bucket_schedule(o, n, k, delta):
     b = o.initial_bucket_count(n, k, delta)
-    bs = set()
+    bs = []
     for _ in range(int(math.ceil(math.log2(k))) + 2):
-        bs.add(b)
+        if b not in bs:
+            bs.append(b)
         b = b // 2 if b > 32 else b
-    with cf.ThreadPoolExecutor(len(bs)) as ex:
-        list(ex.map(lambda bb: o.window(n, bb, delta, False), sorted(bs)))
+    return bs
+
+
+def prewarm(o, n, k, delta, workers=None):
+    """Designs every window of the transform's schedule in parallel threads
+    (the reference's process cache, window.cpp:179-193, designs outside its
+    lock).  At n=2^27 one design holds ~5.5 GB, so `workers` bounds memory."""
+    bs = bucket_schedule(o, n, k, delta)
+    with cf.ThreadPoolExecutor(workers or len(bs)) as ex:
+        list(ex.map(lambda bb: o.window(n, bb, delta, False), sorted(bs, reverse=True)))
+
+
+def window_shas(o, n, k, delta):
+    out = []
+    for b in bucket_schedule(o, n, k, delta):
+        w, g = o.window(n, b, delta)
+        out.append({"n": n, "b": b, "delta": delta, "w": w,
+                    "taps_sha256": hashlib.sha256(g.astype("<f8").tobytes()).hexdigest(),
+                    "taps_mid": hx(g[(w - 1) // 2])})
+        del g
+    return out
 
 
 def dump(name, obj):
@@ -210,6 +242,20 @@ def main(names):
     if "c3" in names:
         prewarm(o, 1 << 24, 1000, 1e-6)
         dump("sfft4_c3", [run_case(o, c) for c in c3_cases()])
+    if "c3more" in names:
+        prewarm(o, 1 << 24, 1000, 1e-6)
+        dump("sfft4_c3_more", [run_case(o, c) for c in c3_more_cases()])
+    if "c5" in names:
+        # ~1 h of window design (6 concurrent, ~5.5 GB each) then ~1-1.5 h of
+        # single-threaded sfft4; run in the background.
+        c = c5_case()
+        t = time.time()
+        prewarm(o, c["n"], c["k"], c["delta"], workers=6)
+        wins = window_shas(o, c["n"], c["k"], c["delta"])
+        dump("sfft4_c5_windows", {"design_wall_s": time.time() - t, "windows": wins})
+        res = run_case(o, c)
+        res["windows"] = wins
+        dump("sfft4_c5", res)
 
 
 if __name__ == "__main__":

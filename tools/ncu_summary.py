@@ -12,7 +12,12 @@ import argparse
 import csv
 import io
 import json
+import os
 import subprocess
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2011_05698_b200.provenance import csrc_sha256  # noqa: E402
 
 KEYS = {
     "gpu__time_duration.sum": "duration",
@@ -87,6 +92,8 @@ if __name__ == "__main__":
     s = summarize(a.report)
     if a.workload:
         s["workload"] = a.workload
+    # the native sources the capture ran on (run this on the same tree)
+    s["csrc_sha256"] = csrc_sha256()
     print(json.dumps(s, indent=1))
     if a.traffic:
         rd = scaled_bytes(s.get("dram_read"), s.get("dram_read_unit"))
@@ -99,7 +106,7 @@ if __name__ == "__main__":
         rec = {"kernel": s["kernel"], "batch": a.batch, "n": a.n,
                "dram_bytes_per_launch": int(rd + wr),
                "dram_bytes_read": int(rd), "dram_bytes_write": int(wr),
-               "duration_ms_under_ncu": dur_ms,
+               "duration_ms_under_ncu": dur_ms, "csrc_sha256": s["csrc_sha256"],
                "source": f"{a.report} (ncu --set full --clock-control none)"}
         with open(a.traffic, "w") as f:
             json.dump(rec, f, indent=1)
