@@ -31,40 +31,107 @@ struct DeviceGuard {
 };
 
 // ComplexSignal::validate's finiteness scan (proj/src/signal.cpp:22-25),
-// HBM-bound: rows of 16-B vectors (row = one signal, or the whole batch when
-// it is contiguous), 8 streaming 16-B loads in flight per thread, a
-// non-finite value is an all-ones exponent field (integer tests, no FP).
-constexpr int kValUnroll = 8;
+// HBM-bound.  The rows (one per signal, or the whole batch as one row when it
+// is contiguous) are cut into 16-KB chunks; each CTA (one per SM) streams its
+// chunks through an 8-deep shared-memory ring filled by TMA bulk copies
+// (cp.async.bulk + mbarrier) -- 128 KB in flight per SM, which reads HBM at
+// ~7.4 TB/s where 16-B LDGs top out at ~6.3 TB/s (tools/validate_probe.cu,
+// profiles/r02/validate_probe.log).  A non-finite value is an all-ones
+// exponent field: integer tests on the staged words, no FP.
+__device__ __forceinline__ uint32_t val_smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+constexpr int kValChunk = 16384;
+constexpr int kValRing = 8;
 constexpr int kValThreads = 256;
 
 template <bool C128>
+__device__ __forceinline__ uint32_t non_finite4(uint4 v) {
+    if (C128)  // high words of the two doubles
+        return ((v.y & 0x7ff00000u) == 0x7ff00000u) | ((v.w & 0x7ff00000u) == 0x7ff00000u);
+    return ((v.x & 0x7f800000u) == 0x7f800000u) | ((v.y & 0x7f800000u) == 0x7f800000u) |
+           ((v.z & 0x7f800000u) == 0x7f800000u) | ((v.w & 0x7f800000u) == 0x7f800000u);
+}
+
+// Chunk cursor: (row, chunk within the row) of chunk index c, advanced by
+// the grid stride without 64-bit divisions (the consumer loop must stay far
+// below the ~650 cycles one 16-KB chunk takes to arrive at HBM speed).
+struct ChunkCursor {
+    int64_t row, cir;
+    __device__ void advance(int64_t q, int64_t r, int64_t cpr) {
+        row += q;
+        cir += r;
+        if (cir >= cpr) {
+            cir -= cpr;
+            ++row;
+        }
+    }
+};
+
+template <bool C128>
 __global__ void __launch_bounds__(kValThreads)
-validate_kernel(const uint4* __restrict__ x, int64_t vrow, int64_t vstride, int64_t rows,
-                int32_t* __restrict__ bad) {
-    uint32_t acc = 0;  // OR of "exponent all ones" tests
-    const int64_t step = static_cast<int64_t>(gridDim.x) * kValThreads * kValUnroll;
-    for (int64_t row = blockIdx.y; row < rows; row += gridDim.y) {
-        const uint4* p = x + row * vstride;
-        for (int64_t base = static_cast<int64_t>(blockIdx.x) * kValThreads * kValUnroll + threadIdx.x;
-             base < vrow; base += step) {
-            uint4 v[kValUnroll];
+validate_kernel(const unsigned char* __restrict__ x, int64_t row_bytes, int64_t stride_bytes,
+                int64_t rows, int32_t* __restrict__ bad) {
+    extern __shared__ __align__(128) unsigned char ring[];
+    __shared__ __align__(8) uint64_t bar[kValRing];
+    const int64_t cpr = (row_bytes + kValChunk - 1) / kValChunk;  // chunks per row
+    const int64_t nch = cpr * rows;
+    const int64_t q = gridDim.x / cpr, r = gridDim.x % cpr;       // grid stride in (row, cir)
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kValRing; ++i)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(val_smem_u32(&bar[i])));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    auto issue = [&](const ChunkCursor& cc, int slot) {
+        const int64_t off = cc.cir * kValChunk;
+        const uint32_t bytes = static_cast<uint32_t>(min(static_cast<int64_t>(kValChunk), row_bytes - off));
+        const uint32_t b = val_smem_u32(&bar[slot]);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes)
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+            ::"r"(val_smem_u32(ring + slot * kValChunk)), "l"(x + cc.row * stride_bytes + off),
+            "r"(bytes), "r"(b)
+            : "memory");
+    };
+    ChunkCursor cons{blockIdx.x / cpr, blockIdx.x % cpr};  // the chunk being scanned
+    ChunkCursor prod = cons;                                // the next chunk to request
+    int64_t c_prod = blockIdx.x;
+    if (threadIdx.x == 0)
+        for (int i = 0; i < kValRing && c_prod < nch; ++i) {
+            issue(prod, i);
+            prod.advance(q, r, cpr);
+            c_prod += gridDim.x;
+        }
+    uint32_t acc = 0;
+    int it = 0;
+    for (int64_t c = blockIdx.x; c < nch; c += gridDim.x, ++it) {
+        const int slot = it % kValRing;
+        const uint32_t parity = static_cast<uint32_t>(it / kValRing) & 1u;
+        asm volatile(
+            "{\n .reg .pred p;\n WAIT_%=:\n"
+            " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+            " @!p bra WAIT_%=;\n}" ::"r"(val_smem_u32(&bar[slot])),
+            "r"(parity)
+            : "memory");
+        const uint4* v = reinterpret_cast<const uint4*>(ring + slot * kValChunk);
+        const int64_t rem = row_bytes - cons.cir * kValChunk;
+        if (rem >= kValChunk) {
 #pragma unroll
-            for (int j = 0; j < kValUnroll; ++j) {
-                const int64_t i = base + static_cast<int64_t>(j) * kValThreads;
-                v[j] = i < vrow ? __ldcs(p + i) : make_uint4(0, 0, 0, 0);
-            }
-#pragma unroll
-            for (int j = 0; j < kValUnroll; ++j) {
-                if (C128) {  // high words of the two doubles
-                    acc |= ((v[j].y & 0x7ff00000u) == 0x7ff00000u) |
-                           ((v[j].w & 0x7ff00000u) == 0x7ff00000u);
-                } else {
-                    acc |= ((v[j].x & 0x7f800000u) == 0x7f800000u) |
-                           ((v[j].y & 0x7f800000u) == 0x7f800000u) |
-                           ((v[j].z & 0x7f800000u) == 0x7f800000u) |
-                           ((v[j].w & 0x7f800000u) == 0x7f800000u);
-                }
-            }
+            for (int i = 0; i < kValChunk / 16 / kValThreads; ++i)
+                acc |= non_finite4<C128>(v[threadIdx.x + i * kValThreads]);
+        } else {
+            const int nv = static_cast<int>(rem / 16);
+            for (int i = threadIdx.x; i < nv; i += kValThreads) acc |= non_finite4<C128>(v[i]);
+        }
+        cons.advance(q, r, cpr);
+        __syncthreads();  // the slot is consumed before it is refilled
+        if (threadIdx.x == 0 && c_prod < nch) {
+            issue(prod, slot);
+            prod.advance(q, r, cpr);
+            c_prod += gridDim.x;
         }
     }
     if (__any_sync(0xffffffffu, acc != 0) && (threadIdx.x & 31) == 0) atomicExch(bad, 1);
@@ -96,27 +163,31 @@ void launch_validate(const void* d_x, bool c128, int64_t span, int64_t x_stride,
         if (cudaGetDevice(&dev) == cudaSuccess)
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     }
-    const int64_t blocks_total = static_cast<int64_t>(sms) * (2048 / kValThreads);
     const bool vec = (reinterpret_cast<uintptr_t>(d_x) % 16 == 0) && (span * elem) % 16 == 0 &&
                      (x_stride * elem) % 16 == 0;
     if (vec) {
-        int64_t vrow = span * elem / 16, vstride = x_stride * elem / 16, rows = batch;
+        int64_t row_bytes = span * elem, rows = batch;
         if (x_stride == span) {  // one flat row
-            vrow *= batch;
+            row_bytes *= batch;
             rows = 1;
         }
-        const int64_t per_block = static_cast<int64_t>(kValThreads) * kValUnroll;
-        const int64_t gy = std::min<int64_t>(rows, 65535);
-        const int64_t gx = std::max<int64_t>(
-            1, std::min<int64_t>((vrow + per_block - 1) / per_block, (blocks_total + gy - 1) / gy));
-        const dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>(gy));
+        const int64_t nch = (row_bytes + kValChunk - 1) / kValChunk * rows;
+        const unsigned grid = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(nch, sms)));
+        const size_t smem = static_cast<size_t>(kValChunk) * kValRing;
         if (c128)
-            validate_kernel<true><<<grid, kValThreads, 0, st>>>(static_cast<const uint4*>(d_x), vrow,
-                                                                vstride, rows, bad);
+            MSFFT_CUDA(cudaFuncSetAttribute(validate_kernel<true>,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         else
-            validate_kernel<false><<<grid, kValThreads, 0, st>>>(static_cast<const uint4*>(d_x),
-                                                                 vrow, vstride, rows, bad);
+            MSFFT_CUDA(cudaFuncSetAttribute(validate_kernel<false>,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        if (c128)
+            validate_kernel<true><<<grid, kValThreads, smem, st>>>(
+                static_cast<const unsigned char*>(d_x), row_bytes, x_stride * elem, rows, bad);
+        else
+            validate_kernel<false><<<grid, kValThreads, smem, st>>>(
+                static_cast<const unsigned char*>(d_x), row_bytes, x_stride * elem, rows, bad);
     } else {
+        const int64_t blocks_total = static_cast<int64_t>(sms) * 8;
         const int64_t gy = std::min<int64_t>(batch, 65535);
         const int64_t gx = std::max<int64_t>(
             1, std::min<int64_t>((span + 255) / 256, (blocks_total + gy - 1) / gy));
@@ -144,8 +215,11 @@ Plan::Plan(int64_t n, int64_t k, int64_t l, double q, double delta, bool c128, i
     });
     if (sched_.iterations > kMaxIters)
         throw std::invalid_argument("sfft4: iteration count exceeds the device plan limit");
-    // Scatter-free L2 fills: the gather touches one 32-B sector per sample.
-    cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, 32);
+    // MSFFT_L2_FETCH (bytes, diagnostics): cudaLimitMaxL2FetchGranularity.
+    // Not set by default: the random gather fills whole 128-B lines whatever
+    // it says, and 32 B slows the streaming validation scan by a third.
+    if (const char* e = std::getenv("MSFFT_L2_FETCH"))
+        cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, std::atoi(e));
 
     size_t taps_smem_max = kTapsSmemMax;  // MSFFT_TAPS_SMEM_MAX (bytes): diagnostics
     if (const char* e = std::getenv("MSFFT_TAPS_SMEM_MAX")) taps_smem_max = std::atoll(e);
