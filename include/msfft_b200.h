@@ -289,12 +289,70 @@ int msfft_sigma_plan(uint64_t seed, int64_t n, int32_t iterations, int64_t* sigm
 int msfft_tau_plan(double l_width, int64_t n, int64_t l, double q, int64_t* taus, int32_t cap,
                    int32_t* rounds, char* err, size_t errlen);
 
+/* ---- the reference's scalar plan helpers (host; same code the plan uses) -----
+ * mod_inverse      proj/src/bucketize.cpp:21-37 (errors: even sigma, bad n)
+ * bucket_of        proj/src/bucketize.cpp:63-68 (returns -1 for l_width/b <= 0)
+ * stage_count      proj/src/locate.cpp:44-53 (the reference loops forever when
+ *                  l/(q+1) <= 1; here that is the MultiscaleConfig error)
+ * tau_schedule     proj/src/locate.cpp:39-42
+ * config_validate  MultiscaleConfig::validate, proj/src/locate.cpp:25-30
+ * check_parameter_bounds  proj/src/locate.cpp:125-132 (q unused, as there)
+ * initial_bucket_count    proj/src/sfft4.cpp:115-129 (windows designed on the
+ *                  GPU, so it needs a device) */
+int msfft_mod_inverse(int64_t sigma, int64_t n, int64_t* out, char* err, size_t errlen);
+int64_t msfft_bucket_of(int64_t u, int64_t l_width, int64_t b);
+int msfft_stage_count(double region_length, int64_t l, double q, int32_t* out, char* err,
+                      size_t errlen);
+int msfft_tau_schedule(double region_length, int64_t n, int64_t* out, char* err, size_t errlen);
+int msfft_config_validate(int64_t l, double q, char* err, size_t errlen);
+int msfft_check_parameter_bounds(double max_dphi, int64_t l, double q, int32_t* l_ok,
+                                 double* q_min, char* err, size_t errlen);
+int msfft_initial_bucket_count(int64_t n, int64_t k, double delta, int64_t* out, char* err,
+                               size_t errlen);
+
+/* ---- the locate arithmetic, batched on the device ---------------------------
+ * Each evaluates, for `count` host-array entries, the same device functions
+ * the fused / wide decodes run (so callers and tests see the GPU's
+ * arithmetic):
+ * phase_of                 proj/src/locate.cpp:32-37: z interleaved complex128,
+ *                          status[k] = 1 where z == 0 (the reference throws
+ *                          std::domain_error "phase_of: zero value")
+ * position_phase           proj/src/locate.cpp:19-23 (n a power of two)
+ * circular_phase_distance  proj/src/locate.cpp:14-17
+ * locate_step              proj/src/locate.cpp:63-81: measurement (phi[k],
+ *                          tau[k]), region[k] -> out[k] */
+typedef struct msfft_locate_region {  /* LocateRegion, locate.hpp:23-32 */
+    double u_min;
+    double length;
+    int32_t stage;
+    int32_t reserved;
+} msfft_locate_region;
+int msfft_phase_of(const double* z, int64_t count, double* phase, int32_t* status, char* err,
+                   size_t errlen);
+int msfft_position_phase(const double* u, const int64_t* tau, int64_t count, int64_t n,
+                         double* out, char* err, size_t errlen);
+int msfft_circular_phase_distance(const double* a, const double* b, int64_t count, double* out,
+                                  char* err, size_t errlen);
+int msfft_locate_step(const double* phi, const int64_t* tau, const msfft_locate_region* region,
+                      int64_t count, int64_t l, double q, int64_t n, msfft_locate_region* out,
+                      char* err, size_t errlen);
+
+/* bucketize_fn<Sampler> (proj/include/msfft/bucketize.hpp:63-86): the caller
+ * evaluates its sampler once per tap in increasing tap order (the reference's
+ * contract) into values[r][h + t], t = -h..h (w = window support, complex128,
+ * host); the GPU folds per bin in ascending t, runs the radix-2 DIT and
+ * scales by 1/n: out [rounds][b] complex128 (host), bit-identical to the
+ * reference's fold.  *samples_read (optional) = w. */
+int msfft_bucketize_taps(int64_t n, int64_t b, double delta, const double* values, int64_t rounds,
+                         double* out, int64_t* samples_read, char* err, size_t errlen);
+
 /* ---- kernel-level entry points (parity tests) ------------------------------
  * Window taps/support exactly as design_flat_window (window.cpp:105-177). */
 int msfft_window(int64_t n, int64_t b, double delta, int32_t device, int64_t* w, double* taps,
                  int64_t taps_cap, char* err, size_t errlen);
-/* G_d from the device response table (FlatWindow::response_at, window.cpp:89-99);
- * |idx| <= 3L/2 + 1. */
+/* FlatWindow::response_at (window.cpp:89-99) at any integer offsets idx[k]
+ * (reduced mod n), evaluated on the device with the series the decode's
+ * response table uses (for |idx| <= 3L/2 + 1 exactly the table's values). */
 int msfft_window_response(int64_t n, int64_t b, double delta, int32_t device,
                           const int64_t* idx, int64_t count, double* out, char* err,
                           size_t errlen);

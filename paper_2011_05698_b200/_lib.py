@@ -32,7 +32,11 @@ EXPORTED = (
     "msfft_error_metrics", "msfft_signal_file_length", "msfft_read_signal_file",
     "msfft_write_signal_file", "msfft_write_truth_csv", "msfft_read_truth_csv",
     "msfft_phase_experiment", "msfft_plan_sync", "msfft_bucketize", "msfft_predict_buckets",
-    "msfft_locate_frequency", "msfft_estimate_values",
+    "msfft_locate_frequency", "msfft_estimate_values", "msfft_mod_inverse", "msfft_bucket_of",
+    "msfft_stage_count", "msfft_tau_schedule", "msfft_config_validate",
+    "msfft_check_parameter_bounds", "msfft_initial_bucket_count", "msfft_phase_of",
+    "msfft_position_phase", "msfft_circular_phase_distance", "msfft_locate_step",
+    "msfft_bucketize_taps",
 )
 
 i64, u64, f64, i32, u32 = C.c_int64, C.c_uint64, C.c_double, C.c_int32, C.c_uint32
@@ -156,6 +160,25 @@ def lib() -> C.CDLL:
         for fn in ("msfft_bucketize", "msfft_predict_buckets", "msfft_locate_frequency",
                    "msfft_estimate_values"):
             getattr(L, fn).restype = C.c_int
+    # scalar plan helpers (host) and the batched locate arithmetic (device)
+    L.msfft_mod_inverse.argtypes = [i64, i64, P(i64)] + E
+    L.msfft_bucket_of.argtypes = [i64, i64, i64]
+    L.msfft_bucket_of.restype = i64
+    L.msfft_stage_count.argtypes = [f64, i64, f64, P(i32)] + E
+    L.msfft_tau_schedule.argtypes = [f64, i64, P(i64)] + E
+    L.msfft_config_validate.argtypes = [i64, f64] + E
+    L.msfft_check_parameter_bounds.argtypes = [f64, i64, f64, P(i32), P(f64)] + E
+    L.msfft_initial_bucket_count.argtypes = [i64, i64, f64, P(i64)] + E
+    L.msfft_phase_of.argtypes = [VP, i64, VP, VP] + E
+    L.msfft_position_phase.argtypes = [VP, VP, i64, i64, VP] + E
+    L.msfft_circular_phase_distance.argtypes = [VP, VP, i64, VP] + E
+    L.msfft_locate_step.argtypes = [VP, VP, VP, i64, i64, f64, i64, VP] + E
+    L.msfft_bucketize_taps.argtypes = [i64, i64, f64, VP, i64, VP, P(i64)] + E
+    for fn in ("msfft_mod_inverse", "msfft_stage_count", "msfft_tau_schedule",
+               "msfft_config_validate", "msfft_check_parameter_bounds",
+               "msfft_initial_bucket_count", "msfft_phase_of", "msfft_position_phase",
+               "msfft_circular_phase_distance", "msfft_locate_step", "msfft_bucketize_taps"):
+        getattr(L, fn).restype = C.c_int
     L.msfft_window.argtypes = [i64, i64, f64, i32, P(i64), P(f64), i64] + E
     L.msfft_window_response.argtypes = [i64, i64, f64, i32, P(i64), i64, P(f64)] + E
     L.msfft_trace.argtypes = [VP, i64, i32, i64, i64, f64, u64, f64, P(f64), P(f64), P(i64),

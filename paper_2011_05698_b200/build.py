@@ -21,7 +21,7 @@ LIB = os.path.join(HERE, "libmsfft_b200.so")
 CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
 CU_SOURCES = ["fft.cu", "window.cu", "sigma.cu", "encode.cu", "decode.cu", "fused.cu", "engine.cu",
-              "signal_ops.cu", "phase_mc.cu", "wide_decode.cu", "components.cu"]
+              "signal_ops.cu", "phase_mc.cu", "wide_decode.cu", "components.cu", "locate_ops.cu"]
 CXX_SOURCES = ["host_plan.cpp", "ingest.cpp", "signal_io.cpp", "capi.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC",
@@ -77,10 +77,12 @@ def build(verbose: bool = False, ptxas_verbose: bool = False) -> str:
         objs.append(o)
         if _stale(o, [s] + hdrs):
             _run([cxx] + CXX_FLAGS + CXX_FILE_FLAGS.get(src, []) + ["-c", s, "-o", o], verbose)
-    if _stale(LIB, objs):
+    exports = os.path.join(CSRC, "exports.map")
+    if _stale(LIB, objs + [exports]):
         tmp = LIB + ".tmp"
         _run([NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", tmp] + objs +
-             ["-Xlinker", "--exclude-libs,ALL", "-lpthread"], verbose)
+             ["-Xlinker", "--exclude-libs,ALL", "-Xlinker", f"--version-script={exports}",
+              "-lpthread"], verbose)
         os.replace(tmp, LIB)
     return LIB
 

@@ -217,6 +217,130 @@ def sigma_plan(seed: int, n: int, iterations: int) -> list[PermutationParams]:
     return [PermutationParams(int(a), int(b), 0) for a, b in zip(s, si)]
 
 
+# ---- scalar helpers (host plan code) and locate arithmetic (device) ---------
+
+def mod_inverse(sigma: int, n: int) -> int:
+    """bucketize.cpp:21-37."""
+    out = C.c_int64()
+    e = _err()
+    _raise(_L.lib().msfft_mod_inverse(int(sigma), int(n), C.byref(out), e, 1024), e)
+    return out.value
+
+
+def bucket_of(u: int, l_width: int, b: int) -> int:
+    """bucketize.cpp:63-68: round(u/L) mod b, ties away from zero."""
+    return int(_L.lib().msfft_bucket_of(int(u), int(l_width), int(b)))
+
+
+def stage_count(region_length: float, cfg: MultiscaleConfig | None = None) -> int:
+    """locate.cpp:44-53."""
+    cfg = cfg or MultiscaleConfig()
+    out = C.c_int32()
+    e = _err()
+    _raise(_L.lib().msfft_stage_count(float(region_length), int(cfg.l), float(cfg.q),
+                                      C.byref(out), e, 1024), e)
+    return out.value
+
+
+def tau_schedule(region_length: float, n: int) -> int:
+    """locate.cpp:39-42."""
+    out = C.c_int64()
+    e = _err()
+    _raise(_L.lib().msfft_tau_schedule(float(region_length), int(n), C.byref(out), e, 1024), e)
+    return out.value
+
+
+def initial_bucket_count(n: int, k: int, delta: float) -> int:
+    """sfft4.cpp:115-129 (windows designed on the GPU)."""
+    out = C.c_int64()
+    e = _err()
+    _raise(_L.lib().msfft_initial_bucket_count(int(n), int(k), float(delta), C.byref(out), e,
+                                               1024), e)
+    return out.value
+
+
+def check_parameter_bounds(max_dphi: float, l: int, q: float = 0.0):
+    """locate.cpp:125-132 -> (l_ok, q_min)."""
+    ok, qm = C.c_int32(), C.c_double()
+    e = _err()
+    _raise(_L.lib().msfft_check_parameter_bounds(float(max_dphi), int(l), float(q), C.byref(ok),
+                                                 C.byref(qm), e, 1024), e)
+    return bool(ok.value), qm.value
+
+
+def phase_of(z):
+    """phase_of (locate.cpp:32-37) of each complex z on the device (the
+    decode's arithmetic): (phases, status) with status 1 where z == 0."""
+    z = np.ascontiguousarray(np.atleast_1d(np.asarray(z, np.complex128)))
+    ph = np.zeros(z.size, np.float64)
+    st = np.zeros(z.size, np.int32)
+    e = _err()
+    _raise(_L.lib().msfft_phase_of(C.c_void_p(z.ctypes.data), z.size, C.c_void_p(ph.ctypes.data),
+                                   C.c_void_p(st.ctypes.data), e, 1024), e)
+    return ph, st
+
+
+def position_phase(u, tau, n: int) -> np.ndarray:
+    """position_phase (locate.cpp:19-23), elementwise on the device."""
+    u = np.ascontiguousarray(np.atleast_1d(np.asarray(u, np.float64)))
+    tau = np.ascontiguousarray(np.broadcast_to(np.asarray(tau, np.int64), u.shape))
+    out = np.zeros(u.size, np.float64)
+    e = _err()
+    _raise(_L.lib().msfft_position_phase(C.c_void_p(u.ctypes.data), C.c_void_p(tau.ctypes.data),
+                                         u.size, int(n), C.c_void_p(out.ctypes.data), e, 1024), e)
+    return out
+
+
+def circular_phase_distance(a, b) -> np.ndarray:
+    """circular_phase_distance (locate.cpp:14-17), elementwise on the device."""
+    a = np.ascontiguousarray(np.atleast_1d(np.asarray(a, np.float64)))
+    b = np.ascontiguousarray(np.broadcast_to(np.asarray(b, np.float64), a.shape))
+    out = np.zeros(a.size, np.float64)
+    e = _err()
+    _raise(_L.lib().msfft_circular_phase_distance(C.c_void_p(a.ctypes.data),
+                                                  C.c_void_p(b.ctypes.data), a.size,
+                                                  C.c_void_p(out.ctypes.data), e, 1024), e)
+    return out
+
+
+_REGION = np.dtype([("u_min", np.float64), ("length", np.float64), ("stage", np.int32),
+                    ("reserved", np.int32)])
+
+
+def locate_step(phi, tau, u_min, length, stage, cfg: MultiscaleConfig, n: int):
+    """locate_step (locate.cpp:63-81) for arrays of (measurement, region):
+    returns (u_min, length, stage) arrays of the next regions."""
+    phi = np.ascontiguousarray(np.atleast_1d(np.asarray(phi, np.float64)))
+    m = phi.size
+    tau = np.ascontiguousarray(np.broadcast_to(np.asarray(tau, np.int64), (m,)))
+    reg = np.zeros(m, _REGION)
+    reg["u_min"], reg["length"], reg["stage"] = u_min, length, stage
+    out = np.zeros(m, _REGION)
+    e = _err()
+    _raise(_L.lib().msfft_locate_step(C.c_void_p(phi.ctypes.data), C.c_void_p(tau.ctypes.data),
+                                      C.c_void_p(reg.ctypes.data), m, int(cfg.l), float(cfg.q),
+                                      int(n), C.c_void_p(out.ctypes.data), e, 1024), e)
+    return out["u_min"].copy(), out["length"].copy(), out["stage"].copy()
+
+
+def bucketize_fn(n: int, sample, win: FlatWindow, params: PermutationParams) -> BucketSet:
+    """bucketize_fn<Sampler> (bucketize.hpp:63-86): `sample(idx)` is called
+    once per tap in increasing tap order on this thread; the fold, DIT and
+    1/n run on the GPU (bit-identical to the reference's loop)."""
+    h = (win.w - 1) // 2
+    mask = n - 1
+    v = np.zeros(win.w, np.complex128)
+    for t in range(-h, h + 1):
+        v[h + t] = sample((params.sigma * ((t - params.tau) & mask)) & mask)
+    out = np.zeros(win.b, np.complex128)
+    w = C.c_int64()
+    e = _err()
+    _raise(_L.lib().msfft_bucketize_taps(int(n), int(win.b), float(win.delta),
+                                         C.c_void_p(v.ctypes.data), 1,
+                                         C.c_void_p(out.ctypes.data), C.byref(w), e, 1024), e)
+    return BucketSet(n, win.b, out, params, int(w.value))
+
+
 class Rng:
     """The draws sfft4 makes from its Rng (rng.hpp:19-59): one
     random_params(n, rng, 0) per iteration (sfft4.cpp:48), reproduced from

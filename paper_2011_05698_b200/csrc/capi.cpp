@@ -321,6 +321,115 @@ int msfft_tau_plan(double l_width, int64_t n, int64_t l, double q, int64_t* taus
     });
 }
 
+int msfft_mod_inverse(int64_t sigma, int64_t n, int64_t* out, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] { *out = mod_inverse(sigma, n); });
+}
+
+int64_t msfft_bucket_of(int64_t u, int64_t l_width, int64_t b) {
+    if (l_width <= 0 || b <= 0) return -1;
+    return bucket_of(u, l_width, b);
+}
+
+int msfft_stage_count(double region_length, int64_t l, double q, int32_t* out, char* err,
+                      size_t errlen) {
+    return guarded(err, errlen, [&] {
+        // the reference loops forever when l/(q+1) <= 1; report the config error
+        if (!(static_cast<double>(l) / (q + 1.0) > 1.0)) validate_cfg(l, q);
+        *out = stage_count(region_length, l, q);
+    });
+}
+
+int msfft_tau_schedule(double region_length, int64_t n, int64_t* out, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        if (n < 2) throw std::invalid_argument("tau_schedule: need n >= 2");
+        *out = tau_schedule(region_length, n);
+    });
+}
+
+int msfft_config_validate(int64_t l, double q, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] { validate_cfg(l, q); });
+}
+
+int msfft_check_parameter_bounds(double max_dphi, int64_t l, double q, int32_t* l_ok,
+                                 double* q_min, char* err, size_t errlen) {
+    (void)q;  // unused by the reference as well (locate.cpp:125)
+    return guarded(err, errlen, [&] {
+        bool ok = false;
+        check_parameter_bounds(max_dphi, l, &ok, q_min);
+        *l_ok = ok ? 1 : 0;
+    });
+}
+
+int msfft_initial_bucket_count(int64_t n, int64_t k, double delta, int64_t* out, char* err,
+                               size_t errlen) {
+    return guarded(err, errlen, [&] {
+        require_device();
+        int64_t b = 4;
+        while (b < 4 * k) b *= 2;
+        b = std::min(b, n / 4);
+        b = std::max<int64_t>(b, 4);
+        for (;;) {
+            try {
+                window_support(n, b, delta);  // get_flat_window on the GPU designer
+                *out = b;
+                return;
+            } catch (const std::invalid_argument&) {
+                if (b <= 4) throw;
+                b /= 2;
+            }
+        }
+    });
+}
+
+int msfft_phase_of(const double* z, int64_t count, double* phase, int32_t* status, char* err,
+                   size_t errlen) {
+    return guarded(err, errlen, [&] {
+        require_device();
+        phase_of_host(z, count, phase, status, nullptr);
+    });
+}
+
+int msfft_position_phase(const double* u, const int64_t* tau, int64_t count, int64_t n,
+                         double* out, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        require_device();
+        if (n < 2 || !is_pow2_u(static_cast<uint64_t>(n)))
+            throw std::invalid_argument("position_phase: n must be a power of two");
+        position_phase_host(u, tau, count, n, out, nullptr);
+    });
+}
+
+int msfft_circular_phase_distance(const double* a, const double* b, int64_t count, double* out,
+                                  char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        require_device();
+        circular_phase_distance_host(a, b, count, out, nullptr);
+    });
+}
+
+int msfft_locate_step(const double* phi, const int64_t* tau, const msfft_locate_region* region,
+                      int64_t count, int64_t l, double q, int64_t n, msfft_locate_region* out,
+                      char* err, size_t errlen) {
+    static_assert(sizeof(msfft_locate_region) == sizeof(LocateRegionDev), "region layout");
+    return guarded(err, errlen, [&] {
+        require_device();
+        if (n < 2 || !is_pow2_u(static_cast<uint64_t>(n)))
+            throw std::invalid_argument("locate_step: n must be a power of two");
+        if (l < 1) throw std::invalid_argument("MultiscaleConfig: l must be >= 2");
+        locate_step_host(phi, tau, reinterpret_cast<const LocateRegionDev*>(region), count, l, q,
+                         n, reinterpret_cast<LocateRegionDev*>(out), nullptr);
+    });
+}
+
+int msfft_bucketize_taps(int64_t n, int64_t b, double delta, const double* values, int64_t rounds,
+                         double* out, int64_t* samples_read, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        require_device();
+        const int64_t w = bucketize_taps_host(n, b, delta, values, rounds, out, nullptr);
+        if (samples_read) *samples_read = w;
+    });
+}
+
 int msfft_plan_gather_traffic(msfft_plan plan, int64_t batch, const uint64_t* seeds,
                               int64_t* loads, int64_t* sectors) {
     if (!plan || !seeds || !loads || !sectors) return MSFFT_ERR_INVALID_ARGUMENT;
@@ -371,15 +480,7 @@ int msfft_window_response(int64_t n, int64_t b, double delta, int32_t device,
     return guarded(err, errlen, [&] {
         require_device();
         if (device >= 0) MSFFT_CUDA(cudaSetDevice(device));
-        auto win = get_device_window(n, b, delta);
-        std::vector<double> table(static_cast<size_t>(2 * win->gmax + 1));
-        MSFFT_CUDA(cudaMemcpy(table.data(), win->d_ghat, sizeof(double) * table.size(),
-                              cudaMemcpyDeviceToHost));
-        for (int64_t i = 0; i < count; ++i) {
-            if (idx[i] < -win->gmax || idx[i] > win->gmax)
-                throw std::invalid_argument("msfft_window_response: offset outside the table");
-            out[i] = table[static_cast<size_t>(idx[i] + win->gmax)];
-        }
+        window_response_list(n, b, delta, idx, count, out);
     });
 }
 

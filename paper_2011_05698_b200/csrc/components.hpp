@@ -54,4 +54,34 @@ void estimate_values_device(int64_t n, int64_t b, double delta, const double2* d
                             const int64_t* d_u, int64_t count, double2* d_out, int32_t* d_status,
                             cudaStream_t st);
 
+// ---- scalar locate helpers and the sampler-driven fold (locate_ops.cu) ----
+// Batched over host arrays; each evaluates the device functions the decodes
+// use.  LocateRegionDev mirrors LocateRegion (locate.hpp:23-32).
+struct LocateRegionDev {
+    double u_min;
+    double length;
+    int32_t stage;
+    int32_t reserved;
+};
+
+// phase_of (locate.cpp:32-37) of z[k] (interleaved complex128): phase in
+// [0, 2pi), status 1 where z == 0 (the reference throws domain_error).
+void phase_of_host(const double* z, int64_t count, double* phase, int32_t* status,
+                   cudaStream_t st);
+// position_phase(u[k], tau[k], n) (locate.cpp:19-23).
+void position_phase_host(const double* u, const int64_t* tau, int64_t count, int64_t n,
+                         double* out, cudaStream_t st);
+// circular_phase_distance(a[k], b[k]) (locate.cpp:14-17).
+void circular_phase_distance_host(const double* a, const double* b, int64_t count, double* out,
+                                  cudaStream_t st);
+// locate_step({phi[k], tau[k]}, region[k], {l, q}, n) (locate.cpp:63-81).
+void locate_step_host(const double* phi, const int64_t* tau, const LocateRegionDev* region,
+                      int64_t count, int64_t l, double q, int64_t n, LocateRegionDev* out,
+                      cudaStream_t st);
+// bucketize_fn (bucketize.hpp:63-86) for `rounds` sample sequences the caller
+// evaluated in tap order: values [rounds][w] complex128, values[r][h + t] =
+// sample(src_t); out [rounds][b].  Returns w.
+int64_t bucketize_taps_host(int64_t n, int64_t b, double delta, const double* values,
+                            int64_t rounds, double* out, cudaStream_t st);
+
 }  // namespace msfft_b200

@@ -40,6 +40,20 @@ int stage_count(double region_length, int64_t l, double q) {
     return r;
 }
 
+int64_t bucket_of(int64_t u, int64_t l_width, int64_t b) {
+    const int64_t i = static_cast<int64_t>(
+        std::floor(static_cast<double>(u) / static_cast<double>(l_width) + 0.5));
+    return ((i % b) + b) % b;
+}
+
+void check_parameter_bounds(double max_dphi, int64_t l, bool* l_ok, double* q_min) {
+    if (!(max_dphi > 0.0))
+        throw std::invalid_argument("check_parameter_bounds: max_dphi must be positive");
+    constexpr double kPi = 3.141592653589793238462643383279502884;
+    *l_ok = static_cast<double>(l) <= kPi / max_dphi;
+    *q_min = max_dphi * static_cast<double>(l) / kPi;
+}
+
 int64_t ceil_log2(int64_t k) {
     int64_t r = 0;
     while ((int64_t{1} << r) < k) ++r;

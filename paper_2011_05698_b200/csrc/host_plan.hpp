@@ -42,6 +42,12 @@ int64_t tau_schedule(double region_length, int64_t n);
 // proj/src/locate.cpp:44-53.
 int stage_count(double region_length, int64_t l, double q);
 
+// proj/src/bucketize.cpp:63-68: round(u/L) mod b, ties away from zero.
+int64_t bucket_of(int64_t u, int64_t l_width, int64_t b);
+
+// proj/src/locate.cpp:125-132.  Throws std::invalid_argument for max_dphi <= 0.
+void check_parameter_bounds(double max_dphi, int64_t l, bool* l_ok, double* q_min);
+
 // proj/src/sfft4.cpp:14-18, 20-23.
 int64_t ceil_log2(int64_t k);
 inline int64_t next_bucket_count(int64_t b) { return b > 32 ? b / 2 : b; }

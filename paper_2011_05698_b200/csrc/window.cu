@@ -196,6 +196,38 @@ __global__ void response_table_warp_kernel(double* __restrict__ ghat,
     if (lane == 0) ghat[idx] = (taps[h] + acc) / nd;
 }
 
+// response_at(idx[k]) for arbitrary offsets (any residue mod n): the same
+// two series as the table kernels above, chosen by the same h threshold, so
+// an offset inside the table gets exactly the table's value.
+__global__ void response_list_kernel(double* __restrict__ out, const int64_t* __restrict__ idx,
+                                     int64_t count, const double* __restrict__ taps, int64_t n,
+                                     int64_t h, int warp_per_entry) {
+    const int64_t gt = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t k = warp_per_entry ? (gt >> 5) : gt;
+    const int lane = warp_per_entry ? static_cast<int>(threadIdx.x & 31) : 0;
+    if (k >= count) return;
+    const uint64_t mask = static_cast<uint64_t>(n - 1);
+    const uint64_t i0 = static_cast<uint64_t>(idx[k]) & mask;
+    const double nd = static_cast<double>(n);
+    if (!warp_per_entry) {
+        double acc = taps[h];
+        for (int64_t t = 1; t <= h; ++t) {
+            const uint64_t m = (i0 * static_cast<uint64_t>(t)) & mask;
+            const double a = kTwoPi * static_cast<double>(m) / nd;
+            acc += 2.0 * taps[h + t] * cos(a);
+        }
+        out[k] = acc / nd;
+        return;
+    }
+    double acc = 0.0;
+    for (int64_t t = 1 + lane; t <= h; t += 32) {
+        const uint64_t m = (i0 * static_cast<uint64_t>(t)) & mask;
+        acc += 2.0 * taps[h + t] * cos(kTwoPi * static_cast<double>(m) / nd);
+    }
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) out[k] = (taps[h] + acc) / nd;
+}
+
 struct Key {
     int device;
     int64_t n, b;
@@ -360,6 +392,28 @@ std::shared_ptr<const DeviceWindow> get_device_window(int64_t n, int64_t b, doub
 
 int64_t window_support(int64_t n, int64_t b, double delta) {
     return get_device_window(n, b, delta)->w;
+}
+
+void window_response_list(int64_t n, int64_t b, double delta, const int64_t* idx, int64_t count,
+                          double* out) {
+    auto win = get_device_window(n, b, delta);
+    if (count <= 0) return;
+    int64_t* d_idx = nullptr;
+    double* d_out = nullptr;
+    MSFFT_CUDA(cudaMalloc(&d_idx, sizeof(int64_t) * count));
+    MSFFT_CUDA(cudaMalloc(&d_out, sizeof(double) * count));
+    MSFFT_CUDA(cudaMemcpy(d_idx, idx, sizeof(int64_t) * count, cudaMemcpyHostToDevice));
+    const int wpe = win->h > 8192 ? 1 : 0;
+    const int64_t threads = wpe ? count * 32 : count;
+    response_list_kernel<<<static_cast<unsigned>((threads + 255) / 256), 256>>>(
+        d_out, d_idx, count, win->d_taps, n, win->h, wpe);
+    const cudaError_t le = cudaGetLastError();
+    cudaError_t ce = cudaSuccess;
+    if (le == cudaSuccess) ce = cudaMemcpy(out, d_out, sizeof(double) * count, cudaMemcpyDeviceToHost);
+    cudaFree(d_idx);
+    cudaFree(d_out);
+    MSFFT_CUDA(le);
+    MSFFT_CUDA(ce);
 }
 
 }  // namespace msfft_b200

@@ -35,4 +35,10 @@ std::shared_ptr<const DeviceWindow> get_device_window(int64_t n, int64_t b, doub
 // w only (designs and caches the window on the current device).
 int64_t window_support(int64_t n, int64_t b, double delta);
 
+// FlatWindow::response_at (window.cpp:89-99) at arbitrary offsets idx[k]
+// (any integer; reduced mod n), computed on the device exactly as the
+// response table is (same series, same summation scheme): host arrays.
+void window_response_list(int64_t n, int64_t b, double delta, const int64_t* idx, int64_t count,
+                          double* out);
+
 }  // namespace msfft_b200
