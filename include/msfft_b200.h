@@ -177,9 +177,25 @@ int64_t msfft_plan_values_per_signal(msfft_plan plan);
 int msfft_encode_values(msfft_plan plan, int64_t batch, const void* x, int64_t x_stride,
                         int64_t x_lo, int64_t x_hi, const uint64_t* seeds, double* y,
                         uint32_t flags, void* stream, char* err, size_t errlen);
+/* Tap-range sharding (x replicated on every rank): part `part` of `parts`
+ * walks only its contiguous share of every encode task's t' segments (all
+ * rounds, all iterations) and writes PARTIAL bucket values; the parts' vectors
+ * sum to the full vector.  Per-rank encode work is 1/parts of the whole
+ * (msfft_encode_values' index-range split walks every tap on every rank).
+ * x holds whole signals (x_stride >= n); the finiteness check covers the
+ * part-th slice of each signal.  Iterations with b > 256 are written as FOLDS
+ * (before their b-point FFT, which is linear): decode the summed vector with
+ * msfft_decode_folds, which runs those FFTs once and then decodes. */
+int msfft_encode_values_part(msfft_plan plan, int64_t batch, const void* x, int64_t x_stride,
+                             int64_t part, int64_t parts, const uint64_t* seeds, double* y,
+                             uint32_t flags, void* stream, char* err, size_t errlen);
 int msfft_decode_values(msfft_plan plan, int64_t batch, double* y, const uint64_t* seeds,
                         int64_t* out_f, double* out_c, int64_t* out_count, void* stream,
                         char* err, size_t errlen);
+
+int msfft_decode_folds(msfft_plan plan, int64_t batch, double* y, const uint64_t* seeds,
+                       int64_t* out_f, double* out_c, int64_t* out_count, void* stream,
+                       char* err, size_t errlen);
 
 /* ---- signal helpers: the steps either side of the path -------
  * Reference: proj/src/signal.cpp, proj/src/io.cpp, proj/src/bench.cpp:33-46.

@@ -120,6 +120,13 @@ class SfftResult:
     stats: TransformStats
 
 
+def _torch_stream(device) -> int:
+    """The current torch stream of `device` (its handle), so the split-phase
+    calls order after the caller's producers."""
+    import torch
+    return int(torch.cuda.current_stream(device).cuda_stream)
+
+
 def _is_torch(x) -> bool:
     return type(x).__module__.startswith("torch")
 
@@ -350,12 +357,47 @@ class Plan:
             self._h, batch, C.c_void_p(xl.data_ptr()), row_stride, int(x_lo),
             int(x_lo) + span, seeds.ctypes.data_as(C.POINTER(C.c_uint64)),
             C.c_void_p(y.data_ptr()), _L.MSFFT_FLAG_ASSUME_VALID if assume_valid else 0,
-            C.c_void_p(0), err, 1024)
+            C.c_void_p(_torch_stream(xl.device)), err, 1024)
         _raise(status, err)
         return y
 
-    def decode_values(self, y, seeds, out=None):
+    def encode_values_part(self, x, seeds, part: int, parts: int, y=None,
+                           assume_valid: bool = False):
+        """Tap-range sharding (x replicated: whole signals on this rank):
+        PARTIAL bucket values from this part's share of every encode task's
+        taps; the `parts` vectors sum to the full vector.  Per-rank encode
+        work is 1/parts of the transform's.  Iterations with b > 256 are left
+        as folds: decode the sum with decode_values(..., folds=True)."""
+        import torch
+        if not (_is_torch(x) and x.is_cuda):
+            raise InvalidArgument("Plan.encode_values_part: x must be a CUDA tensor")
+        want = torch.complex128 if self.dtype in ("complex128", "c128") else torch.complex64
+        if x.dtype != want:
+            raise InvalidArgument(f"Plan.encode_values_part: x must be {want}")
+        xl = x.reshape(1, -1) if x.dim() == 1 else x
+        if xl.stride(-1) != 1 or int(xl.shape[1]) != self.n:
+            raise InvalidArgument("Plan.encode_values_part: x rows must be whole contiguous signals")
+        batch = int(xl.shape[0])
+        row_stride = self.n if batch == 1 else int(xl.stride(0))
+        seeds = np.ascontiguousarray(np.asarray(seeds, dtype=np.uint64).reshape(-1))
+        if seeds.size != batch:
+            raise InvalidArgument("Plan.encode_values_part: need one seed per signal")
+        if y is None:
+            y = torch.empty((batch, self.values_per_signal), dtype=torch.complex128,
+                            device=xl.device)
+        err = C.create_string_buffer(1024)
+        status = self._lib.msfft_encode_values_part(
+            self._h, batch, C.c_void_p(xl.data_ptr()), row_stride, int(part), int(parts),
+            seeds.ctypes.data_as(C.POINTER(C.c_uint64)), C.c_void_p(y.data_ptr()),
+            _L.MSFFT_FLAG_ASSUME_VALID if assume_valid else 0,
+            C.c_void_p(_torch_stream(xl.device)), err, 1024)
+        _raise(status, err)
+        return y
+
+    def decode_values(self, y, seeds, out=None, folds: bool = False):
         """Selection / locate / estimate on summed bucket values y (consumed).
+        folds=True: y is a sum of encode_values_part outputs, whose b > 256
+        iterations are still folds (their FFTs run first, once).
         Returns (f, c, count) CUDA tensors ([B,k] int64, [B,k] complex128, [B])."""
         import torch
         if not (_is_torch(y) and y.is_cuda and y.dtype == torch.complex128 and y.is_contiguous()):
@@ -370,10 +412,11 @@ class Plan:
                    torch.zeros(batch, dtype=torch.int64, device=y.device))
         f, c, cnt = out
         err = C.create_string_buffer(1024)
-        status = self._lib.msfft_decode_values(
+        fn = self._lib.msfft_decode_folds if folds else self._lib.msfft_decode_values
+        status = fn(
             self._h, batch, C.c_void_p(y.data_ptr()), seeds.ctypes.data_as(C.POINTER(C.c_uint64)),
             C.c_void_p(f.data_ptr()), C.c_void_p(c.data_ptr()), C.c_void_p(cnt.data_ptr()),
-            C.c_void_p(0), err, 1024)
+            C.c_void_p(_torch_stream(y.device)), err, 1024)
         _raise(status, err)
         return f, c, cnt
 

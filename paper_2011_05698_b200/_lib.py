@@ -27,6 +27,7 @@ EXPORTED = (
     "msfft_window", "msfft_window_response", "msfft_trace", "msfft_plan_stage_times",
     "msfft_plan_gather_traffic", "msfft_sigma_plan", "msfft_tau_plan",
     "msfft_plan_values_per_signal", "msfft_encode_values", "msfft_decode_values",
+    "msfft_encode_values_part", "msfft_decode_folds",
     "msfft_plan_ingest_samples", "msfft_plan_copy_bytes", "msfft_validate_signal", "msfft_generate_test_signal", "msfft_synthesize",
     "msfft_add_awgn", "msfft_dft_dense", "msfft_idft_dense", "msfft_top_k_spectrum",
     "msfft_error_metrics", "msfft_signal_file_length", "msfft_read_signal_file",
@@ -124,6 +125,11 @@ def lib() -> C.CDLL:
         L.msfft_encode_values.argtypes = [VP, i64, VP, i64, i64, i64, P(u64), VP, u32, VP] + E
         L.msfft_encode_values.restype = C.c_int
         L.msfft_decode_values.argtypes = [VP, i64, VP, P(u64), VP, VP, VP, VP] + E
+        L.msfft_encode_values_part.argtypes = [VP, i64, VP, i64, i64, i64, P(u64), VP, u32,
+                                               VP] + E
+        L.msfft_encode_values_part.restype = C.c_int
+        L.msfft_decode_folds.argtypes = [VP, i64, VP, P(u64), VP, VP, VP, VP] + E
+        L.msfft_decode_folds.restype = C.c_int
         L.msfft_decode_values.restype = C.c_int
     if hasattr(L, "msfft_generate_test_signal"):
         CP = C.c_char_p

@@ -288,6 +288,19 @@ int msfft_encode_values(msfft_plan plan, int64_t batch, const void* x, int64_t x
     });
 }
 
+int msfft_encode_values_part(msfft_plan plan, int64_t batch, const void* x, int64_t x_stride,
+                             int64_t part, int64_t parts, const uint64_t* seeds, double* y,
+                             uint32_t flags, void* stream, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        if (!plan) throw std::invalid_argument("msfft_encode_values_part: null plan");
+        std::lock_guard<std::mutex> lock(plan->plan->mutex());
+        plan->plan->encode_values_part(batch, x, x_stride, part, parts, seeds,
+                                       reinterpret_cast<double2*>(y),
+                                       !(flags & MSFFT_FLAG_ASSUME_VALID),
+                                       static_cast<cudaStream_t>(stream));
+    });
+}
+
 int msfft_decode_values(msfft_plan plan, int64_t batch, double* y, const uint64_t* seeds,
                         int64_t* out_f, double* out_c, int64_t* out_count, void* stream,
                         char* err, size_t errlen) {
@@ -297,6 +310,18 @@ int msfft_decode_values(msfft_plan plan, int64_t batch, double* y, const uint64_
         plan->plan->decode_values(batch, reinterpret_cast<double2*>(y), seeds, out_f,
                                   reinterpret_cast<double2*>(out_c), out_count,
                                   static_cast<cudaStream_t>(stream));
+    });
+}
+
+int msfft_decode_folds(msfft_plan plan, int64_t batch, double* y, const uint64_t* seeds,
+                       int64_t* out_f, double* out_c, int64_t* out_count, void* stream,
+                       char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        if (!plan) throw std::invalid_argument("msfft_decode_folds: null plan");
+        std::lock_guard<std::mutex> lock(plan->plan->mutex());
+        plan->plan->decode_values(batch, reinterpret_cast<double2*>(y), seeds, out_f,
+                                  reinterpret_cast<double2*>(out_c), out_count,
+                                  static_cast<cudaStream_t>(stream), true);
     });
 }
 

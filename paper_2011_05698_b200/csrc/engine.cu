@@ -388,7 +388,32 @@ const Plan::TaskSet& Plan::tasks_for(int64_t batch) {
     ts.d.reset(v.size());
     MSFFT_CUDA(cudaMemcpy(ts.d.get(), v.data(), v.size() * sizeof(EncTask),
                           cudaMemcpyHostToDevice));
+    ts.host = std::move(v);
     return tasks_.emplace(batch, std::move(ts)).first->second;
+}
+
+const Plan::TaskSet& Plan::tasks_for_part(int64_t batch, int64_t part, int64_t parts) {
+    const auto key = std::make_tuple(batch, part, parts);
+    auto it = part_tasks_.find(key);
+    if (it != part_tasks_.end()) return it->second;
+    std::vector<EncTask> v = tasks_for(batch).host;
+    for (EncTask& t : v)
+        for (int i = 0; i < t.nseg; ++i) {
+            // piece `part` of [lo, hi]: every t' of the segment lands in
+            // exactly one piece; an empty piece has hi < lo (no trips)
+            const int64_t lo = t.seg_lo[i], len = static_cast<int64_t>(t.seg_hi[i]) - lo + 1;
+            const int64_t a = lo + len * part / parts, e = lo + len * (part + 1) / parts;
+            t.seg_cpos[i] += static_cast<int32_t>(a - lo);
+            t.seg_lo[i] = static_cast<int32_t>(a);
+            t.seg_hi[i] = static_cast<int32_t>(e - 1);
+        }
+    TaskSet ts;
+    ts.count = static_cast<int64_t>(v.size());
+    ts.d.reset(v.size());
+    MSFFT_CUDA(cudaMemcpy(ts.d.get(), v.data(), v.size() * sizeof(EncTask),
+                          cudaMemcpyHostToDevice));
+    ts.host = std::move(v);
+    return part_tasks_.emplace(key, std::move(ts)).first->second;
 }
 
 const Plan::FusedSet& Plan::fused_for(int64_t batch, int slot) {
@@ -696,8 +721,18 @@ void Plan::execute(int64_t batch, const void* x, int64_t x_stride, const uint64_
                             !opt.sel_bucket;
     if (async_call && !(opt.x_on_device && opt.out_on_device))
         throw std::invalid_argument("msfft_execute: MSFFT_FLAG_ASYNC needs device input and output");
+    // A PDL launch may overlap the previous one's last decodes, so it must not
+    // write the outputs that launch writes, and the two-set buffer rotation
+    // assumes one stream: otherwise launch stream-ordered.
+    const bool pdl_safe = last_out_[0] == nullptr ||
+                          (st == last_stream_ && out_f != last_out_[0] && out_c != last_out_[1] &&
+                           out_count != last_out_[2]);
+    last_stream_ = st;
+    last_out_[0] = out_f;
+    last_out_[1] = out_c;
+    last_out_[2] = out_count;
     if (async_call && pdl_enabled_ && fused_enabled_ && !opt.force_serial && big_b_iters_.empty() &&
-        !lay_.big && lay_.in_smem &&
+        !lay_.big && lay_.in_smem && pdl_safe &&
         fused_for(batch).fw.n_items >= fused_slots(c128_, fused_smem_)) {
         // PDL needs a grid that fills every CTA slot (see execute_pdl)
         execute_pdl(batch, x, x_stride, seeds, out_f, reinterpret_cast<double2*>(out_c), out_count,
@@ -728,6 +763,7 @@ void Plan::execute(int64_t batch, const void* x, int64_t x_stride, const uint64_
     double2* d_oc = opt.out_on_device ? reinterpret_cast<double2*>(out_c) : out_c_.get();
     int64_t* d_ocnt = opt.out_on_device ? out_count : out_count_.get();
 
+    pdl_count_ = 0;  // a stream-ordered call ends any PDL chain
     stage_ms_[0] = stage_ms_[1] = stage_ms_[2] = 0.0;
     h2d_bytes_ = 0;
     d2h_bytes_ = 0;
@@ -997,11 +1033,39 @@ void Plan::encode_values(int64_t batch, const void* d_x, int64_t x_stride, int64
     check_flags(st);
 }
 
+void Plan::encode_values_part(int64_t batch, const void* d_x, int64_t x_stride, int64_t part,
+                              int64_t parts, const uint64_t* seeds, double2* d_y, bool validate,
+                              cudaStream_t stream) {
+    DeviceGuard dg(device_);
+    if (batch <= 0) return;
+    const int64_t n = sched_.n;
+    if (parts < 1 || part < 0 || part >= parts)
+        throw std::invalid_argument("msfft_encode_values_part: need 0 <= part < parts");
+    if (x_stride < n) throw std::invalid_argument("msfft_encode_values_part: x_stride < n");
+    cudaStream_t st = stream ? stream : own_stream_;
+    MSFFT_CUDA(cudaMemsetAsync(flags_.get(), 0, 2 * sizeof(int32_t), st));
+    upload_sigmas(batch, seeds, st);
+    if (validate) {  // this rank checks its slice of every signal
+        const int64_t lo = n * part / parts, hi = n * (part + 1) / parts;
+        const size_t elem = c128_ ? sizeof(double2) : sizeof(float2);
+        launch_validate(static_cast<const unsigned char*>(d_x) + lo * elem, c128_, hi - lo,
+                        x_stride, batch, flags_.get() + 1, st);
+    }
+    const TaskSet& ts = tasks_for_part(batch, part, parts);
+    launch_encode(dplan_, ts.d.get(), ts.count, d_x, c128_, x_stride, batch, sig_.get(), d_y,
+                  enc_smem_, st);
+    // iterations with b > 256 stay folds: their b-point FFTs (linear) run
+    // once on the summed vector (decode_values with folds = true), not per rank
+    check_flags(st);
+}
+
 void Plan::decode_values(int64_t batch, double2* d_y, const uint64_t* seeds, int64_t* d_out_f,
-                         double2* d_out_c, int64_t* d_out_count, cudaStream_t stream) {
+                         double2* d_out_c, int64_t* d_out_count, cudaStream_t stream,
+                         bool folds) {
     DeviceGuard dg(device_);
     if (batch <= 0) return;
     cudaStream_t st = stream ? stream : own_stream_;
+    if (folds) bucket_ffts(d_y, batch, st);
     if (!lay_.in_smem) dec_work_.ensure(static_cast<size_t>(batch * lay_.bytes));
     MSFFT_CUDA(cudaMemsetAsync(flags_.get(), 0, 2 * sizeof(int32_t), st));
     upload_sigmas(batch, seeds, st);
@@ -1011,6 +1075,12 @@ void Plan::decode_values(int64_t batch, double2* d_y, const uint64_t* seeds, int
                                                   rounds_max_);
         const int iters = sched_.iterations;
         const int64_t k = sched_.k, vps = dplan_.values_per_signal;
+        // decode from the plan's own bucket buffer: the caller's vector stays
+        // untouched and the captured graphs are keyed on a stable address
+        y_.ensure(static_cast<size_t>(batch * vps));
+        MSFFT_CUDA(cudaMemcpyAsync(y_.get(), d_y, sizeof(double2) * batch * vps,
+                                   cudaMemcpyDeviceToDevice, st));
+        d_y = y_.get();
         for (int64_t s = 0; s < batch; ++s)
             wide_->run(d_y + s * vps, sig_.get() + s * iters, sig_inv_.get() + s * iters,
                        d_out_f + s * k, d_out_c + s * k, d_out_count + s, flags_.get(), st);

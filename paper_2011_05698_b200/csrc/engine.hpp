@@ -14,6 +14,7 @@
 #include <map>
 #include <memory>
 #include <mutex>
+#include <tuple>
 #include <vector>
 
 #include "cuda_check.hpp"
@@ -71,8 +72,20 @@ public:
     void encode_values(int64_t batch, const void* d_x, int64_t x_stride, int64_t x_lo,
                        int64_t x_hi, const uint64_t* seeds, double2* d_y, bool validate,
                        cudaStream_t stream);
+    // Tap-range sharding of one signal (x replicated on every rank): rank
+    // `part` of `parts` walks only its share of every task's t' segments
+    // and writes PARTIAL bucket values of every round; the partial vectors
+    // of parts 0..parts-1 sum to the full vector (bucketize is a sum over
+    // taps).  Per-rank encode work is 1/parts of the transform's.  The
+    // finiteness check covers the part-th slice of each signal.
+    void encode_values_part(int64_t batch, const void* d_x, int64_t x_stride, int64_t part,
+                            int64_t parts, const uint64_t* seeds, double2* d_y, bool validate,
+                            cudaStream_t stream);
+    // folds: d_y holds encode_values_part's sums, whose b > 256 iterations
+    // are still folds; their bucket FFTs run first.
     void decode_values(int64_t batch, double2* d_y, const uint64_t* seeds, int64_t* d_out_f,
-                       double2* d_out_c, int64_t* d_out_count, cudaStream_t stream);
+                       double2* d_out_c, int64_t* d_out_count, cudaStream_t stream,
+                       bool folds = false);
     int64_t values_per_signal() const { return dplan_.values_per_signal; }
 
     int64_t launches(int64_t batch, bool validate, bool serial = false) const;
@@ -102,6 +115,7 @@ private:
     struct TaskSet {
         DeviceBuffer<EncTask> d;
         int64_t count = 0;
+        std::vector<EncTask> host;
     };
     struct FusedSet {
         DeviceBuffer<EncTask> tasks;
@@ -109,6 +123,9 @@ private:
         FusedWork fw;
     };
     const TaskSet& tasks_for(int64_t batch);
+    // tasks_for(batch) with every task's t' segments cut to the part-th of
+    // `parts` equal contiguous pieces (tap-range sharding)
+    const TaskSet& tasks_for_part(int64_t batch, int64_t part, int64_t parts);
     // slot 0: synchronous launches; 1, 2: the two alternating buffer sets of
     // programmatic (PDL) asynchronous launches
     const FusedSet& fused_for(int64_t batch, int slot = 0);
@@ -145,6 +162,7 @@ private:
     int64_t b_max_ = 0, budget_max_ = 0;
     std::vector<int> big_b_iters_;  // iterations needing the separate FFT
     std::map<int64_t, TaskSet> tasks_;
+    std::map<std::tuple<int64_t, int64_t, int64_t>, TaskSet> part_tasks_;
     std::map<int64_t, FusedSet> fused_;
     bool fused_enabled_ = true;   // persistent encode+decode launch when all b <= 256
     int64_t fused_chunk_ = 64;    // signals per fused chunk
@@ -208,6 +226,9 @@ private:
     // tools/pdl_probe.py) -- the decode tail overlaps little
     bool pdl_enabled_ = false;
     int64_t pdl_count_ = 0;
+    // stream and outputs of the previous execute (PDL chaining guard)
+    cudaStream_t last_stream_ = nullptr;
+    const void* last_out_[3] = {nullptr, nullptr, nullptr};
     DeviceBuffer<double2> y_pdl_[2];
     DeviceBuffer<int64_t> sig_pdl_[2], sig_inv_pdl_[2];
     uint64_t* h_pdl_seeds_[2] = {nullptr, nullptr};  // pinned, read by sigma_kernel

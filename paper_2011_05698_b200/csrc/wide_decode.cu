@@ -1337,6 +1337,13 @@ void WideDecoder::run(double2* y, const int64_t* sigma, const int64_t* sigma_inv
     } else {
         const GraphKey key{y, sigma, sigma_inv, err};
         auto it = graphs_.find(key);
+        if (it == graphs_.end() && graphs_.size() >= 8) {
+            // bounded: callers that pass fresh buffers every call
+            // recapture instead of accumulating executable graphs
+            MSFFT_CUDA(cudaStreamSynchronize(st));
+            for (auto& kv : graphs_) cudaGraphExecDestroy(kv.second);
+            graphs_.clear();
+        }
         if (it == graphs_.end()) {
             cudaStream_t cap = nullptr;
             MSFFT_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));

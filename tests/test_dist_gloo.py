@@ -129,3 +129,42 @@ def test_index_range_partials_sum_to_full(world):
     assert res[0][1] == 0 and res[-1][2] == 1 << 14
     assert all(a[2] == b[1] for a, b in zip(res, res[1:]))
     assert max(r[3] for r in res) < 1e-13
+
+
+def _agree_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+    sys.path.insert(0, REPO)
+    from paper_2011_05698_b200 import dist as D
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    out = []
+    # round 1: nobody fails; round 2: rank 1 fails (e.g. a non-finite sample)
+    for fail_rank in (None, 1):
+        exc = ValueError("ComplexSignal: non-finite sample") if rank == fail_rank else None
+        try:
+            D._agree_or_raise(exc, torch.device("cpu"))
+            out.append("ok")
+        except Exception as e:  # noqa: BLE001
+            out.append(type(e).__name__ + ": " + str(e))
+    dist.barrier()  # nobody is left blocked in a collective
+    q.put((rank, out))
+    dist.destroy_process_group()
+
+
+def test_sharded_error_agreement():
+    """a rank that fails before the data all-reduce makes every
+    rank raise instead of leaving the others blocked."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_agree_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res[0][0] == res[1][0] == "ok"
+    assert res[1][1].startswith("ValueError: ComplexSignal: non-finite sample")
+    assert res[0][1].startswith("InvalidArgument: sharded_sfft4: another rank failed")

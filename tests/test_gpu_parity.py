@@ -423,3 +423,28 @@ def test_async_pdl_chain(oracle, monkeypatch):
     for i, o in zip(order, outs):
         got = [t.cpu().numpy() for t in o]
         assert all(np.array_equal(a, b) for a, b in zip(got, ref[i]))
+
+
+def test_async_pdl_shared_outputs(monkeypatch):
+    """consecutive asynchronous calls that share one output set
+    (different seeds) must not chain programmatically -- a late decode of
+    call i would overwrite call i+1's result.  The final outputs equal the
+    last call's synchronous result."""
+    import torch
+    monkeypatch.setenv("MSFFT_PDL", "1")
+    n, k, B = 1 << 18, 40, 320
+    rng = np.random.default_rng(6)
+    xs = (rng.standard_normal((B, n)) + 1j * rng.standard_normal((B, n))).astype(np.complex64)
+    xs[:, 3] += 50.0
+    plan = M.Plan(n, k, M.MultiscaleConfig(), 1e-6, "complex64")
+    xd = torch.as_tensor(xs).cuda()
+    o = (torch.empty((B, k), dtype=torch.int64, device="cuda"),
+         torch.empty((B, k), dtype=torch.complex128, device="cuda"),
+         torch.empty((B,), dtype=torch.int64, device="cuda"))
+    seeds = [np.arange(B, dtype=np.uint64) * np.uint64(31) + np.uint64(i) for i in range(6)]
+    for sd in seeds:
+        plan.execute(xd, sd, out=o, assume_valid=True, async_=True)
+    plan.sync()
+    got = [t.cpu().numpy() for t in o]
+    ref = plan.execute(xs, seeds[-1], assume_valid=True)[:3]
+    assert all(np.array_equal(a, b) for a, b in zip(got, ref))

@@ -97,3 +97,65 @@ def test_encode_values_rejects_bad_ranges():
     x[0, 5] = float("nan")
     with pytest.raises(M.InvalidArgument, match="ComplexSignal: non-finite sample"):
         plan.encode_values(x, [1], 0)
+
+
+def _tap_sharded(plan, xd, seeds, world):
+    """Tap-range sharding (x replicated): the parts' partial vectors summed in
+    rank order (what the all-reduce computes), then decoded."""
+    import torch
+    y = None
+    for r in range(world):
+        part = plan.encode_values_part(xd, seeds, r, world)
+        y = part if y is None else y + part
+    y_sum = y.clone()
+    f, c, cnt = plan.decode_values(y.contiguous(), seeds, folds=True)  # consumes y
+    torch.cuda.synchronize()
+    return f.cpu().numpy(), c.cpu().numpy(), cnt.cpu().numpy(), y_sum
+
+
+def test_tap_split_one_part_equals_execute(oracle, golden):
+    """encode_values_part(0, 1) + decode_values == execute, bitwise."""
+    import torch
+    for rec in _cases(golden)[:6]:
+        x = make_signal(oracle, rec)
+        plan = M.Plan(rec["n"], rec["k"], M.MultiscaleConfig(rec["l"], rec["q"]), rec["delta"],
+                      rec["dtype"])
+        seeds = np.array([rec["algo_seed"]], np.uint64)
+        f0, c0, n0, _ = plan.execute(x[None, :], seeds)
+        f1, c1, n1, _ = _tap_sharded(plan, torch.as_tensor(x[None, :]).cuda(), seeds, 1)
+        m = int(n0[0])
+        assert int(n1[0]) == m
+        assert np.array_equal(f1[0, :m], f0[0, :m]) and np.array_equal(c1[0, :m], c0[0, :m])
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_tap_sharded_matches_reference(oracle, golden, world):
+    import torch
+    for rec in _cases(golden):
+        x = make_signal(oracle, rec)
+        plan = M.Plan(rec["n"], rec["k"], M.MultiscaleConfig(rec["l"], rec["q"]), rec["delta"],
+                      rec["dtype"])
+        seeds = np.array([rec["algo_seed"]], np.uint64)
+        xd = torch.as_tensor(x[None, :]).cuda()
+        f, c, cnt, y = _tap_sharded(plan, xd, seeds, world)
+        y1 = plan.encode_values_part(xd, seeds, 0, 1)
+        # the partial sums add up to the single-part vector up to rounding
+        scale = float(torch.max(torch.abs(y1)).item())
+        assert float(torch.max(torch.abs(y - y1)).item()) <= 1e-13 * max(scale, 1e-300)
+        gf, gc, _ = golden_result(rec)
+        m = int(cnt[0])
+        assert_parity(gf, gc, f[0, :m], c[0, :m], rec["k"], rec["delta"], TOL[rec["dtype"]])
+
+
+def test_tap_sharded_large_golden(oracle, golden):
+    """The C5-law large-size goldens (b up to 8192, budget 2000) over 4 parts."""
+    import torch
+    for rec in golden("sfft4_big"):
+        x = make_signal(oracle, rec)
+        plan = M.Plan(rec["n"], rec["k"], M.MultiscaleConfig(rec["l"], rec["q"]), rec["delta"],
+                      rec["dtype"])
+        seeds = np.array([rec["algo_seed"]], np.uint64)
+        f, c, cnt, _ = _tap_sharded(plan, torch.as_tensor(x[None, :]).cuda(), seeds, 4)
+        gf, gc, _ = golden_result(rec)
+        m = int(cnt[0])
+        assert_parity(gf, gc, f[0, :m], c[0, :m], rec["k"], rec["delta"], TOL[rec["dtype"]])

@@ -70,13 +70,45 @@ if a.shards:
     ev[1].record()
     torch.cuda.synchronize()
     ms_ = int(ns[0])
+    index_decode_ms = ev[0].elapsed_time(ev[1])
     fs, cs = fs.cpu().numpy(), cs.cpu().numpy()
     same = bool(ms_ == m and np.array_equal(fs[0, :m], f1[0, :m]))
     rel = float(np.max(np.abs(cs[0, :m] - c1[0, :m]) / np.maximum(np.abs(c1[0, :m]), 1e-300))) \
         if same and m else None
+    # tap-range split (x replicated): each part walks 1/G of the taps
+    tenc_ms, yt = [], None
+    for r in range(a.shards):
+        plan.encode_values_part(x, seeds, r, a.shards, assume_valid=True)  # warm
+        ev[0].record()
+        part = plan.encode_values_part(x, seeds, r, a.shards, assume_valid=True)
+        ev[1].record()
+        torch.cuda.synchronize()
+        tenc_ms.append(ev[0].elapsed_time(ev[1]))
+        yt = part if yt is None else yt + part
+    ev[0].record()
+    ft, ct, nt = plan.decode_values(yt, seeds, folds=True)
+    ev[1].record()
+    torch.cuda.synchronize()
+    dec_folds_ms = ev[0].elapsed_time(ev[1])
+    mt = int(nt[0].item())
+    ft, ct = ft.cpu().numpy(), ct.cpu().numpy()
+    same_t = bool(mt == m and np.array_equal(ft[0, :mt], f1[0, :m]))
+    rel_t = float(np.max(np.abs(ct[0, :mt] - c1[0, :m]) / np.maximum(np.abs(c1[0, :m]), 1e-300))) \
+        if same_t and m else None
+    one = []
+    for _ in range(3):
+        ev[0].record()
+        plan.encode_values_part(x, seeds, 0, 1, assume_valid=True)
+        ev[1].record()
+        torch.cuda.synchronize()
+        one.append(ev[0].elapsed_time(ev[1]))
     shard = {"shards": a.shards, "encode_ms_per_rank": enc_ms,
+             "tap_split": {"encode_ms_per_rank": tenc_ms, "encode_ms_one_part": min(one),
+                           "bucket_ffts_plus_decode_ms": dec_folds_ms,
+                           "same_support_as_single_gpu": same_t,
+                           "max_rel_diff_vs_single_gpu": rel_t},
              "bucket_values_mb": y.numel() * 16 / 1e6,
-             "decode_ms": ev[0].elapsed_time(ev[1]), "same_support_as_single_gpu": same,
+             "decode_ms": index_decode_ms, "same_support_as_single_gpu": same,
              "max_rel_diff_vs_single_gpu": rel}
 pos, coef = truth[0]
 hit = len(set(f1[0, :m].tolist()) & set(pos.tolist()))
