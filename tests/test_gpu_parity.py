@@ -448,3 +448,64 @@ def test_async_pdl_shared_outputs(monkeypatch):
     got = [t.cpu().numpy() for t in o]
     ref = plan.execute(xs, seeds[-1], assume_valid=True)[:3]
     assert all(np.array_equal(a, b) for a, b in zip(got, ref))
+
+
+@pytest.mark.slow
+def test_c3_more_seeds(oracle, golden):
+    """C3 on two more seeds (302, 303), complex128 and complex64."""
+    for rec in golden("sfft4_c3_more"):
+        x = make_signal(oracle, rec)
+        r = M.sfft4(x, rec["k"], M.MultiscaleConfig(), rec["algo_seed"], rec["delta"])
+        f, c, stats = golden_result(rec)
+        assert_parity(f, c, r.spectrum.positions, r.spectrum.coeffs, rec["k"], rec["delta"],
+                      TOL[rec["dtype"]])
+        assert r.stats.samples_used == stats["samples_used"]
+        assert r.stats.samples_round_sum == stats["samples_round_sum"]
+        assert r.stats.stage_counts == stats["stage_counts"]
+
+
+@pytest.mark.slow
+def test_c5_full_size_golden(oracle, golden):
+    """C5 at full size (BASELINE.json configs[4]: N=2^27, K=10^4, c128,
+    log-uniform |c| in [0.1, 10], 20 dB) against the reference's own sfft4
+    run on the same bytes (tests/golden/make_golden.py c5, ~1-2 h of CPU):
+    the 12 windows bit-exact (w and sha256 of the taps, window.cpp:105-177),
+    identical support, coefficients within 1e-9 (with the 10*K*delta floor),
+    identical stats -- through the fused one-shot path and through the
+    tap-range sharded split (8 parts summed, then decoded)."""
+    import hashlib
+    import torch
+    rec = golden("sfft4_c5")
+    for wrec in rec["windows"]:
+        w, taps = M.window(wrec["n"], wrec["b"], wrec["delta"])
+        assert w == wrec["w"], wrec["b"]
+        assert hashlib.sha256(taps.astype("<f8").tobytes()).hexdigest() == wrec["taps_sha256"]
+    x = make_signal(oracle, rec)
+    f, c, stats = golden_result(rec)
+    k, delta = rec["k"], rec["delta"]
+    plan = M.Plan(rec["n"], k, M.MultiscaleConfig(rec["l"], rec["q"]), delta, "complex128")
+    xd = torch.as_tensor(x).cuda().reshape(1, -1)
+    del x
+    seeds = np.array([rec["algo_seed"]], np.uint64)
+    out = (torch.empty((1, k), dtype=torch.int64, device="cuda"),
+           torch.empty((1, k), dtype=torch.complex128, device="cuda"),
+           torch.empty((1,), dtype=torch.int64, device="cuda"))
+    plan.execute(xd, seeds, out=out)
+    m = int(out[2].item())
+    err = assert_parity(f, c, out[0][0, :m].cpu().numpy(), out[1][0, :m].cpu().numpy(), k, delta,
+                        1e-9)
+    st = plan.stats()
+    assert st.samples_round_sum == stats["samples_round_sum"]
+    assert st.b_first == stats["b_first"] and st.iterations == stats["iterations"]
+    assert st.stage_counts == stats["stage_counts"]
+    r1 = M.sfft4(xd[0], k, M.MultiscaleConfig(rec["l"], rec["q"]), rec["algo_seed"], delta)
+    assert r1.stats.samples_used == stats["samples_used"]
+    # tap-range sharded over 8 parts (what 8 ranks + one all-reduce compute)
+    y = None
+    for p in range(8):
+        part = plan.encode_values_part(xd, seeds, p, 8)
+        y = part if y is None else y + part
+    fs, cs, ns = plan.decode_values(y, seeds, folds=True)
+    ms = int(ns[0].item())
+    err8 = assert_parity(f, c, fs[0, :ms].cpu().numpy(), cs[0, :ms].cpu().numpy(), k, delta, 1e-9)
+    print(f"C5 parity: {m} entries, max rel err {err:.3g} (one GPU), {err8:.3g} (8 parts)")
