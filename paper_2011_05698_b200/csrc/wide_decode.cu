@@ -934,32 +934,38 @@ __global__ void k6b_count(const int64_t* __restrict__ cand_f, int64_t budget, in
 
 __global__ void k6b_scatter(const int64_t* __restrict__ cand_f, int64_t budget, int shift,
                             const int32_t* __restrict__ start, int32_t* __restrict__ cursor,
-                            int32_t* __restrict__ tmp) {
+                            int32_t* __restrict__ tmp, int64_t* __restrict__ tmpf) {
     pdl_entry();
     GRID_LOOP(r, budget) {
         const int64_t f = cand_f[r];
         if (f < 0) continue;
         const int64_t bk = f >> shift;
-        tmp[start[bk] + atomicAdd(&cursor[bk], 1)] = static_cast<int32_t>(r);
+        const int32_t q = start[bk] + atomicAdd(&cursor[bk], 1);
+        tmp[q] = static_cast<int32_t>(r);
+        tmpf[q] = f;  // the key beside the rank: k6b_sort streams (f, rank) pairs
     }
 }
 
-__global__ void k6b_sort(const int64_t* __restrict__ cand_f, int64_t budget, int shift,
-                         const int32_t* __restrict__ start, const int32_t* __restrict__ cnt,
-                         const int32_t* __restrict__ tmp, int32_t* __restrict__ byf) {
+__global__ void k6b_sort(int shift, const int32_t* __restrict__ start,
+                         const int32_t* __restrict__ cnt, const int32_t* __restrict__ tmp,
+                         const int64_t* __restrict__ tmpf, int32_t* __restrict__ byf) {
     pdl_entry();
     // one thread per accepted entry (start[kF6B] of them), ranked within its
-    // bucket: a dense cluster of f costs O(len) per entry, not O(len^2)
-    // in one thread
+    // bucket by streaming the bucket's (f, rank) pairs: entries are laid out
+    // bucket by bucket, so the lanes of a warp mostly scan the same bucket and
+    // each pair is one broadcast load -- a spectrum clustered into one bucket
+    // costs O(len) coalesced steps per warp, not O(len) dependent
+    // random loads per thread
     GRID_LOOP(p, static_cast<int64_t>(start[kF6B])) {
         const int32_t ri = tmp[p];
-        const int64_t fi = cand_f[ri];
+        const int64_t fi = tmpf[p];
         const int64_t bk = fi >> shift;
         const int32_t s0 = start[bk], len = cnt[bk];
         int32_t rank = 0;
+#pragma unroll 4
         for (int32_t j = 0; j < len; ++j) {
+            const int64_t fj = tmpf[s0 + j];
             const int32_t rj = tmp[s0 + j];
-            const int64_t fj = cand_f[rj];
             rank += fj < fi || (fj == fi && rj < ri);
         }
         byf[s0 + rank] = ri;
@@ -1441,10 +1447,11 @@ void WideDecoder::enqueue(double2* y, const int64_t* sigma, const int64_t* sigma
                            cand_f_.get(), budget, shift, f6cnt_.get(), f6cur_.get(), naccepted);
                 launch_pdl(pdl_, scan_kernel, 1, kScanT, 0, st, f6cnt_.get(), int64_t{kF6B}, nullptr,
                            f6start_.get(), f6start_.get() + kF6B);
+                // newf_ is free until k6_newf: it holds the keys of the bucket sort
                 launch_pdl(pdl_, k6b_scatter, grid_of(budget), kT, 0, st, cand_f_.get(), budget, shift,
-                           f6start_.get(), f6cur_.get(), pos_.get());
-                launch_pdl(pdl_, k6b_sort, grid_of(budget), kT, 0, st, cand_f_.get(), budget, shift,
-                           f6start_.get(), f6cnt_.get(), pos_.get(), byf_.get());
+                           f6start_.get(), f6cur_.get(), pos_.get(), newf_.get());
+                launch_pdl(pdl_, k6b_sort, grid_of(budget), kT, 0, st, shift, f6start_.get(),
+                           f6cnt_.get(), pos_.get(), newf_.get(), byf_.get());
             } else {
                 const unsigned tiles = static_cast<unsigned>((budget + kT - 1) / kT);
                 const unsigned split = std::max(1u, std::min(64u, 1184u / tiles));

@@ -509,3 +509,27 @@ def test_c5_full_size_golden(oracle, golden):
     ms = int(ns[0].item())
     err8 = assert_parity(f, c, fs[0, :ms].cpu().numpy(), cs[0, :ms].cpu().numpy(), k, delta, 1e-9)
     print(f"C5 parity: {m} entries, max rel err {err:.3g} (one GPU), {err8:.3g} (8 parts)")
+
+
+def test_wide_decode_clustered_spectrum(monkeypatch):
+    """a support packed into a narrow band puts every accepted
+    candidate of an iteration into one or a few buckets of the K6 (f, rank)
+    bucket sort (budgets >= 2048); the wide decode must still equal the
+    one-CTA decode bit for bit (and finish in normal time)."""
+    n, k = 1 << 21, 3000
+    rng = np.random.default_rng(11)
+    f0 = 123457
+    pos = np.sort(f0 + rng.choice(4096, k, replace=False)).astype(np.int64)
+    spec = np.zeros(n, np.complex128)
+    spec[pos] = 10.0 ** rng.uniform(-1, 1, k) * np.exp(2j * np.pi * rng.random(k))
+    x = np.fft.ifft(spec) * n
+    noise = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    x = x + np.sqrt(np.sum(np.abs(x) ** 2) * 1e-2 / np.sum(np.abs(noise) ** 2)) * noise
+    res = []
+    for wide in ("8", "0"):
+        monkeypatch.setenv("MSFFT_WIDE_MAX_BATCH", wide)
+        plan = M.Plan(n, k, M.MultiscaleConfig(), 1e-6, "complex128")
+        res.append(plan.execute(x[None, :], [77]))
+    (f1, c1, n1, _), (f0_, c0, n0, _) = res
+    assert int(n1[0]) == int(n0[0]) > 0
+    assert np.array_equal(f1, f0_) and np.array_equal(c1, c0)
