@@ -53,10 +53,13 @@ def to_float(v):
         return None
 
 
-def summarize(rep):
+def summarize(rep, kernel=None):
+    import re
     header, units, data = raw_rows(rep)
-    row = data[0]
     col = {h: i for i, h in enumerate(header)}
+    row = data[0]
+    if kernel:
+        row = next(r for r in data if re.search(kernel, r[col["Kernel Name"]]))
     s = {"kernel": row[col["Kernel Name"]] if "Kernel Name" in col else None}
     for metric, name in KEYS.items():
         if metric in col:
@@ -88,8 +91,9 @@ if __name__ == "__main__":
     ap.add_argument("--traffic")
     ap.add_argument("--batch", type=int)
     ap.add_argument("--n", type=int)
+    ap.add_argument("--kernel", help="regex: summarise the first launch whose name matches")
     a = ap.parse_args()
-    s = summarize(a.report)
+    s = summarize(a.report, a.kernel)
     if a.workload:
         s["workload"] = a.workload
     # the native sources the capture ran on (run this on the same tree)

@@ -28,6 +28,9 @@ out = (torch.empty((1, k), dtype=torch.int64, device=dev),
        torch.empty((1, k), dtype=torch.complex128, device=dev),
        torch.empty((1,), dtype=torch.int64, device=dev))
 plan.execute(xd, seeds, out=out)
+if os.environ.get("MSFFT_PROFILE_AFTER_PLAN"):
+    torch.cuda.synchronize()
+    torch.cuda.profiler.start()  # ncu --profile-from-start off: skip window design
 for r in range(a.reps):
     _, _, _, ms = plan.execute(xd, seeds, out=out, assume_valid=True, stage_times=True, serial=True)
     print(f"rep {r}: {ms:.3f} ms  stages {plan.stage_times()}", flush=True)

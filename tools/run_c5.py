@@ -40,6 +40,9 @@ out = (torch.empty((1, k), dtype=torch.int64, device=dev),
        torch.empty((1,), dtype=torch.int64, device=dev))
 sh = torch.cuda.current_stream().cuda_stream
 plan.execute(x, seeds, out=out, stream=sh)  # validating call
+if os.environ.get("MSFFT_PROFILE_AFTER_PLAN"):
+    torch.cuda.synchronize()
+    torch.cuda.profiler.start()  # ncu --profile-from-start off: skip window design
 times, stages = [], []
 for _ in range(a.reps):
     _, _, _, ms = plan.execute(x, seeds, out=out, assume_valid=True, stream=sh, stage_times=True)
