@@ -42,30 +42,41 @@ def gpu_time(x_host, k, l, q, seed, delta, dtype, reps=7):
            torch.empty((1, k), dtype=torch.complex128, device=dev),
            torch.empty((1,), dtype=torch.int64, device=dev))
     plan.execute(xd, seeds, out=out)  # validating call + warm-up
-    ms = []
+    ms, msv = [], []
     for _ in range(reps):
         _, _, _, t = plan.execute(xd, seeds, out=out, assume_valid=True)
         ms.append(t)
+        _, _, _, t = plan.execute(xd, seeds, out=out)  # validates every sample, as sfft4.cpp:133
+        msv.append(t)
     plan.execute(xd, seeds, out=out, assume_valid=True, stage_times=True, serial=True)
     stages = plan.stage_times()
     f, c, cnt = out[0].cpu().numpy(), out[1].cpu().numpy(), int(out[2].cpu().numpy()[0])
-    return statistics.median(ms), stages, f[0, :cnt], c[0, :cnt]
+    return statistics.median(ms), statistics.median(msv), stages, f[0, :cnt], c[0, :cnt]
 
 
 NO_REF = "--no-ref" in sys.argv
 
 
-def cell(name, x, k, l, q, seed, delta, dtype, ref=True):
+def cell(name, x, k, l, q, seed, delta, dtype, ref=True, golden=None):
     ref = ref and not NO_REF
     row = {"config": name, "n": int(x.shape[-1]), "k": k, "l": l, "q": q, "dtype": dtype}
     try:
-        g_ms, stages, f, c = gpu_time(x, k, l, q, seed, delta, dtype)
+        g_ms, g_ms_val, stages, f, c = gpu_time(x, k, l, q, seed, delta, dtype)
     except Exception as e:  # noqa: BLE001  (invalid (l, q) cells raise like the reference)
         row["gpu_error"] = str(e)
         g_ms = None
     if g_ms is not None:
-        row.update(gpu_ms=g_ms, gpu_stage_ms={"encode": stages[0], "bucket_fft": stages[1],
-                                              "decode": stages[2]})
+        row.update(gpu_ms=g_ms, gpu_ms_validating=g_ms_val,
+                   gpu_stage_ms={"encode": stages[0], "bucket_fft": stages[1],
+                                 "decode": stages[2]})
+    if golden is not None and g_ms is not None:
+        # the reference's result on the same bytes from a committed fixture
+        from helpers import golden_result
+        gf, gc, _ = golden_result(golden)
+        same, err, _ = parity(gf, gc, f, c, k, delta, TOL[dtype])
+        row.update(ref_ms=golden["ref_runtime_ms"], ref_source="tests/golden/sfft4_c5.json",
+                   speedup=golden["ref_runtime_ms"] / g_ms, support_identical=bool(same),
+                   max_rel_err=err)
     if ref:
         try:
             prewarm_windows(R, int(x.shape[-1]), k, delta)  # untimed, as sfft4.cpp:146-154
@@ -107,13 +118,21 @@ def main(names):
         rows.append(cell("C4 (one signal)", x, 64, 16, 1.0, splitmix64(101 ^ 0x53), 1e-6,
                          "complex64"))
     if "C5" in names:
-        s = signal_seed(0xC5C50000, 0)
-        xb, _ = make_batch(1 << 27, 10000, [s], 20.0, dev, "complex128",
-                           magnitude="loguniform_0.1_10", chunk=1)
-        x = xb[0].cpu().numpy()
-        del xb
-        torch.cuda.empty_cache()
-        rows.append(cell("C5", x, 10000, 16, 1.0, algo_seed(s), 1e-6, "complex128", ref=False))
+        gpath = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                             "tests", "golden", "sfft4_c5.json")
+        if os.path.exists(gpath):  # the reference ran on these bytes (make_golden.py c5)
+            rec = json.load(open(gpath))
+            x = make_signal(R, rec)
+            rows.append(cell("C5", x, rec["k"], rec["l"], rec["q"], rec["algo_seed"],
+                             rec["delta"], "complex128", ref=False, golden=rec))
+        else:
+            s = signal_seed(0xC5C50000, 0)
+            xb, _ = make_batch(1 << 27, 10000, [s], 20.0, dev, "complex128",
+                               magnitude="loguniform_0.1_10", chunk=1)
+            x = xb[0].cpu().numpy()
+            del xb
+            torch.cuda.empty_cache()
+            rows.append(cell("C5", x, 10000, 16, 1.0, algo_seed(s), 1e-6, "complex128", ref=False))
     print("SUMMARY " + json.dumps(rows))
 
 
