@@ -123,16 +123,16 @@ int msfft_sfft4(const void* x, int64_t n, int32_t dtype, int32_t x_location, int
         if (n < 4 || !is_pow2_u(static_cast<uint64_t>(n)))
             throw std::invalid_argument("ComplexSignal: n must be a power of two >= 4");
         const bool on_dev = x_location == MSFFT_DEVICE;
-        std::shared_ptr<Plan> plan;
+        PlanLease lease;
         try {
-            plan = cached_plan(n, k, l, q, delta, c128, current_or(-1));
+            lease = lease_plan(n, k, l, q, delta, c128, current_or(-1));
         } catch (const std::invalid_argument&) {
             // sfft4 validates x before its other arguments (sfft4.cpp:133-135)
             if (has_non_finite(x, n, c128, on_dev))
                 throw std::invalid_argument("ComplexSignal: non-finite sample");
             throw;
         }
-        std::lock_guard<std::mutex> lock(plan->mutex());
+        Plan* plan = lease.plan.get();
         std::vector<int64_t> f(static_cast<size_t>(k));
         std::vector<double> c(static_cast<size_t>(2 * k));
         int64_t count = 0;
@@ -516,8 +516,8 @@ int msfft_trace(const void* x, int64_t n, int32_t dtype, int64_t k, int64_t l, d
     return guarded(err, errlen, [&] {
         require_device();
         const bool c128 = dtype == MSFFT_C128;
-        auto plan = cached_plan(n, k, l, q, delta, c128, current_or(-1));
-        std::lock_guard<std::mutex> lock(plan->mutex());
+        PlanLease lease = lease_plan(n, k, l, q, delta, c128, current_or(-1));
+        Plan* plan = lease.plan.get();
         std::vector<int64_t> f(static_cast<size_t>(k));
         std::vector<double> c(static_cast<size_t>(2 * k));
         int64_t count = 0;

@@ -1091,18 +1091,33 @@ void Plan::decode_values(int64_t batch, double2* d_y, const uint64_t* seeds, int
     check_flags(st);
 }
 
-std::shared_ptr<Plan> cached_plan(int64_t n, int64_t k, int64_t l, double q, double delta,
-                                  bool c128, int device) {
+PlanLease lease_plan(int64_t n, int64_t k, int64_t l, double q, double delta, bool c128,
+                     int device) {
     using Key = std::tuple<int, int64_t, int64_t, int64_t, double, double, bool>;
     static std::mutex mu;
-    static std::map<Key, std::shared_ptr<Plan>> cache;
+    static std::map<Key, std::vector<std::shared_ptr<Plan>>> cache;
     const Key key{device, n, k, l, q, delta, c128};
-    std::lock_guard<std::mutex> lock(mu);
-    auto it = cache.find(key);
-    if (it != cache.end()) return it->second;
-    auto p = std::make_shared<Plan>(n, k, l, q, delta, c128, device);
-    cache.emplace(key, p);
-    return p;
+    std::vector<std::shared_ptr<Plan>> have;
+    {
+        std::lock_guard<std::mutex> g(mu);
+        have = cache[key];
+    }
+    // an idle plan of this geometry, if any
+    for (auto& p : have) {
+        std::unique_lock<std::mutex> lk(p->mutex(), std::try_to_lock);
+        if (lk.owns_lock()) return PlanLease{p, std::move(lk)};
+    }
+    if (have.size() < static_cast<size_t>(kPlansPerKey)) {
+        // construct outside the cache lock: window design can take seconds and
+        // must not block other geometries (as get_flat_window, window.cpp:179-193)
+        auto p = std::make_shared<Plan>(n, k, l, q, delta, c128, device);
+        std::unique_lock<std::mutex> lk(p->mutex());
+        std::lock_guard<std::mutex> g(mu);
+        cache[key].push_back(p);
+        return PlanLease{p, std::move(lk)};
+    }
+    std::unique_lock<std::mutex> lk(have.front()->mutex());  // all busy: wait for one
+    return PlanLease{have.front(), std::move(lk)};
 }
 
 }  // namespace msfft_b200

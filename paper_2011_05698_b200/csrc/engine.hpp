@@ -238,9 +238,17 @@ private:
 };
 
 // Process-wide plan cache for the one-shot API (keyed by device and all
-// plan parameters).
-std::shared_ptr<Plan> cached_plan(int64_t n, int64_t k, int64_t l, double q, double delta,
-                                  bool c128, int device);
+// plan parameters), with up to kPlansPerKey plans per key so concurrent
+// same-geometry calls (the reference's run_sweep threads, bench.cpp:242-280)
+// run side by side instead of queueing on one plan.  The lease holds the
+// plan's mutex; plans are built outside the cache lock.
+constexpr int kPlansPerKey = 4;
+struct PlanLease {
+    std::shared_ptr<Plan> plan;
+    std::unique_lock<std::mutex> lock;
+};
+PlanLease lease_plan(int64_t n, int64_t k, int64_t l, double q, double delta, bool c128,
+                     int device);
 
 // ComplexSignal::validate's finiteness scan on the device: `batch` rows of
 // `span` samples, `x_stride` samples apart; sets *bad to 1 if any is

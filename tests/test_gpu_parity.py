@@ -533,3 +533,21 @@ def test_wide_decode_clustered_spectrum(monkeypatch):
     (f1, c1, n1, _), (f0_, c0, n0, _) = res
     assert int(n1[0]) == int(n0[0]) > 0
     assert np.array_equal(f1, f0_) and np.array_equal(c1, c0)
+
+
+def test_concurrent_one_shot_calls(oracle):
+    """The reference's run_sweep calls sfft4 from several threads at once
+    (bench.cpp:242-280).  Same-geometry one-shot calls from 4 threads lease
+    separate plans (up to 4 per geometry) and return exactly the sequential
+    results."""
+    import concurrent.futures as cf
+    n, k = 1 << 16, 50
+    xs = [oracle.generate_test_signal(n, k, M.splitmix64(s ^ 0x51))[0] for s in range(8)]
+    seeds = [M.splitmix64(s ^ 0x53) for s in range(8)]
+    seq = [M.sfft4(x, k, M.MultiscaleConfig(), sd, 1e-8) for x, sd in zip(xs, seeds)]
+    with cf.ThreadPoolExecutor(4) as ex:
+        par = list(ex.map(lambda a: M.sfft4(a[0], k, M.MultiscaleConfig(), a[1], 1e-8),
+                          zip(xs, seeds)))
+    for a, b in zip(seq, par):
+        assert np.array_equal(a.spectrum.positions, b.spectrum.positions)
+        assert np.array_equal(a.spectrum.coeffs, b.spectrum.coeffs)
