@@ -3,8 +3,11 @@
 
 #include <cuda_runtime.h>
 
+#include <map>
+#include <mutex>
 #include <stdexcept>
 #include <string>
+#include <utility>
 
 namespace msfft_b200 {
 
@@ -21,6 +24,44 @@ inline void cuda_check(cudaError_t e, const char* what) {
 
 #define MSFFT_CUDA(call) ::msfft_b200::cuda_check((call), #call)
 #define MSFFT_LAUNCH_CHECK(name) ::msfft_b200::cuda_check(cudaGetLastError(), name)
+
+// cudaFuncSetAttribute(fn, MaxDynamicSharedMemorySize, bytes) on the current
+// device, issued only when the kernel's limit must grow: the driver call
+// costs microseconds, which small launches would pay on every call.
+inline void smem_attr(const void* fn, size_t bytes) {
+    static std::mutex mu;
+    static std::map<std::pair<int, const void*>, size_t> set;
+    int dev = 0;
+    cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+    std::lock_guard<std::mutex> lock(mu);
+    size_t& cur = set[{dev, fn}];
+    if (bytes > cur) {
+        cuda_check(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(bytes)),
+                   "cudaFuncSetAttribute");
+        cur = bytes;
+    }
+}
+template <class F>
+inline void smem_attr(F* fn, size_t bytes) {
+    smem_attr(reinterpret_cast<const void*>(fn), bytes);
+}
+
+// SM count of the current device (cached per device).
+inline int sm_count() {
+    static std::mutex mu;
+    static std::map<int, int> cache;
+    int dev = 0;
+    cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find(dev);
+    if (it != cache.end()) return it->second;
+    int sms = 0;
+    cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev),
+               "cudaDeviceGetAttribute");
+    cache[dev] = sms;
+    return sms;
+}
 
 // RAII device buffer.
 template <class T>

@@ -24,6 +24,10 @@
 #include "encode.hpp"
 #include "plan_dev.cuh"
 
+#ifndef DEC_TL_MARK
+#define DEC_TL_MARK(m) do { } while (0)
+#endif
+
 namespace msfft_b200 {
 namespace {
 
@@ -179,6 +183,9 @@ __device__ __forceinline__ void decode_signal(const DevPlan& plan, const DecLayo
                 __threadfence();
             }
             gsync();
+#ifdef MSFFT_TIMELINE
+            DEC_TL_MARK(m);
+#endif
         }
         const DevIter& it = plan.it[m];
         const int64_t b = it.b, L = it.l_width;

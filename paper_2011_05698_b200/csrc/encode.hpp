@@ -14,7 +14,13 @@ namespace msfft_b200 {
 // K1+K2 (encode.cu).  smem_bytes >= max(staged taps, 256*kEncRounds*16).
 void launch_encode(const DevPlan& plan, const EncTask* d_tasks, int64_t ntasks, const void* x,
                    bool x_c128, int64_t x_stride, int64_t batch, const int64_t* d_sigma,
-                   double2* d_y, size_t smem_bytes, cudaStream_t stream);
+                   double2* d_y, size_t smem_bytes, cudaStream_t stream,
+                   int32_t* d_done = nullptr);
+// d_done (optional, gated launches): each task adds 1 to d_done[task.m] once
+// its buckets are written, or to d_done[2 iters + 1 + task.m] once its folds
+// are (b > 256: the gated bucket FFT consumes them).  Layout of the gate
+// words: [need iters][done iters][exit 1][fold need iters][fold done iters],
+// d_done pointing at "done".
 
 // Per-signal decode scratch, carved from shared memory when it fits,
 // otherwise from a global workspace of `stride_bytes` per signal.
@@ -49,6 +55,17 @@ void launch_decode(const DevPlan& plan, const DecLayout& lay, double2* d_y,
                    int64_t* d_out_count, int32_t* d_err, cudaStream_t stream,
                    int64_t* tr_bucket = nullptr, int64_t* tr_f = nullptr,
                    double2* tr_v = nullptr);
+
+// The decode as a programmatic dependent launch behind an encode launched
+// with d_done: it starts while the encode runs and waits, per iteration m,
+// until d_done[m] reaches d_need[m] (that iteration's encode tasks).
+// d_done: the gate words above (zero between calls); the last decode CTA
+// out waits for every producer and resets them.
+void launch_decode_gated(const DevPlan& plan, const DecLayout& lay, double2* d_y,
+                         const int64_t* d_sigma, const int64_t* d_sigma_inv, int64_t batch,
+                         unsigned char* d_work, int64_t* d_out_f, double2* d_out_c,
+                         int64_t* d_out_count, int32_t* d_err, const int32_t* d_need,
+                         int32_t* d_done, cudaStream_t stream);
 
 // Error flags raised by the decode (mirrors exceptions that escape sfft4).
 enum : int32_t { kDecErrNone = 0, kDecErrPhaseZero = 1, kDecErrRounds = 2 };

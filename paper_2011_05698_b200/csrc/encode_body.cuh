@@ -29,6 +29,13 @@
 #include "common.cuh"
 #include "plan_dev.cuh"
 
+#ifndef ENC_TL_MARK
+#define ENC_TL_MARK(i) do { } while (0)
+#endif
+#ifndef ENC_TL_BATCH
+#define ENC_TL_BATCH() do { } while (0)
+#endif
+
 namespace msfft_b200 {
 namespace {
 
@@ -56,10 +63,18 @@ enum LoadMode { kLoadFull = 0, kLoadShard = 1, kLoadCompact = 2 };
 // Walks the task's merged t' segments for residue class c (t' = c mod b) in
 // increasing t' and adds g[h + t' + tau_r] * x into acc[r] for every round r
 // whose tap interval covers t'.
-template <class T, int kMode>
+// kSmemTaps: `taps` points into shared memory (the staged window), so the
+// per-(sample, round) tap reads are LDS; otherwise read-only global loads.
+// Per batch of U samples the rounds go outermost (nr is uniform, one branch
+// per round) and each round's U tap reads are issued together from clamped,
+// always-valid indices; only the adds are predicated on the tap interval.
+// acc[r] still receives its terms in increasing t' (u ascending within a
+// batch, batches ascending), the reference's order.
+template <class T, int kMode, bool kSmemTaps>
 __device__ __forceinline__ void gather_accumulate(const DevPlan& plan, const EncTask& task,
                                                   const T* __restrict__ xs, uint32_t sg,
-                                                  const double* taps, int64_t h, uint32_t wu,
+                                                  const double* __restrict__ taps, int64_t h,
+                                                  uint32_t wu,
                                                   const int64_t* taus, int nr, int64_t b, int c,
                                                   double2 (&acc)[kEncRounds]) {
     const uint32_t mask = static_cast<uint32_t>(plan.n - 1);
@@ -77,10 +92,13 @@ __device__ __forceinline__ void gather_accumulate(const DevPlan& plan, const Enc
         constexpr int U = 8;
         const int64_t stride = b;
         for (; t <= B; t += U * stride) {
+            ENC_TL_BATCH();
             T v[U];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const int64_t tt = t + u * stride;
+                v[u].x = 0;
+                v[u].y = 0;
                 if (tt <= B) {
                     if (kMode == kLoadCompact) {
                         MSFFT_DCHECK(task.seg_cpos[sgi] + (tt - A) >= 0 &&
@@ -98,23 +116,31 @@ __device__ __forceinline__ void gather_accumulate(const DevPlan& plan, const Enc
                     }
                 }
             }
+            double xr[U], xi[U];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-                const int64_t tt = t + u * stride;
-                if (tt <= B) {
-                    const double xr = static_cast<double>(v[u].x);
-                    const double xi = static_cast<double>(v[u].y);
+                xr[u] = static_cast<double>(v[u].x);
+                xi[u] = static_cast<double>(v[u].y);
+            }
 #pragma unroll
-                    for (int r = 0; r < kEncRounds; ++r) {
-                        if (r < nr) {
-                            const uint32_t idx = static_cast<uint32_t>(tt) + th[r];
-                            if (idx < wu) {
-                                const double g = taps[idx];
-                                acc[r].x += g * xr;
-                                acc[r].y += g * xi;
-                            }
-                        }
+            for (int r = 0; r < kEncRounds; ++r) {
+                if (r < nr) {
+                    double g[U];
+                    bool in[U];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const int64_t tt = t + u * stride;
+                        const uint32_t idx = static_cast<uint32_t>(tt) + th[r];
+                        in[u] = tt <= B && idx < wu;
+                        const uint32_t ci = in[u] ? idx : 0u;
+                        g[u] = kSmemTaps ? taps[ci] : __ldg(taps + ci);
                     }
+#pragma unroll
+                    for (int u = 0; u < U; ++u)
+                        if (in[u]) {
+                            acc[r].x += g[u] * xr[u];
+                            acc[r].y += g[u] * xi[u];
+                        }
                 }
             }
         }
@@ -141,7 +167,6 @@ __device__ __forceinline__ void encode_task(const DevPlan& plan, const EncTask& 
     const int64_t* taus = plan.taus + it.tau_off + task.r0;
 
     // ---- stage the window taps: one TMA bulk copy, completion on an mbarrier
-    const double* taps = it.taps;
     if (it.taps_in_smem) {
         const uint32_t bytes = static_cast<uint32_t>((it.w + 1) * sizeof(double));
         if (tid == 0) {
@@ -167,8 +192,8 @@ __device__ __forceinline__ void encode_task(const DevPlan& plan, const EncTask& 
             " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)), "r"(phase)
             : "memory");
         phase ^= 1u;
-        taps = reinterpret_cast<const double*>(smem_raw);
     }
+    ENC_TL_MARK(3);
 
     // ---- thread -> (signal, residue class)
     int sl, c;
@@ -189,15 +214,27 @@ __device__ __forceinline__ void encode_task(const DevPlan& plan, const EncTask& 
     if (active) {
         const uint32_t sg = static_cast<uint32_t>(sigma[s * plan.iters + task.m]);
         const T* xs = x + s * x_stride;
-        // the load mode is uniform per launch: branch once, not per sample
-        if (plan.x_compact)
-            gather_accumulate<T, kLoadCompact>(plan, task, xs, sg, taps, h, wu, taus, nr, b, c, acc);
-        else if (plan.x_lo == 0 && plan.x_hi == plan.n)
-            gather_accumulate<T, kLoadFull>(plan, task, xs, sg, taps, h, wu, taus, nr, b, c, acc);
-        else
-            gather_accumulate<T, kLoadShard>(plan, task, xs, sg, taps, h, wu, taus, nr, b, c, acc);
+        // the load mode and the tap source are uniform per task: branch once,
+        // not per sample
+        const double* st = reinterpret_cast<const double*>(smem_raw);
+        if (it.taps_in_smem) {
+            if (plan.x_compact)
+                gather_accumulate<T, kLoadCompact, true>(plan, task, xs, sg, st, h, wu, taus, nr, b, c, acc);
+            else if (plan.x_lo == 0 && plan.x_hi == plan.n)
+                gather_accumulate<T, kLoadFull, true>(plan, task, xs, sg, st, h, wu, taus, nr, b, c, acc);
+            else
+                gather_accumulate<T, kLoadShard, true>(plan, task, xs, sg, st, h, wu, taus, nr, b, c, acc);
+        } else {
+            if (plan.x_compact)
+                gather_accumulate<T, kLoadCompact, false>(plan, task, xs, sg, it.taps, h, wu, taus, nr, b, c, acc);
+            else if (plan.x_lo == 0 && plan.x_hi == plan.n)
+                gather_accumulate<T, kLoadFull, false>(plan, task, xs, sg, it.taps, h, wu, taus, nr, b, c, acc);
+            else
+                gather_accumulate<T, kLoadShard, false>(plan, task, xs, sg, it.taps, h, wu, taus, nr, b, c, acc);
+        }
     }
 
+    ENC_TL_MARK(4);
     const double inv_n = plan.inv_n;
     const int64_t vps = plan.values_per_signal;
     if (!task.fused) {

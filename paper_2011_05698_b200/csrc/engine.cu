@@ -157,12 +157,7 @@ void launch_validate(const void* d_x, bool c128, int64_t span, int64_t x_stride,
                      int32_t* bad, cudaStream_t st) {
     if (span <= 0 || batch <= 0) return;
     const int64_t elem = c128 ? 16 : 8;
-    int sms = 148;
-    {
-        int dev = 0;
-        if (cudaGetDevice(&dev) == cudaSuccess)
-            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
+    const int sms = sm_count();
     const bool vec = (reinterpret_cast<uintptr_t>(d_x) % 16 == 0) && (span * elem) % 16 == 0 &&
                      (x_stride * elem) % 16 == 0;
     if (vec) {
@@ -175,11 +170,9 @@ void launch_validate(const void* d_x, bool c128, int64_t span, int64_t x_stride,
         const unsigned grid = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(nch, sms)));
         const size_t smem = static_cast<size_t>(kValChunk) * kValRing;
         if (c128)
-            MSFFT_CUDA(cudaFuncSetAttribute(validate_kernel<true>,
-                                            cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            smem_attr(validate_kernel<true>, smem);
         else
-            MSFFT_CUDA(cudaFuncSetAttribute(validate_kernel<false>,
-                                            cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            smem_attr(validate_kernel<false>, smem);
         if (c128)
             validate_kernel<true><<<grid, kValThreads, smem, st>>>(
                 static_cast<const unsigned char*>(d_x), row_bytes, x_stride * elem, rows, bad);
@@ -203,7 +196,44 @@ void launch_validate(const void* d_x, bool c128, int64_t span, int64_t x_stride,
 }
 
 namespace {
+
+// Device twin of the host ingest gather (ingest.hpp): compact[s][cpos + i] =
+// x[s][sigma_m * (lo + i) mod n] for every interval of the iterations'
+// t' unions.  Small launches gather through it so the random reads of one
+// signal are spread over every SM (an SM serves ~1 random access per clock,
+// so a single-signal encode task reading them itself is bound by its own
+// SM's L1), and the encode then reads its samples coalesced.
+template <class T>
+__global__ void __launch_bounds__(256)
+compact_gather_kernel(const GatherIv* __restrict__ ivs, const T* __restrict__ x, int64_t x_stride,
+                      const int64_t* __restrict__ sigma, int iters, uint64_t mask,
+                      int64_t per_signal, T* __restrict__ out) {
+    const GatherIv iv = ivs[blockIdx.y];
+    const int64_t s = blockIdx.z;
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= iv.len) return;
+    const uint64_t sg = static_cast<uint64_t>(sigma[s * iters + iv.m]);
+    const uint64_t t = static_cast<uint64_t>(iv.lo + i);
+    out[s * per_signal + iv.cpos + i] = x[s * x_stride + static_cast<int64_t>((sg * t) & mask)];
+}
+
 }  // namespace
+
+void Plan::launch_compact_gather(int64_t batch, const void* d_x, int64_t x_stride,
+                                 const int64_t* d_sig, void* out, cudaStream_t st) const {
+    const dim3 grid(static_cast<unsigned>((giv_max_len_ + 255) / 256),
+                    static_cast<unsigned>(n_givs_), static_cast<unsigned>(batch));
+    const uint64_t mask = static_cast<uint64_t>(sched_.n - 1);
+    if (c128_)
+        compact_gather_kernel<double2><<<grid, 256, 0, st>>>(
+            givs_.get(), static_cast<const double2*>(d_x), x_stride, d_sig, sched_.iterations,
+            mask, imap_.per_signal, static_cast<double2*>(out));
+    else
+        compact_gather_kernel<float2><<<grid, 256, 0, st>>>(
+            givs_.get(), static_cast<const float2*>(d_x), x_stride, d_sig, sched_.iterations,
+            mask, imap_.per_signal, static_cast<float2*>(out));
+    MSFFT_LAUNCH_CHECK("compact_gather_kernel");
+}
 
 Plan::Plan(int64_t n, int64_t k, int64_t l, double q, double delta, bool c128, int device)
     : device_(device), c128_(c128) {
@@ -321,6 +351,12 @@ Plan::Plan(int64_t n, int64_t k, int64_t l, double q, double delta, bool c128, i
     if (const char* e = std::getenv("MSFFT_ENC_SMEM_PAD")) enc_smem_pad_ = std::atoll(e);
     fused_smem_ = std::max(enc_smem_, lay_.in_smem ? static_cast<size_t>(lay_.bytes) : size_t{0});
     if (const char* e = std::getenv("MSFFT_ENC_SPLIT")) split_enabled_ = std::atoi(e) != 0;
+    if (const char* e = std::getenv("MSFFT_GATED_MAX_BATCH")) gated_max_batch_ = std::atoll(e);
+    if (const char* e = std::getenv("MSFFT_GATED_GRAPH")) gated_graphs_ = std::atoi(e) != 0;
+    // gated launches need the one-CTA decode and every bucket FFT in one
+    // shared-memory launch
+    gated_ok_ = !lay_.big && big_b_iters_.size() <= static_cast<size_t>(kMaxFftSets);
+    for (int m : big_b_iters_) gated_ok_ = gated_ok_ && dplan_.it[m].b <= kSmemFftMax;
     if (const char* e = std::getenv("MSFFT_FUSED_SMEM_PAD"))  // diagnostic: L1 carve-out experiments
         fused_smem_ += static_cast<size_t>(std::max(0LL, std::atoll(e)));
     flags_.reset(2);
@@ -328,6 +364,20 @@ Plan::Plan(int64_t n, int64_t k, int64_t l, double q, double delta, bool c128, i
     for (int i = 0; i < 2; ++i)
         MSFFT_CUDA(cudaEventCreateWithFlags(&ev_seeds_[i], cudaEventDisableTiming));
     imap_ = make_ingest_map(sched_);
+    {
+        std::vector<GatherIv> iv;
+        for (int m = 0; m < sched_.iterations; ++m)
+            for (size_t j = 0; j < imap_.uni[m].size(); ++j) {
+                const auto& u = imap_.uni[m][j];
+                iv.push_back(GatherIv{m, 0, u.first, u.second - u.first + 1, imap_.pos[m][j]});
+                giv_max_len_ = std::max(giv_max_len_, u.second - u.first + 1);
+            }
+        n_givs_ = static_cast<int>(iv.size());
+        givs_.reset(iv.size());
+        MSFFT_CUDA(cudaMemcpy(givs_.get(), iv.data(), iv.size() * sizeof(GatherIv),
+                              cudaMemcpyHostToDevice));
+    }
+    if (const char* e = std::getenv("MSFFT_COMPACT_GATHER")) compact_gather_ = std::atoi(e) != 0;
     dplan_compact_ = dplan_;
     dplan_compact_.x_compact = 1;
     dplan_compact_.x_row = imap_.per_signal;
@@ -348,6 +398,8 @@ Plan::~Plan() {
     int cur = 0;
     if (cudaGetDevice(&cur) != cudaSuccess) return;
     cudaSetDevice(device_);
+    for (auto& kv : gated_graphs_map_)
+        if (kv.second) cudaGraphExecDestroy(kv.second);
     if (own_stream_) cudaStreamDestroy(own_stream_);
     if (copy_stream_) cudaStreamDestroy(copy_stream_);
     if (ev_start_) cudaEventDestroy(ev_start_);
@@ -387,6 +439,21 @@ const Plan::TaskSet& Plan::tasks_for(int64_t batch) {
     ts.count = static_cast<int64_t>(v.size());
     ts.d.reset(v.size());
     MSFFT_CUDA(cudaMemcpy(ts.d.get(), v.data(), v.size() * sizeof(EncTask),
+                          cudaMemcpyHostToDevice));
+    // gate words (encode.hpp): decode need per iteration -- its encode tasks
+    // (b <= 256) or its bucket-FFT CTAs (b > 256) --, done, exit, the folds'
+    // encode tasks per iteration, their done
+    const int iters = sched_.iterations;
+    std::vector<int32_t> gate(static_cast<size_t>(4 * iters + 1), 0);
+    for (const EncTask& t : v) {
+        if (dplan_.it[t.m].b > kEncThreads)
+            ++gate[2 * iters + 1 + t.m];
+        else
+            ++gate[t.m];
+    }
+    for (int m : big_b_iters_) gate[m] = static_cast<int32_t>(batch * dplan_.it[m].nrounds);
+    ts.gate.reset(gate.size());
+    MSFFT_CUDA(cudaMemcpy(ts.gate.get(), gate.data(), gate.size() * sizeof(int32_t),
                           cudaMemcpyHostToDevice));
     ts.host = std::move(v);
     return tasks_.emplace(batch, std::move(ts)).first->second;
@@ -486,16 +553,16 @@ const Plan::FusedSet& Plan::fused_for(int64_t batch, int slot) {
 // K2 for the iterations with b > 256 (the encode's fused epilogue does the
 // rest): their b-point transforms and the 1/n scale, as few launches as the
 // sizes allow.
-void Plan::bucket_ffts(double2* y, int64_t batch, cudaStream_t st) const {
+void Plan::bucket_ffts(double2* y, int64_t batch, cudaStream_t st, const FftGate* gate) const {
     std::vector<FftSet> sets;
     for (int m : big_b_iters_) {
         const DevIter& di = dplan_.it[m];
-        sets.push_back(FftSet{di.yoff, di.b, di.nrounds});
+        sets.push_back(FftSet{di.yoff, di.b, di.nrounds, m});
     }
     for (size_t i = 0; i < sets.size(); i += kMaxFftSets)
         fft_radix2_sets(y, sets.data() + i,
                         static_cast<int>(std::min<size_t>(kMaxFftSets, sets.size() - i)), batch,
-                        dplan_.values_per_signal, -1, dplan_.inv_n, st);
+                        dplan_.values_per_signal, -1, dplan_.inv_n, st, gate);
 }
 
 bool Plan::split_tasks(int64_t n_tasks) const {
@@ -579,6 +646,9 @@ void Plan::append_tasks(std::vector<EncTask>& v, int64_t s_begin, int64_t s_end,
 }
 
 int64_t Plan::launches(int64_t batch, bool validate, bool serial) const {
+    if (!serial && gated_ok_ && batch <= gated_max_batch_)  // sigma (+ gather) + encode
+        return 3 + (compact_gather_ ? 1 : 0) + (big_b_iters_.empty() ? 0 : 1) +
+               (validate ? 1 : 0);  // (+ bucket FFTs) + decode (+ validate)
     if (!serial && fused_enabled_ && big_b_iters_.empty() && !lay_.big)
         return 2 + (validate ? 1 : 0);  // sigma + fused (+ validate)
     // per (sub-)chunk: encode + bucket FFTs for b > 256 + decode
@@ -598,14 +668,101 @@ int64_t Plan::launches(int64_t batch, bool validate, bool serial) const {
     return 1 + (validate ? 1 : 0) + chunks * per_chunk;  // + sigma (+ validate)
 }
 
+// The small-batch launch sequence: [validate] [compact gather] encode
+// [gated bucket FFTs] gated decode.  The decode is a programmatic dependent
+// launch that starts while the encode runs and waits per iteration for that
+// iteration's tasks (one CTA per signal, the standalone decode's registers
+// and shared-memory scratch).
+void Plan::enqueue_gated(int64_t batch, const void* d_x, int64_t x_stride, const int64_t* d_sig,
+                         const int64_t* d_sig_inv, int64_t* d_out_f, double2* d_out_c,
+                         int64_t* d_out_count, bool validate, bool compact, cudaStream_t st) {
+    if (validate) launch_validate(d_x, c128_, sched_.n, x_stride, batch, flags_.get() + 1, st);
+    const TaskSet& ts = tasks_for(batch);
+    int32_t* gate = const_cast<int32_t*>(ts.gate.get());
+    const int iters = sched_.iterations;
+    const DevPlan* EP = compact ? &dplan_compact_ : &dplan_;
+    const void* ex = d_x;
+    int64_t es = x_stride;
+    if (compact_gather_ && !compact && n_givs_ <= 65535) {
+        // the samples of every iteration, gathered over all SMs first
+        launch_compact_gather(batch, d_x, x_stride, d_sig, xcompact_.get(), st);
+        EP = &dplan_compact_;
+        ex = xcompact_.get();
+        es = imap_.per_signal;
+    }
+    launch_encode(*EP, ts.d.get(), ts.count, ex, c128_, es, batch, d_sig, y_.get(),
+                  enc_smem_ + enc_smem_pad_, st, gate + iters);
+    if (!big_b_iters_.empty()) {
+        // b > 256: the bucket FFTs as a gated launch between the two
+        const FftGate g{gate + 3 * iters + 1, gate + 2 * iters + 1, gate + iters};
+        bucket_ffts(y_.get(), batch, st, &g);
+    }
+    launch_decode_gated(dplan_, lay_dec_, y_.get(), d_sig, d_sig_inv, batch, dec_work_.get(),
+                        d_out_f, d_out_c, d_out_count, flags_.get(), gate, gate + iters, st);
+}
+
 void Plan::run_chunk(int64_t batch, const void* d_x, int64_t x_stride, const int64_t* d_sig,
                      const int64_t* d_sig_inv, int64_t* d_out_f, double2* d_out_c,
                      int64_t* d_out_count, bool validate, cudaStream_t st,
                      const ExecOptions& opt, bool compact) {
     const int64_t n = sched_.n;
     const DevPlan& P = compact ? dplan_compact_ : dplan_;
-    if (validate) launch_validate(d_x, c128_, n, x_stride, batch, flags_.get() + 1, st);
     const bool traced = opt.pre || opt.post || opt.sel_bucket;
+    if (!traced && !opt.stage_times && !opt.force_serial && gated_ok_ && batch <= gated_max_batch_) {
+        // small batches: a latency path, so the launch sequence is replayed
+        // from a CUDA graph once it has run eagerly for these buffers
+        const bool use_gather = compact_gather_ && !compact && n_givs_ <= 65535;
+        if (use_gather) {
+            const size_t elem = c128_ ? sizeof(double2) : sizeof(float2);
+            xcompact_.ensure(static_cast<size_t>(batch * imap_.per_signal) * elem);
+        }
+        const GatedKey key{batch, d_x, x_stride, d_sig, d_sig_inv, d_out_f, d_out_c, d_out_count,
+                           y_.get(), dec_work_.get(), xcompact_.get(), validate, compact};
+        if (!gated_graphs_) {
+            enqueue_gated(batch, d_x, x_stride, d_sig, d_sig_inv, d_out_f, d_out_c, d_out_count,
+                          validate, compact, st);
+            return;
+        }
+        auto it = gated_graphs_map_.find(key);
+        if (it == gated_graphs_map_.end()) {
+            // first use of these buffers: eager (allocates lazily built
+            // tables), and remembered so the next call captures
+            if (gated_graphs_map_.size() >= 8) {
+                MSFFT_CUDA(cudaStreamSynchronize(st));
+                for (auto& kv : gated_graphs_map_)
+                    if (kv.second) cudaGraphExecDestroy(kv.second);
+                gated_graphs_map_.clear();
+            }
+            gated_graphs_map_.emplace(key, nullptr);
+            enqueue_gated(batch, d_x, x_stride, d_sig, d_sig_inv, d_out_f, d_out_c, d_out_count,
+                          validate, compact, st);
+            return;
+        }
+        if (!it->second) {
+            cudaStream_t cap = nullptr;
+            MSFFT_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+            cudaGraph_t g = nullptr;
+            MSFFT_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+            try {
+                enqueue_gated(batch, d_x, x_stride, d_sig, d_sig_inv, d_out_f, d_out_c,
+                              d_out_count, validate, compact, cap);
+            } catch (...) {
+                cudaStreamEndCapture(cap, &g);
+                if (g) cudaGraphDestroy(g);
+                cudaStreamDestroy(cap);
+                throw;
+            }
+            MSFFT_CUDA(cudaStreamEndCapture(cap, &g));
+            cudaGraphExec_t ex = nullptr;
+            MSFFT_CUDA(cudaGraphInstantiate(&ex, g, 0));
+            cudaGraphDestroy(g);
+            cudaStreamDestroy(cap);
+            it->second = ex;
+        }
+        MSFFT_CUDA(cudaGraphLaunch(it->second, st));
+        return;
+    }
+    if (validate) launch_validate(d_x, c128_, n, x_stride, batch, flags_.get() + 1, st);
     if (!traced && !opt.force_serial && fused_enabled_ && big_b_iters_.empty() && !lay_.big) {
         // one persistent launch: encode and decode share the SMs
         const FusedSet& fs = fused_for(batch);

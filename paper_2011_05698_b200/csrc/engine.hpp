@@ -19,6 +19,7 @@
 
 #include "cuda_check.hpp"
 #include "encode.hpp"
+#include "fft.hpp"
 #include "fused.hpp"
 #include "host_plan.hpp"
 #include "ingest.hpp"
@@ -27,6 +28,12 @@
 #include "window.hpp"
 
 namespace msfft_b200 {
+
+// one interval of an iteration's t' union and its compact position
+struct GatherIv {
+    int32_t m, pad_;
+    int64_t lo, len, cpos;
+};
 
 struct ExecOptions {
     bool x_on_device = false;
@@ -116,6 +123,9 @@ private:
         DeviceBuffer<EncTask> d;
         int64_t count = 0;
         std::vector<EncTask> host;
+        // gated decode (launch_decode_gated): [need per iteration][done per
+        // iteration][exit count]; done/exit are zero between calls
+        DeviceBuffer<int32_t> gate;
     };
     struct FusedSet {
         DeviceBuffer<EncTask> tasks;
@@ -132,7 +142,10 @@ private:
     // split: one task per merged t' segment (more CTAs for small batches)
     void append_tasks(std::vector<EncTask>& v, int64_t s_begin, int64_t s_end, bool split) const;
     bool split_tasks(int64_t n_tasks) const;
-    void bucket_ffts(double2* y, int64_t batch, cudaStream_t st) const;
+    void launch_compact_gather(int64_t batch, const void* d_x, int64_t x_stride,
+                               const int64_t* d_sig, void* out, cudaStream_t st) const;
+    void bucket_ffts(double2* y, int64_t batch, cudaStream_t st,
+                     const FftGate* gate = nullptr) const;
     void upload_sigmas(int64_t batch, const uint64_t* seeds, cudaStream_t st);
     void check_flags(cudaStream_t st);
     void run_chunk(int64_t batch, const void* d_x, int64_t x_stride, const int64_t* d_sig,
@@ -169,6 +182,37 @@ private:
     int64_t fused_lag_ = 2;       // chunks a decode trails its encode by
     int64_t fused_tail_ = 0;      // last chunks whose decodes follow their encodes at once
     bool split_enabled_ = true;   // split encode tasks per segment when a launch is small
+    // batches up to this size run the encode and a gated decode launch behind
+    // it (the decode starts while the encode runs, one CTA per signal with
+    // the standalone decode's scratch) instead of the fused kernel
+    int64_t gated_max_batch_ = 16;
+    bool gated_ok_ = false;
+    // small launches gather their samples over every SM into compact rows
+    // first (compact_gather_kernel), then encode from those (coalesced)
+    bool compact_gather_ = true;
+    DeviceBuffer<GatherIv> givs_;
+    int n_givs_ = 0;
+    int64_t giv_max_len_ = 0;
+    mutable DeviceBuffer<unsigned char> xcompact_;
+    // CUDA graphs of the small-batch sequence, per buffer set (bounded)
+    struct GatedKey {
+        int64_t batch;
+        const void* x;
+        int64_t x_stride;
+        const void *sig, *sig_inv, *out_f, *out_c, *out_count, *y, *work, *xc;
+        bool validate, compact;
+        bool operator<(const GatedKey& o) const {
+            return std::tie(batch, x, x_stride, sig, sig_inv, out_f, out_c, out_count, y, work, xc,
+                            validate, compact) <
+                   std::tie(o.batch, o.x, o.x_stride, o.sig, o.sig_inv, o.out_f, o.out_c,
+                            o.out_count, o.y, o.work, o.xc, o.validate, o.compact);
+        }
+    };
+    bool gated_graphs_ = true;
+    std::map<GatedKey, cudaGraphExec_t> gated_graphs_map_;
+    void enqueue_gated(int64_t batch, const void* d_x, int64_t x_stride, const int64_t* d_sig,
+                       const int64_t* d_sig_inv, int64_t* d_out_f, double2* d_out_c,
+                       int64_t* d_out_count, bool validate, bool compact, cudaStream_t st);
     size_t fused_smem_ = 0;
     size_t enc_smem_pad_ = 0;     // diagnostics: extra encode smem (lowers occupancy)
 

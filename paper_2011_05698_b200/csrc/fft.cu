@@ -118,7 +118,6 @@ __global__ void __launch_bounds__(512) stages_kernel(double2* __restrict__ data,
 // Whole transform of one array (size <= kSmemFftMax) in shared memory: the
 // bit-reversal permutation folded into the load, then every radix-2 stage
 // with the same butterflies and twiddles as stages_kernel (bit-identical).
-constexpr int64_t kSmemFftMax = 4096;
 __global__ void __launch_bounds__(512) fft_smem_kernel(double2* __restrict__ data, int64_t size,
                                                        int log2size, int64_t inner,
                                                        int64_t outer_stride, int sign,
@@ -163,16 +162,34 @@ struct SmemFftSets {
     int64_t first[kMaxFftSets + 1];  // first block of each set
     int64_t off[kMaxFftSets], size[kMaxFftSets], inner[kMaxFftSets];
     int log2size[kMaxFftSets];
+    int m[kMaxFftSets];
     const double2* tw[kMaxFftSets];
 };
 
 __global__ void __launch_bounds__(512) fft_smem_sets_kernel(double2* __restrict__ data,
                                                             const __grid_constant__ SmemFftSets S,
                                                             int64_t outer_stride, int sign,
-                                                            double scale) {
+                                                            double scale, FftGate gate) {
     extern __shared__ double2 buf[];
     int si = 0;
     while (si + 1 < S.nsets && static_cast<int64_t>(blockIdx.x) >= S.first[si + 1]) ++si;
+    if (gate.post_done) {
+        // gated: let the decode behind this grid be scheduled, then wait for
+        // this set's iteration to be encoded (acquire, then drop stale L1)
+        asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+        if (threadIdx.x == 0) {
+            const int m = S.m[si];
+            for (;;) {
+                int32_t v;
+                asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v)
+                             : "l"(gate.wait_done + m) : "memory");
+                if (v >= gate.wait_need[m]) break;
+                __nanosleep(64);
+            }
+            __threadfence();
+        }
+        __syncthreads();
+    }
     const int64_t bi = static_cast<int64_t>(blockIdx.x) - S.first[si];
     const int64_t size = S.size[si];
     const int log2size = S.log2size[si];
@@ -203,6 +220,13 @@ __global__ void __launch_bounds__(512) fft_smem_sets_kernel(double2* __restrict_
         if (do_scale) v = make_double2(v.x * scale, v.y * scale);
         a[e] = v;
     }
+    if (gate.post_done) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            atomicAdd(gate.post_done + S.m[si], 1);
+        }
+    }
 }
 
 void smem_fft_attribute(const void* fn) {
@@ -222,13 +246,15 @@ void smem_fft_attribute(const void* fn) {
 }  // namespace
 
 void fft_radix2_sets(double2* data, const FftSet* sets, int nsets, int64_t batch,
-                     int64_t outer_stride, int sign, double scale, cudaStream_t stream) {
+                     int64_t outer_stride, int sign, double scale, cudaStream_t stream,
+                     const FftGate* gate) {
     SmemFftSets S{};
     int64_t blocks = 0, max_size = 0;
     for (int i = 0; i < nsets; ++i) {
         const FftSet& f = sets[i];
         if (f.size <= 1 || batch <= 0) continue;
         if (f.size > kSmemFftMax || S.nsets == kMaxFftSets) {
+            if (gate) throw CudaError("fft_radix2_sets: gated sets must fit one launch");
             fft_radix2_batched(data + f.off, f.size, batch * f.inner, f.inner, outer_stride, sign,
                                scale, stream);
             continue;
@@ -240,6 +266,7 @@ void fft_radix2_sets(double2* data, const FftSet* sets, int nsets, int64_t batch
         S.size[S.nsets] = f.size;
         S.inner[S.nsets] = f.inner;
         S.log2size[S.nsets] = lg;
+        S.m[S.nsets] = f.m;
         S.tw[S.nsets] = device_twiddles(f.size);
         ++S.nsets;
         blocks += batch * f.inner;
@@ -250,9 +277,18 @@ void fft_radix2_sets(double2* data, const FftSet* sets, int nsets, int64_t batch
     if (blocks > 0x7fffffff) throw CudaError("fft_radix2_sets: too many arrays");
     smem_fft_attribute(reinterpret_cast<const void*>(fft_smem_sets_kernel));
     const int threads = static_cast<int>(std::min<int64_t>(512, std::max<int64_t>(32, max_size / 2)));
-    fft_smem_sets_kernel<<<static_cast<unsigned>(blocks), threads,
-                           sizeof(double2) * static_cast<size_t>(max_size), stream>>>(
-        data, S, outer_stride, sign, scale);
+    const FftGate g = gate ? *gate : FftGate{nullptr, nullptr, nullptr};
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(blocks));
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = sizeof(double2) * static_cast<size_t>(max_size);
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = gate ? 1 : 0;
+    MSFFT_CUDA(cudaLaunchKernelEx(&cfg, fft_smem_sets_kernel, data, S, outer_stride, sign, scale, g));
     MSFFT_LAUNCH_CHECK("fft_smem_sets_kernel");
 }
 

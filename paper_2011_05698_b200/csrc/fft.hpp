@@ -32,13 +32,26 @@ void fft_radix2_batched(double2* data, int64_t size, int64_t batch, int64_t inne
 // data + off + row * outer_stride.
 struct FftSet {
     int64_t off, size, inner;
+    int m = 0;  // iteration (gated launches: the counter slot of the set)
 };
 constexpr int kMaxFftSets = 16;
+constexpr int64_t kSmemFftMax = 4096;  // largest array transformed in one CTA
+
+// Gated launch of fft_radix2_sets (every set <= kSmemFftMax): a programmatic
+// dependent launch behind the encode whose CTA for a set of iteration m
+// starts once wait_done[m] reaches wait_need[m], and adds 1 to post_done[m]
+// when its array is transformed.
+struct FftGate {
+    const int32_t* wait_done;
+    const int32_t* wait_need;
+    int32_t* post_done;
+};
 
 // fft_radix2_batched of several sets: the sets with size <= 4096 go into ONE
 // launch (one CTA per array, shared memory), larger ones through the
 // multi-pass path.  Bit-identical to transforming each set separately.
 void fft_radix2_sets(double2* data, const FftSet* sets, int nsets, int64_t batch,
-                     int64_t outer_stride, int sign, double scale, cudaStream_t stream);
+                     int64_t outer_stride, int sign, double scale, cudaStream_t stream,
+                     const FftGate* gate = nullptr);
 
 }  // namespace msfft_b200

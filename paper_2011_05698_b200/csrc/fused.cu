@@ -13,6 +13,10 @@
 // on the counter, __threadfence, __syncthreads).  Compiled with --fmad=false.
 #include <cuda_runtime.h>
 
+#include <map>
+#include <mutex>
+#include <tuple>
+
 #include "decode_body.cuh"
 #include "encode_body.cuh"
 #include "fused.hpp"
@@ -127,12 +131,25 @@ void launch_t(const DevPlan& plan, const DecLayout& lay, const FusedWork& fw, co
               double2* d_out_c, int64_t* d_out_count, int32_t* d_err, size_t smem,
               cudaStream_t stream, bool programmatic) {
     auto k = fused_kernel<T>;
-    MSFFT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(smem)));
-    int dev = 0, sms = 0, per_sm = 0;
-    MSFFT_CUDA(cudaGetDevice(&dev));
-    MSFFT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    MSFFT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kEncThreads, smem));
+    smem_attr(k, smem);
+    const int sms = sm_count();
+    int per_sm = 0;
+    {
+        // occupancy per (device, kernel, shared memory), queried once
+        static std::mutex mu;
+        static std::map<std::tuple<int, const void*, size_t>, int> occ;
+        int dev = 0;
+        MSFFT_CUDA(cudaGetDevice(&dev));
+        std::lock_guard<std::mutex> lock(mu);
+        const auto key = std::make_tuple(dev, reinterpret_cast<const void*>(k), smem);
+        auto it = occ.find(key);
+        if (it == occ.end()) {
+            MSFFT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kEncThreads, smem));
+            occ[key] = per_sm;
+        } else {
+            per_sm = it->second;
+        }
+    }
     if (per_sm < 1) throw CudaError("fused_kernel: does not fit on an SM");
     const int64_t grid = std::min<int64_t>(static_cast<int64_t>(sms) * per_sm, fw.n_items);
     // counters are zero: from creation, then reset by the previous launch's

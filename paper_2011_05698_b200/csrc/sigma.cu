@@ -28,6 +28,10 @@ __device__ __forceinline__ uint64_t temper(uint64_t y) {
     return y;
 }
 
+#ifdef MSFFT_TIMELINE
+__device__ unsigned long long g_sig_tl[2];
+#endif
+
 template <int MAXD>
 __global__ void sigma_kernel(const uint64_t* __restrict__ seeds, int64_t batch, int iters,
                              int64_t n, int64_t* __restrict__ sigma,
@@ -35,6 +39,11 @@ __global__ void sigma_kernel(const uint64_t* __restrict__ seeds, int64_t batch, 
     // programmatic dependent launch: the next kernel may be scheduled now
     // (it waits for this grid's results with griddepcontrol.wait)
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#ifdef MSFFT_TIMELINE
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t0));
+    if (blockIdx.x == 0 && threadIdx.x == 0) g_sig_tl[0] = t0;
+#endif
     const int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (s >= batch) return;
     // seeded state words 0..MAXD and kMM..kMM+MAXD
@@ -65,9 +74,18 @@ __global__ void sigma_kernel(const uint64_t* __restrict__ seeds, int64_t batch, 
         sigma[s * iters + d] = static_cast<int64_t>(sg);
         sigma_inv[s * iters + d] = static_cast<int64_t>(inv & mask);
     }
+#ifdef MSFFT_TIMELINE
+    if (s == 0) asm volatile("mov.u64 %0, %globaltimer;" : "=l"(g_sig_tl[1]));
+#endif
 }
 
 }  // namespace
+
+#ifdef MSFFT_TIMELINE
+extern "C" int msfft_debug_sigma_timeline(void* dst) {
+    return static_cast<int>(cudaMemcpyFromSymbol(dst, g_sig_tl, 16));
+}
+#endif
 
 void launch_sigma(const uint64_t* d_seeds, int64_t batch, int iters, int64_t n, int64_t* d_sigma,
                   int64_t* d_sigma_inv, cudaStream_t stream, bool programmatic) {

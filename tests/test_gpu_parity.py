@@ -551,3 +551,58 @@ def test_concurrent_one_shot_calls(oracle):
     for a, b in zip(seq, par):
         assert np.array_equal(a.spectrum.positions, b.spectrum.positions)
         assert np.array_equal(a.spectrum.coeffs, b.spectrum.coeffs)
+
+
+@pytest.mark.parametrize("batch,n,k,l,q", [(1, 1 << 18, 64, 16, 1.0), (5, 1 << 18, 64, 16, 1.0),
+                                           (16, 1 << 18, 64, 16, 1.0),
+                                           # b = 512, 256, ...: the gated bucket FFT in between
+                                           (1, 1 << 20, 100, 4, 1.0), (3, 1 << 20, 100, 8, 2.0)])
+def test_gated_decode_matches_fused_and_serial(oracle, monkeypatch, batch, n, k, l, q):
+    import torch
+    """Small batches run the encode and a gated decode launch behind it (the
+    decode starts while the encode runs and waits per iteration on the
+    encode's (or, b > 256, the gated bucket FFT's) completion counters).
+    Results equal the ungated launches (the fused persistent kernel, or
+    encode -> FFT -> decode when b > 256) and the serial path bit for bit, on repeated calls (the
+    last decode CTA resets the counters) and after a call whose input fails
+    validation (its decodes are skipped; the counters must still drain) --
+    with host and device-resident inputs (the latter through the device
+    compact gather and, on repeated buffers, a replayed CUDA graph)."""
+    mk = __import__("paper_2011_05698_b200.workloads", fromlist=["x"]).make_signal_np
+    x = np.stack([mk(n, k, 40 + i, 25.0, "complex64")[0] for i in range(batch)]).astype(np.complex64)
+    seeds = [1000 + i for i in range(batch)]
+    res = {}
+    for name, gmax, graph in (("ungated", "0", "1"), ("gated", "64", "1"), ("gated_nograph", "64", "0")):
+        monkeypatch.setenv("MSFFT_GATED_MAX_BATCH", gmax)
+        monkeypatch.setenv("MSFFT_GATED_GRAPH", graph)
+        plan = M.Plan(n, k, M.MultiscaleConfig(l, q), 1e-6, "complex64")
+        out = [plan.execute(x, seeds)]
+        bad = x.copy()
+        bad[batch - 1, 777] = np.nan
+        with pytest.raises(M.InvalidArgument, match="non-finite"):
+            plan.execute(bad, seeds)
+        out.append(plan.execute(x, seeds))
+        out.append(plan.execute(x, seeds, assume_valid=True))
+        # device-resident input and outputs: the device compact gather and,
+        # from the second call on the same buffers, the captured CUDA graph
+        xd = torch.as_tensor(x).to("cuda")
+        od = (torch.empty((batch, k), dtype=torch.int64, device="cuda"),
+              torch.empty((batch, k), dtype=torch.complex128, device="cuda"),
+              torch.empty((batch,), dtype=torch.int64, device="cuda"))
+        for i in range(4):
+            od[0].fill_(-7)
+            plan.execute(xd, seeds, out=od, assume_valid=i % 2 == 1)
+            out.append(tuple(t.cpu().numpy() for t in od) + (0.0,))
+        bad_d = torch.as_tensor(bad).to("cuda")
+        with pytest.raises(M.InvalidArgument, match="non-finite"):
+            plan.execute(bad_d, seeds, out=od)
+        plan.execute(xd, seeds, out=od)
+        out.append(tuple(t.cpu().numpy() for t in od) + (0.0,))
+        res[name] = out
+        if name == "gated":
+            res["serial"] = [plan.execute(x, seeds, serial=True)]
+    f0, c0, n0, _ = res["ungated"][0]
+    assert (n0 > 0).all()
+    for name in res:
+        for f, c, cnt, _ in res[name]:
+            assert np.array_equal(cnt, n0) and np.array_equal(f, f0) and np.array_equal(c, c0), name
