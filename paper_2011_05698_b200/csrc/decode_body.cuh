@@ -19,6 +19,8 @@
 
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #include "common.cuh"
 #include "cta_sort.cuh"
 #include "encode.hpp"
@@ -193,9 +195,13 @@ __device__ __forceinline__ void decode_signal(const DevPlan& plan, const DecLayo
         const double invL = 1.0 / Ld;  // exact: L is a power of two
         const int nr = it.nrounds;
         const int64_t* taus = plan.taus + it.tau_off;
-        if (tid < kMaxStageTable) {  // read after the next group barrier (K3 or K4)
-            sh.st_len[tid] = it.stage_len[tid];
-            sh.st_blk[tid] = it.stage_blk[tid];
+        // stage tables of up to kMaxStageTable stages in shared memory (read
+        // after the next group barrier, K3 or K4); longer schedules take the
+        // general locate loop
+        const int nst_tab = it.nstage_tab < kMaxStageTable ? it.nstage_tab : -1;
+        if (tid < kMaxStageTable) {
+            if (tid <= nst_tab) sh.st_len[tid] = it.stage_len[tid];
+            if (tid < nst_tab) sh.st_blk[tid] = it.stage_blk[tid];
             sh.st_tau[tid] = tid < nr ? taus[tid] : 0;
         }
         const auto tau_at = [&](int r) { return r < kMaxStageTable ? sh.st_tau[r] : taus[r]; };
@@ -402,7 +408,7 @@ __device__ __forceinline__ void decode_signal(const DevPlan& plan, const DecLayo
         // stage-chain operands converted once: q/2, n and the taus as doubles
         const int64_t lcfg = plan.l;
         const double q = plan.q, hq = plan.q / 2.0, nd_r = static_cast<double>(n), inv_n_r = inv_n;
-        const int nst_r = it.nstage_tab;
+        const int nst_r = nst_tab;
         // group size: enough lanes for the l blocks, shrunk (each lane then
         // scans several blocks) until every ranked bucket fits in one pass
         int gsz = lcfg > 16 ? 32 : (lcfg > 8 ? 16 : (lcfg > 4 ? 8 : 4));
@@ -426,7 +432,125 @@ __device__ __forceinline__ void decode_signal(const DevPlan& plan, const DecLayo
             double u_min = (2.0 * static_cast<double>(beta) - 1.0) * Ld / 2.0;
             double len = Ld;
             const int nst = nst_r;  // host-precomputed stage lengths (or -1)
-            if (nst >= 0 && nst < nr) {
+            const int64_t jpl = (lcfg + gsz - 1) / gsz;  // blocks per lane
+            if (nst >= 0 && nst < nr && jpl <= 4 && gsz >= 2 && gsz <= 16) {
+                // the usual case, shortest chain.  Stage operands are known up
+                // front: each stage first loads the next stage's (clamped
+                // index, no branch), and per lane the next block offsets
+                // (j + 0.5) * rblk, the u_min steps (j - q/2) * rblk and tau/n
+                // are formed off the chain; the argmin carries the winner's
+                // step.  With the group size and blocks per lane fixed at
+                // compile time a stage is one basic block, so those loads and
+                // products overlap the chain center -> phase -> distance ->
+                // argmin -> u_min + step.  Every value equals the
+                // reference's: tau/n and the 1/n scalings are exact powers of
+                // two, so (center * tau/n) - trunc(..) is fmod(center * tau,
+                // n) / n, and round(f * 2pi) is the reference's
+                // round(round(x * 2pi) / n) (locate.cpp:19-23).
+                const auto run = [&](auto gtag, auto jtag) {
+                    constexpr int GSZ = decltype(gtag)::value;
+                    constexpr int JPL = decltype(jtag)::value;
+                    double jd[JPL];
+                    bool jv[JPL];
+#pragma unroll
+                    for (int i = 0; i < JPL; ++i) {
+                        const int64_t j = glane + static_cast<int64_t>(i) * GSZ;
+                        jv[i] = j < lcfg;
+                        jd[i] = static_cast<double>(j);
+                    }
+                    const int64_t pe0 = rank * ns;
+                    const int64_t pe_last = pe0 + (nst > 0 ? nst - 1 : 0);
+                    int code = live && nst > 0 ? S.pcode[pe0] : 1;
+                    double ph = live && nst > 0 ? S.phi[pe0] : 0.0;
+                    double rb = sh.st_blk[0];
+                    double offc[JPL], step[JPL];
+#pragma unroll
+                    for (int i = 0; i < JPL; ++i) {
+                        offc[i] = (jd[i] + 0.5) * rb;
+                        step[i] = (jd[i] - hq) * rb;
+                    }
+                    double step0 = (0.0 - hq) * rb;  // block 0: all distances NaN
+                    double ton = static_cast<double>(tau_at(1)) * inv_n_r;
+                    bool err2 = false;
+                    for (int stage = 1; stage <= nst; ++stage) {
+                        // the next stage's operands (the last stage reloads its own)
+                        const int64_t pn = min(pe0 + stage, pe_last);
+                        const int sn = stage < nst ? stage : nst - 1;
+                        const int code_n = live ? S.pcode[pn] : 1;
+                        const double phi_n = live ? S.phi[pn] : 0.0;
+                        const double rb_n = sh.st_blk[sn];
+                        const int64_t tau_n = tau_at(sn + 1);
+                        // this stage's chain
+                        double best_d = INFINITY, best_step = step0;
+                        int best_j = 0x7fffffff;
+#pragma unroll
+                        for (int i = 0; i < JPL; ++i) {
+                            const double y = (u_min + offc[i]) * ton;
+                            double f = y - trunc(y);
+                            f = f < 0 ? f + 1.0 : f;
+                            const double d = circular_phase_distance(f * kTwoPi, ph);
+                            const bool better = jv[i] && d < best_d;
+                            best_d = better ? d : best_d;
+                            best_j = better ? glane + i * GSZ : best_j;
+                            best_step = better ? step[i] : best_step;
+                        }
+                        // 1: locate_frequency returns nullopt; 2: phase_of throws
+                        err2 = err2 || (ok && code == 2);
+                        ok = ok && code == 0;
+                        // lowest block index wins ties (strict < in ascending order)
+#pragma unroll
+                        for (int o = GSZ >> 1; o > 0; o >>= 1) {
+                            const double od = __shfl_xor_sync(0xffffffffu, best_d, o);
+                            const int oj = __shfl_xor_sync(0xffffffffu, best_j, o);
+                            const double os = __shfl_xor_sync(0xffffffffu, best_step, o);
+                            const bool take = od < best_d || (od == best_d && oj < best_j);
+                            best_d = take ? od : best_d;
+                            best_j = take ? oj : best_j;
+                            best_step = take ? os : best_step;
+                        }
+                        u_min = u_min + best_step;
+                        code = code_n;
+                        ph = phi_n;
+#pragma unroll
+                        for (int i = 0; i < JPL; ++i) {
+                            offc[i] = (jd[i] + 0.5) * rb_n;
+                            step[i] = (jd[i] - hq) * rb_n;
+                        }
+                        step0 = (0.0 - hq) * rb_n;
+                        ton = static_cast<double>(tau_n) * inv_n_r;
+                    }
+                    if (err2 && glane == 0) atomicCAS(A.err, 0, kDecErrPhaseZero);
+                    if (nst > 0) len = sh.st_len[nst];
+                };
+                using std::integral_constant;
+#ifdef MSFFT_DECODE_PROFILE
+                const long long t_chain0 = clock64();
+#endif
+#define MSFFT_RUN_G(G)                                                   \
+    do {                                                                 \
+        if (jpl == 1)                                                    \
+            run(integral_constant<int, G>{}, integral_constant<int, 1>{}); \
+        else if (jpl == 2)                                               \
+            run(integral_constant<int, G>{}, integral_constant<int, 2>{}); \
+        else                                                             \
+            run(integral_constant<int, G>{}, integral_constant<int, 4>{}); \
+    } while (0)
+                if (gsz == 16)
+                    MSFFT_RUN_G(16);
+                else if (gsz == 8)
+                    MSFFT_RUN_G(8);
+                else if (gsz == 4)
+                    MSFFT_RUN_G(4);
+                else
+                    MSFFT_RUN_G(2);
+#undef MSFFT_RUN_G
+#ifdef MSFFT_DECODE_PROFILE
+                if (tid == 0 && s < 1)
+                    printf("DECPROF chain m=%d nst=%d jpl=%lld gsz=%d cycles=%lld (%.0f per stage)\n", m,
+                           nst, (long long)jpl, gsz, clock64() - t_chain0,
+                           nst > 0 ? (double)(clock64() - t_chain0) / nst : 0.0);
+#endif
+            } else if (nst >= 0 && nst < nr) {
                 // the usual case: the stage count and every stage's operands
                 // are known up front, so the next stage's phase code, phase,
                 // tau, block width and length load while this stage runs;

@@ -124,7 +124,9 @@ __device__ __forceinline__ void gather_accumulate(const DevPlan& plan, const Enc
             }
 #pragma unroll
             for (int r = 0; r < kEncRounds; ++r) {
-                if (r < nr) {
+                // skip a round whose tap interval misses the whole batch
+                const int64_t a = t + static_cast<int64_t>(th[r]);
+                if (r < nr && a + (U - 1) * stride >= 0 && a < static_cast<int64_t>(wu)) {
                     double g[U];
                     bool in[U];
 #pragma unroll

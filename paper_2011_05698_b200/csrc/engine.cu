@@ -1,5 +1,6 @@
 // engine.cu -- see engine.hpp.
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -267,6 +268,8 @@ Plan::Plan(int64_t n, int64_t k, int64_t l, double q, double delta, bool c128, i
     P.acc_cap = sched_.acc_cap;
     int tau_off = 0;
     int64_t yoff = 0;
+    std::vector<double> stab_len, stab_blk;  // locate stage tables of every iteration
+    std::vector<std::array<int64_t, 2>> stage_off(static_cast<size_t>(sched_.iterations));
     for (int m = 0; m < sched_.iterations; ++m) {
         const IterationPlan& ip = sched_.iters[m];
         auto win = get_device_window(n, ip.b, delta);
@@ -292,13 +295,15 @@ Plan::Plan(int64_t n, int64_t k, int64_t l, double q, double delta, bool c128, i
             // locate stage lengths, same IEEE operations as locate_step
             double len = static_cast<double>(ip.l_width);
             int st = 0;
-            while (len > 1.0 + 1e-9 && st < kMaxStageTable - 1) {
-                it.stage_len[st] = len;
-                it.stage_blk[st] = len / static_cast<double>(l);
+            stage_off[m][0] = static_cast<int64_t>(stab_len.size());
+            stage_off[m][1] = static_cast<int64_t>(stab_blk.size());
+            while (len > 1.0 + 1e-9 && st < kMaxStages - 1) {
+                stab_len.push_back(len);
+                stab_blk.push_back(len / static_cast<double>(l));
                 len = len * (q + 1.0) / static_cast<double>(l);
                 ++st;
             }
-            it.stage_len[st] = len;
+            stab_len.push_back(len);
             it.nstage_tab = (len > 1.0 + 1e-9) ? -1 : st;
         }
         const size_t taps_bytes = static_cast<size_t>(win->w + 1) * sizeof(double);
@@ -316,6 +321,16 @@ Plan::Plan(int64_t n, int64_t k, int64_t l, double q, double delta, bool c128, i
             big_b_iters_.push_back(m);
         b_max_ = std::max(b_max_, ip.b);
         budget_max_ = std::max(budget_max_, ip.budget);
+    }
+    stage_tab_.reset(stab_len.size() + stab_blk.size() + 1);
+    std::vector<double> stab(stab_len);
+    stab.insert(stab.end(), stab_blk.begin(), stab_blk.end());
+    stab.push_back(0.0);
+    MSFFT_CUDA(cudaMemcpy(stage_tab_.get(), stab.data(), stab.size() * sizeof(double),
+                          cudaMemcpyHostToDevice));
+    for (int m = 0; m < sched_.iterations; ++m) {
+        P.it[m].stage_len = stage_tab_.get() + stage_off[m][0];
+        P.it[m].stage_blk = stage_tab_.get() + stab_len.size() + stage_off[m][1];
     }
     int64_t rounds_max = 0;
     for (const auto& ip : sched_.iters)

@@ -191,6 +191,7 @@ private:
     // first (compact_gather_kernel), then encode from those (coalesced)
     bool compact_gather_ = true;
     DeviceBuffer<GatherIv> givs_;
+    DeviceBuffer<double> stage_tab_;  // locate stage tables (DevIter::stage_len/blk)
     int n_givs_ = 0;
     int64_t giv_max_len_ = 0;
     mutable DeviceBuffer<unsigned char> xcompact_;

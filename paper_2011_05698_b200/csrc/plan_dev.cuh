@@ -18,14 +18,18 @@ constexpr int kMaxTaus = 1024;
 constexpr int kEncRounds = 8;       // rounds fused into one gather pass
 constexpr int kEncThreads = 256;    // encode CTA size
 constexpr int kDecThreads = 256;    // decode CTA size
-constexpr int kMaxStageTable = 24;  // precomputed locate stage lengths
+constexpr int kMaxStageTable = 64;  // locate stages the decode keeps in shared memory
+constexpr int kMaxStages = 4096;    // longest precomputed locate stage table
 
 struct DevIter {
     // Locate region lengths of every stage, len_0 = L, len_{k+1} =
     // len_k*(q+1)/l, and block widths len_k/l (locate.cpp:64, 78), computed on
     // the host with the same IEEE operations; nstage_tab = stages the locate
-    // loop runs (len_k > 1 + 1e-9), or -1 if the table is too short.
-    double stage_len[kMaxStageTable], stage_blk[kMaxStageTable];
+    // loop runs (len_k > 1 + 1e-9), or -1 if it exceeds kMaxStages.
+    // (device arrays owned by the plan: nstage_tab + 1 lengths, nstage_tab
+    // block widths)
+    const double* stage_len;
+    const double* stage_blk;
     int32_t nstage_tab, pad0_;
     int64_t b, l_width, w, h;
     int64_t budget, k_m;
