@@ -844,9 +844,15 @@ void Plan::run_chunk(int64_t batch, const void* d_x, int64_t x_stride, const int
         if (!wide_)
             wide_ = std::make_unique<WideDecoder>(dplan_, sched_.acc_cap, b_max_, budget_max_,
                                                   rounds_max_);
-        int32_t bad = 0;  // unvalidated non-finite input: the call throws, skip the decode
-        MSFFT_CUDA(cudaMemcpyAsync(&bad, flags_.get() + 1, sizeof(bad), cudaMemcpyDeviceToHost, st));
-        MSFFT_CUDA(cudaStreamSynchronize(st));
+        // a non-finite sample found by this call's validation makes the call
+        // throw: skip the decode (without validation the flag is clear --
+        // check_flags resets it after every call -- and the decode is
+        // enqueued without waiting for the encode)
+        int32_t bad = 0;
+        if (validate) {
+            MSFFT_CUDA(cudaMemcpyAsync(&bad, flags_.get() + 1, sizeof(bad), cudaMemcpyDeviceToHost, st));
+            MSFFT_CUDA(cudaStreamSynchronize(st));
+        }
         if (!bad) {
             const int iters = sched_.iterations;
             const int64_t k = sched_.k, vps = dplan_.values_per_signal;

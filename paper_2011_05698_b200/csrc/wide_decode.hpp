@@ -45,9 +45,9 @@ public:
     ~WideDecoder();
 
 private:
-    // the fixed kernel sequence of one decode (outputs to internal buffers)
+    // the fixed kernel sequence of one decode (K7 writes out_f/out_c/out_count)
     void enqueue(double2* y, const int64_t* sigma, const int64_t* sigma_inv, int32_t* err,
-                 cudaStream_t st);
+                 int64_t* out_f, double2* out_c, int64_t* out_count, cudaStream_t st);
     void select_kth(const uint64_t* key, int64_t n_max, const int32_t* n_dev, int64_t kth_host,
                     const int32_t* kth_dev, cudaStream_t st);
     void compact_selected(const uint64_t* key, int64_t n_max, const int32_t* n_dev,
@@ -79,11 +79,10 @@ private:
     DeviceBuffer<int64_t> cand_f_, newf_;
     DeviceBuffer<int32_t> f6cnt_, f6cur_, f6start_;  // K6 bucket sort of large budgets
     // outputs, copied to the caller's buffers after the graph
-    DeviceBuffer<int64_t> out_f_, out_count_;
-    DeviceBuffer<double2> out_c_;
     // one instantiated CUDA graph per (y, sigma, sigma_inv, err) tuple: the
     // ~40 launches per iteration replay without per-launch host overhead
-    using GraphKey = std::tuple<const void*, const void*, const void*, const void*>;
+    using GraphKey = std::tuple<const void*, const void*, const void*, const void*, const void*,
+                                const void*, const void*>;
     std::map<GraphKey, cudaGraphExec_t> graphs_;
     bool use_graphs_ = true;  // MSFFT_WIDE_GRAPH=0 launches eagerly
     bool pdl_ = true;         // MSFFT_WIDE_PDL=0: plain stream order between the kernels
