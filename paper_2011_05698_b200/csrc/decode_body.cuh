@@ -104,6 +104,128 @@ __device__ __forceinline__ double2 unit_root(int64_t n, double inv_n, int64_t e)
     return make_double2(c, s);
 }
 
+// ---- the locate stage chain (locate_frequency's narrowing loop,
+// proj/src/locate.cpp:63-123) for one ranked bucket, shortest form.  The
+// stage count and every stage's operands are known up front: each stage
+// first loads the next stage's phase code and phase (clamped index, no
+// branch), and per lane the next block offsets (j + 0.5) * rblk, the u_min
+// steps (j - q/2) * rblk and tau/n are formed off the chain; the argmin
+// carries the winner's step.  With the group size and the blocks per lane
+// fixed at compile time a stage is one basic block, so those loads and
+// products overlap the chain center -> phase -> distance -> argmin -> u_min.
+// Every value equals the reference's: tau/n and the 1/n scalings are exact
+// powers of two, so (center * tau/n) - trunc(..) is fmod(center * tau, n) /
+// n, and round(f * 2pi) equals round(round(x * 2pi) / n) (locate.cpp:19-23).
+//   phi/code: the bucket's per-stage phase and phase code (stage s at [s-1]);
+//   st_blk[s-1]: block width of stage s; st_tau[s]: tau of stage s.
+// Lanes glane = 0..GSZ-1 of the group hold blocks glane + i*GSZ.  Returns
+// the final u_min; clears `ok` on a nullopt / throwing phase and raises
+// kDecErrPhaseZero in *err for the latter.
+template <int GSZ, int JPL, class PhiP, class CodeP, class BlkP, class TauP>
+__device__ __forceinline__ double locate_stages(double u_min, int nst, bool live, bool& ok,
+                                                int glane, int64_t lcfg, double hq, double inv_n,
+                                                PhiP phi, CodeP code_p, BlkP st_blk, TauP st_tau,
+                                                int32_t* err) {
+    double jd[JPL];
+    bool jv[JPL];
+#pragma unroll
+    for (int i = 0; i < JPL; ++i) {
+        const int64_t j = glane + static_cast<int64_t>(i) * GSZ;
+        jv[i] = j < lcfg;
+        jd[i] = static_cast<double>(j);
+    }
+    const int last = nst > 0 ? nst - 1 : 0;
+    int code = live && nst > 0 ? code_p[0] : 1;
+    double ph = live && nst > 0 ? phi[0] : 0.0;
+    double rb = st_blk[0];
+    double offc[JPL], step[JPL];
+#pragma unroll
+    for (int i = 0; i < JPL; ++i) {
+        offc[i] = (jd[i] + 0.5) * rb;
+        step[i] = (jd[i] - hq) * rb;
+    }
+    double step0 = (0.0 - hq) * rb;  // block 0: every distance NaN
+    double ton = static_cast<double>(st_tau[1]) * inv_n;
+    bool err2 = false;
+    for (int stage = 1; stage <= nst; ++stage) {
+        // the next stage's operands (the last stage reloads its own)
+        const int sn = stage < nst ? stage : last;
+        const int code_n = live ? static_cast<int>(code_p[sn]) : 1;
+        const double phi_n = live ? static_cast<double>(phi[sn]) : 0.0;
+        const double rb_n = st_blk[sn];
+        const int64_t tau_n = st_tau[sn + 1];
+        // this stage's chain
+        double best_d = INFINITY, best_step = step0;
+        int best_j = 0x7fffffff;
+#pragma unroll
+        for (int i = 0; i < JPL; ++i) {
+            const double y = (u_min + offc[i]) * ton;
+            double f = y - trunc(y);
+            f = f < 0 ? f + 1.0 : f;
+            const double d = circular_phase_distance(f * kTwoPi, ph);
+            const bool better = jv[i] && d < best_d;
+            best_d = better ? d : best_d;
+            best_j = better ? glane + i * GSZ : best_j;
+            best_step = better ? step[i] : best_step;
+        }
+        // 1: locate_frequency returns nullopt; 2: phase_of throws
+        err2 = err2 || (ok && code == 2);
+        ok = ok && code == 0;
+        // lowest block index wins ties (strict < in ascending order)
+#pragma unroll
+        for (int o = GSZ >> 1; o > 0; o >>= 1) {
+            const double od = __shfl_xor_sync(0xffffffffu, best_d, o);
+            const int oj = __shfl_xor_sync(0xffffffffu, best_j, o);
+            const double os = __shfl_xor_sync(0xffffffffu, best_step, o);
+            const bool take = od < best_d || (od == best_d && oj < best_j);
+            best_d = take ? od : best_d;
+            best_j = take ? oj : best_j;
+            best_step = take ? os : best_step;
+        }
+        u_min = u_min + best_step;
+        code = code_n;
+        ph = phi_n;
+#pragma unroll
+        for (int i = 0; i < JPL; ++i) {
+            offc[i] = (jd[i] + 0.5) * rb_n;
+            step[i] = (jd[i] - hq) * rb_n;
+        }
+        step0 = (0.0 - hq) * rb_n;
+        ton = static_cast<double>(tau_n) * inv_n;
+    }
+    if (err2 && glane == 0) atomicCAS(err, 0, kDecErrPhaseZero);
+    return u_min;
+}
+
+// locate_stages covers group sizes 2..16 with up to 4 blocks per lane
+__device__ __forceinline__ bool locate_fast_ok(int gsz, int64_t jpl) {
+    return jpl <= 4 && gsz >= 2 && gsz <= 16;
+}
+
+template <class PhiP, class CodeP, class BlkP, class TauP>
+__device__ __forceinline__ double locate_stages_dispatch(int gsz, int64_t jpl, double u_min,
+                                                         int nst, bool live, bool& ok, int glane,
+                                                         int64_t lcfg, double hq, double inv_n,
+                                                         PhiP phi, CodeP code, BlkP st_blk,
+                                                         TauP st_tau, int32_t* err) {
+#define MSFFT_LOCATE_G(G)                                                                  \
+    do {                                                                                   \
+        if (jpl == 1)                                                                      \
+            return locate_stages<G, 1>(u_min, nst, live, ok, glane, lcfg, hq, inv_n, phi, code, \
+                                       st_blk, st_tau, err);                               \
+        if (jpl == 2)                                                                      \
+            return locate_stages<G, 2>(u_min, nst, live, ok, glane, lcfg, hq, inv_n, phi, code, \
+                                       st_blk, st_tau, err);                               \
+        return locate_stages<G, 4>(u_min, nst, live, ok, glane, lcfg, hq, inv_n, phi, code,    \
+                                   st_blk, st_tau, err);                                   \
+    } while (0)
+    if (gsz == 16) MSFFT_LOCATE_G(16);
+    if (gsz == 8) MSFFT_LOCATE_G(8);
+    if (gsz == 4) MSFFT_LOCATE_G(4);
+    MSFFT_LOCATE_G(2);
+#undef MSFFT_LOCATE_G
+}
+
 // Barrier of a decode group: the whole CTA (bar_id 0, __syncthreads) or a
 // warp-aligned group of kThreads threads on named barrier bar_id.
 template <int kThreads>
@@ -433,117 +555,15 @@ __device__ __forceinline__ void decode_signal(const DevPlan& plan, const DecLayo
             double len = Ld;
             const int nst = nst_r;  // host-precomputed stage lengths (or -1)
             const int64_t jpl = (lcfg + gsz - 1) / gsz;  // blocks per lane
-            if (nst >= 0 && nst < nr && jpl <= 4 && gsz >= 2 && gsz <= 16) {
-                // the usual case, shortest chain.  Stage operands are known up
-                // front: each stage first loads the next stage's (clamped
-                // index, no branch), and per lane the next block offsets
-                // (j + 0.5) * rblk, the u_min steps (j - q/2) * rblk and tau/n
-                // are formed off the chain; the argmin carries the winner's
-                // step.  With the group size and blocks per lane fixed at
-                // compile time a stage is one basic block, so those loads and
-                // products overlap the chain center -> phase -> distance ->
-                // argmin -> u_min + step.  Every value equals the
-                // reference's: tau/n and the 1/n scalings are exact powers of
-                // two, so (center * tau/n) - trunc(..) is fmod(center * tau,
-                // n) / n, and round(f * 2pi) is the reference's
-                // round(round(x * 2pi) / n) (locate.cpp:19-23).
-                const auto run = [&](auto gtag, auto jtag) {
-                    constexpr int GSZ = decltype(gtag)::value;
-                    constexpr int JPL = decltype(jtag)::value;
-                    double jd[JPL];
-                    bool jv[JPL];
-#pragma unroll
-                    for (int i = 0; i < JPL; ++i) {
-                        const int64_t j = glane + static_cast<int64_t>(i) * GSZ;
-                        jv[i] = j < lcfg;
-                        jd[i] = static_cast<double>(j);
-                    }
-                    const int64_t pe0 = rank * ns;
-                    const int64_t pe_last = pe0 + (nst > 0 ? nst - 1 : 0);
-                    int code = live && nst > 0 ? S.pcode[pe0] : 1;
-                    double ph = live && nst > 0 ? S.phi[pe0] : 0.0;
-                    double rb = sh.st_blk[0];
-                    double offc[JPL], step[JPL];
-#pragma unroll
-                    for (int i = 0; i < JPL; ++i) {
-                        offc[i] = (jd[i] + 0.5) * rb;
-                        step[i] = (jd[i] - hq) * rb;
-                    }
-                    double step0 = (0.0 - hq) * rb;  // block 0: all distances NaN
-                    double ton = static_cast<double>(tau_at(1)) * inv_n_r;
-                    bool err2 = false;
-                    for (int stage = 1; stage <= nst; ++stage) {
-                        // the next stage's operands (the last stage reloads its own)
-                        const int64_t pn = min(pe0 + stage, pe_last);
-                        const int sn = stage < nst ? stage : nst - 1;
-                        const int code_n = live ? S.pcode[pn] : 1;
-                        const double phi_n = live ? S.phi[pn] : 0.0;
-                        const double rb_n = sh.st_blk[sn];
-                        const int64_t tau_n = tau_at(sn + 1);
-                        // this stage's chain
-                        double best_d = INFINITY, best_step = step0;
-                        int best_j = 0x7fffffff;
-#pragma unroll
-                        for (int i = 0; i < JPL; ++i) {
-                            const double y = (u_min + offc[i]) * ton;
-                            double f = y - trunc(y);
-                            f = f < 0 ? f + 1.0 : f;
-                            const double d = circular_phase_distance(f * kTwoPi, ph);
-                            const bool better = jv[i] && d < best_d;
-                            best_d = better ? d : best_d;
-                            best_j = better ? glane + i * GSZ : best_j;
-                            best_step = better ? step[i] : best_step;
-                        }
-                        // 1: locate_frequency returns nullopt; 2: phase_of throws
-                        err2 = err2 || (ok && code == 2);
-                        ok = ok && code == 0;
-                        // lowest block index wins ties (strict < in ascending order)
-#pragma unroll
-                        for (int o = GSZ >> 1; o > 0; o >>= 1) {
-                            const double od = __shfl_xor_sync(0xffffffffu, best_d, o);
-                            const int oj = __shfl_xor_sync(0xffffffffu, best_j, o);
-                            const double os = __shfl_xor_sync(0xffffffffu, best_step, o);
-                            const bool take = od < best_d || (od == best_d && oj < best_j);
-                            best_d = take ? od : best_d;
-                            best_j = take ? oj : best_j;
-                            best_step = take ? os : best_step;
-                        }
-                        u_min = u_min + best_step;
-                        code = code_n;
-                        ph = phi_n;
-#pragma unroll
-                        for (int i = 0; i < JPL; ++i) {
-                            offc[i] = (jd[i] + 0.5) * rb_n;
-                            step[i] = (jd[i] - hq) * rb_n;
-                        }
-                        step0 = (0.0 - hq) * rb_n;
-                        ton = static_cast<double>(tau_n) * inv_n_r;
-                    }
-                    if (err2 && glane == 0) atomicCAS(A.err, 0, kDecErrPhaseZero);
-                    if (nst > 0) len = sh.st_len[nst];
-                };
-                using std::integral_constant;
+            if (nst >= 0 && nst < nr && locate_fast_ok(gsz, jpl)) {
 #ifdef MSFFT_DECODE_PROFILE
                 const long long t_chain0 = clock64();
 #endif
-#define MSFFT_RUN_G(G)                                                   \
-    do {                                                                 \
-        if (jpl == 1)                                                    \
-            run(integral_constant<int, G>{}, integral_constant<int, 1>{}); \
-        else if (jpl == 2)                                               \
-            run(integral_constant<int, G>{}, integral_constant<int, 2>{}); \
-        else                                                             \
-            run(integral_constant<int, G>{}, integral_constant<int, 4>{}); \
-    } while (0)
-                if (gsz == 16)
-                    MSFFT_RUN_G(16);
-                else if (gsz == 8)
-                    MSFFT_RUN_G(8);
-                else if (gsz == 4)
-                    MSFFT_RUN_G(4);
-                else
-                    MSFFT_RUN_G(2);
-#undef MSFFT_RUN_G
+                const int64_t pe0 = rank * ns;
+                u_min = locate_stages_dispatch(gsz, jpl, u_min, nst, live, ok, glane, lcfg, hq,
+                                               inv_n_r, &S.phi[pe0], &S.pcode[pe0], sh.st_blk,
+                                               sh.st_tau, A.err);
+                if (nst > 0) len = sh.st_len[nst];
 #ifdef MSFFT_DECODE_PROFILE
                 if (tid == 0 && s < 1)
                     printf("DECPROF chain m=%d nst=%d jpl=%lld gsz=%d cycles=%lld (%.0f per stage)\n", m,

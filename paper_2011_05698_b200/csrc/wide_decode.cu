@@ -804,6 +804,19 @@ k5_locate(const DevPlan* __restrict__ P, int m, const int64_t* __restrict__ sigm
     const int gsz = lcfg > 16 ? 32 : (lcfg > 8 ? 16 : (lcfg > 4 ? 8 : 4));
     const int lane = threadIdx.x & 31;
     const int glane = lane & (gsz - 1);
+    // stage tables in shared memory for the short chain (decode_body.cuh
+    // locate_stages), when the schedule fits them
+    __shared__ double s_blk[kMaxStageTable];
+    __shared__ int64_t s_tau[kMaxStageTable + 1];
+    const int nst_all = it.nstage_tab;
+    const int64_t jpl = (lcfg + gsz - 1) / gsz;
+    const bool fast = nst_all >= 0 && nst_all < kMaxStageTable && nst_all < nr &&
+                      locate_fast_ok(gsz, jpl);
+    if (fast) {
+        if (threadIdx.x < nst_all) s_blk[threadIdx.x] = it.stage_blk[threadIdx.x];
+        if (threadIdx.x <= nst_all) s_tau[threadIdx.x] = taus[threadIdx.x];
+        __syncthreads();
+    }
     const int64_t gid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / gsz;
     const int64_t ngroups = (static_cast<int64_t>(gridDim.x) * blockDim.x) / gsz;
     const int64_t rounds_up = (budget + ngroups - 1) / ngroups * ngroups;
@@ -822,7 +835,14 @@ k5_locate(const DevPlan* __restrict__ P, int m, const int64_t* __restrict__ sigm
         double len = Ld;
         int stage = 0;
         const int nst = it.nstage_tab;
-        while (nst >= 0 ? stage < nst : len > 1.0 + 1e-9) {
+        if (fast) {
+            u_min = locate_stages_dispatch(gsz, jpl, u_min, nst, live, ok, glane, lcfg, q / 2.0,
+                                           inv_n, phi_t + rank * ns, pcode + rank * ns, s_blk,
+                                           s_tau, err);
+            if (nst > 0) len = it.stage_len[nst];
+            stage = nst;  // the loop below has nothing left
+        }
+        while (!fast && (nst >= 0 ? stage < nst : len > 1.0 + 1e-9)) {
             ++stage;
             if (stage >= nr) {
                 if (ok && glane == 0) atomicCAS(err, 0, kDecErrRounds);
