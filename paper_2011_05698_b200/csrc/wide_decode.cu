@@ -1108,12 +1108,17 @@ __global__ void k6_merge_new(const int64_t* __restrict__ AF, const int32_t* __re
 // f" flags, then the merge into the ascending accumulated list.
 constexpr int kSmallK6 = 1024;
 constexpr int64_t kSmallK6Acc = 16384;  // accumulated-list cap for the one-CTA merge
+constexpr int64_t kK6StageMax = 8192;   // accumulated f staged in its shared memory
 __global__ void __launch_bounds__(kSmallK6)
 k6_small(const DevPlan* __restrict__ P, int m, const int64_t* __restrict__ cand_f,
-         const double2* __restrict__ cand_v, const int64_t* __restrict__ AF,
+         const double2* __restrict__ cand_v, const int64_t* __restrict__ AF_g,
          const double2* __restrict__ AC, int32_t* __restrict__ scal, int64_t* __restrict__ NF,
-         double2* __restrict__ NC) {
+         double2* __restrict__ NC, int32_t stage_cap) {
     pdl_entry();
+    // the accumulated f list is binary-searched per accepted f: staged in
+    // shared memory (dynamic, stage_cap entries) when it fits, so the
+    // searches are ~30-cycle steps instead of L2 round trips
+    extern __shared__ int64_t s_af[];
     __shared__ int64_t sf[kSmallK6];     // f by rank, then f at sorted position
     __shared__ int32_t byf[kSmallK6];    // rank at sorted position
     __shared__ double2 rsum[kSmallK6];   // run sums at run starts
@@ -1127,6 +1132,10 @@ k6_small(const DevPlan* __restrict__ P, int m, const int64_t* __restrict__ cand_
     const int64_t fr = tid < budget ? cand_f[tid] : -1;
     __syncthreads();
     const int an = s_acc;
+    const bool staged = an <= stage_cap;
+    if (staged)
+        for (int j = tid; j < an; j += kSmallK6) s_af[j] = AF_g[j];
+    const int64_t* AF = staged ? s_af : AF_g;
     // accepted ranks in (f, rank) order: a bitonic sort of the unique keys
     // f * 1024 + rank (rejected ranks sort last); newf is free until later
     static_assert(kSmallK6 == 1024, "one key per thread, rank in 10 bits");
@@ -1318,6 +1327,8 @@ WideDecoder::WideDecoder(const DevPlan& plan, int64_t acc_cap, int64_t b_max, in
     if (const char* e = std::getenv("MSFFT_WIDE_GRAPH")) use_graphs_ = std::atoi(e) != 0;
     if (const char* e = std::getenv("MSFFT_WIDE_PDL")) pdl_ = std::atoi(e) != 0;
     // kernel attributes are set before any capture
+    k6_stage_cap_ = std::min<int64_t>(acc_cap_, kK6StageMax);
+    smem_attr(k6_small, static_cast<size_t>(k6_stage_cap_) * sizeof(int64_t));
 }
 
 void WideDecoder::select_kth(const uint64_t* key, int64_t n_max, const int32_t* n_dev,
@@ -1445,8 +1456,9 @@ void WideDecoder::enqueue(double2* y, const int64_t* sigma, const int64_t* sigma
         MSFFT_LAUNCH_CHECK("wide K4/K5");
         // ---- K6
         if (budget <= kSmallK6 && acc_cap_ <= kSmallK6Acc) {
-            launch_pdl(pdl_, k6_small, 1, kSmallK6, 0, st, P, m, cand_f_.get(), cand_v_.get(), AF, AC, scal_.get(),
-                                             acc_f_[nxt].get(), acc_c_[nxt].get());
+            launch_pdl(pdl_, k6_small, 1, kSmallK6, k6_stage_cap_ * sizeof(int64_t), st, P, m,
+                       cand_f_.get(), cand_v_.get(), AF, AC, scal_.get(), acc_f_[nxt].get(),
+                       acc_c_[nxt].get(), static_cast<int32_t>(k6_stage_cap_));
         } else {
             if (budget >= kF6BucketMin) {
                 int nbits = 0;

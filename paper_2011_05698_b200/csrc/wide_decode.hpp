@@ -84,6 +84,7 @@ private:
     using GraphKey = std::tuple<const void*, const void*, const void*, const void*, const void*,
                                 const void*, const void*>;
     std::map<GraphKey, cudaGraphExec_t> graphs_;
+    int64_t k6_stage_cap_ = 0;  // k6_small: accumulated f staged in shared memory
     bool use_graphs_ = true;  // MSFFT_WIDE_GRAPH=0 launches eagerly
     bool pdl_ = true;         // MSFFT_WIDE_PDL=0: plain stream order between the kernels
 };
