@@ -358,6 +358,10 @@ Plan::Plan(int64_t n, int64_t k, int64_t l, double q, double delta, bool c128, i
     MSFFT_CUDA(cudaStreamCreateWithPriority(&dec_stream_, cudaStreamDefault, hi_prio));
     MSFFT_CUDA(cudaEventCreateWithFlags(&ev_chunk_, cudaEventDisableTiming));
     MSFFT_CUDA(cudaEventCreateWithFlags(&ev_dec_done_, cudaEventDisableTiming));
+    for (auto& e : ev_group_) MSFFT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    if (const char* e = std::getenv("MSFFT_WIDE_OVERLAP_MIN")) wide_overlap_min_ = std::atoll(e);
+    if (const char* e = std::getenv("MSFFT_WIDE_GROUPS"))
+        wide_groups_ = std::max(1, std::min(kMaxWideGroups, std::atoi(e)));
     if (const char* e = std::getenv("MSFFT_OVERLAP_CHUNK")) overlap_chunk_ = std::atoll(e);
     if (const char* e = std::getenv("MSFFT_FUSED")) fused_enabled_ = std::atoi(e) != 0;
     if (const char* e = std::getenv("MSFFT_FUSED_CHUNK")) fused_chunk_ = std::max(1LL, std::atoll(e));
@@ -415,6 +419,8 @@ Plan::~Plan() {
     cudaSetDevice(device_);
     for (auto& kv : gated_graphs_map_)
         if (kv.second) cudaGraphExecDestroy(kv.second);
+    for (auto& e : ev_group_)
+        if (e) cudaEventDestroy(e);
     if (own_stream_) cudaStreamDestroy(own_stream_);
     if (copy_stream_) cudaStreamDestroy(copy_stream_);
     if (ev_start_) cudaEventDestroy(ev_start_);
@@ -568,9 +574,11 @@ const Plan::FusedSet& Plan::fused_for(int64_t batch, int slot) {
 // K2 for the iterations with b > 256 (the encode's fused epilogue does the
 // rest): their b-point transforms and the 1/n scale, as few launches as the
 // sizes allow.
-void Plan::bucket_ffts(double2* y, int64_t batch, cudaStream_t st, const FftGate* gate) const {
+void Plan::bucket_ffts(double2* y, int64_t batch, cudaStream_t st, const FftGate* gate, int m0,
+                       int m1) const {
     std::vector<FftSet> sets;
     for (int m : big_b_iters_) {
+        if (m < m0 || (m1 >= 0 && m >= m1)) continue;
         const DevIter& di = dplan_.it[m];
         sets.push_back(FftSet{di.yoff, di.b, di.nrounds, m});
     }
@@ -716,6 +724,61 @@ void Plan::enqueue_gated(int64_t batch, const void* d_x, int64_t x_stride, const
                         d_out_f, d_out_c, d_out_count, flags_.get(), gate, gate + iters, st);
 }
 
+// Large single signals (wide decode): the encode and the bucket FFTs go out
+// in iteration groups [0,1), [1,2), [2,4), [4,8), ... (the early iterations
+// have the large b and the small windows, so they encode fastest), each
+// group ending in an event; the wide decode of a group's iterations runs on
+// the high-priority decode stream once its event fires, so the decode of
+// the early iterations overlaps the encode of the later ones.
+void Plan::run_wide_overlapped(int64_t batch, const void* d_x, int64_t x_stride,
+                               const int64_t* d_sig, const int64_t* d_sig_inv, int64_t* d_out_f,
+                               double2* d_out_c, int64_t* d_out_count, bool validate,
+                               const DevPlan& P, cudaStream_t st) {
+    if (validate) {
+        // a non-finite sample makes the call throw: nothing to decode (the
+        // scan was launched by run_chunk; this waits for it alone)
+        int32_t bad = 0;
+        MSFFT_CUDA(cudaMemcpyAsync(&bad, flags_.get() + 1, sizeof(bad), cudaMemcpyDeviceToHost, st));
+        MSFFT_CUDA(cudaStreamSynchronize(st));
+        if (bad) return;
+    }
+    if (!wide_)
+        wide_ = std::make_unique<WideDecoder>(dplan_, sched_.acc_cap, b_max_, budget_max_,
+                                              rounds_max_);
+    const TaskSet& ts = tasks_for(batch);
+    const int iters = sched_.iterations;
+    const int64_t k = sched_.k, vps = dplan_.values_per_signal;
+    std::vector<std::pair<int, int>> groups;
+    for (int m0 = 0; m0 < iters;) {
+        const int m1 = static_cast<int>(groups.size()) + 1 >= wide_groups_
+                           ? iters
+                           : std::min(iters, m0 == 0 ? 1 : 2 * m0);
+        groups.emplace_back(m0, m1);
+        m0 = m1;
+    }
+    // tasks are iteration-major (append_tasks)
+    int64_t t0 = 0;
+    for (size_t g = 0; g < groups.size(); ++g) {
+        const auto [m0, m1] = groups[g];
+        int64_t t1 = t0;
+        while (t1 < ts.count && ts.host[t1].m < m1) ++t1;
+        launch_encode(P, ts.d.get() + t0, t1 - t0, d_x, c128_, x_stride, batch, d_sig, y_.get(),
+                      enc_smem_ + enc_smem_pad_, st);
+        bucket_ffts(y_.get(), batch, st, nullptr, m0, m1);
+        MSFFT_CUDA(cudaEventRecord(ev_group_[g], st));
+        t0 = t1;
+    }
+    for (int64_t s = 0; s < batch; ++s)
+        for (size_t g = 0; g < groups.size(); ++g) {
+            if (s == 0) MSFFT_CUDA(cudaStreamWaitEvent(dec_stream_, ev_group_[g], 0));
+            wide_->run_range(y_.get() + s * vps, d_sig + s * iters, d_sig_inv + s * iters,
+                             d_out_f + s * k, d_out_c + s * k, d_out_count + s, flags_.get(),
+                             dec_stream_, groups[g].first, groups[g].second);
+        }
+    MSFFT_CUDA(cudaEventRecord(ev_dec_done_, dec_stream_));
+    MSFFT_CUDA(cudaStreamWaitEvent(st, ev_dec_done_, 0));
+}
+
 void Plan::run_chunk(int64_t batch, const void* d_x, int64_t x_stride, const int64_t* d_sig,
                      const int64_t* d_sig_inv, int64_t* d_out_f, double2* d_out_c,
                      int64_t* d_out_count, bool validate, cudaStream_t st,
@@ -819,6 +882,12 @@ void Plan::run_chunk(int64_t batch, const void* d_x, int64_t x_stride, const int
         }
         MSFFT_CUDA(cudaEventRecord(ev_dec_done_, dec_stream_));
         MSFFT_CUDA(cudaStreamWaitEvent(st, ev_dec_done_, 0));
+        return;
+    }
+    if (!traced && !opt.stage_times && !opt.force_serial && lay_.big && batch <= wide_max_batch_ &&
+        wide_groups_ > 1 && batch * imap_.per_signal >= wide_overlap_min_) {
+        run_wide_overlapped(batch, d_x, x_stride, d_sig, d_sig_inv, d_out_f, d_out_c, d_out_count,
+                            validate, P, st);
         return;
     }
     const TaskSet& ts = tasks_for(batch);

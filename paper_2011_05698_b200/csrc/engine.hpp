@@ -144,8 +144,13 @@ private:
     bool split_tasks(int64_t n_tasks) const;
     void launch_compact_gather(int64_t batch, const void* d_x, int64_t x_stride,
                                const int64_t* d_sig, void* out, cudaStream_t st) const;
-    void bucket_ffts(double2* y, int64_t batch, cudaStream_t st,
-                     const FftGate* gate = nullptr) const;
+    // iterations [m0, m1) only (m1 < 0: to the end)
+    void bucket_ffts(double2* y, int64_t batch, cudaStream_t st, const FftGate* gate = nullptr,
+                     int m0 = 0, int m1 = -1) const;
+    void run_wide_overlapped(int64_t batch, const void* d_x, int64_t x_stride,
+                             const int64_t* d_sig, const int64_t* d_sig_inv, int64_t* d_out_f,
+                             double2* d_out_c, int64_t* d_out_count, bool validate,
+                             const DevPlan& P, cudaStream_t st);
     void upload_sigmas(int64_t batch, const uint64_t* seeds, cudaStream_t st);
     void check_flags(cudaStream_t st);
     void run_chunk(int64_t batch, const void* d_x, int64_t x_stride, const int64_t* d_sig,
@@ -223,6 +228,14 @@ private:
     cudaEvent_t ev_stage_[4] = {nullptr, nullptr, nullptr, nullptr};
     cudaStream_t dec_stream_ = nullptr;  // high-priority decode stream (overlap)
     cudaEvent_t ev_chunk_ = nullptr, ev_dec_done_ = nullptr;
+    // wide decode overlapped with the encode: iteration groups (MSFFT_WIDE_GROUPS,
+    // 1 = encode everything first)
+    static constexpr int kMaxWideGroups = 8;
+    int wide_groups_ = 5;
+    // ... only when the encode has this many samples to gather (C5: 18.7 M;
+    // C3's 1.2 M encode is too short to pay for the extra graph launches)
+    int64_t wide_overlap_min_ = int64_t{1} << 22;
+    cudaEvent_t ev_group_[kMaxWideGroups] = {};
     int64_t overlap_chunk_ = 0;          // signals per encode/decode sub-chunk (0 = serial)
     double stage_ms_[3] = {0, 0, 0};
     int64_t h2d_bytes_ = 0, d2h_bytes_ = 0;

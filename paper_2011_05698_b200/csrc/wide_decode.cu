@@ -1363,15 +1363,16 @@ WideDecoder::~WideDecoder() {
     for (auto& kv : graphs_) cudaGraphExecDestroy(kv.second);
 }
 
-void WideDecoder::run(double2* y, const int64_t* sigma, const int64_t* sigma_inv, int64_t* out_f,
-                      double2* out_c, int64_t* out_count, int32_t* err, cudaStream_t st) {
+void WideDecoder::run_range(double2* y, const int64_t* sigma, const int64_t* sigma_inv,
+                            int64_t* out_f, double2* out_c, int64_t* out_count, int32_t* err,
+                            cudaStream_t st, int m0, int m1) {
     if (!use_graphs_) {
-        enqueue(y, sigma, sigma_inv, err, out_f, out_c, out_count, st);
+        enqueue(y, sigma, sigma_inv, err, out_f, out_c, out_count, st, m0, m1);
     } else {
         // K7 writes the caller's outputs directly, so they are part of the key
-        const GraphKey key{y, sigma, sigma_inv, err, out_f, out_c, out_count};
+        const GraphKey key{y, sigma, sigma_inv, err, out_f, out_c, out_count, m0, m1};
         auto it = graphs_.find(key);
-        if (it == graphs_.end() && graphs_.size() >= 8) {
+        if (it == graphs_.end() && graphs_.size() >= 16) {
             // bounded: callers that pass fresh buffers every call
             // recapture instead of accumulating executable graphs
             MSFFT_CUDA(cudaStreamSynchronize(st));
@@ -1383,7 +1384,7 @@ void WideDecoder::run(double2* y, const int64_t* sigma, const int64_t* sigma_inv
             MSFFT_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
             cudaGraph_t g = nullptr;
             MSFFT_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
-            enqueue(y, sigma, sigma_inv, err, out_f, out_c, out_count, cap);
+            enqueue(y, sigma, sigma_inv, err, out_f, out_c, out_count, cap, m0, m1);
             MSFFT_CUDA(cudaStreamEndCapture(cap, &g));
             cudaGraphExec_t ex = nullptr;
             MSFFT_CUDA(cudaGraphInstantiate(&ex, g, 0));
@@ -1396,16 +1397,17 @@ void WideDecoder::run(double2* y, const int64_t* sigma, const int64_t* sigma_inv
 }
 
 void WideDecoder::enqueue(double2* y, const int64_t* sigma, const int64_t* sigma_inv, int32_t* err,
-                          int64_t* out_f, double2* out_c, int64_t* out_count, cudaStream_t st) {
+                          int64_t* out_f, double2* out_c, int64_t* out_count, cudaStream_t st,
+                          int m0, int m1) {
     const DevPlan& H = hplan_;
     const DevPlan* P = dplan_.get();
     int32_t* acc_n = scal_.get();       // [0]
     int32_t* new_n = scal_.get() + 1;   // [1]
     int32_t* kth = scal_.get() + 2;     // [2]
     int32_t* naccepted = scal_.get() + 4;
-    zero_async(pdl_, scal_.get(), 8 * sizeof(int32_t), st);
+    if (m0 == 0) zero_async(pdl_, scal_.get(), 8 * sizeof(int32_t), st);
     const unsigned gA = grid_of(acc_cap_ * 3);
-    for (int m = 0; m < H.iters; ++m) {
+    for (int m = m0; m < m1; ++m) {
         const DevIter& it = H.it[m];
         const int64_t b = it.b, nr = it.nrounds, budget = it.budget;
         double2* Y = y + it.yoff;
@@ -1500,6 +1502,7 @@ void WideDecoder::enqueue(double2* y, const int64_t* sigma, const int64_t* sigma
         }
         MSFFT_LAUNCH_CHECK("wide K6");
     }
+    if (m1 < H.iters) return;
     // ---- K7: the K largest |c| (stable over ascending f), emitted in f order
     const int fin = H.iters & 1;
     launch_pdl(pdl_, keys_from_values, grid_of(acc_cap_), kT, 0, st, acc_c_[fin].get(), acc_cap_, acc_n, nullptr,

@@ -40,14 +40,23 @@ public:
     // its per-iteration plan (device), outputs out_f[k], out_c[k],
     // *out_count; decode errors go to err[0] (as decode_kernel).
     void run(double2* y, const int64_t* sigma, const int64_t* sigma_inv, int64_t* out_f,
-             double2* out_c, int64_t* out_count, int32_t* err, cudaStream_t st);
+             double2* out_c, int64_t* out_count, int32_t* err, cudaStream_t st) {
+        run_range(y, sigma, sigma_inv, out_f, out_c, out_count, err, st, 0, hplan_.iters);
+    }
+    // Iterations [m0, m1) only (m1 == iters also runs K7): consecutive ranges
+    // on one stream make one decode, so a caller can start the decode of the
+    // early iterations while the later iterations are still being encoded.
+    void run_range(double2* y, const int64_t* sigma, const int64_t* sigma_inv, int64_t* out_f,
+                   double2* out_c, int64_t* out_count, int32_t* err, cudaStream_t st, int m0,
+                   int m1);
 
     ~WideDecoder();
 
 private:
     // the fixed kernel sequence of one decode (K7 writes out_f/out_c/out_count)
     void enqueue(double2* y, const int64_t* sigma, const int64_t* sigma_inv, int32_t* err,
-                 int64_t* out_f, double2* out_c, int64_t* out_count, cudaStream_t st);
+                 int64_t* out_f, double2* out_c, int64_t* out_count, cudaStream_t st, int m0,
+                 int m1);
     void select_kth(const uint64_t* key, int64_t n_max, const int32_t* n_dev, int64_t kth_host,
                     const int32_t* kth_dev, cudaStream_t st);
     void compact_selected(const uint64_t* key, int64_t n_max, const int32_t* n_dev,
@@ -82,7 +91,7 @@ private:
     // one instantiated CUDA graph per (y, sigma, sigma_inv, err) tuple: the
     // ~40 launches per iteration replay without per-launch host overhead
     using GraphKey = std::tuple<const void*, const void*, const void*, const void*, const void*,
-                                const void*, const void*>;
+                                const void*, const void*, int, int>;
     std::map<GraphKey, cudaGraphExec_t> graphs_;
     int64_t k6_stage_cap_ = 0;  // k6_small: accumulated f staged in shared memory
     bool use_graphs_ = true;  // MSFFT_WIDE_GRAPH=0 launches eagerly

@@ -271,11 +271,14 @@ def test_wide_decode_bit_identical_to_cta_decode(oracle, monkeypatch, n, k, dtyp
 
 @pytest.mark.parametrize("knob,values", [("MSFFT_ENC_SPLIT", ("1", "0")),
                                          ("MSFFT_WIDE_PDL", ("1", "0")),
-                                         ("MSFFT_WIDE_GRAPH", ("1", "0"))])
+                                         ("MSFFT_WIDE_GRAPH", ("1", "0")),
+                                         ("MSFFT_WIDE_GROUPS", ("5", "1", "3"))])
 def test_launch_knobs_bit_identical(oracle, monkeypatch, knob, values):
     """Launch-shape knobs change only how the work is spread over CTAs and
     launches: per-segment encode tasks (small launches), programmatic edges
-    and the CUDA graph of the wide decode.  Results are bit-identical."""
+    and the CUDA graph of the wide decode, the wide decode overlapped with
+    the encode in iteration groups.  Results are bit-identical."""
+    monkeypatch.setenv("MSFFT_WIDE_OVERLAP_MIN", "0")
     n, k = 1 << 19, 1200
     x, _, _ = __import__("paper_2011_05698_b200.workloads", fromlist=["x"]).make_signal_np(
         n, k, 9, 20.0, "complex128", "loguniform_0.1_10")
@@ -606,3 +609,35 @@ def test_gated_decode_matches_fused_and_serial(oracle, monkeypatch, batch, n, k,
     for name in res:
         for f, c, cnt, _ in res[name]:
             assert np.array_equal(cnt, n0) and np.array_equal(f, f0) and np.array_equal(c, c0), name
+
+
+def test_wide_overlapped_batch(oracle, monkeypatch):
+    """Large signals decoded while their later iterations are still being
+    encoded (iteration groups, the wide decode on its own stream): a batch of
+    three signals equals the encode-everything-first path and each signal
+    transformed alone, bit for bit, with device-resident and host input."""
+    import torch
+    mk = __import__("paper_2011_05698_b200.workloads", fromlist=["x"]).make_signal_np
+    n, k = 1 << 19, 1200
+    x = np.stack([mk(n, k, 70 + i, 20.0, "complex128", "loguniform_0.1_10")[0] for i in range(3)])
+    seeds = [11, 12, 13]
+    res = {}
+    monkeypatch.setenv("MSFFT_WIDE_OVERLAP_MIN", "0")  # small enough for a test
+    for g in ("5", "1"):
+        monkeypatch.setenv("MSFFT_WIDE_GROUPS", g)
+        plan = M.Plan(n, k, M.MultiscaleConfig(), 1e-6, "complex128")
+        res[g] = plan.execute(x, seeds)
+        xd = torch.as_tensor(x).to("cuda")
+        od = (torch.empty((3, k), dtype=torch.int64, device="cuda"),
+              torch.empty((3, k), dtype=torch.complex128, device="cuda"),
+              torch.empty((3,), dtype=torch.int64, device="cuda"))
+        for i in range(2):
+            plan.execute(xd, seeds, out=od, assume_valid=i == 1)
+            f, c, cnt = (t.cpu().numpy() for t in od)
+            assert np.array_equal(f, res[g][0]) and np.array_equal(c, res[g][1])
+        if g == "5":
+            for i in range(3):
+                f1, c1, n1, _ = plan.execute(x[i:i + 1], [seeds[i]])
+                assert np.array_equal(f1[0], res[g][0][i]) and np.array_equal(c1[0], res[g][1][i])
+    assert (res["5"][2] > 0).all()
+    assert np.array_equal(res["5"][0], res["1"][0]) and np.array_equal(res["5"][1], res["1"][1])

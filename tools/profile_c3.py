@@ -17,6 +17,8 @@ from paper_2011_05698_b200.workloads import make_signal_np  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--dtype", default="complex128")
 ap.add_argument("--reps", type=int, default=2)
+ap.add_argument("--no-stages", action="store_true",
+                help="the production path (no per-stage events, encode/decode overlapped)")
 a = ap.parse_args()
 n, k = 1 << 24, 1000
 x, _, _ = make_signal_np(n, k, 301, 30.0, a.dtype, "uniform_0.5_2", 4 * n // 4096)
@@ -32,5 +34,6 @@ if os.environ.get("MSFFT_PROFILE_AFTER_PLAN"):
     torch.cuda.synchronize()
     torch.cuda.profiler.start()  # ncu --profile-from-start off: skip window design
 for r in range(a.reps):
-    _, _, _, ms = plan.execute(xd, seeds, out=out, assume_valid=True, stage_times=True, serial=True)
+    st = not a.no_stages
+    _, _, _, ms = plan.execute(xd, seeds, out=out, assume_valid=True, stage_times=st, serial=st)
     print(f"rep {r}: {ms:.3f} ms  stages {plan.stage_times()}", flush=True)

@@ -21,6 +21,8 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--log2n", type=int, default=27)
 ap.add_argument("--k", type=int, default=10000)
 ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--no-stages", action="store_true",
+                help="time the production path (no per-stage events: encode/decode overlapped)")
 ap.add_argument("--shards", type=int, default=0,
                 help="also run the index-range-sharded split path with G ranks, one "
                      "after another on this GPU, and compare it with the single-GPU result")
@@ -45,7 +47,8 @@ if os.environ.get("MSFFT_PROFILE_AFTER_PLAN"):
     torch.cuda.profiler.start()  # ncu --profile-from-start off: skip window design
 times, stages = [], []
 for _ in range(a.reps):
-    _, _, _, ms = plan.execute(x, seeds, out=out, assume_valid=True, stream=sh, stage_times=True)
+    _, _, _, ms = plan.execute(x, seeds, out=out, assume_valid=True, stream=sh,
+                               stage_times=not a.no_stages)
     times.append(ms)
     stages.append(plan.stage_times())
 f1, c1, n1 = [t.cpu().numpy() for t in out]
