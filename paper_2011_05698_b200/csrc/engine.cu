@@ -360,6 +360,7 @@ Plan::Plan(int64_t n, int64_t k, int64_t l, double q, double delta, bool c128, i
     MSFFT_CUDA(cudaEventCreateWithFlags(&ev_dec_done_, cudaEventDisableTiming));
     for (auto& e : ev_group_) MSFFT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     if (const char* e = std::getenv("MSFFT_WIDE_OVERLAP_MIN")) wide_overlap_min_ = std::atoll(e);
+    if (const char* e = std::getenv("MSFFT_FFT_TWO_PASS")) fft_two_pass_ = std::atoi(e) != 0;
     if (const char* e = std::getenv("MSFFT_WIDE_GROUPS"))
         wide_groups_ = std::max(1, std::min(kMaxWideGroups, std::atoi(e)));
     if (const char* e = std::getenv("MSFFT_OVERLAP_CHUNK")) overlap_chunk_ = std::atoll(e);
@@ -582,10 +583,17 @@ void Plan::bucket_ffts(double2* y, int64_t batch, cudaStream_t st, const FftGate
         const DevIter& di = dplan_.it[m];
         sets.push_back(FftSet{di.yoff, di.b, di.nrounds, m});
     }
+    // arrays above 4096 points go through the two-pass path, which needs a
+    // scratch copy laid out like y
+    bool big = false;
+    for (const FftSet& f : sets) big = big || f.size > kSmemFftMax;
+    if (big && !gate)
+        fft_scratch_.ensure(static_cast<size_t>(batch * dplan_.values_per_signal));
+    double2* scratch = big && !gate && fft_two_pass_ ? fft_scratch_.get() : nullptr;
     for (size_t i = 0; i < sets.size(); i += kMaxFftSets)
         fft_radix2_sets(y, sets.data() + i,
                         static_cast<int>(std::min<size_t>(kMaxFftSets, sets.size() - i)), batch,
-                        dplan_.values_per_signal, -1, dplan_.inv_n, st, gate);
+                        dplan_.values_per_signal, -1, dplan_.inv_n, st, gate, scratch);
 }
 
 bool Plan::split_tasks(int64_t n_tasks) const {

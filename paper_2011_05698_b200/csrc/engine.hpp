@@ -235,6 +235,9 @@ private:
     // ... only when the encode has this many samples to gather (C5: 18.7 M;
     // C3's 1.2 M encode is too short to pay for the extra graph launches)
     int64_t wide_overlap_min_ = int64_t{1} << 22;
+    // bucket FFTs above 4096 points: two launches over all sets (fft.hpp)
+    bool fft_two_pass_ = true;
+    mutable DeviceBuffer<double2> fft_scratch_;
     cudaEvent_t ev_group_[kMaxWideGroups] = {};
     int64_t overlap_chunk_ = 0;          // signals per encode/decode sub-chunk (0 = serial)
     double stage_ms_[3] = {0, 0, 0};

@@ -1,4 +1,5 @@
 // fft.cu -- see fft.hpp.  Compiled with --fmad=false.
+#include <algorithm>
 #include <cmath>
 #include <map>
 #include <memory>
@@ -229,6 +230,84 @@ __global__ void __launch_bounds__(512) fft_smem_sets_kernel(double2* __restrict_
     }
 }
 
+// Arrays larger than one CTA's shared memory (4096 < size <= 2^18), every
+// set in two launches instead of a bit-reversal pass plus two stage passes
+// per size: pass 1 gathers each 2048-element tile straight from its
+// bit-reversed positions and runs stages 1..11 (span 1, as stages_kernel
+// with s0 = 0), writing to a scratch copy (in place would overwrite samples
+// other tiles still gather); pass 2 runs the remaining stages 12..log2size
+// (lo_tile 16, as stages_kernel with s0 = 11) from the scratch back into the
+// data, scaling after the last butterfly.  Same butterflies, twiddles and
+// order as stages_kernel: bit-identical.
+constexpr int kBigPass1 = 11;
+struct BigFftSets {
+    int nsets;
+    int64_t first[kMaxFftSets + 1];  // first block of each set
+    int64_t off[kMaxFftSets], size[kMaxFftSets], inner[kMaxFftSets];
+    int64_t groups[kMaxFftSets];      // blocks per array
+    int log2size[kMaxFftSets], s0[kMaxFftSets], s1[kMaxFftSets], lo_tile[kMaxFftSets];
+    const double2* tw[kMaxFftSets];
+};
+
+template <bool kGather>
+__global__ void __launch_bounds__(512) stages_sets_kernel(const double2* __restrict__ src,
+                                                          double2* __restrict__ dst,
+                                                          const __grid_constant__ BigFftSets S,
+                                                          int64_t outer_stride, int sign,
+                                                          double scale) {
+    extern __shared__ double2 tile[];
+    int si = 0;
+    while (si + 1 < S.nsets && static_cast<int64_t>(blockIdx.x) >= S.first[si + 1]) ++si;
+    const int64_t blk = static_cast<int64_t>(blockIdx.x) - S.first[si];
+    const int64_t bi = blk / S.groups[si];
+    const int64_t g = blk - bi * S.groups[si];
+    const int64_t size = S.size[si];
+    const int s0 = S.s0[si], s1 = S.s1[si], lo_tile = S.lo_tile[si], log2size = S.log2size[si];
+    const double2* __restrict__ tw = S.tw[si];
+    const int64_t arr = S.off[si] + (bi / S.inner[si]) * outer_stride + (bi % S.inner[si]) * size;
+    const double2* a = src + arr;
+    double2* d = dst + arr;
+    const int G = s1 - s0;
+    const int64_t span = int64_t{1} << s0;
+    const int64_t tiles_per_hi = span / lo_tile;
+    const int64_t hi = g / tiles_per_hi;
+    const int64_t lo0 = (g - hi * tiles_per_hi) * lo_tile;
+    const int count = (1 << G) * lo_tile;
+    const int64_t base = (hi << s1) + lo0;
+    for (int e = threadIdx.x; e < count; e += blockDim.x) {
+        const int kk = e / lo_tile, li = e - kk * lo_tile;
+        const int64_t pos = base + static_cast<int64_t>(kk) * span + li;
+        tile[e] = kGather ? a[bitrev_bits(static_cast<unsigned>(pos), log2size)] : a[pos];
+    }
+    __syncthreads();
+    for (int st = s0 + 1; st <= s1; ++st) {
+        const int hkk = 1 << (st - 1 - s0);
+        const int64_t step = size >> st;
+        for (int bf = threadIdx.x; bf < count / 2; bf += blockDim.x) {
+            const int li = bf % lo_tile;
+            const int p = bf / lo_tile;
+            const int blk2 = p / hkk, off = p - blk2 * hkk;
+            const int kk = blk2 * 2 * hkk + off;
+            const int64_t k = ((static_cast<int64_t>(off) << s0) + lo0 + li) * step;
+            double2 w = tw[k];
+            if (sign > 0) w.y = -w.y;
+            const int e0 = kk * lo_tile + li, e1 = (kk + hkk) * lo_tile + li;
+            const double2 x0 = tile[e0];
+            const double2 t = cmul(tile[e1], w);
+            tile[e1] = make_double2(x0.x - t.x, x0.y - t.y);
+            tile[e0] = make_double2(x0.x + t.x, x0.y + t.y);
+        }
+        __syncthreads();
+    }
+    const bool do_scale = s1 == log2size && scale != 1.0;
+    for (int e = threadIdx.x; e < count; e += blockDim.x) {
+        const int kk = e / lo_tile, li = e - kk * lo_tile;
+        double2 v = tile[e];
+        if (do_scale) v = make_double2(v.x * scale, v.y * scale);
+        d[base + static_cast<int64_t>(kk) * span + li] = v;
+    }
+}
+
 void smem_fft_attribute(const void* fn) {
     // the attribute is per device
     static std::mutex mu;
@@ -247,14 +326,26 @@ void smem_fft_attribute(const void* fn) {
 
 void fft_radix2_sets(double2* data, const FftSet* sets, int nsets, int64_t batch,
                      int64_t outer_stride, int sign, double scale, cudaStream_t stream,
-                     const FftGate* gate) {
+                     const FftGate* gate, double2* scratch) {
     SmemFftSets S{};
+    BigFftSets B{};
     int64_t blocks = 0, max_size = 0;
     for (int i = 0; i < nsets; ++i) {
         const FftSet& f = sets[i];
         if (f.size <= 1 || batch <= 0) continue;
         if (f.size > kSmemFftMax || S.nsets == kMaxFftSets) {
             if (gate) throw CudaError("fft_radix2_sets: gated sets must fit one launch");
+            if (scratch && f.size <= (int64_t{1} << (kBigPass1 + 7)) && B.nsets < kMaxFftSets) {
+                int lg = 0;
+                while ((int64_t{1} << lg) < f.size) ++lg;
+                B.off[B.nsets] = f.off;
+                B.size[B.nsets] = f.size;
+                B.inner[B.nsets] = f.inner;
+                B.log2size[B.nsets] = lg;
+                B.tw[B.nsets] = device_twiddles(f.size);
+                ++B.nsets;
+                continue;
+            }
             fft_radix2_batched(data + f.off, f.size, batch * f.inner, f.inner, outer_stride, sign,
                                scale, stream);
             continue;
@@ -271,6 +362,41 @@ void fft_radix2_sets(double2* data, const FftSet* sets, int nsets, int64_t batch
         ++S.nsets;
         blocks += batch * f.inner;
         max_size = std::max(max_size, f.size);
+    }
+    if (B.nsets > 0) {
+        // the two passes over every large set (see stages_sets_kernel)
+        BigFftSets P1 = B, P2 = B;
+        int64_t b1 = 0, b2 = 0;
+        for (int i = 0; i < B.nsets; ++i) {
+            P1.s0[i] = 0;
+            P1.s1[i] = kBigPass1;
+            P1.lo_tile[i] = 1;
+            P1.groups[i] = B.size[i] >> kBigPass1;
+            P1.first[i] = b1;
+            b1 += batch * B.inner[i] * P1.groups[i];
+            P2.s0[i] = kBigPass1;
+            P2.s1[i] = B.log2size[i];
+            P2.lo_tile[i] = 16;
+            P2.groups[i] = (B.size[i] >> B.log2size[i]) * ((int64_t{1} << kBigPass1) / 16);
+            P2.first[i] = b2;
+            b2 += batch * B.inner[i] * P2.groups[i];
+        }
+        P1.first[B.nsets] = b1;
+        P2.first[B.nsets] = b2;
+        int g2max = 0;
+        for (int i = 0; i < B.nsets; ++i) g2max = std::max(g2max, B.log2size[i] - kBigPass1);
+        const size_t smem1 = sizeof(double2) << kBigPass1;
+        const size_t smem2 = sizeof(double2) * 16 << g2max;
+        smem_attr(stages_sets_kernel<true>, smem1);
+        smem_attr(stages_sets_kernel<false>, smem2);
+        if (b1 > 0x7fffffff || b2 > 0x7fffffff) throw CudaError("fft_radix2_sets: too many tiles");
+        stages_sets_kernel<true><<<static_cast<unsigned>(b1), 512, smem1, stream>>>(
+            data, scratch, P1, outer_stride, sign, scale);
+        MSFFT_LAUNCH_CHECK("stages_sets_kernel (pass 1)");
+        const int t2 = static_cast<int>(std::min<size_t>(512, std::max<size_t>(32, smem2 / 32)));
+        stages_sets_kernel<false><<<static_cast<unsigned>(b2), t2, smem2, stream>>>(
+            scratch, data, P2, outer_stride, sign, scale);
+        MSFFT_LAUNCH_CHECK("stages_sets_kernel (pass 2)");
     }
     if (S.nsets == 0) return;
     S.first[S.nsets] = blocks;

@@ -50,8 +50,12 @@ struct FftGate {
 // fft_radix2_batched of several sets: the sets with size <= 4096 go into ONE
 // launch (one CTA per array, shared memory), larger ones through the
 // multi-pass path.  Bit-identical to transforming each set separately.
+// scratch (optional): a buffer laid out like data (rows of outer_stride):
+// sets with 4096 < size <= 2^18 then take two launches in all (a gathered
+// bit-reversal + stages 1..11, then the remaining stages) instead of three
+// per size.
 void fft_radix2_sets(double2* data, const FftSet* sets, int nsets, int64_t batch,
                      int64_t outer_stride, int sign, double scale, cudaStream_t stream,
-                     const FftGate* gate = nullptr);
+                     const FftGate* gate = nullptr, double2* scratch = nullptr);
 
 }  // namespace msfft_b200

@@ -272,7 +272,8 @@ def test_wide_decode_bit_identical_to_cta_decode(oracle, monkeypatch, n, k, dtyp
 @pytest.mark.parametrize("knob,values", [("MSFFT_ENC_SPLIT", ("1", "0")),
                                          ("MSFFT_WIDE_PDL", ("1", "0")),
                                          ("MSFFT_WIDE_GRAPH", ("1", "0")),
-                                         ("MSFFT_WIDE_GROUPS", ("5", "1", "3"))])
+                                         ("MSFFT_WIDE_GROUPS", ("5", "1", "3")),
+                                         ("MSFFT_FFT_TWO_PASS", ("1", "0"))])
 def test_launch_knobs_bit_identical(oracle, monkeypatch, knob, values):
     """Launch-shape knobs change only how the work is spread over CTAs and
     launches: per-segment encode tasks (small launches), programmatic edges
