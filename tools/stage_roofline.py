@@ -33,11 +33,16 @@ FP64_PEAK = 1.8552e13    # DADD thread-ops/s, tools/fp64_peak.cu on this pool
 def stage_of(name):
     if name.startswith(("encode_kernel", "fused_kernel")):
         return "encode"
-    if name.startswith(("fft_smem", "stages_kernel", "bitrev_inplace")):
+    if name.startswith(("fft_smem", "stages_kernel", "stages_sets_kernel", "bitrev_inplace")):
         return "bucket_fft"
-    if name.startswith(("sigma_kernel", "validate_kernel", "zero_words")):
+    if name.startswith(("sigma_kernel", "validate_kernel", "zero_words", "compact_gather")):
         return "other"
+    if name.startswith(TORCH):  # the caller's own tensor ops (e.g. run_c5's x * 2)
+        return None
     return "decode"
+
+
+TORCH = ("StoreWithoutCast", "elementwise", "vectorized", "direct_copy", "unrolled_elementwise")
 
 
 def main():
@@ -45,15 +50,21 @@ def main():
     ap.add_argument("csv")
     ap.add_argument("--workload", default="")
     ap.add_argument("--anchor", default="encode_kernel")
+    ap.add_argument("--anchor-grid-max", action="store_true",
+                    help="anchor at the last --anchor launch with the largest grid (the serial "
+                         "execute's single encode, not the overlapped path's per-group encodes) "
+                         "and stop at the next --anchor launch")
     a = ap.parse_args()
     lines = open(a.csv).read().splitlines()
     start = next(i for i, l in enumerate(lines) if l.startswith('"ID"'))
     rows = list(csv.reader(lines[start:]))
     h = rows[0]
     ki, mi, vi, ii = h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value"), h.index("ID")
+    gi = h.index("Grid Size")
     launches = {}
     for r in rows[1:]:
-        d = launches.setdefault(int(r[ii]), {"name": r[ki].split("(")[0].split("::")[-1].split("<")[0]})
+        d = launches.setdefault(int(r[ii]), {"name": r[ki].split("(")[0].split("::")[-1].split("<")[0],
+                                             "grid": r[gi]})
         try:
             d[r[mi]] = float(r[vi].replace(",", ""))
         except ValueError:
@@ -61,11 +72,19 @@ def main():
     seq = [launches[i] for i in sorted(launches)]
     starts = [i for i, d in enumerate(seq) if d["name"] == a.anchor]
     last = seq[starts[-1]:]
+    if a.anchor_grid_max:
+        gsize = lambda d: eval(d["grid"].replace("(", "").replace(")", "").replace(", ", "*"))  # noqa: E731
+        big = max(gsize(seq[i]) for i in starts)
+        i0 = [i for i in starts if gsize(seq[i]) == big][-1]
+        nxt = [i for i in starts if i > i0]
+        last = seq[i0:nxt[0] if nxt else len(seq)]
     out, kern = {}, {}
     for d in last:
         us = d.get("gpu__time_duration.sum", 0.0) / 1e3
         ops = sum(d.get(f"sm__sass_thread_inst_executed_op_{o}_pred_on.sum", 0.0)
                   for o in ("dadd", "dmul", "dfma"))
+        if stage_of(d["name"]) is None:
+            continue
         for key, table in ((stage_of(d["name"]), out), (d["name"], kern)):
             st = table.setdefault(key, {"launches": 0, "us": 0.0, "dram_bytes": 0.0,
                                         "fp64_thread_ops": 0.0, "fp64_warp_inst": 0.0,
