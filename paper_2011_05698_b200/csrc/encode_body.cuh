@@ -43,8 +43,25 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-__device__ __forceinline__ float2 ld_sample(const float2* p) { return __ldcs(p); }
-__device__ __forceinline__ double2 ld_sample(const double2* p) { return __ldcs(p); }
+// kKeep: the validating fused kernel streams every sample of the signal
+// next to its encode: the gather's load carries an L2 eviction policy
+// (createpolicy: evict_last keeps the lines it fetches for the scan)
+template <bool kKeep = false>
+__device__ __forceinline__ float2 ld_sample(const float2* p, uint64_t pol = 0) {
+    if (!kKeep) return __ldcs(p);
+    float2 v;
+    asm volatile("ld.global.nc.L2::cache_hint.v2.f32 {%0, %1}, [%2], %3;"
+                 : "=f"(v.x), "=f"(v.y) : "l"(p), "l"(pol));
+    return v;
+}
+template <bool kKeep = false>
+__device__ __forceinline__ double2 ld_sample(const double2* p, uint64_t pol = 0) {
+    if (!kKeep) return __ldcs(p);
+    double2 v;
+    asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+                 : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
+    return v;
+}
 
 // Once per CTA before the first encode_task.
 __device__ __forceinline__ void encode_barrier_init(uint64_t* bar) {
@@ -70,13 +87,13 @@ enum LoadMode { kLoadFull = 0, kLoadShard = 1, kLoadCompact = 2 };
 // always-valid indices; only the adds are predicated on the tap interval.
 // acc[r] still receives its terms in increasing t' (u ascending within a
 // batch, batches ascending), the reference's order.
-template <class T, int kMode, bool kSmemTaps>
+template <class T, int kMode, bool kSmemTaps, bool kKeep = false>
 __device__ __forceinline__ void gather_accumulate(const DevPlan& plan, const EncTask& task,
                                                   const T* __restrict__ xs, uint32_t sg,
                                                   const double* __restrict__ taps, int64_t h,
                                                   uint32_t wu,
                                                   const int64_t* taus, int nr, int64_t b, int c,
-                                                  double2 (&acc)[kEncRounds]) {
+                                                  double2 (&acc)[kEncRounds], uint64_t pol = 0) {
     const uint32_t mask = static_cast<uint32_t>(plan.n - 1);
     const uint32_t lo = static_cast<uint32_t>(plan.x_lo);
     const uint32_t span = static_cast<uint32_t>(plan.x_hi - plan.x_lo);
@@ -103,15 +120,15 @@ __device__ __forceinline__ void gather_accumulate(const DevPlan& plan, const Enc
                     if (kMode == kLoadCompact) {
                         MSFFT_DCHECK(task.seg_cpos[sgi] + (tt - A) >= 0 &&
                                      task.seg_cpos[sgi] + (tt - A) < plan.x_row);
-                        v[u] = ld_sample(cbase + tt);
+                        v[u] = ld_sample<kKeep>(cbase + tt, pol);
                     } else {
                         const uint32_t src = (sg * static_cast<uint32_t>(tt)) & mask;
                         if (kMode == kLoadFull) {
-                            v[u] = ld_sample(xs + src);
+                            v[u] = ld_sample<kKeep>(xs + src, pol);
                         } else {
                             v[u].x = 0;
                             v[u].y = 0;
-                            if (src - lo < span) v[u] = ld_sample(xs + (src - lo));
+                            if (src - lo < span) v[u] = ld_sample<kKeep>(xs + (src - lo), pol);
                         }
                     }
                 }
@@ -292,6 +309,133 @@ __device__ __forceinline__ void encode_task(const DevPlan& plan, const EncTask& 
             const double2 v = F[e];
             y[sig * vps + it.yoff + static_cast<int64_t>(task.r0) * b + rem] =
                 make_double2(v.x * inv_n, v.y * inv_n);
+        }
+    }
+}
+
+// A packed encode item (validating fused kernel): up to kMaxPack sub-tasks,
+// each ONE signal and one iteration with 32 <= b <= 256, side by side on
+// warp-aligned thread ranges [tid0, tid0 + b).  Packing iterations of the
+// same signal (instead of 256/b signals of one iteration) keeps a CTA's
+// random reads inside one or two signals, so they hit the L2 lines the
+// validation stream of those signals brings in.  Per sub-task the arithmetic
+// is encode_task's (same union walk, same radix-2 DIT), so the folds and
+// bucket values are bit-identical to it (kMaxPack sub-tasks at most).
+
+template <class T>
+__device__ __forceinline__ void encode_pack(const DevPlan& plan, const EncTask* __restrict__ sub,
+                                            int nsub, const T* __restrict__ x, int64_t x_stride,
+                                            const int64_t* __restrict__ sigma,
+                                            double2* __restrict__ y, unsigned char* smem_raw,
+                                            uint64_t* bar, uint32_t& phase, uint64_t pol) {
+    const int tid = threadIdx.x;
+    // ---- stage the distinct iterations' taps with one mbarrier transaction
+    uint32_t bytes_total = 0;
+    for (int j = 0; j < nsub; ++j)
+        if (sub[j].stage_taps)
+            bytes_total += static_cast<uint32_t>((plan.it[sub[j].m].w + 1) * sizeof(double));
+    if (bytes_total) {
+        if (tid == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                         ::"r"(smem_u32(bar)), "r"(bytes_total) : "memory");
+            for (int j = 0; j < nsub; ++j) {
+                if (!sub[j].stage_taps) continue;
+                const DevIter& it = plan.it[sub[j].m];
+                const uint32_t bytes = static_cast<uint32_t>((it.w + 1) * sizeof(double));
+                unsigned char* dst = smem_raw + sub[j].taps_off;
+                for (uint32_t off = 0; off < bytes; off += 32768) {
+                    const uint32_t len = bytes - off < 32768 ? bytes - off : 32768;
+                    asm volatile(
+                        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes "
+                        "[%0], [%1], %2, [%3];"
+                        ::"r"(smem_u32(dst + off)),
+                        "l"(reinterpret_cast<const unsigned char*>(it.taps) + off), "r"(len),
+                        "r"(smem_u32(bar))
+                        : "memory");
+                }
+            }
+        }
+        asm volatile(
+            "{\n .reg .pred p;\n WAIT_%=:\n"
+            " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+            " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)), "r"(phase)
+            : "memory");
+        phase ^= 1u;
+    }
+
+    // ---- thread -> sub-task (warp-uniform: tid0 and b are multiples of 32)
+    int j = -1, max_log2b = 0;
+    for (int q = 0; q < nsub; ++q) {
+        const DevIter& iq = plan.it[sub[q].m];
+        max_log2b = iq.log2b > max_log2b ? iq.log2b : max_log2b;
+        if (tid >= sub[q].tid0 && tid < sub[q].tid0 + iq.b) j = q;
+    }
+    const bool active = j >= 0;
+    const EncTask& task = sub[active ? j : 0];
+    const DevIter& it = plan.it[task.m];
+    const int64_t b = it.b;
+    const int log2b = it.log2b;
+    const int nr = task.nr;
+    const int c = tid - task.tid0;
+    const int64_t s = task.sig0;
+    const int64_t* taus = plan.taus + it.tau_off + task.r0;
+
+    double2 acc[kEncRounds];
+#pragma unroll
+    for (int r = 0; r < kEncRounds; ++r) acc[r] = make_double2(0.0, 0.0);
+    if (active) {
+        const uint32_t sg = static_cast<uint32_t>(sigma[s * plan.iters + task.m]);
+        const T* xs = x + s * x_stride;
+        const int64_t h = it.h;
+        const uint32_t wu = static_cast<uint32_t>(it.w);
+        if (task.taps_off >= 0)
+            gather_accumulate<T, kLoadFull, true, true>(
+                plan, task, xs, sg, reinterpret_cast<const double*>(smem_raw + task.taps_off), h,
+                wu, taus, nr, b, c, acc, pol);
+        else
+            gather_accumulate<T, kLoadFull, false, true>(plan, task, xs, sg, it.taps, h, wu, taus,
+                                                         nr, b, c, acc, pol);
+    }
+
+    // ---- b-point radix-2 DIT of every (sub-task, round) in smem
+    __syncthreads();  // the taps region is reused for the arrays
+    double2* F = reinterpret_cast<double2*>(smem_raw) + (active ? task.f_off : 0);
+    if (active) {
+#pragma unroll
+        for (int r = 0; r < kEncRounds; ++r)
+            if (r < nr) {
+                const unsigned bin = static_cast<unsigned>((c + taus[r]) & (b - 1));
+                F[(r << log2b) + bitrev_bits(bin, log2b)] = acc[r];
+            }
+    }
+    __syncthreads();
+    const int nbf = (nr << log2b) >> 1;
+    for (int st = 1; st <= max_log2b; ++st) {
+        if (active && st <= log2b) {
+            const int half = 1 << (st - 1);
+            const int step_sh = log2b - st;
+            for (int bf = c; bf < nbf; bf += static_cast<int>(b)) {
+                const int arr = bf >> (log2b - 1);
+                const int p = bf & ((1 << (log2b - 1)) - 1);
+                const int blk = p >> (st - 1);
+                const int off = p & (half - 1);
+                const int jj = (arr << log2b) + (blk << st) + off;
+                const double2 w = it.tw[off << step_sh];
+                const double2 x0 = F[jj];
+                const double2 tv = cmul(F[jj + half], w);
+                F[jj + half] = make_double2(x0.x - tv.x, x0.y - tv.y);
+                F[jj] = make_double2(x0.x + tv.x, x0.y + tv.y);
+            }
+        }
+        __syncthreads();
+    }
+    if (active) {
+        const double inv_n = plan.inv_n;
+        double2* ys = y + s * plan.values_per_signal + it.yoff + static_cast<int64_t>(task.r0) * b;
+        for (int e = c; e < (nr << log2b); e += static_cast<int>(b)) {
+            const double2 v = F[e];
+            ys[e] = make_double2(v.x * inv_n, v.y * inv_n);
         }
     }
 }

@@ -379,6 +379,19 @@ Plan::Plan(int64_t n, int64_t k, int64_t l, double q, double delta, bool c128, i
     for (int m : big_b_iters_) gated_ok_ = gated_ok_ && dplan_.it[m].b <= kSmemFftMax;
     if (const char* e = std::getenv("MSFFT_FUSED_SMEM_PAD"))  // diagnostic: L1 carve-out experiments
         fused_smem_ += static_cast<size_t>(std::max(0LL, std::atoll(e)));
+    // the validating fused launch packs iterations of one signal per CTA on
+    // warp-aligned lanes: every b in [32, 256], the one-CTA decode
+    val_ok_ = big_b_iters_.empty() && !lay_.big;
+    for (int m = 0; m < sched_.iterations; ++m)
+        val_ok_ = val_ok_ && dplan_.it[m].b >= 32 && dplan_.it[m].b <= kEncThreads;
+    if (const char* e = std::getenv("MSFFT_VAL_FUSED")) val_fused_enabled_ = std::atoi(e) != 0;
+    if (const char* e = std::getenv("MSFFT_VAL_CHUNK_MB"))
+        val_chunk_bytes_ = std::max(1LL, std::atoll(e)) << 20;
+    if (const char* e = std::getenv("MSFFT_VAL_ITEM_KB"))
+        val_item_bytes_ = std::max(16LL, std::atoll(e)) << 10;
+    if (const char* e = std::getenv("MSFFT_VAL_DLAG")) val_dlag_ = std::max(0LL, std::atoll(e));
+    if (const char* e = std::getenv("MSFFT_VAL_SMEM_KB")) val_smem_kb_ = std::max(16LL, std::atoll(e));
+    if (const char* e = std::getenv("MSFFT_VAL_ELAG")) val_elag_ = std::max(0LL, std::atoll(e));
     flags_.reset(2);
     MSFFT_CUDA(cudaMemset(flags_.get(), 0, 2 * sizeof(int32_t)));
     for (int i = 0; i < 2; ++i)
@@ -572,6 +585,200 @@ const Plan::FusedSet& Plan::fused_for(int64_t batch, int slot) {
     return fused_.emplace(key, std::move(fs)).first->second;
 }
 
+bool Plan::val_fused_ok(const void* d_x, int64_t x_stride) const {
+    const int64_t elem = c128_ ? 16 : 8;
+    return val_ok_ && val_fused_enabled_ && fused_enabled_ &&
+           reinterpret_cast<uintptr_t>(d_x) % 16 == 0 && (x_stride * elem) % 16 == 0 &&
+           (sched_.n * elem) % 16 == 0;
+}
+
+// Item list of the validating fused launch (fused.cu fused_val_kernel).
+// Chunk = the signals whose rows fill val_chunk_bytes_ (default 64 MB, half
+// the L2).  Per chunk: its validation items, then its packed encode items
+// (val_elag_ chunks later), then the decodes of the chunk val_dlag_ chunks
+// before.  Packing: the chunk's (signal, iteration, round-group) sub-tasks,
+// first-fit decreasing on b into CTAs of 256 threads (<= kMaxPack each, their
+// b-point arrays within the shared memory); each distinct iteration's taps
+// staged once per pack while they fit, read from global otherwise.
+const Plan::ValSet& Plan::val_for(int64_t batch, int64_t x_stride) {
+    const auto key = std::make_pair(batch, x_stride);
+    auto found = val_.find(key);
+    if (found != val_.end()) return found->second;
+    const int64_t elem = c128_ ? 16 : 8;
+    const int64_t row_bytes = sched_.n * elem;
+    const int64_t chunk = std::max<int64_t>(1, val_chunk_bytes_ / (x_stride * elem));
+    const int64_t nchunks = (batch + chunk - 1) / chunk;
+    const int iters = sched_.iterations;
+    const int64_t item_bytes = std::min(row_bytes, (val_item_bytes_ + 15) / 16 * 16);
+    const int64_t ipr = (row_bytes + item_bytes - 1) / item_bytes;
+    if (batch * ipr >= static_cast<int64_t>(kValItemBase))
+        throw std::invalid_argument("sfft4: validation item index exceeds the item code range");
+    // dynamic shared memory: the encode's taps/arrays, the decode scratch,
+    // and the scan's ring of 16-KB slots -- as large as two CTAs per SM allow
+    size_t smem = std::max(fused_smem_, static_cast<size_t>(val_smem_kb_) << 10);
+    std::vector<EncTask> proto;
+    append_tasks(proto, 0, 1, false);
+    struct Bin {
+        std::vector<EncTask> subs;
+        int threads = 0;
+        size_t f_bytes = 0;
+    };
+    std::vector<EncTask> tasks;
+    std::vector<int2> packs;
+    std::vector<std::vector<int32_t>> enc(nchunks);
+    std::vector<int32_t> need(static_cast<size_t>(nchunks * iters), 0);
+    for (int64_t c = 0; c < nchunks; ++c) {
+        std::vector<EncTask> subs;
+        for (int64_t s = c * chunk; s < std::min(batch, (c + 1) * chunk); ++s)
+            for (EncTask t : proto) {
+                t.sig0 = s;
+                t.nsig = 1;
+                t.fused = 1;
+                t.lane0 = 0;
+                subs.push_back(t);
+                ++need[c * iters + t.m];
+            }
+        std::stable_sort(subs.begin(), subs.end(), [&](const EncTask& a, const EncTask& b) {
+            return dplan_.it[a.m].b > dplan_.it[b.m].b;
+        });
+        std::vector<Bin> bins;
+        for (const EncTask& t : subs) {
+            const int b = static_cast<int>(dplan_.it[t.m].b);
+            const size_t fb = static_cast<size_t>(t.nr) * b * sizeof(double2);
+            Bin* dst = nullptr;
+            for (Bin& bn : bins)
+                if (bn.threads + b <= kEncThreads && static_cast<int>(bn.subs.size()) < kMaxPack &&
+                    bn.f_bytes + fb <= smem) {
+                    dst = &bn;
+                    break;
+                }
+            if (!dst) {
+                bins.emplace_back();
+                dst = &bins.back();
+            }
+            dst->subs.push_back(t);
+            dst->threads += b;
+            dst->f_bytes += fb;
+        }
+        for (Bin& bn : bins) {
+            int tid0 = 0;
+            int32_t f_off = 0;
+            size_t taps_used = 0;
+            for (size_t j = 0; j < bn.subs.size(); ++j) {
+                EncTask& t = bn.subs[j];
+                const DevIter& di = dplan_.it[t.m];
+                t.tid0 = tid0;
+                tid0 += static_cast<int>(di.b);
+                t.f_off = f_off;
+                f_off += static_cast<int32_t>(t.nr * di.b);
+                t.stage_taps = 0;
+                t.taps_off = -1;
+                for (size_t q = 0; q < j; ++q)
+                    if (bn.subs[q].m == t.m && bn.subs[q].taps_off >= 0) t.taps_off = bn.subs[q].taps_off;
+                if (t.taps_off < 0) {
+                    const size_t tb = (static_cast<size_t>(di.w + 1) * sizeof(double) + 127) / 128 * 128;
+                    if (taps_used + tb <= smem) {
+                        t.taps_off = static_cast<int32_t>(taps_used);
+                        t.stage_taps = 1;
+                        taps_used += tb;
+                    }
+                }
+            }
+            enc[c].push_back(static_cast<int32_t>(packs.size()));
+            packs.push_back(make_int2(static_cast<int>(tasks.size()), static_cast<int>(bn.subs.size())));
+            tasks.insert(tasks.end(), bn.subs.begin(), bn.subs.end());
+        }
+    }
+    std::vector<int32_t> items, vneed(static_cast<size_t>(nchunks), 0);
+    auto vitems = [&](int64_t c) {
+        for (int64_t s = c * chunk; s < std::min(batch, (c + 1) * chunk); ++s)
+            for (int64_t p = 0; p < ipr; ++p) {
+                items.push_back(static_cast<int32_t>(kValItemBase + s * ipr + p));
+                ++vneed[c];
+            }
+    };
+    auto decodes = [&](int64_t c) {
+        for (int64_t s = c * chunk; s < std::min(batch, (c + 1) * chunk); ++s)
+            items.push_back(static_cast<int32_t>(-(s + 1)));
+    };
+    // diagnostics (MSFFT_VAL_DEBUG): 1 = validation items only, 2 = no
+    // validation items (the encode and decode alone, reading x from HBM)
+    int debug = 0;
+    if (const char* e = std::getenv("MSFFT_VAL_DEBUG")) debug = std::atoi(e);
+    if (debug == 1)
+        for (auto& e : enc) e.clear();
+    // E(c) goes right before V(c + eoff): eoff = 1 after its own scan, 0
+    // before it, < 0 that many chunks ahead of it (MSFFT_VAL_EOFF).  Default
+    // -4 with policy 7 (gather loads evict_last, scan copies evict_first):
+    // the gathers fetch their lines ~4 chunks (~35 us) before the scan passes
+    // them, the scan hits those lines and its own lines do not push them out.
+    // The scan-first order (eoff >= 1) gets no L2 hits on B200 at all: the
+    // latency-bound gathers of a chunk run long after the scan's lines are
+    // evicted (profiles/r02c).
+    int64_t eoff = val_elag_ ? 1 + val_elag_ : -4;
+    int policy = 7;
+    if (const char* e = std::getenv("MSFFT_VAL_EOFF")) eoff = std::atoll(e);
+    if (const char* e = std::getenv("MSFFT_VAL_POLICY")) policy = std::atoi(e);
+    int64_t next_enc = 0, next_dec = 0, next_v = 0;
+    for (int64_t t = std::min<int64_t>(0, eoff); t < nchunks + std::max<int64_t>(0, eoff); ++t) {
+        const int64_t ce = t - eoff;
+        if (ce >= 0 && ce < nchunks) {
+            items.insert(items.end(), enc[ce].begin(), enc[ce].end());
+            next_enc = ce + 1;
+        }
+        if (t >= 0 && t < nchunks) {
+            if (debug != 2) vitems(t);
+            next_v = t + 1;
+        }
+        for (; next_dec < std::min(next_enc, next_v) - val_dlag_; ++next_dec) decodes(next_dec);
+    }
+    for (; next_enc < nchunks; ++next_enc)
+        items.insert(items.end(), enc[next_enc].begin(), enc[next_enc].end());
+    for (; next_dec < nchunks; ++next_dec) decodes(next_dec);
+    if (debug == 1) items.erase(std::remove_if(items.begin(), items.end(),
+                                               [](int32_t v) { return v < 0; }),
+                                items.end());
+
+    ValSet vs;
+    vs.tasks.reset(tasks.size());
+    vs.items.reset(items.size());
+    vs.need.reset(need.size());
+    vs.vneed.reset(vneed.size());
+    vs.packs.reset(packs.size());
+    const int64_t n_counters = nchunks * iters + nchunks + 2;
+    vs.counters.reset(static_cast<size_t>(n_counters));
+    MSFFT_CUDA(cudaMemcpy(vs.tasks.get(), tasks.data(), tasks.size() * sizeof(EncTask),
+                          cudaMemcpyHostToDevice));
+    MSFFT_CUDA(cudaMemcpy(vs.items.get(), items.data(), items.size() * sizeof(int32_t),
+                          cudaMemcpyHostToDevice));
+    MSFFT_CUDA(cudaMemcpy(vs.need.get(), need.data(), need.size() * sizeof(int32_t),
+                          cudaMemcpyHostToDevice));
+    MSFFT_CUDA(cudaMemcpy(vs.vneed.get(), vneed.data(), vneed.size() * sizeof(int32_t),
+                          cudaMemcpyHostToDevice));
+    MSFFT_CUDA(cudaMemcpy(vs.packs.get(), packs.data(), packs.size() * sizeof(int2),
+                          cudaMemcpyHostToDevice));
+    MSFFT_CUDA(cudaMemset(vs.counters.get(), 0, sizeof(int32_t) * n_counters));
+    vs.vw.fw.tasks = vs.tasks.get();
+    vs.vw.fw.items = vs.items.get();
+    vs.vw.fw.n_items = static_cast<int32_t>(items.size());
+    vs.vw.fw.chunk = chunk;
+    vs.vw.fw.need = vs.need.get();
+    vs.vw.fw.counters = vs.counters.get();
+    vs.vw.fw.n_chunks = nchunks;
+    vs.vw.fw.n_counters = n_counters;
+    vs.vw.packs = vs.packs.get();
+    vs.vw.vneed = vs.vneed.get();
+    vs.vw.row_bytes = row_bytes;
+    vs.vw.stride_bytes = x_stride * elem;
+    vs.vw.item_bytes = item_bytes;
+    vs.vw.items_per_row = ipr;
+    vs.vw.policy = policy;
+    vs.smem = smem;
+    vs.n_packs = static_cast<int64_t>(packs.size());
+    vs.n_vitems = batch * ipr;
+    return val_.emplace(key, std::move(vs)).first->second;
+}
+
 // K2 for the iterations with b > 256 (the encode's fused epilogue does the
 // rest): their b-point transforms and the 1/n scale, as few launches as the
 // sizes allow.
@@ -680,6 +887,8 @@ int64_t Plan::launches(int64_t batch, bool validate, bool serial) const {
     if (!serial && gated_ok_ && batch <= gated_max_batch_)  // sigma (+ gather) + encode
         return 3 + (compact_gather_ ? 1 : 0) + (big_b_iters_.empty() ? 0 : 1) +
                (validate ? 1 : 0);  // (+ bucket FFTs) + decode (+ validate)
+    if (!serial && validate && val_ok_ && val_fused_enabled_ && fused_enabled_)
+        return 2;  // sigma + validating fused (device rows, 16-B aligned)
     if (!serial && fused_enabled_ && big_b_iters_.empty() && !lay_.big)
         return 2 + (validate ? 1 : 0);  // sigma + fused (+ validate)
     // per (sub-)chunk: encode + bucket FFTs for b > 256 + decode
@@ -846,6 +1055,24 @@ void Plan::run_chunk(int64_t batch, const void* d_x, int64_t x_stride, const int
             it->second = ex;
         }
         MSFFT_CUDA(cudaGraphLaunch(it->second, st));
+        return;
+    }
+    if (validate && !traced && !opt.force_serial && !compact && val_fused_ok(d_x, x_stride)) {
+        // one persistent launch: the validation scan, the encode and the
+        // decode, the encode's random reads served from the L2 lines the scan
+        // of the same signals brings in
+        const ValSet& vs = val_for(batch, x_stride);
+        if (opt.stage_times) MSFFT_CUDA(cudaEventRecord(ev_stage_[0], st));
+        launch_fused_validating(P, lay_, vs.vw, d_x, c128_, x_stride, batch, d_sig, d_sig_inv,
+                                y_.get(), dec_work_.get(), d_out_f, d_out_c, d_out_count,
+                                flags_.get(), vs.smem, st);
+        if (opt.stage_times) {
+            MSFFT_CUDA(cudaEventRecord(ev_stage_[1], st));
+            MSFFT_CUDA(cudaEventSynchronize(ev_stage_[1]));
+            float ms = 0.f;
+            MSFFT_CUDA(cudaEventElapsedTime(&ms, ev_stage_[0], ev_stage_[1]));
+            stage_ms_[0] += ms;
+        }
         return;
     }
     if (validate) launch_validate(d_x, c128_, n, x_stride, batch, flags_.get() + 1, st);

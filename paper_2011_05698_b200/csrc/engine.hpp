@@ -139,6 +139,18 @@ private:
     // slot 0: synchronous launches; 1, 2: the two alternating buffer sets of
     // programmatic (PDL) asynchronous launches
     const FusedSet& fused_for(int64_t batch, int slot = 0);
+    // validating fused launch (fused.cu fused_val_kernel): chunks of signals
+    // whose rows fit in L2, each V(c) E(c) D(c - lag)
+    struct ValSet {
+        DeviceBuffer<EncTask> tasks;
+        DeviceBuffer<int32_t> items, need, counters, vneed;
+        DeviceBuffer<int2> packs;
+        ValWork vw;
+        size_t smem = 0;
+        int64_t n_packs = 0, n_vitems = 0;
+    };
+    const ValSet& val_for(int64_t batch, int64_t x_stride);
+    bool val_fused_ok(const void* d_x, int64_t x_stride) const;
     // split: one task per merged t' segment (more CTAs for small batches)
     void append_tasks(std::vector<EncTask>& v, int64_t s_begin, int64_t s_end, bool split) const;
     bool split_tasks(int64_t n_tasks) const;
@@ -182,6 +194,14 @@ private:
     std::map<int64_t, TaskSet> tasks_;
     std::map<std::tuple<int64_t, int64_t, int64_t>, TaskSet> part_tasks_;
     std::map<int64_t, FusedSet> fused_;
+    std::map<std::pair<int64_t, int64_t>, ValSet> val_;
+    bool val_fused_enabled_ = true;             // MSFFT_VAL_FUSED
+    int64_t val_chunk_bytes_ = int64_t{64} << 20;  // MSFFT_VAL_CHUNK_MB: x bytes per chunk
+    int64_t val_item_bytes_ = int64_t{512} << 10;  // MSFFT_VAL_ITEM_KB: one validation item
+    int64_t val_dlag_ = 8;                      // MSFFT_VAL_DLAG: chunks a decode trails
+    int64_t val_elag_ = 0;                      // MSFFT_VAL_ELAG: chunks an encode trails its scan
+    int64_t val_smem_kb_ = 64;                  // MSFFT_VAL_SMEM_KB: dynamic smem floor
+    bool val_ok_ = false;                       // every b in [32, 256], one-CTA decode
     bool fused_enabled_ = true;   // persistent encode+decode launch when all b <= 256
     int64_t fused_chunk_ = 64;    // signals per fused chunk
     int64_t fused_lag_ = 2;       // chunks a decode trails its encode by

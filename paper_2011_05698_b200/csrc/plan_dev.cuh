@@ -17,6 +17,7 @@ constexpr int kMaxIters = 40;
 constexpr int kMaxTaus = 1024;
 constexpr int kEncRounds = 8;       // rounds fused into one gather pass
 constexpr int kEncThreads = 256;    // encode CTA size
+constexpr int kMaxPack = 8;         // sub-tasks of a packed encode item
 constexpr int kDecThreads = 256;    // decode CTA size
 constexpr int kMaxStageTable = 64;  // locate stages the decode keeps in shared memory
 constexpr int kMaxStages = 4096;    // longest precomputed locate stage table
@@ -67,7 +68,13 @@ struct EncTask {
     int64_t sig0;            // first signal
     int32_t nsig;            // signals handled (fused: 256/b)
     int32_t lane0;           // first residue class (non-fused: 256-wide slice)
-    int32_t nseg, pad_;
+    int32_t nseg;
+    // packed tasks (validating fused kernel, fused.cu): this sub-task's
+    // threads are [tid0, tid0 + b) of the CTA; its taps sit at byte taps_off
+    // of the shared staging area (-1: read from global) and are copied there
+    // by this sub-task if stage_taps; its b-point arrays at double2 f_off
+    int32_t tid0;
+    int32_t taps_off, f_off, stage_taps, pad_;
     int32_t seg_lo[kEncRounds], seg_hi[kEncRounds];  // merged t' intervals
     int32_t seg_cpos[kEncRounds];  // compact position of seg_lo (sparse ingest)
 };

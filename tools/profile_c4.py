@@ -19,6 +19,8 @@ ap.add_argument("--k", type=int, default=64)
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--no-stages", action="store_true")
 ap.add_argument("--serial", action="store_true", help="separate encode / decode launches")
+ap.add_argument("--validate", action="store_true",
+                help="every rep validating (the fused_val_kernel launch)")
 a = ap.parse_args()
 n, k, B = 1 << a.log2n, a.k, a.batch
 dev = torch.device("cuda", 0)
@@ -31,7 +33,7 @@ out = (torch.empty((B, k), dtype=torch.int64, device=dev),
        torch.empty((B,), dtype=torch.int64, device=dev))
 sh = torch.cuda.current_stream().cuda_stream
 for r in range(a.reps):
-    _, _, _, ms = plan.execute(x, aseeds, out=out, assume_valid=r > 0, stream=sh,
+    _, _, _, ms = plan.execute(x, aseeds, out=out, assume_valid=r > 0 and not a.validate, stream=sh,
                                stage_times=not a.no_stages, serial=a.serial)
     print(f"rep {r}: {ms:.3f} ms  stages {plan.stage_times()}", flush=True)
 
