@@ -13,7 +13,8 @@ sys.path.insert(0, REPO)
 
 
 def test_traffic_records_match_bench_workload():
-    for name in ("fused_traffic.json", "encode_traffic.json", "validate_traffic.json"):
+    for name in ("fused_traffic.json", "fused_val_traffic.json", "encode_traffic.json",
+                 "validate_traffic.json"):
         with open(os.path.join(REPO, "profiles", name)) as f:
             rec = json.load(f)
         assert rec.get("batch") == 1024 and rec.get("n") == 1 << 22, name
@@ -23,12 +24,12 @@ def test_traffic_records_match_bench_workload():
 
 def test_records_are_for_the_current_sources():
     """The committed summaries were captured on the native sources in this
-    tree (re-capture with tools/r02_evidence.sh after changing csrc/)."""
+    tree (re-capture with tools/r02c_evidence.sh after changing csrc/)."""
     from paper_2011_05698_b200.provenance import csrc_sha256
     cur = csrc_sha256()
-    for name in ("fused_traffic.json", "encode_traffic.json", "validate_traffic.json",
-                 "fused_ncu_summary.json", "decode_c4_ncu_summary.json",
-                 "validate_ncu_summary.json"):
+    for name in ("fused_traffic.json", "fused_val_traffic.json", "encode_traffic.json",
+                 "validate_traffic.json", "fused_ncu_summary.json", "fused_val_ncu_summary.json",
+                 "decode_c4_ncu_summary.json", "validate_ncu_summary.json"):
         with open(os.path.join(REPO, "profiles", name)) as f:
             assert json.load(f).get("csrc_sha256") == cur, name
 
