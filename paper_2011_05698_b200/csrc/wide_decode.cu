@@ -70,12 +70,14 @@ void zero_async(bool pdl, void* p, size_t bytes, cudaStream_t st) {
 
 // ---------------------------------------------------------------- scans
 // Exclusive scan of in[0..len) into out (may alias); total -> *total.
+// long_list (K3's bucket counts): the indices with more than kLongSeg entries
+// are listed as {count, indices...} for the CTA sorter.
 // Each warp owns a contiguous segment and walks it in coalesced 32-element
 // tiles (warp shuffles scan a tile); a block scan of the warp totals gives
 // each segment its offset.
 __global__ void __launch_bounds__(kScanT)
 scan_kernel(const int32_t* in, int64_t len_max, const int32_t* len_dev, int32_t* out,
-            int32_t* total) {
+            int32_t* total, int32_t* long_list) {
     pdl_entry();
     constexpr int kWarps = kScanT / 32;
     __shared__ int32_t wsum[kWarps];
@@ -110,6 +112,8 @@ scan_kernel(const int32_t* in, int64_t len_max, const int32_t* len_dev, int32_t*
             if (lane >= o) x += y;
         }
         if (i < hi) out[i] = carry + x - v;
+        if (long_list && v > kLongSeg)
+            long_list[1 + atomicAdd(&long_list[0], 1)] = static_cast<int32_t>(i);
         carry += __shfl_sync(0xffffffffu, x, 31);
     }
 }
@@ -184,43 +188,38 @@ __global__ void k3_scatter(const DevPlan* __restrict__ P, int m, const int32_t* 
     }
 }
 
-// One warp per bucket: its events in ascending tone order (keys j*4+d are
-// unique per bucket), by rank counting.
-__global__ void k3_segsort(const DevPlan* __restrict__ P, int m, const int32_t* __restrict__ start,
-                           const int32_t* __restrict__ cnt, const int32_t* __restrict__ ev,
-                           int32_t* __restrict__ ev2, int32_t* __restrict__ long_list) {
-    pdl_entry();
-    const int64_t b = P->it[m].b;
-    const int lane = threadIdx.x & 31;
-    const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-    for (int64_t beta = warp; beta < b; beta += nwarps) {
-        const int32_t s0 = start[beta], len = cnt[beta];
-        if (len > kLongSeg) {  // k3_segsort_long takes it: long_list = {count, buckets...}
-            if (lane == 0) long_list[1 + atomicAdd(&long_list[0], 1)] = static_cast<int32_t>(beta);
-            continue;
-        }
-        for (int32_t e = lane; e < len; e += 32) {
-            const int32_t key = ev[s0 + e];
-            int32_t rank = 0;
-            for (int32_t o = 0; o < len; ++o) rank += ev[s0 + o] < key;
-            ev2[s0 + rank] = key;
-        }
-    }
-}
-
-// Long segments (small b): one CTA per bucket sorts the segment's keys in
-// shared memory with a bitonic network (keys are unique; padding sorts last);
-// segments longer than the shared buffer fall back to rank counting.
+// Each bucket's events in ascending tone order (keys j*4+d are unique per
+// bucket).  One launch, two block roles: the first `long_blocks` CTAs take
+// the long segments the scan listed (small b) -- a bitonic network in shared
+// memory, rank counting for segments beyond the buffer -- and the warps of
+// the other CTAs take one short segment each by rank counting.
 constexpr int kLongT = 1024;
 __global__ void __launch_bounds__(kLongT)
-k3_segsort_long(const DevPlan* __restrict__ P, int m, const int32_t* __restrict__ start,
-                const int32_t* __restrict__ cnt, const int32_t* __restrict__ ev,
-                int32_t* __restrict__ ev2, const int32_t* __restrict__ long_list) {
+k3_segsort(const DevPlan* __restrict__ P, int m, const int32_t* __restrict__ start,
+           const int32_t* __restrict__ cnt, const int32_t* __restrict__ ev,
+           int32_t* __restrict__ ev2, const int32_t* __restrict__ long_list, int long_blocks) {
     pdl_entry();
     __shared__ int32_t ks[kLongSmem];
+    if (static_cast<int>(blockIdx.x) >= long_blocks) {
+        const int64_t b = P->it[m].b;
+        const int lane = threadIdx.x & 31;
+        const int64_t warp =
+            (static_cast<int64_t>(blockIdx.x - long_blocks) * blockDim.x + threadIdx.x) >> 5;
+        const int64_t nwarps = (static_cast<int64_t>(gridDim.x - long_blocks) * blockDim.x) >> 5;
+        for (int64_t beta = warp; beta < b; beta += nwarps) {
+            const int32_t s0 = start[beta], len = cnt[beta];
+            if (len > kLongSeg) continue;  // a long-role CTA sorts it
+            for (int32_t e = lane; e < len; e += 32) {
+                const int32_t key = ev[s0 + e];
+                int32_t rank = 0;
+                for (int32_t o = 0; o < len; ++o) rank += ev[s0 + o] < key;
+                ev2[s0 + rank] = key;
+            }
+        }
+        return;
+    }
     const int32_t nlong = long_list[0];
-    for (int32_t li = blockIdx.x; li < nlong; li += gridDim.x) {
+    for (int32_t li = blockIdx.x; li < nlong; li += long_blocks) {
         const int64_t beta = long_list[1 + li];
         const int32_t s0 = start[beta], len = cnt[beta];
         if (len > kLongSmem) {
@@ -357,33 +356,38 @@ k3_sum(const DevPlan* __restrict__ P, int m, const int32_t* __restrict__ start,
 
 // ---------------------------------------------------------------- select
 // keys: value bits + 1 for |.| >= 0 (NaN -> 0, ranks last); larger = earlier.
+// The launch also prepares what the kernels after it need, so no launch is
+// spent on it: (zero_p, zero_n) words cleared (the K4 rank counters), and the
+// radix select's state -- sel = {prefix, prefix mask, rank remaining, blocks
+// done} with rank = min(kth_dev ? *kth_dev : unbounded, kth_host, cap_kth),
+// also stored to *kth_out (K7's keep count), and a clear digit histogram
+// (each select pass's last block clears it again for the next).
 __global__ void keys_from_values(const double2* __restrict__ v, int64_t n_max,
                                  const int32_t* __restrict__ n_dev, double* __restrict__ mag,
-                                 uint64_t* __restrict__ key) {
+                                 uint64_t* __restrict__ key, uint32_t* __restrict__ zero_p,
+                                 int64_t zero_n, uint64_t* __restrict__ sel,
+                                 uint32_t* __restrict__ hist, int64_t kth_host,
+                                 const int32_t* __restrict__ kth_dev, int64_t cap_kth,
+                                 int32_t* __restrict__ kth_out) {
     pdl_entry();
+    GRID_LOOP(i, zero_n) zero_p[i] = 0u;
+    GRID_LOOP(i, kSelBins) hist[i] = 0u;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        int64_t kth = kth_host;
+        if (kth_dev && *kth_dev < kth) kth = *kth_dev;
+        if (kth > cap_kth) kth = cap_kth;
+        if (kth_out) *kth_out = static_cast<int32_t>(kth);
+        sel[0] = 0;
+        sel[1] = 0;
+        sel[2] = static_cast<uint64_t>(kth);
+        sel[3] = 0;
+    }
     const int64_t n = n_or(n_dev, n_max);
     GRID_LOOP(j, n) {
         const double2 x = v[j];
         const double mg = cabs_ref(x.x, x.y);
         if (mag) mag[j] = mg == mg ? mg : -1.0;
         key[j] = mg == mg ? static_cast<uint64_t>(__double_as_longlong(mg)) + 1ull : 0ull;
-    }
-}
-
-// sel = {prefix, prefix mask, rank remaining, blocks done}; also clears the
-// digit histogram for the first pass (each pass's last block clears it for
-// the next).
-__global__ void sel_init(uint64_t* sel, int64_t kth_host, const int32_t* kth_dev,
-                         int64_t cap_kth, uint32_t* hist) {
-    pdl_entry();
-    for (int i = threadIdx.x; i < kSelBins; i += blockDim.x) hist[i] = 0u;
-    if (threadIdx.x == 0) {
-        int64_t kth = kth_dev ? static_cast<int64_t>(*kth_dev) : kth_host;
-        if (kth > cap_kth) kth = cap_kth;
-        sel[0] = 0;
-        sel[1] = 0;
-        sel[2] = static_cast<uint64_t>(kth);
-        sel[3] = 0;
     }
 }
 
@@ -679,12 +683,16 @@ k4_rank(const int32_t* __restrict__ sel_idx, int64_t budget, const double* __res
     if (e < budget && rank) atomicAdd(&rank_out[e], rank);
 }
 
+// The last-ranked selection also gives the 0.2 * kth threshold.
 __global__ void k4_scatter(const int32_t* __restrict__ sel_idx, const int32_t* __restrict__ rank,
-                           int64_t budget, int32_t* __restrict__ order) {
+                           int64_t budget, int32_t* __restrict__ order,
+                           const double* __restrict__ mag, double* __restrict__ thr) {
     pdl_entry();
     GRID_LOOP(e, budget) {
         MSFFT_DCHECK(rank[e] >= 0 && rank[e] < budget);
-        order[rank[e]] = sel_idx[e];
+        const int32_t r = rank[e], idx = sel_idx[e];
+        order[r] = idx;
+        if (r == budget - 1) *thr = 0.2 * mag[idx];
     }
 }
 
@@ -740,20 +748,19 @@ k4_small(const DevPlan* __restrict__ P, int m, const double2* __restrict__ Y,
     if (j == budget - 1) *thr = 0.2 * sm[j];
 }
 
-__global__ void k4_thr(const int32_t* __restrict__ order, int64_t budget,
-                       const double* __restrict__ mag, double* thr) {
-    pdl_entry();
-    *thr = 0.2 * mag[order[budget - 1]];
-}
-
 // ---------------------------------------------------------------- K5
 // Every ranked bucket's round values staged in rank order, and the phases
 // of y0 / y_tau per (rank, stage) -- both read Y directly, so one launch.
 __global__ void k5_stage_phase(const DevPlan* __restrict__ P, int m,
                                const int32_t* __restrict__ order, const double2* __restrict__ Y,
                                double2* __restrict__ yr, double* __restrict__ phi,
-                               int32_t* __restrict__ pcode) {
+                               int32_t* __restrict__ pcode, uint32_t* __restrict__ zero_a,
+                               int64_t zero_an, uint32_t* __restrict__ zero_b, int64_t zero_bn) {
     pdl_entry();
+    // counters of later kernels of the chain, free by now: this iteration's
+    // K6 order counters and the next iteration's K3 bucket counts
+    GRID_LOOP(i, zero_an) zero_a[i] = 0u;
+    GRID_LOOP(i, zero_bn) zero_b[i] = 0u;
     const DevIter& it = P->it[m];
     const int nr = it.nrounds, ns = nr - 1;
     const int64_t total = it.budget * nr;
@@ -1036,16 +1043,6 @@ __global__ void k6_runs(const int64_t* __restrict__ cand_f, const double2* __res
     }
 }
 
-__global__ void k6_newf(const int64_t* __restrict__ cand_f, const int32_t* __restrict__ byf,
-                        const int32_t* __restrict__ naccepted, const int32_t* __restrict__ newflag,
-                        const int32_t* __restrict__ newpos, int64_t* __restrict__ newf) {
-    pdl_entry();
-    const int64_t A = naccepted[0];
-    GRID_LOOP(p, A) {
-        if (newflag[p]) newf[newpos[p]] = cand_f[byf[p]];
-    }
-}
-
 __global__ void k6_merge_acc(const int64_t* __restrict__ AF, const double2* __restrict__ AC,
                              const int32_t* __restrict__ acc_n, const int64_t* __restrict__ newf,
                              const int32_t* __restrict__ nnew_p, const int64_t* __restrict__ cand_f,
@@ -1084,10 +1081,19 @@ __global__ void k6_merge_new(const int64_t* __restrict__ AF, const int32_t* __re
                              const int32_t* __restrict__ naccepted,
                              const int32_t* __restrict__ newflag, const int32_t* __restrict__ newpos,
                              const double2* __restrict__ run_sum, int64_t* __restrict__ NF,
-                             double2* __restrict__ NC) {
+                             double2* __restrict__ NC, const int32_t* __restrict__ new_n,
+                             int32_t* __restrict__ acc_n_next, int32_t* __restrict__ nacc_next,
+                             int64_t acc_cap, int64_t* __restrict__ newf) {
     pdl_entry();
     const int64_t A = naccepted[0];
     const int an = acc_n[0];
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        // the next iteration's slots (the counters alternate per iteration, so
+        // nothing of this launch reads them): acc_n += new_n, accepted = 0
+        MSFFT_DCHECK(an + new_n[0] <= acc_cap);
+        acc_n_next[0] = an + new_n[0];
+        nacc_next[0] = 0;
+    }
     GRID_LOOP(p, A) {
         if (!newflag[p]) continue;
         const int64_t fr = cand_f[byf[p]];
@@ -1097,13 +1103,14 @@ __global__ void k6_merge_new(const int64_t* __restrict__ AF, const int32_t* __re
             if (AF[mid] < fr) lo = mid + 1; else hi = mid;
         }
         const double2 sum = run_sum[p];
+        newf[newpos[p]] = fr;  // the ascending new-f list k6_merge_acc searches
         NF[lo + newpos[p]] = fr;
         NC[lo + newpos[p]] = make_double2(0.0 + sum.x, 0.0 + sum.y);
     }
 }
 
 // budget <= 1024: the whole found-map merge in one CTA (same ordering rules
-// and arithmetic as k6_sortf .. k6_count): accepted candidates ranked by
+// and arithmetic as k6_sortf .. k6_merge_acc): accepted candidates ranked by
 // (f, rank) in shared memory, run sums in rank order, block scan of the "new
 // f" flags, then the merge into the ascending accumulated list.
 constexpr int kSmallK6 = 1024;
@@ -1112,8 +1119,9 @@ constexpr int64_t kK6StageMax = 8192;   // accumulated f staged in its shared me
 __global__ void __launch_bounds__(kSmallK6)
 k6_small(const DevPlan* __restrict__ P, int m, const int64_t* __restrict__ cand_f,
          const double2* __restrict__ cand_v, const int64_t* __restrict__ AF_g,
-         const double2* __restrict__ AC, int32_t* __restrict__ scal, int64_t* __restrict__ NF,
-         double2* __restrict__ NC, int32_t stage_cap) {
+         const double2* __restrict__ AC, const int32_t* __restrict__ acc_n,
+         int32_t* __restrict__ acc_n_next, int32_t* __restrict__ nacc_next,
+         int64_t* __restrict__ NF, double2* __restrict__ NC, int32_t stage_cap) {
     pdl_entry();
     // the accumulated f list is binary-searched per accepted f: staged in
     // shared memory (dynamic, stage_cap entries) when it fits, so the
@@ -1128,7 +1136,7 @@ k6_small(const DevPlan* __restrict__ P, int m, const int64_t* __restrict__ cand_
     __shared__ int32_t s_acc;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t budget = P->it[m].budget;
-    if (tid == 0) s_acc = scal[0];
+    if (tid == 0) s_acc = acc_n[0];
     const int64_t fr = tid < budget ? cand_f[tid] : -1;
     __syncthreads();
     const int an = s_acc;
@@ -1237,24 +1245,12 @@ k6_small(const DevPlan* __restrict__ P, int m, const int64_t* __restrict__ cand_
     __syncthreads();
     if (tid == 0) {
         MSFFT_DCHECK(an + nnew <= P->acc_cap);
-        scal[0] = an + nnew;
-        scal[4] = 0;
+        acc_n_next[0] = an + nnew;
+        nacc_next[0] = 0;
     }
 }
 
-__global__ void k6_count(int32_t* scal, int64_t acc_cap) {
-    pdl_entry();
-    MSFFT_DCHECK(scal[0] + scal[1] <= acc_cap);
-    scal[0] += scal[1];  // acc_n += new_n
-    scal[4] = 0;         // accepted counter for the next iteration
-}
-
 // ---------------------------------------------------------------- K7
-__global__ void k7_kth(int32_t* scal, int64_t K) {
-    pdl_entry();
-    scal[2] = static_cast<int32_t>(std::min<int64_t>(scal[0], K));
-}
-
 __global__ void k7_emit(const int32_t* __restrict__ sel_idx, const int32_t* __restrict__ scal,
                         const int64_t* __restrict__ AF, const double2* __restrict__ AC,
                         int64_t* __restrict__ out_f, double2* __restrict__ out_c,
@@ -1263,7 +1259,7 @@ __global__ void k7_emit(const int32_t* __restrict__ sel_idx, const int32_t* __re
     const int64_t keep = scal[2];
     GRID_LOOP(p, keep) {
         const int32_t j = sel_idx[p];
-        MSFFT_DCHECK(j >= 0 && j < scal[0]);
+        MSFFT_DCHECK(j >= 0);
         out_f[p] = AF[j];
         out_c[p] = AC[j];
     }
@@ -1331,9 +1327,9 @@ WideDecoder::WideDecoder(const DevPlan& plan, int64_t acc_cap, int64_t b_max, in
     smem_attr(k6_small, static_cast<size_t>(k6_stage_cap_) * sizeof(int64_t));
 }
 
+// sel_ and hist_ were prepared by the keys_from_values launch before it.
 void WideDecoder::select_kth(const uint64_t* key, int64_t n_max, const int32_t* n_dev,
-                             int64_t kth_host, const int32_t* kth_dev, cudaStream_t st) {
-    launch_pdl(pdl_, sel_init, 1, kT, 0, st, sel_.get(), kth_host, kth_dev, n_max, hist_.get());
+                             cudaStream_t st) {
     // the top 24 bits over the whole grid, the low 40 in one CTA
     for (int top = 64; top > 40;) {
         const int width = std::min(kSelBits, top);
@@ -1401,10 +1397,14 @@ void WideDecoder::enqueue(double2* y, const int64_t* sigma, const int64_t* sigma
                           int m0, int m1) {
     const DevPlan& H = hplan_;
     const DevPlan* P = dplan_.get();
-    int32_t* acc_n = scal_.get();       // [0]
-    int32_t* new_n = scal_.get() + 1;   // [1]
-    int32_t* kth = scal_.get() + 2;     // [2]
-    int32_t* naccepted = scal_.get() + 4;
+    // scal_: [1] new_n, [2] kth; the accumulated count and the accepted
+    // counter alternate between two slots per iteration ([0]/[5], [4]/[6]),
+    // so an iteration's last kernel can publish the next iteration's values
+    // while its own blocks still read the current ones
+    int32_t* new_n = scal_.get() + 1;
+    int32_t* kth = scal_.get() + 2;
+    auto acc_slot = [&](int par) { return scal_.get() + (par ? 5 : 0); };
+    auto nacc_slot = [&](int par) { return scal_.get() + (par ? 6 : 4); };
     if (m0 == 0) zero_async(pdl_, scal_.get(), 8 * sizeof(int32_t), st);
     const unsigned gA = grid_of(acc_cap_ * 3);
     for (int m = m0; m < m1; ++m) {
@@ -1414,19 +1414,24 @@ void WideDecoder::enqueue(double2* y, const int64_t* sigma, const int64_t* sigma
         const int cur = m & 1, nxt = cur ^ 1;
         const int64_t* AF = acc_f_[cur].get();
         const double2* AC = acc_c_[cur].get();
+        const int32_t* acc_n = acc_slot(cur);
+        int32_t* naccepted = nacc_slot(cur);
         if (m > 0) {
-            // ---- K3
-            zero_async(pdl_, cnt_.get(), b * sizeof(int32_t), st);
+            // ---- K3 (cnt_ was cleared by the previous iteration's k5_stage_phase)
             launch_pdl(pdl_, k3_tones, grid_of(acc_cap_ * nr), kT, 0, st, P, m, sigma, AF, AC, acc_n, tone_u_.get(),
                                                       tone_i_.get(), gc_.get(), cnt_.get(), cursor_.get(),
                                                       long_.get(), rot_.get());
-            launch_pdl(pdl_, scan_kernel, 1, kScanT, 0, st, cnt_.get(), b, nullptr, start_.get(), nullptr);
+            launch_pdl(pdl_, scan_kernel, 1, kScanT, 0, st, cnt_.get(), b, nullptr, start_.get(), nullptr,
+                       long_.get());
             launch_pdl(pdl_, k3_scatter, gA, kT, 0, st, P, m, acc_n, tone_i_.get(), start_.get(), cursor_.get(),
                                           ev_.get());
-            launch_pdl(pdl_, k3_segsort, grid_of(b * 32), kT, 0, st, P, m, start_.get(), cnt_.get(), ev_.get(),
-                                                       ev2_.get(), long_.get());
-            launch_pdl(pdl_, k3_segsort_long, static_cast<unsigned>(std::min<int64_t>(b, 148 * 2)), kLongT, 0, st,
-                P, m, start_.get(), cnt_.get(), ev_.get(), ev2_.get(), long_.get());
+            {
+                const int long_blocks = static_cast<int>(std::min<int64_t>(b, 148 * 2));
+                const int short_blocks = static_cast<int>(
+                    std::max<int64_t>(1, std::min<int64_t>((b * 32 + kLongT - 1) / kLongT, 148 * 4)));
+                launch_pdl(pdl_, k3_segsort, static_cast<unsigned>(long_blocks + short_blocks), kLongT, 0, st,
+                           P, m, start_.get(), cnt_.get(), ev_.get(), ev2_.get(), long_.get(), long_blocks);
+            }
             launch_pdl(pdl_, k3_sum, grid_of(nr * b * 32), kT, 0, st, P, m, start_.get(), cnt_.get(), ev2_.get(),
                                                         gc_.get(), rot_.get(), Y);
             MSFFT_LAUNCH_CHECK("wide K3");
@@ -1435,43 +1440,56 @@ void WideDecoder::enqueue(double2* y, const int64_t* sigma, const int64_t* sigma
         if (b <= kSmallK4) {
             launch_pdl(pdl_, k4_small, 1, kSmallK4, 0, st, P, m, Y, mag_.get(), order_.get(), thr_.get());
         } else {
-            launch_pdl(pdl_, keys_from_values, grid_of(b), kT, 0, st, Y, b, nullptr, mag_.get(), key_.get());
-            select_kth(key_.get(), b, nullptr, budget, nullptr, st);
+            // also clears the K4 rank counters (pos_)
+            launch_pdl(pdl_, keys_from_values, grid_of(b), kT, 0, st, Y, b, nullptr, mag_.get(), key_.get(),
+                       reinterpret_cast<uint32_t*>(pos_.get()), budget, sel_.get(), hist_.get(), budget,
+                       nullptr, b, nullptr);
+            select_kth(key_.get(), b, nullptr, st);
             compact_selected(key_.get(), b, nullptr, sel_idx_.get(), st);
             {
                 const unsigned tiles = static_cast<unsigned>((budget + kT - 1) / kT);
                 const unsigned split = std::max(1u, std::min(64u, 1184u / tiles));
-                zero_async(pdl_, pos_.get(), budget * sizeof(int32_t), st);
                 launch_pdl(pdl_, k4_rank, dim3(tiles, split), kT, 0, st, sel_idx_.get(), budget, mag_.get(), pos_.get());
                 launch_pdl(pdl_, k4_scatter, grid_of(budget), kT, 0, st, sel_idx_.get(), pos_.get(), budget,
-                                                           order_.get());
+                                                           order_.get(), mag_.get(), thr_.get());
             }
-            launch_pdl(pdl_, k4_thr, 1, 1, 0, st, order_.get(), budget, mag_.get(), thr_.get());
         }
         // ---- K5
-        launch_pdl(pdl_, k5_stage_phase, grid_of(budget * nr), kT, 0, st, P, m, order_.get(), Y, yr_.get(),
-                   phi_.get(), pcode_.get());
+        // k5_stage_phase also clears the counters of kernels further down the
+        // chain: the K6 order counters of this iteration (the f-bucket counts
+        // or the all-pairs positions; pos_ is free once K4 has scattered) and
+        // the next iteration's K3 bucket counts
+        const bool k6_small_path = budget <= kSmallK6 && acc_cap_ <= kSmallK6Acc;
+        uint32_t* zero_a = nullptr;
+        int64_t zero_an = 0;
+        if (!k6_small_path) {
+            zero_a = reinterpret_cast<uint32_t*>(budget >= kF6BucketMin ? f6cnt_.get() : pos_.get());
+            zero_an = budget >= kF6BucketMin ? int64_t{kF6B} : budget;
+        }
+        const int64_t zero_bn = m + 1 < H.iters ? H.it[m + 1].b : 0;
+        launch_pdl(pdl_, k5_stage_phase, grid_of(std::max(budget * nr, std::max(zero_an, zero_bn))), kT, 0, st,
+                   P, m, order_.get(), Y, yr_.get(), phi_.get(), pcode_.get(), zero_a, zero_an,
+                   reinterpret_cast<uint32_t*>(cnt_.get()), zero_bn);
         launch_pdl(pdl_, k5_locate, grid_of(budget * 32), kT, 0, st, P, m, sigma_inv, order_.get(), mag_.get(),
                                                        thr_.get(), yr_.get(), phi_.get(),
                                                        pcode_.get(), cand_f_.get(), cand_v_.get(),
                                                        err);
         MSFFT_LAUNCH_CHECK("wide K4/K5");
         // ---- K6
-        if (budget <= kSmallK6 && acc_cap_ <= kSmallK6Acc) {
+        if (k6_small_path) {
             launch_pdl(pdl_, k6_small, 1, kSmallK6, k6_stage_cap_ * sizeof(int64_t), st, P, m,
-                       cand_f_.get(), cand_v_.get(), AF, AC, scal_.get(), acc_f_[nxt].get(),
-                       acc_c_[nxt].get(), static_cast<int32_t>(k6_stage_cap_));
+                       cand_f_.get(), cand_v_.get(), AF, AC, acc_n, acc_slot(nxt), nacc_slot(nxt),
+                       acc_f_[nxt].get(), acc_c_[nxt].get(), static_cast<int32_t>(k6_stage_cap_));
         } else {
             if (budget >= kF6BucketMin) {
                 int nbits = 0;
                 while ((int64_t{1} << nbits) < H.n) ++nbits;
                 const int shift = std::max(0, nbits - 12);  // f >> shift < 4096
-                zero_async(pdl_, f6cnt_.get(), kF6B * sizeof(int32_t), st);
                 launch_pdl(pdl_, k6b_count, grid_of(std::max<int64_t>(budget, kF6B)), kT, 0, st,
                            cand_f_.get(), budget, shift, f6cnt_.get(), f6cur_.get(), naccepted);
                 launch_pdl(pdl_, scan_kernel, 1, kScanT, 0, st, f6cnt_.get(), int64_t{kF6B}, nullptr,
-                           f6start_.get(), f6start_.get() + kF6B);
-                // newf_ is free until k6_newf: it holds the keys of the bucket sort
+                           f6start_.get(), f6start_.get() + kF6B, nullptr);
+                // newf_ is free until k6_merge_new: it holds the keys of the bucket sort
                 launch_pdl(pdl_, k6b_scatter, grid_of(budget), kT, 0, st, cand_f_.get(), budget, shift,
                            f6start_.get(), f6cur_.get(), pos_.get(), newf_.get());
                 launch_pdl(pdl_, k6b_sort, grid_of(budget), kT, 0, st, shift, f6start_.get(),
@@ -1479,7 +1497,6 @@ void WideDecoder::enqueue(double2* y, const int64_t* sigma, const int64_t* sigma
             } else {
                 const unsigned tiles = static_cast<unsigned>((budget + kT - 1) / kT);
                 const unsigned split = std::max(1u, std::min(64u, 1184u / tiles));
-                zero_async(pdl_, pos_.get(), budget * sizeof(int32_t), st);
                 launch_pdl(pdl_, k6_sortf, dim3(tiles, split), kT, 0, st, cand_f_.get(), budget, pos_.get());
                 launch_pdl(pdl_, k6_scatter, grid_of(budget), kT, 0, st, cand_f_.get(), pos_.get(), budget, byf_.get(),
                                                            naccepted);
@@ -1487,28 +1504,30 @@ void WideDecoder::enqueue(double2* y, const int64_t* sigma, const int64_t* sigma
             launch_pdl(pdl_, k6_runs, grid_of(budget), kT, 0, st, cand_f_.get(), cand_v_.get(), byf_.get(),
                                                     naccepted, AF, acc_n, cand_sum_.get(),
                                                     newflag_.get());
-            launch_pdl(pdl_, scan_kernel, 1, kScanT, 0, st, newflag_.get(), budget, naccepted, newpos_.get(), new_n);
-            launch_pdl(pdl_, k6_newf, grid_of(budget), kT, 0, st, cand_f_.get(), byf_.get(), naccepted,
-                                                    newflag_.get(), newpos_.get(), newf_.get());
+            launch_pdl(pdl_, scan_kernel, 1, kScanT, 0, st, newflag_.get(), budget, naccepted, newpos_.get(), new_n,
+                       nullptr);
+            // new entries first (they also list the new f for the accumulated
+            // entries' offsets and publish the next iteration's counters)
+            launch_pdl(pdl_, k6_merge_new, grid_of(budget), kT, 0, st, AF, acc_n, cand_f_.get(), byf_.get(),
+                                                         naccepted, newflag_.get(), newpos_.get(),
+                                                         cand_sum_.get(), acc_f_[nxt].get(),
+                                                         acc_c_[nxt].get(), new_n, acc_slot(nxt),
+                                                         nacc_slot(nxt), acc_cap_, newf_.get());
             launch_pdl(pdl_, k6_merge_acc, grid_of(acc_cap_), kT, 0, st, AF, AC, acc_n, newf_.get(), new_n,
                                                            cand_f_.get(), byf_.get(), naccepted,
                                                            cand_sum_.get(), acc_f_[nxt].get(),
                                                            acc_c_[nxt].get());
-            launch_pdl(pdl_, k6_merge_new, grid_of(budget), kT, 0, st, AF, acc_n, cand_f_.get(), byf_.get(),
-                                                         naccepted, newflag_.get(), newpos_.get(),
-                                                         cand_sum_.get(), acc_f_[nxt].get(),
-                                                         acc_c_[nxt].get());
-            launch_pdl(pdl_, k6_count, 1, 1, 0, st, scal_.get(), acc_cap_);
         }
         MSFFT_LAUNCH_CHECK("wide K6");
     }
     if (m1 < H.iters) return;
     // ---- K7: the K largest |c| (stable over ascending f), emitted in f order
     const int fin = H.iters & 1;
+    const int32_t* acc_n = acc_slot(fin);
     launch_pdl(pdl_, keys_from_values, grid_of(acc_cap_), kT, 0, st, acc_c_[fin].get(), acc_cap_, acc_n, nullptr,
-                                                       key_.get());
-    launch_pdl(pdl_, k7_kth, 1, 1, 0, st, scal_.get(), H.k);
-    select_kth(key_.get(), acc_cap_, acc_n, 0, kth, st);
+                                                       key_.get(), nullptr, int64_t{0}, sel_.get(), hist_.get(),
+                                                       int64_t{H.k}, acc_n, acc_cap_, kth);
+    select_kth(key_.get(), acc_cap_, acc_n, st);
     compact_selected(key_.get(), acc_cap_, acc_n, sel_idx_.get(), st);
     launch_pdl(pdl_, k7_emit, grid_of(H.k), kT, 0, st, sel_idx_.get(), scal_.get(), acc_f_[fin].get(),
                                          acc_c_[fin].get(), out_f, out_c, out_count);

@@ -57,8 +57,7 @@ private:
     void enqueue(double2* y, const int64_t* sigma, const int64_t* sigma_inv, int32_t* err,
                  int64_t* out_f, double2* out_c, int64_t* out_count, cudaStream_t st, int m0,
                  int m1);
-    void select_kth(const uint64_t* key, int64_t n_max, const int32_t* n_dev, int64_t kth_host,
-                    const int32_t* kth_dev, cudaStream_t st);
+    void select_kth(const uint64_t* key, int64_t n_max, const int32_t* n_dev, cudaStream_t st);
     void compact_selected(const uint64_t* key, int64_t n_max, const int32_t* n_dev,
                           int32_t* out_idx, cudaStream_t st);
 
