@@ -593,8 +593,8 @@ bool Plan::val_fused_ok(const void* d_x, int64_t x_stride) const {
 }
 
 // Item list of the validating fused launch (fused.cu fused_val_kernel).
-// Chunk = the signals whose rows fill val_chunk_bytes_ (default 64 MB, half
-// the L2).  Per chunk: its validation items, then its packed encode items
+// Chunk = the signals whose rows fill val_chunk_bytes_ (default 32 MB: one
+// C4 signal).  Per chunk: its validation items, then its packed encode items
 // (val_elag_ chunks later), then the decodes of the chunk val_dlag_ chunks
 // before.  Packing: the chunk's (signal, iteration, round-group) sub-tasks,
 // first-fit decreasing on b into CTAs of 256 threads (<= kMaxPack each, their
@@ -617,7 +617,13 @@ const Plan::ValSet& Plan::val_for(int64_t batch, int64_t x_stride) {
     // and the scan's ring of 16-KB slots -- as large as two CTAs per SM allow
     size_t smem = std::max(fused_smem_, static_cast<size_t>(val_smem_kb_) << 10);
     std::vector<EncTask> proto;
-    append_tasks(proto, 0, 1, false);
+    // one sub-task per merged t' segment (MSFFT_VAL_SPLIT=0: per round group):
+    // 3-4x shorter gather chains per item, so an item's loads finish before
+    // the scan reaches its signal (a late gather misses: the scan's lines are
+    // evict_first) -- DRAM bytes per step and the step time both drop
+    bool vsplit = true;
+    if (const char* e = std::getenv("MSFFT_VAL_SPLIT")) vsplit = std::atoi(e) != 0;
+    append_tasks(proto, 0, 1, vsplit);
     struct Bin {
         std::vector<EncTask> subs;
         int threads = 0;
@@ -710,8 +716,8 @@ const Plan::ValSet& Plan::val_for(int64_t batch, int64_t x_stride) {
     // E(c) goes right before V(c + eoff): eoff = 1 after its own scan, 0
     // before it, < 0 that many chunks ahead of it (MSFFT_VAL_EOFF).  Default
     // -4 with policy 7 (gather loads evict_last, scan copies evict_first):
-    // the gathers fetch their lines ~4 chunks (~35 us) before the scan passes
-    // them, the scan hits those lines and its own lines do not push them out.
+    // the gathers fetch their lines 4 chunks (4 signals at C4, ~20 us) before
+    // the scan passes them, the scan hits those lines and its own lines do not push them out.
     // The scan-first order (eoff >= 1) gets no L2 hits on B200 at all: the
     // latency-bound gathers of a chunk run long after the scan's lines are
     // evicted (profiles/r02c).

@@ -196,8 +196,8 @@ private:
     std::map<int64_t, FusedSet> fused_;
     std::map<std::pair<int64_t, int64_t>, ValSet> val_;
     bool val_fused_enabled_ = true;             // MSFFT_VAL_FUSED
-    int64_t val_chunk_bytes_ = int64_t{64} << 20;  // MSFFT_VAL_CHUNK_MB: x bytes per chunk
-    int64_t val_item_bytes_ = int64_t{512} << 10;  // MSFFT_VAL_ITEM_KB: one validation item
+    int64_t val_chunk_bytes_ = int64_t{32} << 20;  // MSFFT_VAL_CHUNK_MB: x bytes per chunk
+    int64_t val_item_bytes_ = int64_t{1024} << 10;  // MSFFT_VAL_ITEM_KB: one validation item
     int64_t val_dlag_ = 8;                      // MSFFT_VAL_DLAG: chunks a decode trails
     int64_t val_elag_ = 0;                      // MSFFT_VAL_ELAG: chunks an encode trails its scan
     int64_t val_smem_kb_ = 64;                  // MSFFT_VAL_SMEM_KB: dynamic smem floor

@@ -18,7 +18,7 @@ from paper_2011_05698_b200.workloads import algo_seed, make_batch, signal_seed  
 
 KEYS = ("MSFFT_VAL_FUSED", "MSFFT_VAL_CHUNK_MB", "MSFFT_VAL_ITEM_KB", "MSFFT_VAL_DLAG",
         "MSFFT_VAL_ELAG", "MSFFT_VAL_DEBUG", "MSFFT_VAL_EFIRST",
-        "MSFFT_VAL_POLICY", "MSFFT_VAL_EOFF", "MSFFT_VAL_SMEM_KB")
+        "MSFFT_VAL_POLICY", "MSFFT_VAL_EOFF", "MSFFT_VAL_SMEM_KB", "MSFFT_VAL_SPLIT")
 reps = int(os.environ.get("REPS", "7"))
 n, k, B = 1 << 22, 64, int(os.environ.get("BATCH", "1024"))
 dev = torch.device("cuda", 0)
