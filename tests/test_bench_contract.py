@@ -24,7 +24,7 @@ def test_traffic_records_match_bench_workload():
 
 def test_records_are_for_the_current_sources():
     """The committed summaries were captured on the native sources in this
-    tree (re-capture with tools/r02c_evidence.sh after changing csrc/)."""
+    tree (re-capture with tools/evidence.sh after changing csrc/)."""
     from paper_2011_05698_b200.provenance import csrc_sha256
     cur = csrc_sha256()
     for name in ("fused_traffic.json", "fused_val_traffic.json", "encode_traffic.json",

@@ -1,9 +1,9 @@
 # Round-2 (final session) evidence on the current code, under gpurun.  Each
 # ncu pass runs only after the same command exited 0 alone.  Outputs land in
-# gpurun_out/r02c/; the summaries bench.py reads are written there too (copy
+# gpurun_out/r02d/; the summaries bench.py reads are written there too (copy
 # them to profiles/ after checking).
 set -x
-O=gpurun_out/r02c; mkdir -p $O
+O=${EVIDENCE_OUT:-gpurun_out/r02d}; mkdir -p $O
 M="gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__inst_executed_pipe_fp64.sum,sm__sass_thread_inst_executed_op_dadd_pred_on.sum,sm__sass_thread_inst_executed_op_dmul_pred_on.sum,sm__sass_thread_inst_executed_op_dfma_pred_on.sum,sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active,smsp__issue_active.avg.pct_of_peak_sustained_active"
 W="C4: 1024 x N=2^22, K=64, complex64 (tools/profile_c4.py)"
 # C4 batch: fused, validation scan, serial encode/decode (ncu --set full)
@@ -43,4 +43,12 @@ MSFFT_PROFILE_AFTER_PLAN=1 ncu --profile-from-start off --clock-control none --c
 python tools/stage_roofline.py $O/c5_stages.csv --workload "C5: N=2^27, K=10^4, c128 (tools/run_c5.py, serial path)" > $O/c5_stage_roofline.json
 python tools/run_c5.py --no-stages --reps 5 > $O/c5_run.json 2> $O/c5_run.err
 python tools/configs_table.py > $O/configs_table.log 2>&1
+# the bench itself on this box, reading the captures above (same native
+# sources, so roofline.traffic / pipes are filled), then the reference arm
+for f in fused_val_ncu_summary fused_val_traffic fused_ncu_summary fused_traffic validate_ncu_summary \
+         validate_traffic encode_ncu_summary encode_traffic decode_c4_ncu_summary; do
+    cp $O/$f.json profiles/$f.json
+done
+python bench.py > $O/bench.json 2> $O/bench.err
+python bench.py --impl reference > $O/bench_reference.json 2> $O/bench_reference.err
 ls -la $O
