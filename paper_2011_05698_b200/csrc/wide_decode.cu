@@ -1012,11 +1012,15 @@ __global__ void k6_scatter(const int64_t* __restrict__ cand_f, const int32_t* __
 }
 
 // Run starts: the found-map sum in rank order, presence in the accumulated
-// list, and the "new f" flag.
+// list, and the "new f" flag.  The one binary search over the accumulated
+// list serves the whole merge: apos[p] = the run's insertion point (read by
+// k6_merge_new) and hit[j] = p for an f already at position j (read, and
+// reset to -1, by k6_merge_acc), so neither searches again.
 __global__ void k6_runs(const int64_t* __restrict__ cand_f, const double2* __restrict__ cand_v,
                         const int32_t* __restrict__ byf, const int32_t* __restrict__ naccepted,
                         const int64_t* __restrict__ AF, const int32_t* __restrict__ acc_n,
-                        double2* __restrict__ run_sum, int32_t* __restrict__ newflag) {
+                        double2* __restrict__ run_sum, int32_t* __restrict__ newflag,
+                        int32_t* __restrict__ apos, int32_t* __restrict__ hit) {
     pdl_entry();
     const int64_t A = naccepted[0];
     const int an = acc_n[0];
@@ -1038,6 +1042,8 @@ __global__ void k6_runs(const int64_t* __restrict__ cand_f, const double2* __res
                 if (AF[mid] < f) lo = mid + 1; else hi = mid;
             }
             flag = (lo < an && AF[lo] == f) ? 0 : 1;
+            apos[p] = lo;
+            if (!flag) hit[lo] = static_cast<int32_t>(p);
         }
         newflag[p] = flag;
     }
@@ -1045,14 +1051,12 @@ __global__ void k6_runs(const int64_t* __restrict__ cand_f, const double2* __res
 
 __global__ void k6_merge_acc(const int64_t* __restrict__ AF, const double2* __restrict__ AC,
                              const int32_t* __restrict__ acc_n, const int64_t* __restrict__ newf,
-                             const int32_t* __restrict__ nnew_p, const int64_t* __restrict__ cand_f,
-                             const int32_t* __restrict__ byf, const int32_t* __restrict__ naccepted,
+                             const int32_t* __restrict__ nnew_p, int32_t* __restrict__ hit,
                              const double2* __restrict__ run_sum, int64_t* __restrict__ NF,
                              double2* __restrict__ NC) {
     pdl_entry();
     const int64_t an = acc_n[0];
     const int nnew = nnew_p[0];
-    const int A = naccepted[0];
     GRID_LOOP(j, an) {
         const int64_t fj = AF[j];
         int lo = 0, hi = nnew;
@@ -1061,15 +1065,12 @@ __global__ void k6_merge_acc(const int64_t* __restrict__ AF, const double2* __re
             if (newf[mid] < fj) lo = mid + 1; else hi = mid;
         }
         const int before = lo;
-        int plo = 0, phi2 = A;
-        while (plo < phi2) {
-            const int mid = (plo + phi2) >> 1;
-            if (cand_f[byf[mid]] < fj) plo = mid + 1; else phi2 = mid;
-        }
         double2 c = AC[j];
-        if (plo < A && cand_f[byf[plo]] == fj) {
-            const double2 add = run_sum[plo];
+        const int32_t p = hit[j];  // the accepted run with this f (k6_runs), or -1
+        if (p >= 0) {
+            const double2 add = run_sum[p];
             c = make_double2(c.x + add.x, c.y + add.y);
+            hit[j] = -1;
         }
         NF[j + before] = fj;
         NC[j + before] = c;
@@ -1083,7 +1084,8 @@ __global__ void k6_merge_new(const int64_t* __restrict__ AF, const int32_t* __re
                              const double2* __restrict__ run_sum, int64_t* __restrict__ NF,
                              double2* __restrict__ NC, const int32_t* __restrict__ new_n,
                              int32_t* __restrict__ acc_n_next, int32_t* __restrict__ nacc_next,
-                             int64_t acc_cap, int64_t* __restrict__ newf) {
+                             int64_t acc_cap, int64_t* __restrict__ newf,
+                             const int32_t* __restrict__ apos) {
     pdl_entry();
     const int64_t A = naccepted[0];
     const int an = acc_n[0];
@@ -1097,11 +1099,8 @@ __global__ void k6_merge_new(const int64_t* __restrict__ AF, const int32_t* __re
     GRID_LOOP(p, A) {
         if (!newflag[p]) continue;
         const int64_t fr = cand_f[byf[p]];
-        int lo = 0, hi = an;
-        while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if (AF[mid] < fr) lo = mid + 1; else hi = mid;
-        }
+        const int lo = apos[p];  // lower bound of fr in the accumulated list (k6_runs)
+        MSFFT_DCHECK(lo >= 0 && lo <= an && (lo == an || AF[lo] > fr) && (lo == 0 || AF[lo - 1] < fr));
         const double2 sum = run_sum[p];
         newf[newpos[p]] = fr;  // the ascending new-f list k6_merge_acc searches
         NF[lo + newpos[p]] = fr;
@@ -1320,6 +1319,10 @@ WideDecoder::WideDecoder(const DevPlan& plan, int64_t acc_cap, int64_t b_max, in
     newflag_.reset(Q);
     newpos_.reset(Q);
     newf_.reset(Q);
+    // hit_[j] = accepted run whose f is already at accumulated position j; -1
+    // between iterations (k6_merge_acc resets what k6_runs set)
+    hit_.reset(static_cast<size_t>(acc_cap_));
+    MSFFT_CUDA(cudaMemset(hit_.get(), 0xff, static_cast<size_t>(acc_cap_) * sizeof(int32_t)));
     if (const char* e = std::getenv("MSFFT_WIDE_GRAPH")) use_graphs_ = std::atoi(e) != 0;
     if (const char* e = std::getenv("MSFFT_WIDE_PDL")) pdl_ = std::atoi(e) != 0;
     // kernel attributes are set before any capture
@@ -1503,7 +1506,7 @@ void WideDecoder::enqueue(double2* y, const int64_t* sigma, const int64_t* sigma
             }
             launch_pdl(pdl_, k6_runs, grid_of(budget), kT, 0, st, cand_f_.get(), cand_v_.get(), byf_.get(),
                                                     naccepted, AF, acc_n, cand_sum_.get(),
-                                                    newflag_.get());
+                                                    newflag_.get(), pos_.get(), hit_.get());
             launch_pdl(pdl_, scan_kernel, 1, kScanT, 0, st, newflag_.get(), budget, naccepted, newpos_.get(), new_n,
                        nullptr);
             // new entries first (they also list the new f for the accumulated
@@ -1512,10 +1515,9 @@ void WideDecoder::enqueue(double2* y, const int64_t* sigma, const int64_t* sigma
                                                          naccepted, newflag_.get(), newpos_.get(),
                                                          cand_sum_.get(), acc_f_[nxt].get(),
                                                          acc_c_[nxt].get(), new_n, acc_slot(nxt),
-                                                         nacc_slot(nxt), acc_cap_, newf_.get());
+                                                         nacc_slot(nxt), acc_cap_, newf_.get(), pos_.get());
             launch_pdl(pdl_, k6_merge_acc, grid_of(acc_cap_), kT, 0, st, AF, AC, acc_n, newf_.get(), new_n,
-                                                           cand_f_.get(), byf_.get(), naccepted,
-                                                           cand_sum_.get(), acc_f_[nxt].get(),
+                                                           hit_.get(), cand_sum_.get(), acc_f_[nxt].get(),
                                                            acc_c_[nxt].get());
         }
         MSFFT_LAUNCH_CHECK("wide K6");

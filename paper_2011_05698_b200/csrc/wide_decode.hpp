@@ -83,7 +83,7 @@ private:
     // K5 / K6
     DeviceBuffer<double2> yr_, cand_v_, cand_sum_;
     DeviceBuffer<double> phi_;
-    DeviceBuffer<int32_t> pcode_, pos_, byf_, newflag_, newpos_;
+    DeviceBuffer<int32_t> pcode_, pos_, byf_, newflag_, newpos_, hit_;
     DeviceBuffer<int64_t> cand_f_, newf_;
     DeviceBuffer<int32_t> f6cnt_, f6cur_, f6start_;  // K6 bucket sort of large budgets
     // outputs, copied to the caller's buffers after the graph
