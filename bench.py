@@ -515,6 +515,13 @@ def main():
                                            "same lines (fetched ~4 chunks ahead of the scan, "
                                            "which then hits them in L2)",
                       "launch_ms": vmain_avg, "share_of_step": vmain_avg / ms,
+                      "survey_8d_gather_metric": "roofline_gather: SURVEY 8(d) defines the "
+                                                 "filter-gather roofline on the distinct 32-B "
+                                                 "sectors of a transform that does not validate "
+                                                 "(the ASSUME_VALID kernel); this kernel also "
+                                                 "reads every sample for the finiteness scan, "
+                                                 "so its algorithmic bytes are all of x",
+                      "gather_sector_bytes_per_launch": alg_bytes,
                       "csrc_sha256": csrc} if val_fused else None),
         "roofline_gather": {"bound": "hbm",
                      "kernel": "fused_kernel (persistent: gather/window/fold/FFT + decode; "
