@@ -190,16 +190,22 @@ __global__ void k3_scatter(const DevPlan* __restrict__ P, int m, const int32_t* 
 
 // Each bucket's events in ascending tone order (keys j*4+d are unique per
 // bucket).  One launch, two block roles: the first `long_blocks` CTAs take
-// the long segments the scan listed (small b) -- a bitonic network in shared
-// memory, rank counting for segments beyond the buffer -- and the warps of
-// the other CTAs take one short segment each by rank counting.
+// the long segments the scan listed (small b) and the warps of the other CTAs
+// take one short segment each by rank counting.  A long segment's keys are
+// distinct integers below 4 * acc_n, so they sort through a bitmap in shared
+// memory (set a bit per key, popcount prefix over the words, emit the set
+// bits in order: five barriers whatever the length); when the key range does
+// not fit the buffer, a bitonic network, and rank counting for segments
+// beyond the buffer.
 constexpr int kLongT = 1024;
 __global__ void __launch_bounds__(kLongT)
 k3_segsort(const DevPlan* __restrict__ P, int m, const int32_t* __restrict__ start,
            const int32_t* __restrict__ cnt, const int32_t* __restrict__ ev,
-           int32_t* __restrict__ ev2, const int32_t* __restrict__ long_list, int long_blocks) {
+           int32_t* __restrict__ ev2, const int32_t* __restrict__ long_list, int long_blocks,
+           const int32_t* __restrict__ acc_n) {
     pdl_entry();
     __shared__ int32_t ks[kLongSmem];
+    __shared__ int32_t wtot[kLongT / 32];
     if (static_cast<int>(blockIdx.x) >= long_blocks) {
         const int64_t b = P->it[m].b;
         const int lane = threadIdx.x & 31;
@@ -219,9 +225,55 @@ k3_segsort(const DevPlan* __restrict__ P, int m, const int32_t* __restrict__ sta
         return;
     }
     const int32_t nlong = long_list[0];
+    const int32_t nwords = (4 * acc_n[0] + 31) >> 5;  // bitmap over the key range
     for (int32_t li = blockIdx.x; li < nlong; li += long_blocks) {
         const int64_t beta = long_list[1 + li];
         const int32_t s0 = start[beta], len = cnt[beta];
+        if (nwords <= kLongSmem) {
+            uint32_t* bm = reinterpret_cast<uint32_t*>(ks);
+            const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+            __syncthreads();  // the previous segment's emit is done
+            for (int32_t w = tid; w < nwords; w += kLongT) bm[w] = 0u;
+            __syncthreads();
+            for (int32_t e = tid; e < len; e += kLongT) {
+                const int32_t key = ev[s0 + e];
+                MSFFT_DCHECK(key >= 0 && (key >> 5) < nwords);
+                atomicOr(&bm[key >> 5], 1u << (key & 31));
+            }
+            __syncthreads();
+            // thread t owns words [t * per, (t + 1) * per)
+            const int32_t per = (nwords + kLongT - 1) / kLongT;
+            const int32_t w0 = tid * per, w1 = min(nwords, w0 + per);
+            int32_t mine = 0;
+            for (int32_t w = w0; w < w1; ++w) mine += __popc(bm[w]);
+            int32_t x = mine;
+            for (int o = 1; o < 32; o <<= 1) {
+                const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+            }
+            if (lane == 31) wtot[wid] = x;
+            __syncthreads();
+            if (wid == 0) {
+                const int32_t v = wtot[lane];
+                int32_t t = v;
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int32_t y = __shfl_up_sync(0xffffffffu, t, o);
+                    if (lane >= o) t += y;
+                }
+                wtot[lane] = t - v;  // exclusive
+            }
+            __syncthreads();
+            int32_t off = s0 + wtot[wid] + x - mine;
+            for (int32_t w = w0; w < w1; ++w) {
+                uint32_t bits = bm[w];
+                while (bits) {
+                    const int bpos = __ffs(bits) - 1;
+                    bits &= bits - 1;
+                    ev2[off++] = (w << 5) + bpos;
+                }
+            }
+            continue;
+        }
         if (len > kLongSmem) {
             for (int32_t e = threadIdx.x; e < len; e += kLongT) {
                 const int32_t key = ev[s0 + e];
@@ -311,28 +363,28 @@ k3_sum(const DevPlan* __restrict__ P, int m, const int32_t* __restrict__ start,
             const int lr = __shfl_sync(0xffffffffu, r, src);
             double2 pred = make_double2(0.0, 0.0);
             // software-pipelined: while lane 0 adds chunk c, the lanes' loads of
-            // chunk c+1's operands and chunk c+2's event keys are in flight
+            // the operands of chunks c+1 and c+2 and of chunk c+3's event keys
+            // are in flight (an operand load follows its key load, two L2
+            // round trips; one chunk of adds covers about one)
             const auto key_at = [&](int32_t c) { return c + lane < llen ? ev2[ls0 + c + lane] : -1; };
-            int32_t key1 = key_at(32), key2 = -1;
-            double2 g = make_double2(0.0, 0.0), rr = g;
-            {
-                const int32_t key0 = key_at(0);
-                if (key0 >= 0) {
-                    g = gc[(key0 >> 2) * 3 + (key0 & 3)];
-                    rr = rot[static_cast<int64_t>(key0 >> 2) * nr + lr];
+            const auto operands = [&](int32_t key, double2& g, double2& rr) {
+                g = make_double2(0.0, 0.0);
+                rr = g;
+                if (key >= 0) {
+                    g = gc[(key >> 2) * 3 + (key & 3)];
+                    rr = rot[static_cast<int64_t>(key >> 2) * nr + lr];
                 }
-            }
+            };
+            double2 g0, r0, g1, r1;
+            int32_t key2 = key_at(64);
+            operands(key_at(0), g0, r0);
+            operands(key_at(32), g1, r1);
             for (int32_t c0 = 0; c0 < llen; c0 += 32) {
                 const int32_t take = min(32, llen - c0);
-                double2 g_n = make_double2(0.0, 0.0), r_n = g_n;
-                if (c0 + 32 < llen) {
-                    key2 = key_at(c0 + 64);
-                    if (key1 >= 0) {
-                        g_n = gc[(key1 >> 2) * 3 + (key1 & 3)];
-                        r_n = rot[static_cast<int64_t>(key1 >> 2) * nr + lr];
-                    }
-                }
-                if (lane < take) stage[threadIdx.x] = cmul(g, rr);
+                const int32_t key3 = key_at(c0 + 96);
+                double2 g2, r2;
+                operands(key2, g2, r2);
+                if (lane < take) stage[threadIdx.x] = cmul(g0, r0);
                 __syncwarp();
                 if (lane == 0)
                     for (int l = 0; l < take; ++l) {
@@ -341,9 +393,11 @@ k3_sum(const DevPlan* __restrict__ P, int m, const int32_t* __restrict__ start,
                         pred.y += v.y;
                     }
                 __syncwarp();
-                g = g_n;
-                rr = r_n;
-                key1 = key2;
+                g0 = g1;
+                r0 = r1;
+                g1 = g2;
+                r1 = r2;
+                key2 = key3;
             }
             if (lane == 0) {
                 const int64_t le = base + src;
@@ -1433,7 +1487,8 @@ void WideDecoder::enqueue(double2* y, const int64_t* sigma, const int64_t* sigma
                 const int short_blocks = static_cast<int>(
                     std::max<int64_t>(1, std::min<int64_t>((b * 32 + kLongT - 1) / kLongT, 148 * 4)));
                 launch_pdl(pdl_, k3_segsort, static_cast<unsigned>(long_blocks + short_blocks), kLongT, 0, st,
-                           P, m, start_.get(), cnt_.get(), ev_.get(), ev2_.get(), long_.get(), long_blocks);
+                           P, m, start_.get(), cnt_.get(), ev_.get(), ev2_.get(), long_.get(), long_blocks,
+                           acc_n);
             }
             launch_pdl(pdl_, k3_sum, grid_of(nr * b * 32), kT, 0, st, P, m, start_.get(), cnt_.get(), ev2_.get(),
                                                         gc_.get(), rot_.get(), Y);
