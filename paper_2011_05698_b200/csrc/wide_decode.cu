@@ -708,15 +708,20 @@ sel_write(const uint64_t* __restrict__ key, int64_t n_max, const int32_t* __rest
 // ---------------------------------------------------------------- K4
 // rank among the selected buckets by (|y0| desc, bucket asc): blockIdx.x
 // tiles the elements, blockIdx.y the comparison range; partial ranks add up.
+// Compared through the select keys (the magnitude's bit pattern + 1, NaN -> 0:
+// the same order as the magnitudes with NaN as -1), high words first: almost
+// every pair is decided by one 32-bit integer compare instead of two FP64
+// compares on the half-rate pipe.
 __global__ void __launch_bounds__(kT)
-k4_rank(const int32_t* __restrict__ sel_idx, int64_t budget, const double* __restrict__ mag,
+k4_rank(const int32_t* __restrict__ sel_idx, int64_t budget, const uint64_t* __restrict__ key,
         int32_t* __restrict__ rank_out) {
     pdl_entry();
-    __shared__ double tm[kT];
+    __shared__ uint32_t th[kT], tl[kT];
     __shared__ int32_t ti[kT];
     const int64_t e = static_cast<int64_t>(blockIdx.x) * kT + threadIdx.x;
     const int32_t idx = e < budget ? sel_idx[e] : 0;
-    const double mj = e < budget ? mag[idx] : 0.0;
+    const uint64_t kj = e < budget ? key[idx] : 0ull;
+    const uint32_t hj = static_cast<uint32_t>(kj >> 32), lj = static_cast<uint32_t>(kj);
     const int64_t span = (budget + gridDim.y - 1) / gridDim.y;
     const int64_t c0 = blockIdx.y * span, c1 = std::min<int64_t>(c0 + span, budget);
     int32_t rank = 0;
@@ -724,14 +729,21 @@ k4_rank(const int32_t* __restrict__ sel_idx, int64_t budget, const double* __res
         __syncthreads();
         if (t0 + threadIdx.x < c1) {
             const int32_t o = sel_idx[t0 + threadIdx.x];
+            const uint64_t ko = key[o];
             ti[threadIdx.x] = o;
-            tm[threadIdx.x] = mag[o];
+            th[threadIdx.x] = static_cast<uint32_t>(ko >> 32);
+            tl[threadIdx.x] = static_cast<uint32_t>(ko);
         }
         __syncthreads();
         const int lim = static_cast<int>(std::min<int64_t>(kT, c1 - t0));
+#pragma unroll 8
         for (int q = 0; q < lim; ++q) {
-            const double mi = tm[q];
-            rank += (mi > mj) || (mi == mj && ti[q] < idx);
+            const uint32_t hq = th[q];
+            rank += hq > hj;
+            if (hq == hj) {
+                const uint32_t lq = tl[q];
+                rank += (lq > lj) || (lq == lj && ti[q] < idx);
+            }
         }
     }
     if (e < budget && rank) atomicAdd(&rank_out[e], rank);
@@ -1507,7 +1519,7 @@ void WideDecoder::enqueue(double2* y, const int64_t* sigma, const int64_t* sigma
             {
                 const unsigned tiles = static_cast<unsigned>((budget + kT - 1) / kT);
                 const unsigned split = std::max(1u, std::min(64u, 1184u / tiles));
-                launch_pdl(pdl_, k4_rank, dim3(tiles, split), kT, 0, st, sel_idx_.get(), budget, mag_.get(), pos_.get());
+                launch_pdl(pdl_, k4_rank, dim3(tiles, split), kT, 0, st, sel_idx_.get(), budget, key_.get(), pos_.get());
                 launch_pdl(pdl_, k4_scatter, grid_of(budget), kT, 0, st, sel_idx_.get(), pos_.get(), budget,
                                                            order_.get(), mag_.get(), thr_.get());
             }
