@@ -14,7 +14,6 @@ namespace {
 constexpr int kT = 256;               // threads per CTA of the grid kernels
 constexpr int kSelBits = 12;           // radix-select digit (last digit: 4 bits)
 constexpr int kSelBins = 1 << kSelBits;
-constexpr int kChunk = 4096;          // selection compaction chunk
 constexpr int kScanT = 1024;
 constexpr int kLongSeg = 64;          // longer event segments sort with a whole CTA
 constexpr int kLongSmem = 8192;
@@ -593,89 +592,81 @@ sel_finish(const uint64_t* __restrict__ key, int64_t n_max, const int32_t* __res
     }
 }
 
+// Ordered compaction in one launch: indices of the keys > thr and of the
+// first need_eq keys == thr (sel = {thr, mask, need_eq, ...} after the
+// select), in index order.  Blocks draw their chunk from a ticket, publish
+// the chunk's (> thr, == thr) counts in one flagged word, and sum the words
+// of the chunks before theirs -- published by blocks that drew earlier
+// tickets, so they are running or done and the wait cannot deadlock -- then
+// write their own slice.  The last block out clears the words and the ticket
+// for the next use.
+constexpr int kCChunk = 1024;
 __global__ void __launch_bounds__(kT)
-sel_count(const uint64_t* __restrict__ key, int64_t n_max, const int32_t* __restrict__ n_dev,
-          const uint64_t* __restrict__ sel, int32_t* __restrict__ cgt, int32_t* __restrict__ ceq) {
-    pdl_entry();
-    __shared__ int gt_s, eq_s;
-    const int64_t n = n_or(n_dev, n_max);
-    const uint64_t thr = sel[0];
-    if (threadIdx.x == 0) gt_s = eq_s = 0;
-    __syncthreads();
-    int gt = 0, eq = 0;
-    const int64_t base = static_cast<int64_t>(blockIdx.x) * kChunk;
-    for (int i = threadIdx.x; i < kChunk; i += kT) {
-        const int64_t j = base + i;
-        if (j >= n) break;
-        const uint64_t k = key[j];
-        gt += k > thr;
-        eq += k == thr;
-    }
-    atomicAdd(&gt_s, gt);
-    atomicAdd(&eq_s, eq);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        cgt[blockIdx.x] = gt_s;
-        ceq[blockIdx.x] = eq_s;
-    }
-}
-
-// Per chunk: selected before it = gt before + min(eq before, need_eq).
-__global__ void __launch_bounds__(kScanT)
-sel_offsets(const int32_t* __restrict__ cgt, const int32_t* __restrict__ ceq, int64_t nchunks,
-            const uint64_t* __restrict__ sel, int32_t* __restrict__ off_sel,
-            int32_t* __restrict__ off_eq) {
-    pdl_entry();
-    __shared__ int32_t pg[kScanT], pe[kScanT];
-    const int64_t per = (nchunks + kScanT - 1) / kScanT;
-    const int64_t lo = threadIdx.x * per, hi = std::min<int64_t>(lo + per, nchunks);
-    int32_t sg = 0, se = 0;
-    for (int64_t i = lo; i < hi; ++i) {
-        sg += cgt[i];
-        se += ceq[i];
-    }
-    pg[threadIdx.x] = sg;
-    pe[threadIdx.x] = se;
-    __syncthreads();
-    for (int o = 1; o < kScanT; o <<= 1) {
-        const int32_t a = threadIdx.x >= o ? pg[threadIdx.x - o] : 0;
-        const int32_t c = threadIdx.x >= o ? pe[threadIdx.x - o] : 0;
-        __syncthreads();
-        pg[threadIdx.x] += a;
-        pe[threadIdx.x] += c;
-        __syncthreads();
-    }
-    const int64_t need = static_cast<int64_t>(sel[2]);
-    int32_t rg = pg[threadIdx.x] - sg, re = pe[threadIdx.x] - se;
-    for (int64_t i = lo; i < hi; ++i) {
-        off_sel[i] = rg + static_cast<int32_t>(std::min<int64_t>(re, need));
-        off_eq[i] = re;
-        rg += cgt[i];
-        re += ceq[i];
-    }
-}
-
-// Ordered compaction: keys > thr, and the first need_eq keys == thr.
-__global__ void __launch_bounds__(kT)
-sel_write(const uint64_t* __restrict__ key, int64_t n_max, const int32_t* __restrict__ n_dev,
-          const uint64_t* __restrict__ sel, const int32_t* __restrict__ off_sel,
-          const int32_t* __restrict__ off_eq, int32_t* __restrict__ out_idx) {
+sel_compact(const uint64_t* __restrict__ key, int64_t n_max, const int32_t* __restrict__ n_dev,
+            const uint64_t* __restrict__ sel, unsigned long long* __restrict__ pub,
+            int32_t* __restrict__ ctl, int32_t* __restrict__ out_idx) {
     pdl_entry();
     __shared__ int warp_sel[kT / 32], warp_eq[kT / 32];
     __shared__ int64_t run_sel, run_eq;
+    __shared__ int s_bid, gt_s, eq_s, s_last;
     const int64_t n = n_or(n_dev, n_max);
     const uint64_t thr = sel[0];
     const int64_t need_eq = static_cast<int64_t>(sel[2]);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     if (threadIdx.x == 0) {
-        run_sel = off_sel[blockIdx.x];
-        run_eq = off_eq[blockIdx.x];
+        s_bid = atomicAdd(&ctl[0], 1);
+        gt_s = eq_s = 0;
     }
     __syncthreads();
-    const int64_t base = static_cast<int64_t>(blockIdx.x) * kChunk;
-    for (int r = 0; r < kChunk / kT; ++r) {
+    const int bid = s_bid;
+    const int64_t base = static_cast<int64_t>(bid) * kCChunk;
+    constexpr int kR = kCChunk / kT;
+    uint64_t kreg[kR];
+    int gt = 0, eq = 0;
+#pragma unroll
+    for (int r = 0; r < kR; ++r) {
         const int64_t j = base + static_cast<int64_t>(r) * kT + threadIdx.x;
-        const uint64_t k = j < n ? key[j] : 0ull;
+        kreg[r] = j < n ? key[j] : 0ull;
+        gt += j < n && kreg[r] > thr;
+        eq += j < n && kreg[r] == thr;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        gt += __shfl_xor_sync(0xffffffffu, gt, o);
+        eq += __shfl_xor_sync(0xffffffffu, eq, o);
+    }
+    if (lane == 0) {
+        atomicAdd(&gt_s, gt);
+        atomicAdd(&eq_s, eq);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+        *reinterpret_cast<volatile unsigned long long*>(&pub[bid]) =
+            (1ull << 63) | (static_cast<unsigned long long>(gt_s) << 31) |
+            static_cast<unsigned long long>(eq_s);
+    if (wid == 0) {
+        int64_t g = 0, e = 0;
+        for (int q = lane; q < bid; q += 32) {
+            unsigned long long w;
+            do {
+                w = *reinterpret_cast<volatile unsigned long long*>(&pub[q]);
+            } while (!(w >> 63));
+            g += static_cast<int64_t>((w >> 31) & 0x7fffffffull);
+            e += static_cast<int64_t>(w & 0x7fffffffull);
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            g += __shfl_xor_sync(0xffffffffu, g, o);
+            e += __shfl_xor_sync(0xffffffffu, e, o);
+        }
+        if (lane == 0) {
+            run_sel = g + std::min<int64_t>(e, need_eq);
+            run_eq = e;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kR; ++r) {
+        const int64_t j = base + static_cast<int64_t>(r) * kT + threadIdx.x;
+        const uint64_t k = kreg[r];
         const bool is_eq = j < n && k == thr;
         const bool is_gt = j < n && k > thr;
         const unsigned eq_mask = __ballot_sync(0xffffffffu, is_eq);
@@ -702,6 +693,18 @@ sel_write(const uint64_t* __restrict__ key, int64_t n_max, const int32_t* __rest
             run_eq += eq_total;
         }
         __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        __threadfence();
+        s_last = atomicAdd(&ctl[1], 1) == static_cast<int>(gridDim.x) - 1;
+    }
+    __syncthreads();
+    if (s_last) {
+        for (int q = threadIdx.x; q < static_cast<int>(gridDim.x); q += kT) pub[q] = 0ull;
+        if (threadIdx.x == 0) {
+            ctl[0] = 0;
+            ctl[1] = 0;
+        }
     }
 }
 
@@ -1364,11 +1367,13 @@ WideDecoder::WideDecoder(const DevPlan& plan, int64_t acc_cap, int64_t b_max, in
     key_.reset(NK);
     mag_.reset(B);
     hist_.reset(kSelBins);
-    const int64_t nch = (NK + kChunk - 1) / kChunk;
-    chunk_gt_.reset(nch);
-    chunk_eq_.reset(nch);
-    chunk_off_sel_.reset(nch);
-    chunk_off_eq_.reset(nch);
+    // sel_compact: a flagged count word per chunk and {ticket, blocks done},
+    // zero between launches (its last block clears them)
+    const int64_t ncc = (NK + kCChunk - 1) / kCChunk;
+    cpub_.reset(static_cast<size_t>(ncc));
+    cctl_.reset(2);
+    MSFFT_CUDA(cudaMemset(cpub_.get(), 0, static_cast<size_t>(ncc) * sizeof(unsigned long long)));
+    MSFFT_CUDA(cudaMemset(cctl_.get(), 0, 2 * sizeof(int32_t)));
     sel_idx_.reset(std::max(Q, A));
     order_.reset(Q);
     yr_.reset(Q * R);
@@ -1413,14 +1418,9 @@ void WideDecoder::select_kth(const uint64_t* key, int64_t n_max, const int32_t* 
 
 void WideDecoder::compact_selected(const uint64_t* key, int64_t n_max, const int32_t* n_dev,
                                    int32_t* out_idx, cudaStream_t st) {
-    const int64_t nch = (n_max + kChunk - 1) / kChunk;
-    launch_pdl(pdl_, sel_count, static_cast<unsigned>(nch), kT, 0, st, key, n_max, n_dev, sel_.get(),
-                                                         chunk_gt_.get(), chunk_eq_.get());
-    launch_pdl(pdl_, sel_offsets, 1, kScanT, 0, st, chunk_gt_.get(), chunk_eq_.get(), nch, sel_.get(),
-                                      chunk_off_sel_.get(), chunk_off_eq_.get());
-    launch_pdl(pdl_, sel_write, static_cast<unsigned>(nch), kT, 0, st, key, n_max, n_dev, sel_.get(),
-                                                         chunk_off_sel_.get(), chunk_off_eq_.get(),
-                                                         out_idx);
+    const int64_t nch = (n_max + kCChunk - 1) / kCChunk;
+    launch_pdl(pdl_, sel_compact, static_cast<unsigned>(nch), kT, 0, st, key, n_max, n_dev, sel_.get(),
+               cpub_.get(), cctl_.get(), out_idx);
     MSFFT_LAUNCH_CHECK("wide compaction");
 }
 

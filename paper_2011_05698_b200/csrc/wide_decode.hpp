@@ -78,7 +78,8 @@ private:
     // K4 / K7
     DeviceBuffer<uint64_t> key_;
     DeviceBuffer<uint32_t> hist_;
-    DeviceBuffer<int32_t> chunk_gt_, chunk_eq_, chunk_off_sel_, chunk_off_eq_, sel_idx_, order_;
+    DeviceBuffer<int32_t> cctl_, sel_idx_, order_;
+    DeviceBuffer<unsigned long long> cpub_;
     DeviceBuffer<double> mag_;
     // K5 / K6
     DeviceBuffer<double2> yr_, cand_v_, cand_sum_;
