@@ -40,7 +40,7 @@ python tools/stage_roofline.py $O/c3_stages.csv --workload "C3: N=2^24, K=1000, 
 python tools/run_c5.py --reps 2 > $O/c5_plain.json 2> $O/c5_plain.err || exit 1
 MSFFT_PROFILE_AFTER_PLAN=1 ncu --profile-from-start off --clock-control none --csv --metrics $M \
     python tools/run_c5.py --reps 1 > $O/c5_stages.csv 2> $O/c5_stages.err
-python tools/stage_roofline.py $O/c5_stages.csv --workload "C5: N=2^27, K=10^4, c128 (tools/run_c5.py, serial path)" > $O/c5_stage_roofline.json
+python tools/stage_roofline.py $O/c5_stages.csv --anchor-grid-max --workload "C5: N=2^27, K=10^4, c128 (tools/run_c5.py, serial path)" > $O/c5_stage_roofline.json
 python tools/run_c5.py --no-stages --reps 5 > $O/c5_run.json 2> $O/c5_run.err
 python tools/configs_table.py > $O/configs_table.log 2>&1
 # the bench itself on this box, reading the captures above (same native
