@@ -858,13 +858,23 @@ __global__ void k5_stage_phase(const DevPlan* __restrict__ P, int m,
 }
 
 // One lane group per ranked bucket (decode_body.cuh K5 + K6 estimate).
+constexpr int kK5Stage = 1024;  // (lane groups per CTA) x (stages) staged in shared memory
 __global__ void __launch_bounds__(kT)
 k5_locate(const DevPlan* __restrict__ P, int m, const int64_t* __restrict__ sigma_inv,
           const int32_t* __restrict__ order, const double* __restrict__ mag,
           const double* __restrict__ thr_p, const double2* __restrict__ yr,
           const double* __restrict__ phi_t, const int32_t* __restrict__ pcode,
-          int64_t* __restrict__ cand_f, double2* __restrict__ cand_v, int32_t* __restrict__ err) {
+          int64_t* __restrict__ cand_f, double2* __restrict__ cand_v, int32_t* __restrict__ err,
+          const double2* __restrict__ Y, uint32_t* __restrict__ zero_a, int64_t zero_an,
+          uint32_t* __restrict__ zero_b, int64_t zero_bn) {
     pdl_entry();
+    // Y != nullptr: no k5_stage_phase launch ran -- each lane group computes
+    // its bucket's stage phases into shared memory itself (k5_stage_phase's
+    // arithmetic), and this launch clears the counters that kernel would
+    GRID_LOOP(i, zero_an) zero_a[i] = 0u;
+    GRID_LOOP(i, zero_bn) zero_b[i] = 0u;
+    __shared__ double s_phi[kK5Stage];
+    __shared__ int32_t s_code[kK5Stage];
     const DevIter& it = P->it[m];
     const int64_t n = P->n, nmask = n - 1;
     const double inv_n = P->inv_n;
@@ -904,7 +914,38 @@ k5_locate(const DevPlan* __restrict__ P, int m, const int64_t* __restrict__ sigm
         const int64_t beta = live ? order[rank] : 0;
         int64_t f_out = -1;
         double2 v_out = make_double2(0.0, 0.0);
-        const double2 y0 = live ? yr[rank * nr] : make_double2(0.0, 0.0);
+        double2 y0 = make_double2(0.0, 0.0);
+        const double* phi_r = phi_t + rank * ns;
+        const int32_t* code_r = pcode + rank * ns;
+        if (Y) {
+            double* my_phi = s_phi + (threadIdx.x / gsz) * ns;
+            int32_t* my_code = s_code + (threadIdx.x / gsz) * ns;
+            __syncwarp();  // the previous rank's chain is done with the slices
+            if (live) {
+                y0 = Y[beta];
+                for (int st = 1 + glane; st < nr; st += gsz) {
+                    const double2 yt = Y[st * it.b + beta];
+                    int code = 0;
+                    double ph = 0.0;
+                    if (yt.x == 0.0 && yt.y == 0.0) {
+                        code = 1;
+                    } else {
+                        const double2 z = cdiv_ref(y0.x, y0.y, yt.x, yt.y);
+                        if (z.x == 0.0 && z.y == 0.0) code = 2;
+                        ph = atan2(z.y, z.x);
+                        if (ph < 0.0) ph += kTwoPi;
+                        ph = ph + 0.0;
+                    }
+                    my_phi[st - 1] = ph;
+                    my_code[st - 1] = code;
+                }
+            }
+            __syncwarp();
+            phi_r = my_phi;
+            code_r = my_code;
+        } else if (live) {
+            y0 = yr[rank * nr];
+        }
         bool ok = live && mag[beta] > thr;
         if (ok && y0.x == 0.0 && y0.y == 0.0) ok = false;
         double u_min = (2.0 * static_cast<double>(beta) - 1.0) * Ld / 2.0;
@@ -913,8 +954,7 @@ k5_locate(const DevPlan* __restrict__ P, int m, const int64_t* __restrict__ sigm
         const int nst = it.nstage_tab;
         if (fast) {
             u_min = locate_stages_dispatch(gsz, jpl, u_min, nst, live, ok, glane, lcfg, q / 2.0,
-                                           inv_n, phi_t + rank * ns, pcode + rank * ns, s_blk,
-                                           s_tau, err);
+                                           inv_n, phi_r, code_r, s_blk, s_tau, err);
             if (nst > 0) len = it.stage_len[nst];
             stage = nst;  // the loop below has nothing left
         }
@@ -927,8 +967,8 @@ k5_locate(const DevPlan* __restrict__ P, int m, const int64_t* __restrict__ sigm
             }
             double ph = 0.0;
             if (ok) {
-                const int64_t pe = rank * ns + (stage - 1);
-                const int code = pcode[pe];
+                const int pe = stage - 1;
+                const int code = code_r[pe];
                 if (code == 1) {
                     ok = false;
                 } else {
@@ -936,7 +976,7 @@ k5_locate(const DevPlan* __restrict__ P, int m, const int64_t* __restrict__ sigm
                         if (glane == 0) atomicCAS(err, 0, kDecErrPhaseZero);
                         ok = false;
                     }
-                    ph = phi_t[pe];
+                    ph = phi_r[pe];
                 }
             }
             const int64_t tau = taus[stage];
@@ -1537,13 +1577,20 @@ void WideDecoder::enqueue(double2* y, const int64_t* sigma, const int64_t* sigma
             zero_an = budget >= kF6BucketMin ? int64_t{kF6B} : budget;
         }
         const int64_t zero_bn = m + 1 < H.iters ? H.it[m + 1].b : 0;
-        launch_pdl(pdl_, k5_stage_phase, grid_of(std::max(budget * nr, std::max(zero_an, zero_bn))), kT, 0, st,
-                   P, m, order_.get(), Y, yr_.get(), phi_.get(), pcode_.get(), zero_a, zero_an,
-                   reinterpret_cast<uint32_t*>(cnt_.get()), zero_bn);
-        launch_pdl(pdl_, k5_locate, grid_of(budget * 32), kT, 0, st, P, m, sigma_inv, order_.get(), mag_.get(),
-                                                       thr_.get(), yr_.get(), phi_.get(),
-                                                       pcode_.get(), cand_f_.get(), cand_v_.get(),
-                                                       err);
+        // stage phases inside k5_locate (one launch) when its lane groups'
+        // slices fit the shared staging; else the separate kernel first
+        const int gsz = H.l > 16 ? 32 : (H.l > 8 ? 16 : (H.l > 4 ? 8 : 4));
+        const bool k5_one = static_cast<int64_t>(kT / gsz) * (nr - 1) <= kK5Stage;
+        if (!k5_one)
+            launch_pdl(pdl_, k5_stage_phase, grid_of(std::max(budget * nr, std::max(zero_an, zero_bn))), kT, 0,
+                       st, P, m, order_.get(), Y, yr_.get(), phi_.get(), pcode_.get(), zero_a, zero_an,
+                       reinterpret_cast<uint32_t*>(cnt_.get()), zero_bn);
+        launch_pdl(pdl_, k5_locate, grid_of(std::max(budget * 32, k5_one ? std::max(zero_an, zero_bn) : int64_t{0})),
+                   kT, 0, st, P, m, sigma_inv, order_.get(), mag_.get(), thr_.get(), yr_.get(), phi_.get(),
+                   pcode_.get(), cand_f_.get(), cand_v_.get(), err,
+                   k5_one ? static_cast<const double2*>(Y) : nullptr, k5_one ? zero_a : nullptr,
+                   k5_one ? zero_an : int64_t{0},
+                   k5_one ? reinterpret_cast<uint32_t*>(cnt_.get()) : nullptr, k5_one ? zero_bn : int64_t{0});
         MSFFT_LAUNCH_CHECK("wide K4/K5");
         // ---- K6
         if (k6_small_path) {
