@@ -269,6 +269,26 @@ def test_wide_decode_bit_identical_to_cta_decode(oracle, monkeypatch, n, k, dtyp
     assert np.array_equal(f1, f0) and np.array_equal(c1, c0)
 
 
+@pytest.mark.parametrize("l,q", [(4, 1.0), (4, 2.0), (8, 2.0), (32, 1.0)])
+def test_wide_decode_other_multiscale_configs(oracle, monkeypatch, l, q):
+    """The wide decode's locate kernel with other lane-group sizes (l = 4, 8,
+    32 -> groups of 4, 8, 32 lanes) and stage counts: (4, 2) has more stages
+    than the shared staging of k5_locate holds for 64 groups per CTA, so it
+    takes the separate k5_stage_phase launch; the others compute their stage
+    phases inside k5_locate.  Each equals the one-CTA decode bit for bit."""
+    n, k = 1 << 20, 1500
+    x, _, _ = __import__("paper_2011_05698_b200.workloads", fromlist=["x"]).make_signal_np(
+        n, k, 21, 25.0, "complex128", "loguniform_0.1_10")
+    res = []
+    for wide in ("8", "0"):
+        monkeypatch.setenv("MSFFT_WIDE_MAX_BATCH", wide)
+        plan = M.Plan(n, k, M.MultiscaleConfig(l, q), 1e-6, "complex128")
+        res.append(plan.execute(x[None, :], [4242]))
+    (f1, c1, n1, _), (f0, c0, n0, _) = res
+    assert int(n1[0]) == int(n0[0]) > 0
+    assert np.array_equal(f1, f0) and np.array_equal(c1, c0)
+
+
 @pytest.mark.parametrize("knob,values", [("MSFFT_ENC_SPLIT", ("1", "0")),
                                          ("MSFFT_WIDE_PDL", ("1", "0")),
                                          ("MSFFT_WIDE_GRAPH", ("1", "0")),
